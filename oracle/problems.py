@@ -1,0 +1,317 @@
+"""Objective / penalty restatements (test infrastructure only).
+
+Each class restates one reference problem from
+`/root/reference/pkg/src/genopt/builtins.py` with numpy arithmetic in the same
+order as the reference, so float64 results are bit-identical to it.  The
+`Sol` container restates `core.Solution` (core.py:154-200): a d1 x d2 int64
+matrix, per-row effective lengths, objectives and penalty.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+PERM, BINARY, INTEGER = "permutation", "binary", "integer"
+SINGLE, MULTI_FIXED, PARTITION = "single_seq", "multi_fixed", "multi_partition"
+MIN, MAX = "minimize", "maximize"
+
+
+class Sol:
+    """core.py:154-200 — row-organised integer solution."""
+
+    __slots__ = ("data", "sizes", "obj", "pen")
+
+    def __init__(self, data, sizes, m: int = 1):
+        self.data = np.asarray(data, dtype=np.int64)
+        self.sizes = np.asarray(sizes, dtype=np.int64)
+        self.obj = np.full(m, np.nan)
+        self.pen = 0.0
+
+    @property
+    def d1(self):
+        return self.data.shape[0]
+
+    @property
+    def d2(self):
+        return self.data.shape[1]
+
+    def row(self, r):
+        return self.data[r, : self.sizes[r]]
+
+    def flat(self):
+        return np.concatenate([self.row(r) for r in range(self.d1)]) \
+            if self.d1 > 1 else self.row(0).copy()
+
+    def clone(self):
+        out = Sol.__new__(Sol)
+        out.data = self.data.copy()
+        out.sizes = self.sizes.copy()
+        out.obj = self.obj.copy()
+        out.pen = self.pen
+        return out
+
+    def key(self):
+        return (tuple(int(s) for s in self.sizes),
+                tuple(int(v) for r in range(self.d1) for v in self.row(r)))
+
+
+@dataclass
+class Spec:
+    """The slice of core.ProblemConfig (core.py:112-151) the path reads."""
+
+    kind: str
+    d1: int
+    d2: int
+    n: int
+    row_mode: str
+    directions: tuple = (MIN,)
+    weights: tuple = (1.0,)
+    lb: int = 0
+    ub: int = 0
+    penalty_weight: float | None = None
+
+    @property
+    def m(self):
+        return len(self.directions)
+
+
+class Problem:
+    spec: Spec
+
+    def objective(self, i: int, sol: Sol) -> float:
+        raise NotImplementedError
+
+    def penalty(self, sol: Sol) -> float:
+        return 0.0
+
+    def matrices(self):
+        """init_matrices (problems.py:62-64)."""
+        return []
+
+    def payload_nbytes(self) -> int:
+        return sum(m.nbytes for m in self.matrices())
+
+
+def evaluate(problem: Problem, sol: Sol):
+    """problems.py:77-94 with validate=False (the engine's call)."""
+    for i in range(problem.spec.m):
+        sol.obj[i] = problem.objective(i, sol)
+    sol.pen = float(problem.penalty(sol))
+    return sol.obj, sol.pen
+
+
+class Tsp(Problem):
+    """builtins.py:53-77."""
+
+    def __init__(self, dist):
+        self.dist = np.asarray(dist, dtype=np.float64)
+        n = self.dist.shape[0]
+        self.n = n
+        self.spec = Spec(PERM, 1, n, n, SINGLE)
+
+    def objective(self, i, sol):
+        t = sol.row(0)
+        if len(t) < 2:
+            return 0.0
+        return float(self.dist[t[:-1], t[1:]].sum() + self.dist[t[-1], t[0]])
+
+    def matrices(self):
+        return [self.dist]
+
+
+class Routing(Problem):
+    """builtins.py:80-152 (CVRP); customers are values 0..n-1 at matrix c+1."""
+
+    def __init__(self, dist, demands, capacity, vehicles):
+        self.dist = np.asarray(dist, dtype=np.float64)
+        self.demands = np.asarray(demands, dtype=np.float64)
+        self.capacity = float(capacity)
+        self.vehicles = int(vehicles)
+        self.n = len(self.demands)
+        self.spec = Spec(PERM, self.vehicles, self.n, self.n, PARTITION)
+
+    def route_len(self, route) -> float:
+        if len(route) == 0:
+            return 0.0
+        nodes = route + 1
+        total = self.dist[0, nodes[0]] + self.dist[nodes[-1], 0]
+        if len(nodes) > 1:
+            total += self.dist[nodes[:-1], nodes[1:]].sum()
+        return float(total)
+
+    def objective(self, i, sol):
+        return sum(self.route_len(sol.row(r)) for r in range(sol.d1))
+
+    def load_excess(self, sol) -> float:
+        total = 0.0
+        for r in range(sol.d1):
+            load = self.demands[sol.row(r)].sum()
+            total += max(0.0, float(load) - self.capacity)
+        return total
+
+    def penalty(self, sol):
+        return self.load_excess(sol)
+
+    def matrices(self):
+        return [self.dist[1:, 1:]]
+
+    def payload_nbytes(self):
+        return self.dist.nbytes + self.demands.nbytes
+
+
+class Vrptw(Routing):
+    """builtins.py:155-190: capacity excess + sequential lateness."""
+
+    def __init__(self, dist, demands, capacity, vehicles, ready, due, service):
+        super().__init__(dist, demands, capacity, vehicles)
+        self.ready = np.asarray(ready, dtype=np.float64)
+        self.due = np.asarray(due, dtype=np.float64)
+        self.service = np.asarray(service, dtype=np.float64)
+
+    def lateness(self, sol) -> float:
+        total = 0.0
+        for r in range(sol.d1):
+            route = sol.row(r)
+            if len(route) == 0:
+                continue
+            t = self.ready[0]
+            prev = 0
+            for c in route:
+                node = c + 1
+                arrival = max(self.ready[node], t + self.dist[prev, node])
+                total += max(0.0, arrival - self.due[node])
+                t = arrival + self.service[node]
+                prev = node
+            total += max(0.0, t + self.dist[prev, 0] - self.due[0])
+        return float(total)
+
+    def penalty(self, sol):
+        return self.load_excess(sol) + self.lateness(sol)
+
+    def payload_nbytes(self):
+        return super().payload_nbytes() + self.ready.nbytes + self.due.nbytes \
+            + self.service.nbytes
+
+
+class Knapsack(Problem):
+    """builtins.py:240-262 (maximise value, penalty = weight excess)."""
+
+    def __init__(self, weights, values, capacity):
+        self.w = np.asarray(weights, dtype=np.float64)
+        self.v = np.asarray(values, dtype=np.float64)
+        self.capacity = float(capacity)
+        self.n = len(self.w)
+        self.spec = Spec(BINARY, 1, self.n, self.n, SINGLE, directions=(MAX,))
+
+    def objective(self, i, sol):
+        return float(self.v @ sol.row(0))
+
+    def penalty(self, sol):
+        return max(0.0, float(self.w @ sol.row(0)) - self.capacity)
+
+
+class Qap(Problem):
+    """builtins.py:265-290."""
+
+    def __init__(self, flow, dist):
+        self.flow = np.asarray(flow, dtype=np.float64)
+        self.dist = np.asarray(dist, dtype=np.float64)
+        self.n = self.flow.shape[0]
+        self.spec = Spec(PERM, 1, self.n, self.n, SINGLE)
+
+    def objective(self, i, sol):
+        p = sol.row(0)
+        return float((self.flow * self.dist[np.ix_(p, p)]).sum())
+
+    def matrices(self):
+        return [self.flow, self.dist]
+
+
+class JspInt(Problem):
+    """builtins.py:408-456: priority-decoded serial schedule generator."""
+
+    def __init__(self, jobs):
+        self.jobs = [[(int(m), int(d)) for m, d in ops] for ops in jobs]
+        self.n_jobs = len(self.jobs)
+        self.per_job = len(self.jobs[0])
+        self.n_machines = 1 + max(m for ops in self.jobs for m, _ in ops)
+        self.n_ops = self.n_jobs * self.per_job
+        self.spec = Spec(INTEGER, 1, self.n_ops, self.n_ops, SINGLE, lb=0,
+                         ub=self.n_ops - 1)
+
+    def objective(self, i, sol):
+        prio = sol.row(0)
+        nxt = [0] * self.n_jobs
+        job_free = [0.0] * self.n_jobs
+        mach_free = [0.0] * self.n_machines
+        span = 0.0
+        for _ in range(self.n_ops):
+            pick, pick_key = -1, None
+            for j in range(self.n_jobs):
+                k = nxt[j]
+                if k >= self.per_job:
+                    continue
+                op = j * self.per_job + k
+                key = (int(prio[op]), op)
+                if pick_key is None or key < pick_key:
+                    pick, pick_key = j, key
+            m, d = self.jobs[pick][nxt[pick]]
+            done = max(job_free[pick], mach_free[m]) + d
+            job_free[pick] = done
+            mach_free[m] = done
+            nxt[pick] += 1
+            span = max(span, done)
+        return float(span)
+
+
+def scalar_fitness(problem: Problem, sol: Sol, penalty_weight: float) -> float:
+    """engine.py:215-222 via core.scalarize (core.py:292-307)."""
+    spec = problem.spec
+    total = 0.0
+    for value, d, w in zip(sol.obj, spec.directions, spec.weights):
+        total += w * (-value if d == MAX else value)
+    return total + penalty_weight * sol.pen
+
+
+def acceptance_delta(problem, cand: Sol, cur: Sol, penalty_weight: float) -> float:
+    """engine.py:225-235 (Weighted branch — the only one on the path)."""
+    return scalar_fitness(problem, cand, penalty_weight) - \
+        scalar_fitness(problem, cur, penalty_weight)
+
+
+def compare(problem, a: Sol, b: Sol) -> int:
+    """core.py:315-347 (Weighted): -1 a better, 0 equal, 1 b better."""
+    fa_ok, fb_ok = a.pen == 0.0, b.pen == 0.0
+    if fa_ok != fb_ok:
+        return -1 if fa_ok else 1
+    if not fa_ok and a.pen != b.pen:
+        return -1 if a.pen < b.pen else 1
+    fa, fb = _scal(problem, a), _scal(problem, b)
+    if fa == fb:
+        return 0
+    return -1 if fa < fb else 1
+
+
+def _scal(problem, sol):
+    total = 0.0
+    for value, d, w in zip(sol.obj, problem.spec.directions, problem.spec.weights):
+        total += w * (-value if d == MAX else value)
+    return total
+
+
+def validate(problem: Problem, sol: Sol) -> bool:
+    """Structural validity (core.py:212-274), boolean form."""
+    s = problem.spec
+    if sol.data.shape != (s.d1, s.d2) or np.any(sol.sizes < 0) or np.any(sol.sizes > s.d2):
+        return False
+    if s.kind == PERM:
+        if s.row_mode == SINGLE:
+            return sorted(sol.row(0).tolist()) == list(range(s.n))
+        if s.row_mode == MULTI_FIXED:
+            return all(sorted(sol.row(r).tolist()) == list(range(s.n)) for r in range(s.d1))
+        return sorted(sol.flat().tolist()) == list(range(s.n))
+    if s.kind == BINARY:
+        return all(set(sol.row(r).tolist()) <= {0, 1} for r in range(s.d1))
+    return all(((sol.row(r) >= s.lb) & (sol.row(r) <= s.ub)).all() for r in range(s.d1))
