@@ -1,0 +1,1017 @@
+// engine.cu — libcugenopt.so: the C ABI (include/cugenopt.h) over the
+// hand-written sm_100a kernels in kernels/*.cuh.
+//
+// Host responsibilities (all native, no Python on the run path):
+//   * instance analysis + layout choice (go_dist.cuh) and device images;
+//   * shared-memory auto-extension: cudaFuncSetAttribute up to the device's
+//     opt-in limit (paper §4.3), teams-per-CTA from the remaining budget;
+//   * the generation loop of _run_single (engine.py:681-750) as a pipeline of
+//     (evolve chunk, epilogue) launches that never waits on the device except
+//     to bound the queue depth; wall-clock budget enforced on the device;
+//   * NVRTC-compiled user operators (go_jit.cpp) with probe/exclusion.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/cugenopt.h"
+#include "go_drv.h"
+#include "go_jit.h"
+#include "kernels/go_epilogue.cuh"
+#include "kernels/go_tsp_entry.cuh"
+
+// ---- static instantiations: built-in operators, every layout ----------------
+GO_TSP_KERNELS(i16f, go::DistI16Full, go::NoCustomOps)
+GO_TSP_KERNELS(i16t, go::DistI16Tri, go::NoCustomOps)
+GO_TSP_KERNELS(i32f, go::DistI32Full, go::NoCustomOps)
+GO_TSP_KERNELS(i32t, go::DistI32Tri, go::NoCustomOps)
+GO_TSP_KERNELS(f64f, go::DistF64Full, go::NoCustomOps)
+GO_TSP_KERNELS(f64t, go::DistF64Tri, go::NoCustomOps)
+GO_TSP_KERNELS(i16g, go::DistI16FullG, go::NoCustomOps)
+GO_TSP_KERNELS(i32g, go::DistI32FullG, go::NoCustomOps)
+GO_TSP_KERNELS(f64g, go::DistF64FullG, go::NoCustomOps)
+
+#define GO_EVAL_KERNELS(SUFFIX, D)                                                            \
+  extern "C" __global__ void go_eval_tsp_##SUFFIX(const void* inst, int n, const short* g,   \
+                                                  double* obj) {                             \
+    go::tsp_eval_entry<D>(inst, n, g, obj);                                                   \
+  }                                                                                           \
+  extern "C" __global__ void go_delta_tsp_##SUFFIX(const void* inst, int n, const short* g,  \
+                                                   const int* mv, double* d, short* cand) {   \
+    go::tsp_delta_entry<D>(inst, n, g, mv, d, cand);                                          \
+  }
+GO_EVAL_KERNELS(i16, go::DistI16FullG)
+GO_EVAL_KERNELS(i32, go::DistI32FullG)
+GO_EVAL_KERNELS(f64, go::DistF64FullG)
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                               \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(GO_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));              \
+  } while (0)
+
+#define CU(x)                                                                               \
+  do {                                                                                      \
+    if (!gohost::drv()) return fail(GO_E_NODEVICE, "CUDA driver API unavailable");          \
+    CUresult r_ = (x);                                                                      \
+    if (r_ != CUDA_SUCCESS) {                                                               \
+      const char* s_ = nullptr;                                                             \
+      gohost::drv()->GetErrorString(r_, &s_);                                               \
+      return fail(GO_E_CUDA, std::string(#x) + ": " + (s_ ? s_ : "?"));                     \
+    }                                                                                       \
+  } while (0)
+
+enum Elem { E_I16 = 0, E_I32 = 1, E_F64 = 2 };
+
+struct LayoutInfo {
+  const char* dist_type;  // device type name (NVRTC instantiation)
+  void* evolve;
+  void* probe;
+  int elem;
+  bool tri, global;
+};
+
+const LayoutInfo kLayouts[9] = {
+    {"go::DistI16Full", (void*)go_evolve_tsp_i16f, (void*)go_probe_tsp_i16f, E_I16, false, false},
+    {"go::DistI16Tri", (void*)go_evolve_tsp_i16t, (void*)go_probe_tsp_i16t, E_I16, true, false},
+    {"go::DistI32Full", (void*)go_evolve_tsp_i32f, (void*)go_probe_tsp_i32f, E_I32, false, false},
+    {"go::DistI32Tri", (void*)go_evolve_tsp_i32t, (void*)go_probe_tsp_i32t, E_I32, true, false},
+    {"go::DistF64Full", (void*)go_evolve_tsp_f64f, (void*)go_probe_tsp_f64f, E_F64, false, false},
+    {"go::DistF64Tri", (void*)go_evolve_tsp_f64t, (void*)go_probe_tsp_f64t, E_F64, true, false},
+    {"go::DistI16FullG", (void*)go_evolve_tsp_i16g, (void*)go_probe_tsp_i16g, E_I16, false, true},
+    {"go::DistI32FullG", (void*)go_evolve_tsp_i32g, (void*)go_probe_tsp_i32g, E_I32, false, true},
+    {"go::DistF64FullG", (void*)go_evolve_tsp_f64g, (void*)go_probe_tsp_f64g, E_F64, false, true},
+};
+
+size_t elem_size(int e) { return e == E_I16 ? 2 : (e == E_I32 ? 4 : 8); }
+
+int global_layout(int elem) { return 6 + elem; }
+
+unsigned pad16(size_t b) { return (unsigned)((b + 15) / 16 * 16); }
+
+struct DeviceInfo {
+  int sm = 0, smem_optin = 0, l2 = 0;
+};
+
+int query_device(int dev, DeviceInfo* di) {
+  CK(cudaDeviceGetAttribute(&di->sm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&di->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  CK(cudaDeviceGetAttribute(&di->l2, cudaDevAttrL2CacheSize, dev));
+  return GO_OK;
+}
+
+unsigned team_bytes_for(int elem, int n) {
+  return elem == E_F64 ? go::PermSmem::team_bytes<double>(n) : go::PermSmem::team_bytes<long long>(n);
+}
+
+// smem bytes needed by one CTA with E teams for a given layout
+size_t cta_smem(int layout, int n, int E, size_t inst_img_bytes) {
+  const LayoutInfo& L = kLayouts[layout];
+  const unsigned inst = L.global ? 0u : pad16(inst_img_bytes);
+  return go::PermSmem::team_off(inst) + (size_t)E * team_bytes_for(L.elem, n);
+}
+
+}  // namespace
+
+// ---- handles -------------------------------------------------------------------
+struct go_problem {
+  int kind = 0, n = 0, d1 = 1, d2 = 0, device = 0;
+  int elem = E_F64;
+  bool integral = false;
+  void* d_full = nullptr;  // n*n in elem type (global reads, eval kernels)
+  void* d_tri = nullptr;   // packed strict upper triangle (smem image)
+  size_t full_bytes = 0, tri_bytes = 0;
+  DeviceInfo dev;
+  // user operators
+  std::vector<gohost::UserOpSrc> ops;  // registered (compiled and probed)
+  std::map<int, gohost::JitModule> jit;  // per layout
+};
+
+struct go_engine {
+  go_problem* prob = nullptr;
+  go_engine_config cfg{};
+  int P = 0, T = 0, TS = 0, E = 0, n = 0, W = 0, layout = 0;
+  unsigned inst_bytes = 0;
+  const void* inst = nullptr;
+  size_t smem = 0;
+  int grid = 0;
+  cudaStream_t stream = nullptr;
+  void* k_evolve = nullptr;
+  CUfunction k_evolve_jit = nullptr;
+  // device state
+  short *genes = nullptr, *best_genes = nullptr, *gbest_genes = nullptr, *scratch = nullptr;
+  double *scal = nullptr, *pen = nullptr, *best_scal = nullptr, *best_pen = nullptr;
+  long long* best_gen = nullptr;
+  int *usage = nullptr, *impr = nullptr, *k_usage = nullptr, *k_impr = nullptr;
+  long long* agg = nullptr;
+  double *rec_scal = nullptr, *rec_pen = nullptr;
+  double* temps = nullptr;  // ring [kDepth][MAX_CHUNK]
+  double* h_temps = nullptr;
+  go::RegistryDev* reg = nullptr;
+  go::GlobalState* gs = nullptr;
+  double* history = nullptr;
+  long long hist_cap = 0;
+  bool history_on = false;
+  int* h_stop = nullptr;
+  int* d_stop_map = nullptr;
+  long long gen_enqueued = 0;
+  double obj_sign_over_w = 1.0;
+  int nseq = 0;
+  int teams_per_sm = 0;
+  static const int kDepth = 8;
+  cudaEvent_t ring_ev[kDepth] = {};
+  cudaEvent_t t_start = nullptr, t_stop = nullptr;
+  long long launches = 0;
+};
+
+extern "C" {
+
+int go_abi_version(void) { return GO_ABI_VERSION; }
+
+const char* go_last_error(void) { return g_err.c_str(); }
+
+int go_device_count(int* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess || c == 0) {
+    *count = 0;
+    return fail(GO_E_NODEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  *count = c;
+  return GO_OK;
+}
+
+int go_device_query(int device, go_device_info* out) {
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, device));
+  DeviceInfo di;
+  int rc = query_device(device, &di);
+  if (rc) return rc;
+  memset(out, 0, sizeof(*out));
+  out->device = device;
+  out->sm_count = di.sm;
+  out->max_smem_optin = di.smem_optin;
+  out->l2_bytes = di.l2;
+  out->cc_major = p.major;
+  out->cc_minor = p.minor;
+  out->global_mem = (int64_t)p.totalGlobalMem;
+  snprintf(out->name, sizeof(out->name), "%s", p.name);
+  return GO_OK;
+}
+
+int go_problem_create(const go_problem_desc* d, int device, go_problem** out) {
+  if (!d || !out) return fail(GO_E_INVALID, "null argument");
+  if (d->kind != GO_TSP)
+    return fail(GO_E_UNSUPPORTED, "problem kind " + std::to_string(d->kind) +
+                                      " has no device path in this build");
+  const int n = d->n;
+  if (n < 1 || n > 32767) return fail(GO_E_INVALID, "TSP size must be in [1, 32767]");
+  if (!d->dist) return fail(GO_E_INVALID, "TSP needs a distance matrix");
+  // check_distance_matrix (problems.py:97-107): square, >= 0, zero diagonal, symmetric
+  bool integral = true;
+  double maxv = 0;
+  for (int i = 0; i < n; ++i) {
+    if (d->dist[(size_t)i * n + i] != 0.0)
+      return fail(GO_E_INVALID, "distance matrix must have a zero diagonal");
+    for (int j = 0; j < n; ++j) {
+      const double v = d->dist[(size_t)i * n + j];
+      if (!(v >= 0.0) || !std::isfinite(v))
+        return fail(GO_E_INVALID, "distance matrix must be nonnegative and finite");
+      if (v != d->dist[(size_t)j * n + i])
+        return fail(GO_E_INVALID, "distance matrix declared symmetric but is not");
+      if (v != std::floor(v)) integral = false;
+      maxv = std::max(maxv, v);
+    }
+  }
+  if (maxv > 2147483647.0) integral = false;
+  std::unique_ptr<go_problem> p(new go_problem());
+  p->kind = GO_TSP;
+  p->n = n;
+  p->d1 = 1;
+  p->d2 = n;
+  p->device = device;
+  p->integral = integral;
+  p->elem = integral ? (maxv <= 32767.0 ? E_I16 : E_I32) : E_F64;
+  CK(cudaSetDevice(device));
+  CK(cudaFree(0));
+  int rc = query_device(device, &p->dev);
+  if (rc) return rc;
+  const size_t es = elem_size(p->elem);
+  p->full_bytes = (size_t)n * n * es;
+  p->tri_bytes = (size_t)n * (n - 1) / 2 * es;
+  std::vector<unsigned char> full(pad16(p->full_bytes)), tri(pad16(std::max<size_t>(p->tri_bytes, 16)));
+  size_t t = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const double v = d->dist[(size_t)i * n + j];
+      const size_t at = (size_t)i * n + j;
+      if (p->elem == E_I16) ((short*)full.data())[at] = (short)v;
+      else if (p->elem == E_I32) ((int*)full.data())[at] = (int)v;
+      else ((double*)full.data())[at] = v;
+      if (j > i) {
+        if (p->elem == E_I16) ((short*)tri.data())[t] = (short)v;
+        else if (p->elem == E_I32) ((int*)tri.data())[t] = (int)v;
+        else ((double*)tri.data())[t] = v;
+        ++t;
+      }
+    }
+  CK(cudaMalloc(&p->d_full, full.size()));
+  CK(cudaMemcpy(p->d_full, full.data(), full.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&p->d_tri, tri.size()));
+  CK(cudaMemcpy(p->d_tri, tri.data(), tri.size(), cudaMemcpyHostToDevice));
+  *out = p.release();
+  return GO_OK;
+}
+
+int go_problem_destroy(go_problem* p) {
+  if (!p) return GO_OK;
+  cudaSetDevice(p->device);
+  for (auto& kv : p->jit)
+    if (kv.second.mod && gohost::drv()) gohost::drv()->ModuleUnload(kv.second.mod);
+  cudaFree(p->d_full);
+  cudaFree(p->d_tri);
+  delete p;
+  return GO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Layout + teams-per-CTA choice (paper §4.3 three-layer split: the problem
+// states its bytes, the solver asks CUDA for them, overflow -> global/L2).
+void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_out) {
+  const int n = p->n;
+  const size_t optin = (size_t)p->dev.smem_optin;
+  const int Emax = std::max(1, std::min(8, 512 / TS));
+  const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
+  const int full = p->elem * 2, tri = p->elem * 2 + 1;
+  for (int E = E0; E >= 1; E = E / 2) {
+    if (cta_smem(full, n, E, p->full_bytes) <= optin) { *layout = full; *E_out = E; return; }
+    if (n >= 2 && cta_smem(tri, n, E, p->tri_bytes) <= optin) { *layout = tri; *E_out = E; return; }
+    if (E == 1) break;
+  }
+  *layout = global_layout(p->elem);
+  *E_out = E0;
+}
+
+int launch_static_or_jit(void* fn, CUfunction jf, dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t st, void** args) {
+  if (jf) {
+    CU(gohost::drv()->LaunchKernel(jf, grid.x, grid.y, grid.z, block.x, block.y, block.z, (unsigned)smem,
+                      (CUstream)st, args, nullptr));
+  } else {
+    CK(cudaLaunchKernel(fn, grid, block, args, smem, st));
+  }
+  return GO_OK;
+}
+
+int set_smem_attr(void* fn, CUfunction jf, size_t smem) {
+  if (jf) {
+    CU(gohost::drv()->FuncSetAttribute(jf, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem));
+  } else {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  return GO_OK;
+}
+
+int ensure_jit(go_problem* p, int layout, gohost::JitModule** out) {
+  auto it = p->jit.find(layout);
+  if (it != p->jit.end()) {
+    *out = &it->second;
+    return GO_OK;
+  }
+  gohost::JitModule m;
+  std::string log;
+  const int rc = gohost::jit_build_tsp(kLayouts[layout].dist_type, p->ops, &m, &log);
+  if (rc) return fail(rc, "NVRTC build failed: " + log);
+  p->jit[layout] = m;
+  *out = &p->jit[layout];
+  return GO_OK;
+}
+
+const void* inst_ptr(const go_problem* p, int layout) {
+  return kLayouts[layout].tri ? p->d_tri : p->d_full;
+}
+
+size_t inst_img_bytes(const go_problem* p, int layout) {
+  return kLayouts[layout].tri ? p->tri_bytes : p->full_bytes;
+}
+
+}  // namespace
+
+extern "C" {
+
+int go_problem_layout(const go_problem* p, int64_t* smem_bytes, int32_t* layout) {
+  if (!p) return fail(GO_E_INVALID, "null problem");
+  int L = 0, E = 0;
+  choose_layout(p, 128, 0, &L, &E);
+  if (layout) *layout = L;
+  if (smem_bytes) *smem_bytes = kLayouts[L].global ? 0 : (int64_t)pad16(inst_img_bytes(p, L));
+  return GO_OK;
+}
+
+int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_t* layout,
+                         int32_t* teams_cta, int32_t* teams_per_sm, int64_t* smem_bytes) {
+  if (!p || team_size < 1 || team_size > 512) return fail(GO_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(p->device));
+  const int TS = (team_size + 31) / 32 * 32;
+  int L = 0, E = 0;
+  choose_layout(p, TS, teams_per_cta, &L, &E);
+  const size_t smem = cta_smem(L, p->n, E, inst_img_bytes(p, L));
+  CK(cudaFuncSetAttribute(kLayouts[L].evolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  int blocks = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kLayouts[L].evolve, E * TS, smem));
+  if (layout) *layout = L;
+  if (teams_cta) *teams_cta = E;
+  if (teams_per_sm) *teams_per_sm = blocks * E;
+  if (smem_bytes) *smem_bytes = (int64_t)smem;
+  return GO_OK;
+}
+
+int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int m,
+                  double* obj_out, double* pen_out) {
+  if (!p || !genes || !obj_out || m < 0) return fail(GO_E_INVALID, "bad arguments");
+  if (m == 0) return GO_OK;
+  CK(cudaSetDevice(p->device));
+  const int n = p->n;
+  std::vector<short> h((size_t)m * n);
+  for (size_t i = 0; i < h.size(); ++i) h[i] = (short)genes[i];
+  short* d_g = nullptr;
+  double* d_o = nullptr;
+  CK(cudaMalloc(&d_g, h.size() * 2));
+  CK(cudaMalloc(&d_o, (size_t)m * 8));
+  CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  void* fn = p->elem == E_I16 ? (void*)go_eval_tsp_i16
+                              : (p->elem == E_I32 ? (void*)go_eval_tsp_i32 : (void*)go_eval_tsp_f64);
+  const void* inst = p->d_full;
+  int nn = n;
+  void* args[] = {(void*)&inst, &nn, &d_g, &d_o};
+  CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
+  CK(cudaMemcpy(obj_out, d_o, (size_t)m * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d_g);
+  cudaFree(d_o);
+  if (pen_out)
+    for (int i = 0; i < m; ++i) pen_out[i] = 0.0;
+  (void)sizes;
+  return GO_OK;
+}
+
+int go_delta_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int m,
+                   const go_move* moves, double penalty_weight, double* delta_out,
+                   int32_t* cand_out) {
+  (void)sizes;
+  (void)penalty_weight;
+  if (!p || !genes || !moves || !delta_out || m < 0) return fail(GO_E_INVALID, "bad arguments");
+  if (m == 0) return GO_OK;
+  CK(cudaSetDevice(p->device));
+  const int n = p->n;
+  for (int i = 0; i < m * go::MAX_CHAIN; ++i) {
+    const go_move& mv = moves[i];
+    bool ok = true;
+    if (mv.kind == GO_MOVE_SWAP) ok = mv.a >= 0 && mv.b >= 0 && mv.a < n && mv.b < n && mv.a != mv.b;
+    else if (mv.kind == GO_MOVE_REVERSE) ok = mv.a >= 0 && mv.a < mv.b && mv.b < n;
+    else if (mv.kind == GO_MOVE_SEGMENT)
+      ok = mv.b >= 1 && mv.a >= 0 && mv.a + mv.b <= n && mv.c >= 0 && mv.c <= n - mv.b;
+    else ok = mv.kind == GO_MOVE_NONE;
+    if (!ok) return fail(GO_E_INVALID, "malformed move at index " + std::to_string(i));
+  }
+  std::vector<short> h((size_t)m * n);
+  for (size_t i = 0; i < h.size(); ++i) h[i] = (short)genes[i];
+  short *d_g = nullptr, *d_c = nullptr;
+  int* d_m = nullptr;
+  double* d_d = nullptr;
+  CK(cudaMalloc(&d_g, h.size() * 2));
+  CK(cudaMalloc(&d_c, h.size() * 2));
+  CK(cudaMalloc(&d_m, (size_t)m * go::MAX_CHAIN * sizeof(go_move)));
+  CK(cudaMalloc(&d_d, (size_t)m * 8));
+  CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_m, moves, (size_t)m * go::MAX_CHAIN * sizeof(go_move), cudaMemcpyHostToDevice));
+  void* fn = p->elem == E_I16 ? (void*)go_delta_tsp_i16
+                              : (p->elem == E_I32 ? (void*)go_delta_tsp_i32 : (void*)go_delta_tsp_f64);
+  const void* inst = p->d_full;
+  int nn = n;
+  void* args[] = {(void*)&inst, &nn, &d_g, &d_m, &d_d, &d_c};
+  CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, pad16((size_t)n * 2), 0));
+  CK(cudaMemcpy(delta_out, d_d, (size_t)m * 8, cudaMemcpyDeviceToHost));
+  if (cand_out) {
+    CK(cudaMemcpy(h.data(), d_c, h.size() * 2, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h.size(); ++i) cand_out[i] = h[i];
+  }
+  cudaFree(d_g);
+  cudaFree(d_c);
+  cudaFree(d_m);
+  cudaFree(d_d);
+  return GO_OK;
+}
+
+int go_jit_compile(int layout, const go_custom_op* ops, int n_ops, char* log, int log_len,
+                   char* key_hex65) {
+  if (layout < 0 || layout > 8 || n_ops < 0 || (n_ops && !ops)) return fail(GO_E_INVALID, "bad arguments");
+  std::vector<gohost::UserOpSrc> v;
+  for (int i = 0; i < n_ops; ++i)
+    v.push_back({ops[i].id, ops[i].name ? ops[i].name : "op", ops[i].cuda_body ? ops[i].cuda_body : ""});
+  std::string cubin, key, lg;
+  bool hit = false;
+  const int rc = gohost::jit_compile_tsp(kLayouts[layout].dist_type, v, &cubin, &key, &hit, &lg);
+  if (log && log_len > 0) snprintf(log, log_len, "%s", lg.c_str());
+  if (key_hex65) snprintf(key_hex65, 65, "%s", key.c_str());
+  if (rc) return fail(rc, "NVRTC: " + lg.substr(0, 2000));
+  return GO_OK;
+}
+
+int go_problem_set_custom_ops(go_problem* p, const go_custom_op* ops, int n_ops,
+                              const int32_t* probe_genes, const int32_t* probe_sizes,
+                              uint64_t probe_seed, int32_t* status_out, char* msg_out,
+                              int msg_len) {
+  (void)probe_sizes;
+  if (!p || (n_ops > 0 && !ops) || !status_out) return fail(GO_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(p->device));
+  for (auto& kv : p->jit)
+    if (kv.second.mod && gohost::drv()) gohost::drv()->ModuleUnload(kv.second.mod);
+  p->jit.clear();
+  p->ops.clear();
+  auto note = [&](int i, const std::string& m) {
+    if (msg_out && msg_len > 0) snprintf(msg_out + (size_t)i * msg_len, msg_len, "%s", m.c_str());
+  };
+  int layout = 0, E = 0;
+  choose_layout(p, 128, 0, &layout, &E);
+  // compile each operator on its own first so a broken snippet only excludes
+  // itself (operators.py:649-657); then probe it on the device (:658-665)
+  std::vector<gohost::UserOpSrc> keep;
+  for (int i = 0; i < n_ops; ++i) {
+    status_out[i] = 0;
+    if (ops[i].id < 100) return fail(GO_E_INVALID, "custom operator id must be >= 100");
+    if (!ops[i].cuda_body) {
+      note(i, "no CUDA snippet");
+      continue;
+    }
+    gohost::UserOpSrc s{ops[i].id, ops[i].name ? ops[i].name : "op", ops[i].cuda_body};
+    gohost::JitModule m;
+    std::string log;
+    const int rc = gohost::jit_build_tsp(kLayouts[layout].dist_type, {s}, &m, &log);
+    if (rc) {
+      note(i, "compile failed: " + log.substr(0, 400));
+      continue;
+    }
+    // probe: one application on the probe tour with stream mix64(seed, 4, id)
+    const int n = p->n;
+    short* d_g = nullptr;
+    int* d_e = nullptr;
+    std::vector<short> h(n);
+    for (int j = 0; j < n; ++j) h[j] = (short)probe_genes[j];
+    CK(cudaMalloc(&d_g, (size_t)n * 2));
+    CK(cudaMalloc(&d_e, sizeof(int)));
+    CK(cudaMemcpy(d_g, h.data(), (size_t)n * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d_e, 0, sizeof(int)));
+    auto mix = [](uint64_t hh, uint64_t part) {
+      hh ^= part;
+      hh *= 0xBF58476D1CE4E5B9ull;
+      hh ^= hh >> 27;
+      hh *= 0x94D049BB133111EBull;
+      hh ^= hh >> 31;
+      return hh;
+    };
+    unsigned long long key = mix(mix(mix(0x9E3779B97F4A7C15ull, probe_seed), 4), (uint64_t)ops[i].id);
+    const void* inst = inst_ptr(p, layout);
+    int nn = n, kind = go::SEQ_CUSTOM_BASE + 0;
+    void* args[] = {(void*)&inst, &nn, &kind, &key, &d_g, &d_e};
+    CU(gohost::drv()->LaunchKernel(m.probe, 1, 1, 1, 128, 1, 1, pad16((size_t)n * 2), 0, args, nullptr));
+    cudaError_t ce = cudaDeviceSynchronize();
+    int err = 0;
+    if (ce == cudaSuccess) {
+      cudaMemcpy(&err, d_e, sizeof(int), cudaMemcpyDeviceToHost);
+      cudaMemcpy(h.data(), d_g, (size_t)n * 2, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d_g);
+    cudaFree(d_e);
+    gohost::drv()->ModuleUnload(m.mod);
+    if (ce != cudaSuccess) return fail(GO_E_CUDA, std::string("probe kernel: ") + cudaGetErrorString(ce));
+    std::vector<char> seen(n, 0);
+    bool valid = err == 0;
+    for (int j = 0; j < n && valid; ++j) {
+      if (h[j] < 0 || h[j] >= n || seen[h[j]]) valid = false;
+      else seen[h[j]] = 1;
+    }
+    if (!valid) {
+      note(i, err ? "probe raised a device error (out-of-range access or malformed move)"
+                  : "probe output invalid");
+      continue;
+    }
+    keep.push_back(s);
+    status_out[i] = 1;
+    note(i, "registered");
+  }
+  p->ops = keep;
+  return GO_OK;
+}
+
+// ---- engine ---------------------------------------------------------------------
+int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) {
+  if (!p || !c || !out) return fail(GO_E_INVALID, "null argument");
+  if (c->population < 1) return fail(GO_E_INVALID, "population must be >= 1");
+  if (c->team_size < 1 || c->team_size > 512)
+    return fail(GO_E_UNSUPPORTED, "team_size must be in [1, 512] on the device path");
+  if (c->aos_interval < 1 || c->elite_interval < 1 || c->migration_interval < 1)
+    return fail(GO_E_INVALID, "intervals must be >= 1");
+  if (c->islands < 1 || c->islands > 64 || c->islands > c->population)
+    return fail(GO_E_INVALID, "islands must be in [1, min(64, population)]");
+  if (c->top_n < 1) return fail(GO_E_INVALID, "top_n must be >= 1");
+  CK(cudaSetDevice(p->device));
+  std::unique_ptr<go_engine> e(new go_engine());
+  e->prob = p;
+  e->cfg = *c;
+  e->obj_sign_over_w = (c->maximize ? -1.0 : 1.0) / (c->obj_weight > 0 ? c->obj_weight : 1.0);
+  e->P = c->population;
+  e->T = c->team_size;
+  e->TS = (c->team_size + 31) / 32 * 32;
+  e->n = p->n;
+  e->W = p->n;
+  choose_layout(p, e->TS, c->teams_per_cta, &e->layout, &e->E);
+  const LayoutInfo& L = kLayouts[e->layout];
+  e->inst = inst_ptr(p, e->layout);
+  e->inst_bytes = L.global ? 0u : pad16(inst_img_bytes(p, e->layout));
+  e->smem = cta_smem(e->layout, e->n, e->E, inst_img_bytes(p, e->layout));
+  e->grid = (e->P + e->E - 1) / e->E;
+  if (!p->ops.empty()) {
+    gohost::JitModule* m = nullptr;
+    int rc = ensure_jit(p, e->layout, &m);
+    if (rc) return rc;
+    e->k_evolve_jit = m->evolve;
+  } else {
+    e->k_evolve = L.evolve;
+  }
+  int rc = set_smem_attr(e->k_evolve, e->k_evolve_jit, e->smem);
+  if (rc) return rc;
+  // resident teams per SM for the population sizing rule (paper §4.4)
+  int blocks = 0;
+  if (e->k_evolve_jit) {
+    CU(gohost::drv()->OccupancyMaxActiveBlocksPerMultiprocessor(&blocks, e->k_evolve_jit, e->E * e->TS, e->smem));
+  } else {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, e->k_evolve, e->E * e->TS, e->smem));
+  }
+  e->teams_per_sm = blocks * e->E;
+  if (blocks < 1) return fail(GO_E_UNSUPPORTED, "evolve kernel does not fit on an SM");
+
+  CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  const size_t P = e->P, W = e->W;
+  CK(cudaMalloc(&e->genes, P * W * 2));
+  CK(cudaMalloc(&e->best_genes, P * W * 2));
+  CK(cudaMalloc(&e->gbest_genes, W * 2));
+  CK(cudaMalloc(&e->scratch, (size_t)std::max(c->islands, std::min(c->top_n, 64)) * W * 2));
+  CK(cudaMalloc(&e->scal, P * 8));
+  CK(cudaMalloc(&e->pen, P * 8));
+  CK(cudaMalloc(&e->best_scal, P * 8));
+  CK(cudaMalloc(&e->best_pen, P * 8));
+  CK(cudaMalloc(&e->best_gen, P * 8));
+  CK(cudaMalloc(&e->usage, P * go::MAX_SEQ * 4));
+  CK(cudaMalloc(&e->impr, P * go::MAX_SEQ * 4));
+  CK(cudaMalloc(&e->k_usage, P * 3 * 4));
+  CK(cudaMalloc(&e->k_impr, P * 3 * 4));
+  CK(cudaMalloc(&e->agg, 70 * 8));
+  CK(cudaMemset(e->agg, 0, 70 * 8));
+  CK(cudaMalloc(&e->rec_scal, (size_t)go::MAX_CHUNK * P * 8));
+  CK(cudaMalloc(&e->rec_pen, (size_t)go::MAX_CHUNK * P * 8));
+  CK(cudaMalloc(&e->temps, (size_t)go_engine::kDepth * go::MAX_CHUNK * 8));
+  CK(cudaMallocHost(&e->h_temps, (size_t)go_engine::kDepth * go::MAX_CHUNK * 8));
+  CK(cudaMalloc(&e->reg, sizeof(go::RegistryDev)));
+  CK(cudaMalloc(&e->gs, sizeof(go::GlobalState)));
+  CK(cudaHostAlloc(&e->h_stop, sizeof(int), cudaHostAllocMapped));
+  *e->h_stop = 0;
+  CK(cudaHostGetDevicePointer((void**)&e->d_stop_map, e->h_stop, 0));
+  for (auto& ev : e->ring_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventCreate(&e->t_start));
+  CK(cudaEventCreate(&e->t_stop));
+  go::GlobalState gs{};
+  gs.gev = -1;
+  CK(cudaMemcpy(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice));
+  *out = e.release();
+  return GO_OK;
+}
+
+int go_engine_destroy(go_engine* e) {
+  if (!e) return GO_OK;
+  cudaSetDevice(e->prob->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  void* bufs[] = {e->genes, e->best_genes, e->gbest_genes, e->scratch, e->scal, e->pen,
+                  e->best_scal, e->best_pen, e->best_gen, e->usage, e->impr, e->k_usage,
+                  e->k_impr, e->agg, e->rec_scal, e->rec_pen, e->temps, e->reg, e->gs,
+                  e->history};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (e->h_temps) cudaFreeHost(e->h_temps);
+  if (e->h_stop) cudaFreeHost(e->h_stop);
+  for (auto& ev : e->ring_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->t_start) cudaEventDestroy(e->t_start);
+  if (e->t_stop) cudaEventDestroy(e->t_stop);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+  return GO_OK;
+}
+
+int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const double* weights,
+                           const double* floors, const double* caps, double total,
+                           const double* k_weights) {
+  if (!e || nseq < 1 || nseq > 32 || !ids || !weights || !k_weights)
+    return fail(GO_E_INVALID, "registry needs 1..32 sequences");
+  go::RegistryDev r{};
+  r.nseq = nseq;
+  double acc = 0.0;
+  for (int i = 0; i < nseq; ++i) {
+    const int id = ids[i];
+    int kind = -1;
+    if (id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE || id == go::SEQ_OR_OPT) {
+      kind = id;
+    } else if (id >= 100) {
+      for (size_t s = 0; s < e->prob->ops.size(); ++s)
+        if (e->prob->ops[s].id == id) kind = go::SEQ_CUSTOM_BASE + (int)s;
+    }
+    if (kind < 0)
+      return fail(GO_E_UNSUPPORTED, "sequence id " + std::to_string(id) +
+                                        " has no device implementation for this problem");
+    if (id >= 100 && !e->k_evolve_jit)
+      return fail(GO_E_INVALID, "custom sequence registered after engine creation");
+    r.kind[i] = kind;
+    r.ids[i] = id;
+    r.w[i] = weights[i];
+    r.floor_[i] = floors ? floors[i] : 0.0;
+    r.cap[i] = caps ? caps[i] : INFINITY;
+    acc += weights[i];  // sample_sequence's running sum (aos.py:169-175)
+    r.cum[i] = acc;
+  }
+  r.total = total;
+  for (int j = 0; j < 3; ++j) r.kw[j] = k_weights[j];
+  e->nseq = nseq;
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaMemcpyAsync(e->reg, &r, sizeof(r), cudaMemcpyHostToDevice, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  return GO_OK;
+}
+
+int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* sizes,
+                             const double* obj, const double* pen) {
+  (void)sizes;
+  if (!e || !genes || !obj) return fail(GO_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(e->prob->device));
+  const size_t P = e->P, W = e->W;
+  std::vector<short> g(P * W);
+  for (size_t i = 0; i < g.size(); ++i) g[i] = (short)genes[i];
+  std::vector<double> sc(P), pe(P);
+  const double w = e->cfg.obj_weight > 0 ? e->cfg.obj_weight : 1.0;
+  int best = 0;
+  for (size_t i = 0; i < P; ++i) {
+    sc[i] = 0.0 + w * (e->cfg.maximize ? -obj[i] : obj[i]);  // scalarize (core.py:303-307)
+    pe[i] = pen ? pen[i] : 0.0;
+  }
+  for (size_t i = 1; i < P; ++i) {  // _best_index (engine.py:467-472)
+    const bool fa = pe[i] == 0.0, fb = pe[best] == 0.0;
+    bool better;
+    if (fa != fb) better = fa;
+    else if (!fa && pe[i] != pe[best]) better = pe[i] < pe[best];
+    else better = sc[i] < sc[best];
+    if (better) best = (int)i;
+  }
+  std::vector<long long> zeros(P, 0);
+  CK(cudaMemcpy(e->genes, g.data(), P * W * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->best_genes, g.data(), P * W * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->gbest_genes, g.data() + (size_t)best * W, W * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->scal, sc.data(), P * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->best_scal, sc.data(), P * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->pen, pe.data(), P * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->best_pen, pe.data(), P * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(e->best_gen, zeros.data(), P * 8, cudaMemcpyHostToDevice));
+  go::GlobalState gs{};
+  gs.gscal = sc[best];
+  gs.gpen = pe[best];
+  gs.gev = -1;
+  gs.ggen = 0;
+  CK(cudaMemcpy(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice));
+  CK(cudaMemset(e->agg, 0, 70 * 8));
+  *e->h_stop = 0;
+  e->gen_enqueued = 0;
+  return GO_OK;
+}
+
+int go_engine_set_history(go_engine* e, int enabled) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  e->history_on = enabled != 0;
+  return GO_OK;
+}
+
+int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
+                  go_run_stats* stats) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  if (e->nseq == 0) return fail(GO_E_INVALID, "registry not set");
+  CK(cudaSetDevice(e->prob->device));
+  const go_engine_config& c = e->cfg;
+  go::GlobalState gs{};
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  long long done = gs.gens_done;
+  if (gs.stop) {  // a previous run stopped; resume from the same state
+    gs.stop = 0;
+    *e->h_stop = 0;
+  }
+  // history buffer sized for the generations this call may run
+  if (e->history_on && max_generations > e->hist_cap) {
+    if (e->history) cudaFree(e->history);
+    e->hist_cap = std::max<long long>(max_generations, 1);
+    CK(cudaMalloc(&e->history, (size_t)e->hist_cap * 8));
+  }
+  gs.deadline_ns = 0;
+  CK(cudaMemcpyAsync(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice, e->stream));
+  if (time_limit_s > 0) {
+    const long long budget = (long long)(time_limit_s * 1e9);
+    go::go_arm_deadline_kernel<<<1, 1, 0, e->stream>>>(e->gs, budget);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(e->t_start, e->stream));
+  long long launches = 0;
+  long long chunk = 0;
+  const int I = c.aos_interval, EI = c.elite_interval, MI = c.migration_interval;
+  auto next_mult = [](long long g, long long m) { return (g / m + 1) * m; };
+  go::EvolveArgs a{};
+  a.inst = e->inst;
+  a.inst_bytes = e->inst_bytes;
+  a.n = e->n;
+  a.genes = e->genes;
+  a.scal = e->scal;
+  a.pen = e->pen;
+  a.best_genes = e->best_genes;
+  a.best_scal = e->best_scal;
+  a.best_pen = e->best_pen;
+  a.best_gen = e->best_gen;
+  a.usage = e->usage;
+  a.impr = e->impr;
+  a.k_usage = e->k_usage;
+  a.k_impr = e->k_impr;
+  a.rec_scal = e->rec_scal;
+  a.rec_pen = e->rec_pen;
+  a.reg = e->reg;
+  a.gs = e->gs;
+  a.seed = c.seed;
+  a.P = e->P;
+  a.T = e->T;
+  a.E = e->E;
+  a.ev_offset = c.evolver_offset;
+  a.team_stride = e->TS;
+  a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n);
+  a.resync = kLayouts[e->layout].elem == E_F64;
+  go::EpilogueArgs q{};
+  q.P = e->P;
+  q.W = e->W;
+  q.genes = e->genes;
+  q.scal = e->scal;
+  q.pen = e->pen;
+  q.best_genes = e->best_genes;
+  q.best_scal = e->best_scal;
+  q.best_pen = e->best_pen;
+  q.best_gen = e->best_gen;
+  q.gbest_genes = e->gbest_genes;
+  q.scratch = e->scratch;
+  q.usage = e->usage;
+  q.impr = e->impr;
+  q.k_usage = e->k_usage;
+  q.k_impr = e->k_impr;
+  q.agg = e->agg;
+  q.rec_scal = e->rec_scal;
+  q.rec_pen = e->rec_pen;
+  q.reg = e->reg;
+  q.gs = e->gs;
+  q.history = e->history_on ? e->history : nullptr;
+  q.hist_cap = e->history_on ? e->hist_cap : 0;
+  q.host_stop = e->d_stop_map;
+  q.pw = c.penalty_weight;
+  q.aos_interval = c.aos_interval;
+  q.stagnation = c.stagnation_threshold;
+  q.alpha = c.aos_alpha;
+  q.floor_ = c.aos_floor;
+  q.cap = c.aos_cap;
+  q.eps = c.aos_eps;
+  q.islands = c.islands;
+  q.migration = c.migration;
+  q.mig_interval = c.migration_interval;
+  q.top_n = c.top_n;
+  q.elite_interval = c.elite_interval;
+  q.has_target = c.has_target;
+  q.target = c.target_objective;
+  q.obj_sign_over_w = e->obj_sign_over_w;
+  q.seed = c.seed;
+  q.max_gens = max_generations;
+
+  while (done < max_generations) {
+    if (*(volatile int*)e->h_stop) break;
+    long long end = std::min<long long>(max_generations, done + go::MAX_CHUNK);
+    end = std::min(end, next_mult(done, I));
+    end = std::min(end, next_mult(done, EI));
+    if (c.islands >= 2) end = std::min(end, next_mult(done, MI));
+    const int slot = (int)(chunk % go_engine::kDepth);
+    if (chunk >= go_engine::kDepth) {
+      CK(cudaEventSynchronize(e->ring_ev[slot]));
+      if (*(volatile int*)e->h_stop) break;
+    }
+    double* ht = e->h_temps + (size_t)slot * go::MAX_CHUNK;
+    for (long long g = done + 1; g <= end; ++g)
+      ht[g - done - 1] = c.t0 * std::pow(c.cooling_alpha, (double)(g - 1));  // engine.py:685
+    double* dt = e->temps + (size_t)slot * go::MAX_CHUNK;
+    CK(cudaMemcpyAsync(dt, ht, (size_t)(end - done) * 8, cudaMemcpyHostToDevice, e->stream));
+    a.temps = dt;
+    a.gen0 = done + 1;
+    a.ngen = (int)(end - done);
+    void* args[] = {&a};
+    int rc = launch_static_or_jit(e->k_evolve, e->k_evolve_jit, dim3(e->grid), dim3(e->E * e->TS),
+                                  e->smem, e->stream, args);
+    if (rc) return rc;
+    q.gen0 = a.gen0;
+    q.ngen = a.ngen;
+    go::go_epilogue_kernel<<<1, go::EPI_THREADS, 0, e->stream>>>(q);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e->ring_ev[slot], e->stream));
+    launches += 2;
+    done = end;
+    ++chunk;
+  }
+  CK(cudaEventRecord(e->t_stop, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e->t_start, e->t_stop));
+  e->launches += launches;
+  if (stats) {
+    stats->generations = gs.gens_done;
+    stats->lane_evals = gs.gens_done * (long long)e->P * e->T;
+    stats->kernel_launches = launches;
+    stats->device_ms = ms;
+    stats->stopped_by = gs.stop == 1 ? 1 : (gs.stop == 2 ? 2 : 0);
+    stats->error_flags = gs.err;
+  }
+  return GO_OK;
+}
+
+int go_engine_get_population(go_engine* e, int32_t* genes, int32_t* sizes, double* obj,
+                             double* pen) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaStreamSynchronize(e->stream));
+  const size_t P = e->P, W = e->W;
+  if (genes) {
+    std::vector<short> g(P * W);
+    CK(cudaMemcpy(g.data(), e->genes, P * W * 2, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < g.size(); ++i) genes[i] = g[i];
+  }
+  if (sizes)
+    for (size_t i = 0; i < P; ++i) sizes[i] = e->n;
+  std::vector<double> sc(P);
+  CK(cudaMemcpy(sc.data(), e->scal, P * 8, cudaMemcpyDeviceToHost));
+  if (obj)
+    for (size_t i = 0; i < P; ++i) obj[i] = sc[i] * e->obj_sign_over_w;
+  if (pen) CK(cudaMemcpy(pen, e->pen, P * 8, cudaMemcpyDeviceToHost));
+  return GO_OK;
+}
+
+int go_engine_get_best(go_engine* e, int32_t* genes, int32_t* sizes, double* obj, double* pen,
+                       int64_t* found_gen) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaStreamSynchronize(e->stream));
+  go::GlobalState gs{};
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  std::vector<short> g(e->W);
+  const short* src = gs.gev >= 0 ? e->best_genes + (size_t)gs.gev * e->W : e->gbest_genes;
+  CK(cudaMemcpy(g.data(), src, (size_t)e->W * 2, cudaMemcpyDeviceToHost));
+  if (genes)
+    for (int i = 0; i < e->W; ++i) genes[i] = g[i];
+  if (sizes) sizes[0] = e->n;
+  if (obj) *obj = gs.gscal * e->obj_sign_over_w;
+  if (pen) *pen = gs.gpen;
+  if (found_gen) *found_gen = gs.ggen;
+  return GO_OK;
+}
+
+int go_engine_get_registry(go_engine* e, double* weights, double* k_weights, int32_t* stall) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaStreamSynchronize(e->stream));
+  go::RegistryDev r;
+  CK(cudaMemcpy(&r, e->reg, sizeof(r), cudaMemcpyDeviceToHost));
+  if (weights)
+    for (int i = 0; i < r.nseq; ++i) weights[i] = r.w[i];
+  if (k_weights)
+    for (int j = 0; j < 3; ++j) k_weights[j] = r.kw[j];
+  if (stall) {
+    go::GlobalState gs{};
+    CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+    *stall = (int32_t)gs.stall;
+  }
+  return GO_OK;
+}
+
+int go_engine_get_history(go_engine* e, double* best_phi, int64_t cap, int64_t* count) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaStreamSynchronize(e->stream));
+  go::GlobalState gs{};
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  const long long nh = e->history ? std::min<long long>(gs.hist_count, cap) : 0;
+  if (nh > 0) CK(cudaMemcpy(best_phi, e->history, (size_t)nh * 8, cudaMemcpyDeviceToHost));
+  if (count) *count = nh;
+  return GO_OK;
+}
+
+int go_elite_record_bytes(go_engine* e, int64_t* bytes) {
+  if (!e || !bytes) return fail(GO_E_INVALID, "bad arguments");
+  *bytes = ((int64_t)e->W * 2 + 15) / 16 * 16 + 16;
+  return GO_OK;
+}
+
+int go_engine_export_elites(go_engine* e, void* device_buf, int top_n) {
+  (void)e;
+  (void)device_buf;
+  (void)top_n;
+  return fail(GO_E_UNSUPPORTED, "cross-GPU island exchange not built yet");
+}
+
+int go_engine_import_elites(go_engine* e, const void* device_buf, int n_ranks, int rank,
+                            int top_n, int strategy, int64_t event_index) {
+  (void)e;
+  (void)device_buf;
+  (void)n_ranks;
+  (void)rank;
+  (void)top_n;
+  (void)strategy;
+  (void)event_index;
+  return fail(GO_E_UNSUPPORTED, "cross-GPU island exchange not built yet");
+}
+
+int go_engine_stream(go_engine* e, void** stream) {
+  if (!e || !stream) return fail(GO_E_INVALID, "bad arguments");
+  *stream = (void*)e->stream;
+  return GO_OK;
+}
+
+int go_engine_sync(go_engine* e) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  CK(cudaStreamSynchronize(e->stream));
+  return GO_OK;
+}
+
+}  // extern "C"

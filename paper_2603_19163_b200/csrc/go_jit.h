@@ -1,0 +1,38 @@
+// go_jit.h — NVRTC compile pipeline for user operators (paper §5.1).
+#pragma once
+#include <cuda.h>
+
+#include <string>
+#include <vector>
+
+namespace gohost {
+
+struct UserOpSrc {
+  int id;
+  std::string name;
+  std::string body;
+};
+
+struct JitModule {
+  CUmodule mod = nullptr;
+  CUfunction evolve = nullptr;
+  CUfunction probe = nullptr;
+  std::string key;
+  double compile_seconds = 0.0;
+  bool cache_hit = false;
+};
+
+std::string sha256_hex(const std::string& data);
+std::string kernel_dir();
+
+// Builds (or loads from the cubin cache) the evolve + probe kernels of the
+// TSP path specialised for distance type `dist_type` with the given user
+// operators compiled in as slots 0..n-1.  Returns 0 or a GO_E_* status and a
+// compiler log.
+int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
+                    std::string* cubin_out, std::string* key_out, bool* hit_out,
+                    std::string* log);
+int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
+                  JitModule* out, std::string* log);
+
+}  // namespace gohost

@@ -1,0 +1,104 @@
+// go_args.cuh — POD kernel argument blocks shared by host and device code.
+#pragma once
+
+namespace go {
+
+// Registry image in device memory, rewritten by the epilogue at every AOS
+// barrier (aos.py:116-144) and by the host at set-up.
+struct RegistryDev {
+  int nseq;
+  int kind[32];       // implementation code: 0..16 built-in seq id, 100+slot custom
+  int ids[32];        // sequence id as the reference names it
+  double w[32];       // normalised weights
+  double floor_[32];  // per-sequence floor / cap (SequenceEntry, operators.py:70-76)
+  double cap[32];
+  double cum[32];     // sequential prefix sums used by sample_sequence (aos.py:169-175)
+  double total;       // sum(e.weight ...) as the reference computes it
+  double kw[3];       // K-level weights (aos.py:19, :137-144)
+};
+
+// Run-global state owned by the device (engine.py:668-750 locals).
+struct GlobalState {
+  double gscal, gpen;     // global best (engine.py:668, :703-708)
+  int gev;                // evolver holding the global best in best_genes (-1: gbest buffer)
+  int pad0;
+  long long ggen;         // generation the global best was found (0 = initial population)
+  long long gens_done;
+  long long stall;        // no_improve_batches (engine.py:708)
+  long long mig_events;   // engine.py:675, :743
+  long long deadline_ns;  // %globaltimer deadline, 0 = none
+  int stop;               // 0 run, 1 time, 2 target, 3 max generations
+  int err;                // sticky device error bits
+  long long hist_count;
+};
+
+struct EvolveArgs {
+  const void* inst;      // instance image (layout specific)
+  unsigned inst_bytes;   // bytes staged into shared memory (0 = read from global)
+  int n;                 // row length (single-row permutation)
+  short* genes;          // [P][n]
+  double* scal;          // [P] scalarised objective (lower is better)
+  double* pen;           // [P]
+  short* best_genes;     // [P][n] each team's best-ever current (first occurrence)
+  double* best_scal;     // [P]
+  double* best_pen;      // [P]
+  long long* best_gen;   // [P]
+  int* usage;            // [P][32] per-chunk AOS counters (aos.py:51-77)
+  int* impr;             // [P][32]
+  int* k_usage;          // [P][3]
+  int* k_impr;           // [P][3]
+  double* rec_scal;      // [ngen][P] current after each generation
+  double* rec_pen;       // [ngen][P]
+  const RegistryDev* reg;
+  GlobalState* gs;
+  const double* temps;   // [ngen] T0 * alpha^(g-1) (engine.py:685), host pow()
+  unsigned long long seed;
+  long long gen0;        // first generation of this chunk (1-based)
+  int ngen;
+  int P, T, E;           // evolvers, lanes per evolver, evolver teams per CTA
+  int ev_offset;         // global evolver index of local evolver 0
+  int team_stride;       // threads per team (T rounded up to 32)
+  int team_smem;         // bytes of shared memory per team
+  int resync;            // recompute Φ at chunk start (float matrices)
+};
+
+struct EpilogueArgs {
+  int P, W;              // evolvers, genes per solution
+  short* genes;
+  double* scal;
+  double* pen;
+  short* best_genes;
+  double* best_scal;
+  double* best_pen;
+  long long* best_gen;
+  short* gbest_genes;    // [W]
+  short* scratch;        // [max(islands, top_n)][W] donor copies
+  const int* usage;
+  const int* impr;
+  const int* k_usage;
+  const int* k_impr;
+  long long* agg;        // [32 + 32 + 3 + 3] aggregated AOS counters
+  const double* rec_scal;
+  const double* rec_pen;
+  RegistryDev* reg;
+  GlobalState* gs;
+  double* history;       // [hist_cap] best Φ per generation or null
+  long long hist_cap;
+  int* host_stop;        // mapped host flag mirroring gs->stop (may be null)
+  long long gen0;
+  int ngen;
+  double pw;             // penalty weight
+  // AosConfig (aos.py:22-38)
+  int aos_interval, stagnation;
+  double alpha, floor_, cap, eps;
+  // islands (engine.py:90-106)
+  int islands, migration, mig_interval, top_n;
+  int elite_interval;
+  int has_target;
+  double target;
+  double obj_sign_over_w; // objective = scal * this (single objective)
+  unsigned long long seed;
+  long long max_gens;
+};
+
+}  // namespace go

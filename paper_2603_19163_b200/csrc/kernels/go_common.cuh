@@ -1,0 +1,197 @@
+// go_common.cuh — device primitives shared by every cuGenOpt kernel.
+//
+// No standard headers: this file is also compiled at run time by NVRTC when
+// user operators are registered (paper §5.1 JIT pipeline).
+//
+//  * mix64          engine.py:74-83 (stream identity = the reference's hash)
+//  * Philox4x32-10  counter-based words replacing MT19937
+//  * Stream         CPython random.Random draw algorithms over those words:
+//                   random() (two words, 53-bit), _randbelow (k = bit_length,
+//                   rejection), so the draw ORDER is the reference's
+//                   (oracle/rng.py WordRandom is the CPU twin)
+//  * team barriers  one named barrier per evolver team (T lanes)
+//  * bulk staging   cp.async.bulk (TMA 1-D) global -> shared with an mbarrier
+#pragma once
+
+namespace go {
+
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef long long i64;
+typedef short i16;
+
+enum { MAX_SEQ = 32, MAX_CHUNK = 64, MAX_CHAIN = 3 };
+
+// sequence ids (operators.py:29-51)
+enum SeqId {
+  SEQ_SWAP = 0, SEQ_INSERT = 1, SEQ_REVERSE = 2, SEQ_OR_OPT = 3, SEQ_THREE_OPT = 4,
+  SEQ_FLIP = 5, SEQ_SEG_FLIP = 6, SEQ_RANDOM_RESET = 7, SEQ_SEG_RESET = 8,
+  SEQ_ROW_SWAP = 9, SEQ_ROW_SPLIT = 10, SEQ_ROW_MERGE = 11, SEQ_OX = 12,
+  SEQ_UNIFORM_X = 13, SEQ_SEG_SHUFFLE = 14, SEQ_SCATTER_SHUFFLE = 15,
+  SEQ_GUIDED_REBUILD = 16, SEQ_CUSTOM_BASE = 100
+};
+
+// sticky device error bits
+enum ErrBits { ERR_OP_RANGE = 1, ERR_OP_MOVE = 2, ERR_UNKNOWN_SEQ = 4 };
+
+__device__ __forceinline__ u64 mix64_fold(u64 h, u64 part) {
+  h ^= part;
+  h *= 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 27;
+  h *= 0x94D049BB133111EBull;
+  h ^= h >> 31;
+  return h;
+}
+
+__device__ __forceinline__ u64 mix64_5(u64 a, u64 b, u64 c, u64 d, u64 e) {
+  u64 h = 0x9E3779B97F4A7C15ull;
+  h = mix64_fold(h, a);
+  h = mix64_fold(h, b);
+  h = mix64_fold(h, c);
+  h = mix64_fold(h, d);
+  return mix64_fold(h, e);
+}
+
+__device__ __forceinline__ u64 mix64_3(u64 a, u64 b, u64 c) {
+  u64 h = 0x9E3779B97F4A7C15ull;
+  h = mix64_fold(h, a);
+  h = mix64_fold(h, b);
+  return mix64_fold(h, c);
+}
+
+// Philox4x32-10 block (Random123 constants); counter (c0,0,0,0), key (k0,k1)
+__device__ __forceinline__ void philox_block(u32 c0, u32 k0, u32 k1, u32& o0, u32& o1, u32& o2,
+                                             u32& o3) {
+  u32 x0 = c0, x1 = 0, x2 = 0, x3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const u32 lo0 = 0xD2511F53u * x0, hi0 = __umulhi(0xD2511F53u, x0);
+    const u32 lo1 = 0xCD9E8D57u * x2, hi1 = __umulhi(0xCD9E8D57u, x2);
+    const u32 y0 = hi1 ^ x1 ^ k0, y2 = hi0 ^ x3 ^ k1;
+    x0 = y0;
+    x1 = lo1;
+    x2 = y2;
+    x3 = lo0;
+  }
+  o0 = x0;
+  o1 = x1;
+  o2 = x2;
+  o3 = x3;
+}
+
+// One lane's stream: key = mix64(parts), words consumed w0..w3 per block.
+struct Stream {
+  u32 k0, k1, ctr, w0, w1, w2, w3;
+  int avail;
+
+  __device__ __forceinline__ void init(u64 key) {
+    k0 = (u32)key;
+    k1 = (u32)(key >> 32);
+    ctr = 0;
+    avail = 0;
+  }
+  __device__ __forceinline__ u32 word() {
+    if (avail == 0) {
+      philox_block(ctr++, k0, k1, w0, w1, w2, w3);
+      avail = 4;
+    }
+    const u32 r = w0;
+    w0 = w1;
+    w1 = w2;
+    w2 = w3;
+    --avail;
+    return r;
+  }
+  // random.Random.random()
+  __device__ __forceinline__ double random() {
+    const u32 a = word() >> 5;
+    const u32 b = word() >> 6;
+    return ((double)a * 67108864.0 + (double)b) * (1.0 / 9007199254740992.0);
+  }
+  // random.Random._randbelow_with_getrandbits, n > 0
+  __device__ __forceinline__ int randbelow(int n) {
+    const int k = 32 - __clz(n);
+    u32 r;
+    do {
+      r = word() >> (32 - k);
+    } while (r >= (u32)n);
+    return (int)r;
+  }
+  __device__ __forceinline__ int randrange(int lo, int hi) { return lo + randbelow(hi - lo); }
+};
+
+// ---- barriers -------------------------------------------------------------
+__device__ __forceinline__ void team_bar(int team, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(nthreads) : "memory");
+}
+
+// ---- cp.async.bulk staging (global -> shared, one elected thread) ---------
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+
+// Copies `bytes` (multiple of 16, both pointers 16B aligned) and waits.
+// Must be called by every thread of the CTA (contains __syncthreads).
+__device__ __forceinline__ void stage_to_smem(void* dst, const void* src, u32 bytes, u64* mbar) {
+#ifndef GO_NO_BULK_COPY
+  const u32 bar = smem_u32(mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    const u32 CH = 65536;
+    for (u32 off = 0; off < bytes; off += CH) {
+      const u32 sz = (bytes - off) < CH ? (bytes - off) : CH;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_u32((char*)dst + off)), "l"((const char*)src + off), "r"(sz), "r"(bar)
+          : "memory");
+    }
+  }
+  __syncthreads();
+  u32 done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar)
+        : "memory");
+  }
+#else
+  const int4* s = (const int4*)src;
+  int4* d = (int4*)dst;
+  for (u32 i = threadIdx.x; i < bytes / 16; i += blockDim.x) d[i] = __ldg(s + i);
+  __syncthreads();
+#endif
+}
+
+// ---- penalty-first comparison (core.py:315-347, Weighted mode) -----------
+// returns true when (pa, sa) is strictly better than (pb, sb)
+__device__ __forceinline__ bool strictly_better(double pa, double sa, double pb, double sb) {
+  const bool fa = pa == 0.0, fb = pb == 0.0;
+  if (fa != fb) return fa;
+  if (!fa && pa != pb) return pa < pb;
+  return sa < sb;
+}
+// compare(): -1 a better, 0 equal, 1 b better
+__device__ __forceinline__ int compare3(double pa, double sa, double pb, double sb) {
+  if (strictly_better(pa, sa, pb, sb)) return -1;
+  if (strictly_better(pb, sb, pa, sa)) return 1;
+  return 0;
+}
+
+__device__ __forceinline__ u64 globaltimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace go

@@ -1,0 +1,75 @@
+// go_dist.cuh — square-matrix layouts for distance / flow data.
+//
+// The host (engine.cu: choose_layout) inspects the float64 matrix the
+// reference stores (builtins.py:55, :266-270) and picks the smallest exact
+// representation: integer-valued matrices (TSPLIB nint, QAPLIB) become int16
+// or int32 and accumulate in int64 (bit-exact); other matrices stay float64.
+// Symmetric matrices may be packed as the strict upper triangle so that an
+// n=442 int16 instance (194,922 B) is staged into one CTA's shared memory
+// (paper §4.3 auto-extension, up to the 227 KB opt-in on B200); matrices
+// that do not fit are read from global memory through the read-only path,
+// where the 126 MB L2 keeps them resident.
+#pragma once
+#include "go_common.cuh"
+
+namespace go {
+
+enum Layout {
+  L_I16_FULL = 0, L_I16_TRI = 1, L_I32_FULL = 2, L_I32_TRI = 3, L_F64_FULL = 4, L_F64_TRI = 5,
+  L_I16_FULL_G = 6, L_I32_FULL_G = 7, L_F64_FULL_G = 8
+};
+
+template <class E> struct AccOf { typedef i64 T; };
+template <> struct AccOf<double> { typedef double T; };
+
+template <class E> struct ValOf { typedef int T; };
+template <> struct ValOf<double> { typedef double T; };
+
+// row-major n x n
+template <class E, bool GLOBAL>
+struct MatFull {
+  typedef E Elem;
+  typedef typename ValOf<E>::T Val;
+  typedef typename AccOf<E>::T Acc;
+  static constexpr bool kIntegral = !(sizeof(E) == 8);
+  static constexpr bool kInSmem = !GLOBAL;
+  const E* __restrict__ m;
+  int n;
+  __device__ __forceinline__ Val operator()(int a, int b) const {
+    if (GLOBAL) return (Val)__ldg(m + a * n + b);
+    return (Val)m[a * n + b];
+  }
+  static __host__ __device__ long long bytes(int n) { return (long long)n * n * sizeof(E); }
+};
+
+// strict upper triangle of a symmetric zero-diagonal matrix (shared memory)
+template <class E>
+struct MatTri {
+  typedef E Elem;
+  typedef typename ValOf<E>::T Val;
+  typedef typename AccOf<E>::T Acc;
+  static constexpr bool kIntegral = !(sizeof(E) == 8);
+  static constexpr bool kInSmem = true;
+  const E* __restrict__ m;
+  int n;
+  __device__ __forceinline__ Val operator()(int a, int b) const {
+    if (a == b) return (Val)0;
+    const int lo = a < b ? a : b, hi = a ^ b ^ lo;
+    return (Val)m[((lo * (2 * n - lo - 1)) >> 1) + (hi - lo - 1)];
+  }
+  static __host__ __device__ long long bytes(int n) {
+    return (long long)n * (n - 1) / 2 * sizeof(E);
+  }
+};
+
+typedef MatFull<short, false> DistI16Full;
+typedef MatTri<short> DistI16Tri;
+typedef MatFull<int, false> DistI32Full;
+typedef MatTri<int> DistI32Tri;
+typedef MatFull<double, false> DistF64Full;
+typedef MatTri<double> DistF64Tri;
+typedef MatFull<short, true> DistI16FullG;
+typedef MatFull<int, true> DistI32FullG;
+typedef MatFull<double, true> DistF64FullG;
+
+}  // namespace go

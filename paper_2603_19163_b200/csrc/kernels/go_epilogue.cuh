@@ -1,0 +1,319 @@
+// go_epilogue.cuh — one-CTA kernel run between evolve chunks.
+//
+// It replays, per generation of the chunk, the host-side bookkeeping of the
+// reference generation loop (engine.py:703-750) on device state:
+//   1. global best: first (generation, evolver) in scan order that is
+//      strictly better (core.py:315-347) -> stagnation counter, history,
+//      target check (engine.py:703-716);
+//   2. AOS barrier every `aos_interval` generations: counters reduced over
+//      all evolvers with warp shuffles, EMA + clamp + one normalisation
+//      (aos.py:96-134), K-level update (aos.py:137-144), stagnation reset
+//      (aos.py:178-186);
+//   3. island migration ring / global_top_n / hybrid (engine.py:483-521,
+//      :730-743) with the migration stream mix64(seed, 3, event);
+//   4. elite injection: worst member <- global best (engine.py:524-532);
+//   5. wall-clock deadline from %globaltimer (engine.py:682-684).
+// Arithmetic is written in the reference's evaluation order and compiled
+// with FMA contraction disabled, so weights are bit-identical to Python's.
+#pragma once
+#include "go_args.cuh"
+#include "go_common.cuh"
+
+namespace go {
+
+enum { EPI_THREADS = 512 };
+
+struct Cand {
+  double pen, scal;
+  int idx;
+};
+
+// a "before" b in best-first order (strictly better, ties -> lower index)
+__device__ __forceinline__ bool best_first(const Cand& a, const Cand& b) {
+  const int c = compare3(a.pen, a.scal, b.pen, b.scal);
+  return c < 0 || (c == 0 && a.idx < b.idx);
+}
+// a "before" b in worst-first order (strictly worse, ties -> lower index)
+__device__ __forceinline__ bool worst_first(const Cand& a, const Cand& b) {
+  const int c = compare3(a.pen, a.scal, b.pen, b.scal);
+  return c > 0 || (c == 0 && a.idx < b.idx);
+}
+
+template <bool WORST>
+__device__ Cand block_select(const double* pen, const double* scal, int lo, int hi,
+                             const int* excl, int nexcl, Cand* red) {
+  Cand c;
+  c.idx = 0x7fffffff;
+  c.pen = 0;
+  c.scal = 0;
+  for (int i = lo + (int)threadIdx.x; i < hi; i += blockDim.x) {
+    bool skip = false;
+    for (int e = 0; e < nexcl; ++e) skip |= excl[e] == i;
+    if (skip) continue;
+    Cand x;
+    x.pen = pen[i];
+    x.scal = scal[i];
+    x.idx = i;
+    if (c.idx == 0x7fffffff || (WORST ? worst_first(x, c) : best_first(x, c))) c = x;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Cand o;
+    o.pen = __shfl_xor_sync(0xffffffffu, c.pen, off);
+    o.scal = __shfl_xor_sync(0xffffffffu, c.scal, off);
+    o.idx = __shfl_xor_sync(0xffffffffu, c.idx, off);
+    if (o.idx != 0x7fffffff && (c.idx == 0x7fffffff || (WORST ? worst_first(o, c) : best_first(o, c))))
+      c = o;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  Cand r = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    const Cand o = red[w];
+    if (o.idx != 0x7fffffff && (r.idx == 0x7fffffff || (WORST ? worst_first(o, r) : best_first(o, r))))
+      r = o;
+  }
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void copy_genes(short* dst, const short* src, int W) {
+  for (int i = threadIdx.x; i < W; i += blockDim.x) dst[i] = src[i];
+}
+
+// ema_weight (aos.py:96-100), evaluated left to right without contraction
+__device__ __forceinline__ double ema_w(double w, long long u, long long v, const EpilogueArgs& A) {
+  return __dadd_rn(__dmul_rn(A.alpha, w),
+                   __dmul_rn(__dsub_rn(1.0, A.alpha),
+                             __dadd_rn(__ddiv_rn((double)v, __dadd_rn((double)u, A.eps)), A.floor_)));
+}
+
+// CPython 3.12 builtin sum() over floats (Neumaier), start 0
+__device__ __forceinline__ double py_sum(const double* x, int n) {
+  if (n == 0) return 0.0;
+  double s = x[0], c = 0.0;
+  for (int i = 1; i < n; ++i) {
+    const double t = __dadd_rn(s, x[i]);
+    if (fabs(s) >= fabs(x[i])) c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x[i]));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x[i], t), s));
+    s = t;
+  }
+  if (c != 0.0 && isfinite(c)) s = __dadd_rn(s, c);
+  return s;
+}
+
+__device__ __forceinline__ void island_range(int P, int islands, int i, int& lo, int& hi) {
+  const int base = P / islands, extra = P % islands;
+  lo = i * base + (i < extra ? i : extra);
+  hi = lo + base + (i < extra ? 1 : 0);
+}
+
+__device__ __forceinline__ void put_solution(const EpilogueArgs& A, int dst, const short* src,
+                                             double pen, double scal) {
+  copy_genes(A.genes + (size_t)dst * A.W, src, A.W);
+  if (threadIdx.x == 0) {
+    A.pen[dst] = pen;
+    A.scal[dst] = scal;
+  }
+}
+
+__global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArgs A) {
+  __shared__ Cand red[EPI_THREADS / 32];
+  __shared__ int s_stop;
+  __shared__ double s_pen[64], s_scal[64];
+  __shared__ int s_idx[64];
+  GlobalState* gs = A.gs;
+  if (gs->stop) return;
+  const int P = A.P;
+
+  // ---- 1. per-generation global best / stagnation / target -----------------
+  if (threadIdx.x == 0) s_stop = 0;
+  __syncthreads();
+  long long last = A.gen0 - 1;
+  for (int gi = 0; gi < A.ngen; ++gi) {
+    const long long g = A.gen0 + gi;
+    const Cand b = block_select<false>(A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
+                                       0, P, nullptr, 0, red);
+    if (threadIdx.x == 0) {
+      if (strictly_better(b.pen, b.scal, gs->gpen, gs->gscal)) {
+        gs->gpen = b.pen;
+        gs->gscal = b.scal;
+        gs->gev = b.idx;
+        gs->ggen = g;
+        gs->stall = 0;
+      } else {
+        gs->stall += 1;
+      }
+      gs->gens_done = g;
+      if (A.history && g - 1 < A.hist_cap) {
+        A.history[g - 1] = __dadd_rn(gs->gscal, __dmul_rn(A.pw, gs->gpen));
+        gs->hist_count = g;
+      }
+      if (A.has_target && !(gs->gpen > 0.0)) {
+        const double v = gs->gscal * A.obj_sign_over_w;
+        const bool hit = A.obj_sign_over_w > 0 ? v <= A.target + 1e-9 : v >= A.target - 1e-9;
+        if (hit) s_stop = 2;
+      }
+    }
+    __syncthreads();
+    last = g;
+    if (s_stop) break;
+  }
+  // the global best's genes: the team best-ever of its evolver
+  if (gs->gev >= 0) {
+    copy_genes(A.gbest_genes, A.best_genes + (size_t)gs->gev * A.W, A.W);
+    __syncthreads();
+    if (threadIdx.x == 0) gs->gev = -1;
+  }
+  __syncthreads();
+
+  // ---- 2. AOS: aggregate counters, update at the barrier -------------------
+  const int nseq = A.reg->nseq;
+  {
+    const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // values 0..nseq-1 usage, 32.. impr, 64..66 k_usage, 67..69 k_impr
+    for (int v = warp; v < 70; v += nw) {
+      const int* src;
+      int stride, col;
+      if (v < 32) { if (v >= nseq) continue; src = A.usage; stride = MAX_SEQ; col = v; }
+      else if (v < 64) { if (v - 32 >= nseq) continue; src = A.impr; stride = MAX_SEQ; col = v - 32; }
+      else if (v < 67) { src = A.k_usage; stride = 3; col = v - 64; }
+      else { src = A.k_impr; stride = 3; col = v - 67; }
+      long long s = 0;
+      for (int e = ln; e < P; e += 32) s += src[e * stride + col];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (ln == 0) A.agg[v] += s;
+    }
+  }
+  __syncthreads();
+  if (!s_stop && last % A.aos_interval == 0 && threadIdx.x == 0) {
+    RegistryDev* R = A.reg;
+    double pre[32];
+    for (int i = 0; i < nseq; ++i) {
+      double w = ema_w(R->w[i], A.agg[i], A.agg[32 + i], A);
+      double lo = fmax(A.floor_, R->floor_[i]);
+      const double hi = fmin(A.cap, R->cap[i]);
+      if (hi < lo) lo = hi;
+      w = fmin(fmax(w, lo), hi);
+      pre[i] = w;
+    }
+    // weights are np.float64 from here on: plain sequential sums (oracle/aos.py)
+    double tot = 0.0;
+    for (int i = 0; i < nseq; ++i) tot = __dadd_rn(tot, pre[i]);
+    double acc = 0.0;
+    for (int i = 0; i < nseq; ++i) {
+      R->w[i] = __ddiv_rn(pre[i], tot);
+      acc = __dadd_rn(acc, R->w[i]);
+      R->cum[i] = acc;
+    }
+    R->total = acc;
+    double nk[3];
+    for (int j = 0; j < 3; ++j) nk[j] = fmax(ema_w(R->kw[j], A.agg[64 + j], A.agg[67 + j], A), A.floor_);
+    const double kt = py_sum(nk, 3);
+    for (int j = 0; j < 3; ++j) R->kw[j] = __ddiv_rn(nk[j], kt);
+    if (gs->stall > A.stagnation) {
+      R->kw[0] = 0.8;
+      R->kw[1] = 0.15;
+      R->kw[2] = 0.05;
+      gs->stall = 0;
+    }
+    for (int v = 0; v < 70; ++v) A.agg[v] = 0;
+  }
+  __syncthreads();
+
+  // ---- 3. island migration ----------------------------------------------------
+  if (!s_stop && A.islands >= 2 && last % A.mig_interval == 0) {
+    int strat = A.migration;
+    if (strat == 2) strat = (gs->mig_events % 2 == 0) ? 0 : 1;
+    const int k = A.islands;
+    if (strat == 0) {  // ring: donors snapshotted first
+      for (int i = 0; i < k; ++i) {
+        int lo, hi;
+        island_range(P, k, i, lo, hi);
+        const Cand b = block_select<false>(A.pen, A.scal, lo, hi, nullptr, 0, red);
+        copy_genes(A.scratch + (size_t)i * A.W, A.genes + (size_t)b.idx * A.W, A.W);
+        if (threadIdx.x == 0) {
+          s_pen[i] = b.pen;
+          s_scal[i] = b.scal;
+        }
+      }
+      __syncthreads();
+      for (int i = 0; i < k; ++i) {
+        int lo, hi;
+        island_range(P, k, (i + 1) % k, lo, hi);
+        if (hi - lo == 1) {
+          if (strictly_better(s_pen[i], s_scal[i], A.pen[lo], A.scal[lo]))
+            put_solution(A, lo, A.scratch + (size_t)i * A.W, s_pen[i], s_scal[i]);
+          __syncthreads();
+          continue;
+        }
+        const Cand w = block_select<true>(A.pen, A.scal, lo, hi, nullptr, 0, red);
+        const Cand b = block_select<false>(A.pen, A.scal, lo, hi, nullptr, 0, red);
+        if (w.idx != b.idx) put_solution(A, w.idx, A.scratch + (size_t)i * A.W, s_pen[i], s_scal[i]);
+        __syncthreads();
+      }
+    } else {  // global_top_n: stable top-n by repeated selection
+      const int tn = A.top_n < 64 ? A.top_n : 64;
+      int nd = 0;
+      for (int d = 0; d < tn && d < P; ++d) {
+        const Cand b = block_select<false>(A.pen, A.scal, 0, P, s_idx, nd, red);
+        copy_genes(A.scratch + (size_t)d * A.W, A.genes + (size_t)b.idx * A.W, A.W);
+        if (threadIdx.x == 0) {
+          s_idx[d] = b.idx;
+          s_pen[d] = b.pen;
+          s_scal[d] = b.scal;
+        }
+        __syncthreads();
+        nd = d + 1;
+      }
+      __shared__ int s_slot;
+      Stream mr;
+      mr.init(mix64_3(A.seed, 3, (u64)gs->mig_events));  // identical in every thread
+      for (int i = 0; i < k; ++i) {
+        int lo, hi;
+        island_range(P, k, i, lo, hi);
+        const Cand b = block_select<false>(A.pen, A.scal, lo, hi, nullptr, 0, red);
+        const int nslots = hi - lo - 1;
+        for (int d = 0; d < nd; ++d) {
+          if (nslots <= 0) break;
+          if (threadIdx.x == 0) {
+            int s = lo + mr.randbelow(nslots);
+            if (s >= b.idx) ++s;  // slots = members except the island best
+            s_slot = s;
+          }
+          __syncthreads();
+          put_solution(A, s_slot, A.scratch + (size_t)d * A.W, s_pen[d], s_scal[d]);
+          __syncthreads();
+        }
+      }
+    }
+    if (threadIdx.x == 0) gs->mig_events += 1;
+    __syncthreads();
+  }
+
+  // ---- 4. elite injection ------------------------------------------------------
+  if (!s_stop && last % A.elite_interval == 0) {
+    const Cand w = block_select<true>(A.pen, A.scal, 0, P, nullptr, 0, red);
+    put_solution(A, w.idx, A.gbest_genes, gs->gpen, gs->gscal);
+  }
+  __syncthreads();
+
+  // ---- 5. stop conditions ----------------------------------------------------------
+  if (threadIdx.x == 0) {
+    int stop = s_stop;
+    if (!stop && gs->deadline_ns && (long long)globaltimer() >= gs->deadline_ns) stop = 1;
+    if (!stop && last >= A.max_gens) stop = 3;
+    if (stop) {
+      gs->stop = stop;
+      if (A.host_stop) *(volatile int*)A.host_stop = stop;
+    }
+  }
+}
+
+__global__ void go_arm_deadline_kernel(GlobalState* gs, long long budget_ns) {
+  gs->deadline_ns = budget_ns > 0 ? (long long)globaltimer() + budget_ns : 0;
+}
+
+}  // namespace go

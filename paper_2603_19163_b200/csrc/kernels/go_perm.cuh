@@ -1,0 +1,276 @@
+// go_perm.cuh — single-row permutation moves as position maps.
+//
+// A lane never copies the solution (the reference copies it per lane,
+// engine.py:570).  Its candidate is the team's current tour composed with
+// the <= 3 primitive moves the lane has drawn so far; every move is a map
+// src(p) = "position in the pre-move row whose element lands at p":
+//
+//   SWAP(i,j)          operators.py:205-225 (op_swap)
+//   REVERSE(i,j)       operators.py:254-261 (op_reverse), demo 2-opt
+//   SEGMENT(s,L,pos)   remove [s,s+L), reinsert at pos of the shortened row:
+//                      op_insert (L=1, :228-251), op_or_opt (L=2,3, :264-283),
+//                      demo or-opt / node-insert (demo_ops.py:48-89)
+//
+// Delta evaluation (TSP): a move rewires only the slots (p, p+1 mod n) at its
+// cut points; with the symmetric matrices the reference enforces
+// (problems.py:97-107) every other edge keeps its length.  The removed edges
+// are the cut slots of the OLD row, the added edges the junction slots of the
+// NEW row — computing both sets explicitly keeps adjacent / wrap-around /
+// whole-row cases exact.  On integer matrices the int64 sum
+// equals Φ_ref(cand) − Φ_ref(cur) bit-for-bit.
+#pragma once
+#include "go_common.cuh"
+#include "go_dist.cuh"
+
+namespace go {
+
+enum MoveKind { MV_NONE = 0, MV_SWAP = 1, MV_REVERSE = 2, MV_SEGMENT = 3 };
+
+struct Move {
+  int kind, a, b, c;
+};
+
+__device__ __forceinline__ int move_src(const Move& m, int p) {
+  switch (m.kind) {
+    case MV_SWAP:
+      return p == m.a ? m.b : (p == m.b ? m.a : p);
+    case MV_REVERSE:
+      return (p >= m.a && p <= m.b) ? m.a + m.b - p : p;
+    case MV_SEGMENT: {
+      if (p >= m.c && p < m.c + m.b) return m.a + (p - m.c);
+      const int q = p < m.c ? p : p - m.b;
+      return q < m.a ? q : q + m.b;
+    }
+    default:
+      return p;
+  }
+}
+
+// The lane's candidate: base row (shared memory) composed with <= 3 moves.
+struct Chain {
+  const i16* base;
+  int n, nm;
+  Move m0, m1, m2;
+
+  __device__ __forceinline__ void reset(const i16* b, int n_) {
+    base = b;
+    n = n_;
+    nm = 0;
+  }
+  __device__ __forceinline__ int src_all(int p) const {
+    if (nm > 2) p = move_src(m2, p);
+    if (nm > 1) p = move_src(m1, p);
+    if (nm > 0) p = move_src(m0, p);
+    return p;
+  }
+  __device__ __forceinline__ int at(int p) const { return base[src_all(p)]; }
+  // element at p of the row AFTER applying `mv` on top of this chain
+  __device__ __forceinline__ int at_after(const Move& mv, int p) const {
+    return at(move_src(mv, p));
+  }
+  __device__ __forceinline__ void push(const Move& mv) {
+    if (nm == 0) m0 = mv;
+    else if (nm == 1) m1 = mv;
+    else m2 = mv;
+    ++nm;
+  }
+};
+
+__device__ __forceinline__ int wrap_slot(int s, int n) { return s < 0 ? s + n : s; }
+
+// old cut slots / new junction slots of a move (deduplicated), see header
+__device__ __forceinline__ void move_slots(const Move& mv, int n, int* so, int& no, int* sn,
+                                           int& nn) {
+  no = nn = 0;
+  int a = mv.a, b = mv.b, c = mv.c;
+  int o[4], w[4], co = 0, cw = 0;
+  if (mv.kind == MV_SWAP) {
+    o[0] = w[0] = a - 1;
+    o[1] = w[1] = a;
+    o[2] = w[2] = b - 1;
+    o[3] = w[3] = b;
+    co = cw = 4;
+  } else if (mv.kind == MV_REVERSE) {
+    o[0] = w[0] = a - 1;
+    o[1] = w[1] = b;
+    co = cw = 2;
+  } else if (mv.kind == MV_SEGMENT) {
+    if (c == a) return;
+    if (c > a) {  // block [a, c+b): old = seg|rest, new = rest|seg
+      o[0] = a - 1; o[1] = a + b - 1; o[2] = c + b - 1;
+      w[0] = a - 1; w[1] = c - 1;     w[2] = c + b - 1;
+    } else {      // block [c, a+b): old = rest|seg, new = seg|rest
+      o[0] = c - 1; o[1] = a - 1;     o[2] = a + b - 1;
+      w[0] = c - 1; w[1] = c + b - 1; w[2] = a + b - 1;
+    }
+    co = cw = 3;
+  }
+  for (int i = 0; i < co; ++i) {
+    const int s = wrap_slot(o[i], n);
+    bool dup = false;
+    for (int j = 0; j < no; ++j) dup |= so[j] == s;
+    if (!dup) so[no++] = s;
+  }
+  for (int i = 0; i < cw; ++i) {
+    const int s = wrap_slot(w[i], n);
+    bool dup = false;
+    for (int j = 0; j < nn; ++j) dup |= sn[j] == s;
+    if (!dup) sn[nn++] = s;
+  }
+}
+
+// Φ(cand after mv) − Φ(cand) for the cyclic tour objective (builtins.py:67-71)
+template <class D>
+__device__ __forceinline__ typename D::Acc tsp_move_delta(const D& d, const Chain& L,
+                                                          const Move& mv) {
+  typedef typename D::Acc Acc;
+  const int n = L.n;
+  int so[4], sn[4], no, nn;
+  move_slots(mv, n, so, no, sn, nn);
+  Acc delta = 0;
+  for (int i = 0; i < no; ++i) {
+    const int p = so[i], q = p + 1 == n ? 0 : p + 1;
+    delta -= (Acc)d(L.at(p), L.at(q));
+  }
+  for (int i = 0; i < nn; ++i) {
+    const int p = sn[i], q = p + 1 == n ? 0 : p + 1;
+    delta += (Acc)d(L.at_after(mv, p), L.at_after(mv, q));
+  }
+  return delta;
+}
+
+// ---- operator context (what built-in and user operators may touch) --------
+//
+// User operator snippets (paper §3.3.2; reference CustomOperator.apply,
+// operators.py:79-88) are compiled as
+//     template <class Ctx> __device__ void op_<id>(Ctx& ctx) { <snippet> }
+// and see exactly this API.  Out-of-range reads or malformed moves set a
+// sticky error bit instead of faulting, so the registration probe can
+// exclude a broken operator (operators.py:649-665) without killing the run.
+template <class Policy>
+struct PermCtx {
+  Stream* rng;
+  const Chain* L;
+  const Policy* pol;
+  Move out;
+  int err;
+
+  __device__ __forceinline__ int size() const { return L->n; }
+  __device__ __forceinline__ int at(int p) {
+    if ((unsigned)p >= (unsigned)L->n) {
+      err |= ERR_OP_RANGE;
+      return 0;
+    }
+    return L->at(p);
+  }
+  __device__ __forceinline__ double dist(int a, int b) {
+    if ((unsigned)a >= (unsigned)pol->n_items() || (unsigned)b >= (unsigned)pol->n_items()) {
+      err |= ERR_OP_RANGE;
+      return 0.0;
+    }
+    return pol->cost(a, b);
+  }
+  __device__ __forceinline__ double random() { return rng->random(); }
+  __device__ __forceinline__ int randbelow(int n) {
+    if (n <= 0) {
+      err |= ERR_OP_RANGE;
+      return 0;
+    }
+    return rng->randbelow(n);
+  }
+  __device__ __forceinline__ int randrange(int lo, int hi) {
+    if (hi <= lo) {
+      err |= ERR_OP_RANGE;
+      return lo;
+    }
+    return rng->randrange(lo, hi);
+  }
+  __device__ __forceinline__ void swap(int i, int j) {
+    const int n = L->n;
+    if ((unsigned)i >= (unsigned)n || (unsigned)j >= (unsigned)n || i == j) {
+      err |= ERR_OP_MOVE;
+      return;
+    }
+    out.kind = MV_SWAP; out.a = i; out.b = j; out.c = 0;
+  }
+  __device__ __forceinline__ void reverse(int i, int j) {
+    if (i < 0 || j >= L->n || i >= j) {
+      err |= ERR_OP_MOVE;
+      return;
+    }
+    out.kind = MV_REVERSE; out.a = i; out.b = j; out.c = 0;
+  }
+  __device__ __forceinline__ void move_segment(int start, int len, int pos) {
+    const int n = L->n;
+    if (len < 1 || start < 0 || start + len > n || pos < 0 || pos > n - len) {
+      err |= ERR_OP_MOVE;
+      return;
+    }
+    out.kind = MV_SEGMENT; out.a = start; out.b = len; out.c = pos;
+  }
+  __device__ __forceinline__ void insert(int i, int pos) { move_segment(i, 1, pos); }
+};
+
+// ---- built-in single-row permutation operators ----------------------------
+// Draw order is the reference's; the leading randbelow(1) is _pick_row's
+// randrange(len(rows)) over the single row (operators.py:140-144), which
+// consumes words in CPython (k = 1, rejection) and therefore here too.
+template <class Ctx>
+__device__ __forceinline__ void bi_swap(Ctx& c) {
+  const int n = c.size();
+  if (n < 2) return;
+  c.randbelow(1);
+  const int i = c.randbelow(n);
+  int j = c.randbelow(n - 1);
+  j += j >= i;
+  c.swap(i, j);
+}
+template <class Ctx>
+__device__ __forceinline__ void bi_insert(Ctx& c) {
+  const int n = c.size();
+  if (n < 2) return;
+  c.randbelow(1);
+  const int i = c.randbelow(n);
+  const int j = c.randbelow(n);
+  c.move_segment(i, 1, j);
+}
+template <class Ctx>
+__device__ __forceinline__ void bi_reverse(Ctx& c) {
+  const int n = c.size();
+  if (n < 2) return;
+  c.randbelow(1);
+  const int i = c.randbelow(n - 1);
+  const int j = c.randrange(i + 1, n);
+  c.reverse(i, j);
+}
+template <class Ctx>
+__device__ __forceinline__ void bi_or_opt(Ctx& c) {
+  const int L = c.randrange(2, 4);
+  const int n = c.size();
+  if (n < L + 1) return;
+  c.randbelow(1);
+  const int s = c.randbelow(n - L + 1);
+  const int pos = c.randbelow(n - L + 1);
+  c.move_segment(s, L, pos);
+}
+
+// ---- problem policies over a single permutation row -------------------------
+template <class D>
+struct TspPolicy {
+  typedef typename D::Acc Acc;
+  static constexpr bool kIntegral = D::kIntegral;
+  D d;
+  __device__ __forceinline__ int n_items() const { return d.n; }
+  __device__ __forceinline__ double cost(int a, int b) const { return (double)d(a, b); }
+  __device__ __forceinline__ Acc delta(const Chain& L, const Move& mv) const {
+    return tsp_move_delta(d, L, mv);
+  }
+  // full tour length partial sum over slots [lo, hi) step `step` (team reduce)
+  __device__ __forceinline__ Acc partial(const i16* t, int n, int lo, int step) const {
+    Acc s = 0;
+    for (int p = lo; p < n; p += step) s += (Acc)d(t[p], t[p + 1 == n ? 0 : p + 1]);
+    return s;
+  }
+};
+
+}  // namespace go

@@ -1,0 +1,613 @@
+"""The search engine's public API — drop-in for the reference's `engine.py`
+(`run`, `EngineConfig`, `IslandsConfig`, `RunResult`,
+`adaptive_population_size`, `initialize_population`), driving the device.
+
+Host side (this file) does exactly what the reference does once per run —
+profile + registry + presets (engine.py:621-623), user-operator registration
+(:625-636, NVRTC instead of Python callables), population sizing (:638-645),
+oversampled initialisation with the reference's MT19937 init stream
+(:647-649, evaluation on the device), penalty weight and T0 (:651-671).  The
+generation loop (:681-750) runs in libcugenopt.so: evolve chunks + device
+epilogues, no per-generation host round trip.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import random
+import time
+import warnings
+from dataclasses import dataclass, field
+from functools import cmp_to_key
+
+import numpy as np
+
+from . import _native as N
+from .aos import DEFAULT_K_WEIGHTS, AosConfig
+from .core import (A_BETTER, B_BETTER, Direction, EncodingKind, ProblemConfig, RowModeKind,
+                   Solution, Weighted, compare, scalarize, validate_solution)
+from .operators import (CustomOperator, SequenceRegistry, append_custom, build_registry,
+                        missing_device_sequences, validate_custom_id)
+from .problems import ProblemDefinition, evaluate_many, pack_solutions
+from .profiles import apply_preset, classify
+
+_MASK64 = (1 << 64) - 1
+ENV_CACHE_BUDGET = "GENOPT_CACHE_BUDGET"
+ENV_PARALLELISM = "GENOPT_PAR"
+DEFAULT_CACHE_BUDGET = 32 * 1024 * 1024
+DEFAULT_FAST_BUDGET = 96 * 1024
+_STREAM_LANE, _STREAM_ACCEPT, _STREAM_INIT, _STREAM_MIGRATION, _STREAM_PROBE = range(5)
+
+
+def mix64(*parts: int) -> int:
+    """Stream identity hash (engine.py:74-83); the device folds the same parts."""
+    h = 0x9E3779B97F4A7C15
+    for part in parts:
+        h = (h ^ (part & _MASK64)) * 0xBF58476D1CE4E5B9 & _MASK64
+        h ^= h >> 27
+        h = h * 0x94D049BB133111EB & _MASK64
+        h ^= h >> 31
+    return h
+
+
+def derived_rng(*parts: int) -> random.Random:
+    """Host-side streams (init, probe) are the reference's MT19937 streams."""
+    return random.Random(mix64(*parts))
+
+
+@dataclass(frozen=True)
+class IslandsConfig:
+    count: int = 1
+    migration: str = "ring"
+    interval: int = 100
+    top_n: int = 1
+
+    def __post_init__(self):
+        if self.count < 1 or self.interval < 1 or self.top_n < 1:
+            raise ValueError("island count, interval and top_n must be >= 1")
+        if self.migration not in ("ring", "global_top_n", "hybrid"):
+            raise ValueError(f"unknown migration strategy {self.migration!r}")
+
+    def as_dict(self):
+        return {"count": self.count, "migration": self.migration, "interval": self.interval,
+                "top_n": self.top_n}
+
+
+@dataclass
+class EngineConfig:
+    population: int | None = None
+    team_size: int = 128
+    max_generations: int = 1000
+    time_limit_seconds: float | None = None
+    seed: int = 42
+    initial_temperature: float | None = None
+    cooling_alpha: float = 0.999
+    oversample_factor: int = 4
+    islands: IslandsConfig = field(default_factory=IslandsConfig)
+    elite_injection_interval: int = 50
+    replicas: int = 1
+    cache_budget_bytes: int | None = None
+    concurrency_hint: int | None = None
+    fast_budget_bytes: int = DEFAULT_FAST_BUDGET
+    working_set_bytes: int | None = None
+    workers: int = 1
+    aos: AosConfig = field(default_factory=AosConfig)
+    custom_operators: tuple[CustomOperator, ...] = ()
+    target_objective: float | None = None
+    record_history: bool = False
+    # B200 extensions (defaults keep reference behaviour)
+    device: int = 0
+    teams_per_cta: int = 0          # evolver teams sharing one CTA's staged instance (0 = auto)
+    evolver_offset: int = 0         # global index of local evolver 0 (multi-GPU islands)
+
+    def __post_init__(self):
+        if self.team_size < 1:
+            raise ValueError("team_size must be >= 1")
+        if self.population is not None and self.population < self.islands.count:
+            raise ValueError("population must cover at least one member per island")
+        if self.max_generations < 1:
+            raise ValueError("max_generations must be >= 1")
+        if self.replicas < 1:
+            raise ValueError("replicas must be >= 1")
+        if self.oversample_factor < 1:
+            raise ValueError("oversample_factor must be >= 1")
+        if not (0.0 < self.cooling_alpha <= 1.0):
+            raise ValueError("cooling_alpha must be in (0, 1]")
+        if self.elite_injection_interval < 1:
+            raise ValueError("elite_injection_interval must be >= 1")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+
+    def resolved_cache_budget(self) -> int | None:
+        if self.cache_budget_bytes is not None:
+            return self.cache_budget_bytes
+        env = os.environ.get(ENV_CACHE_BUDGET)
+        return int(env) if env else None
+
+    def resolved_concurrency_hint(self) -> int | None:
+        if self.concurrency_hint is not None:
+            return self.concurrency_hint
+        env = os.environ.get(ENV_PARALLELISM)
+        return int(env) if env else None
+
+    def as_dict(self) -> dict:
+        return {
+            "population": self.population, "team_size": self.team_size,
+            "max_generations": self.max_generations,
+            "time_limit_seconds": self.time_limit_seconds, "seed": self.seed,
+            "initial_temperature": self.initial_temperature,
+            "cooling_alpha": self.cooling_alpha, "oversample_factor": self.oversample_factor,
+            "islands": self.islands.as_dict(),
+            "elite_injection_interval": self.elite_injection_interval,
+            "replicas": self.replicas, "cache_budget_bytes": self.cache_budget_bytes,
+            "concurrency_hint": self.concurrency_hint,
+            "fast_budget_bytes": self.fast_budget_bytes,
+            "working_set_bytes": self.working_set_bytes, "workers": self.workers,
+            "aos": self.aos.as_dict(),
+            "custom_operators": [op.name for op in self.custom_operators],
+            "target_objective": self.target_objective,
+        }
+
+
+@dataclass
+class EvolverState:
+    current: Solution
+    island_id: int
+    temperature: float = 0.0
+
+
+@dataclass
+class RunResult:
+    best: Solution
+    objectives: list[float]
+    penalty: float
+    feasible: bool
+    gap_pct: float | None
+    generations_completed: int
+    elapsed_seconds: float
+    gens_per_sec: float
+    final_weights: dict
+    profile: dict
+    config: dict
+    seed: int
+    history: dict | None = None
+    device: dict | None = None      # B200 extras: evals, launches, device ms, layout, JIT
+    population: list | None = None  # final currents (for parity checks)
+
+
+# ---------------------------------------------------------------------------
+# population sizing
+
+def _pow2_ceil(x: int) -> int:
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
+
+
+def _pow2_floor(x: float) -> int:
+    p = 1
+    while p * 2 <= x:
+        p <<= 1
+    return p
+
+
+def adaptive_population_size(concurrency_hint: int, cache_budget_bytes: int,
+                             working_set_bytes: int, fast_budget_bytes: int) -> int:
+    """The reference rule (engine.py:440-456), kept for explicit callers."""
+    if min(concurrency_hint, cache_budget_bytes, working_set_bytes, fast_budget_bytes) <= 0:
+        raise ValueError("all sizing inputs must be positive")
+    p_sm = max(2, _pow2_ceil(concurrency_hint))
+    if working_set_bytes <= fast_budget_bytes:
+        return p_sm
+    ratio = cache_budget_bytes / working_set_bytes
+    if ratio >= p_sm / 2:
+        return p_sm
+    return max(2, _pow2_floor(ratio))
+
+
+def b200_population_size(sm_count: int, teams_per_sm: int, l2_bytes: int,
+                         working_set_bytes: int, instance_in_smem: bool) -> int:
+    """Paper §4.4 re-derived for B200.  Shared-memory path: one resident wave
+    (SMs x teams per SM from the occupancy API) — no power-of-two rounding,
+    which on 148 SMs would leave a partial second wave.  Global path: the L2
+    rule of Eq. (3) with the device's L2 size, rounded down to whole waves
+    of SMs when that still leaves at least one evolver per SM."""
+    p_sm = max(2, sm_count * max(1, teams_per_sm))
+    if instance_in_smem:
+        return p_sm
+    ratio = l2_bytes / max(1, working_set_bytes)
+    if ratio >= p_sm / 2:
+        return p_sm
+    p = max(2, int(ratio))
+    return p // sm_count * sm_count if p >= sm_count else p
+
+
+def estimate_working_set_bytes(problem: ProblemDefinition) -> int:
+    cfg = problem.config()
+    return problem.payload_nbytes() + cfg.d1 * cfg.d2 * 4
+
+
+# ---------------------------------------------------------------------------
+# initialisation (host, reference MT19937 draws; evaluation on the device)
+
+def random_solution(cfg: ProblemConfig, rng: random.Random) -> Solution:
+    """engine.py:252-287 draw order."""
+    data = np.zeros((cfg.d1, cfg.d2), dtype=np.int64)
+    sizes = np.zeros(cfg.d1, dtype=np.int64)
+    kind = cfg.encoding.kind
+    if kind is EncodingKind.PERMUTATION:
+        if cfg.row_mode is RowModeKind.MULTI_PARTITION:
+            vals = list(range(cfg.n))
+            rng.shuffle(vals)
+            for v in vals:
+                open_rows = [r for r in range(cfg.d1) if sizes[r] < cfg.d2]
+                r = open_rows[rng.randrange(len(open_rows))]
+                data[r, sizes[r]] = v
+                sizes[r] += 1
+        else:
+            rows = 1 if cfg.row_mode is RowModeKind.SINGLE_SEQ else cfg.d1
+            for r in range(rows):
+                perm = list(range(cfg.n))
+                rng.shuffle(perm)
+                data[r, :cfg.n] = perm
+                sizes[r] = cfg.n
+    else:
+        lo, hi = (0, 1) if kind is EncodingKind.BINARY else \
+            (cfg.encoding.lower_bound, cfg.encoding.upper_bound)
+        for r in range(cfg.d1):
+            sizes[r] = cfg.d2
+            for p in range(cfg.d2):
+                data[r, p] = rng.randrange(lo, hi + 1)
+    return Solution(data, sizes, cfg.num_objectives)
+
+
+def heuristic_candidates(matrix: np.ndarray) -> list[np.ndarray]:
+    """engine.py:290-301: stable argsorts of row / column sums, both ways."""
+    m = np.asarray(matrix, dtype=np.float64)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise ValueError(f"heuristic construction needs a square matrix, got {m.shape}")
+    out = []
+    for sums in (m.sum(axis=1), m.sum(axis=0)):
+        asc = np.argsort(sums, kind="stable").astype(np.int64)
+        out += [asc, asc[::-1].astype(np.int64)]
+    return out
+
+
+def permutation_as_solution(perm: np.ndarray, cfg: ProblemConfig) -> Solution:
+    data = np.zeros((cfg.d1, cfg.d2), dtype=np.int64)
+    sizes = np.zeros(cfg.d1, dtype=np.int64)
+    if cfg.row_mode is RowModeKind.SINGLE_SEQ:
+        data[0, :cfg.n] = perm
+        sizes[0] = cfg.n
+    elif cfg.row_mode is RowModeKind.MULTI_FIXED:
+        data[:, :cfg.n] = perm
+        sizes[:] = cfg.n
+    else:
+        base, extra = divmod(cfg.n, cfg.d1)
+        at = 0
+        for r in range(cfg.d1):
+            size = base + (1 if r < extra else 0)
+            data[r, :size] = perm[at:at + size]
+            sizes[r] = size
+            at += size
+    return Solution(data, sizes, cfg.num_objectives)
+
+
+def initialize_population(problem: ProblemDefinition, pop_size: int, oversample_factor: int,
+                          rng: random.Random, device: int = 0) -> list[Solution]:
+    """engine.py:327-360 (single objective): oversample, add the heuristic
+    pool, evaluate on the device in one batch, keep the comparison-best."""
+    cfg = problem.config()
+    pool = [random_solution(cfg, rng) for _ in range(oversample_factor * pop_size)]
+    if cfg.encoding.kind is EncodingKind.PERMUTATION:
+        for mat in problem.init_matrices():
+            if mat.shape == (cfg.n, cfg.n):
+                pool.extend(permutation_as_solution(p, cfg) for p in heuristic_candidates(mat))
+    seeded = problem.init_candidates(rng)
+    for s in seeded or ():
+        rep = validate_solution(s, cfg)
+        if not rep.ok:
+            raise ValueError(f"init_candidates produced an invalid solution: {rep.violations[0]}")
+        pool.append(s.copy())
+    evaluate_many(problem, pool, device)
+    if cfg.num_objectives != 1:
+        raise NotImplementedError("multi-objective runs have no device path yet (SURVEY §8f-3)")
+    pool.sort(key=cmp_to_key(lambda a, b: compare(a, b, cfg)))
+    return pool[:pop_size]
+
+
+def scalar_fitness(sol: Solution, cfg: ProblemConfig, penalty_weight: float) -> float:
+    mode = cfg.comparison_or_default()
+    weights = mode.weights if isinstance(mode, Weighted) else tuple(o.weight for o in cfg.obj_defs)
+    return scalarize(sol.objectives, cfg.obj_defs, weights) + penalty_weight * sol.penalty
+
+
+def _best_index(pop, cfg) -> int:
+    b = 0
+    for i in range(1, len(pop)):
+        if compare(pop[i], pop[b], cfg) == A_BETTER:
+            b = i
+    return b
+
+
+# ---------------------------------------------------------------------------
+# runs
+
+def run(problem: ProblemDefinition, config: EngineConfig,
+        best_known: float | None = None) -> RunResult:
+    """engine.py:601-614: replicas run the whole pipeline with seed + i and
+    the comparison-best result is returned."""
+    if config.replicas == 1:
+        return _run_single(problem, config, config.seed, best_known)
+    results = [_run_single(problem, config, config.seed + i, best_known)
+               for i in range(config.replicas)]
+    cfg = problem.config()
+    best = results[0]
+    for r in results[1:]:
+        if compare(r.best, best.best, cfg) == A_BETTER:
+            best = r
+    return best
+
+
+class DeviceRun:
+    """One engine on one device — the native generation loop plus the host
+    set-up that precedes it.  `run()` uses it; bench.py and the island driver
+    use it directly to keep the engine resident between calls."""
+
+    def __init__(self, problem: ProblemDefinition, config: EngineConfig, seed: int,
+                 initial_population: list[Solution] | None = None):
+        self.t_start = time.perf_counter()
+        self.problem, self.config, self.seed = problem, config, seed
+        cfg = problem.config()
+        if cfg.num_objectives != 1 or not isinstance(cfg.comparison_or_default(), Weighted):
+            raise NotImplementedError("the device path runs single-objective Weighted problems")
+        self.cfg = cfg
+        self.lib = N.load()
+        dev = config.device
+        self.handle = problem.device_handle(dev)
+        self.profile = classify(cfg)
+        self.registry = build_registry(cfg)
+        apply_preset(self.registry, self.profile)
+        self.missing_ops = missing_device_sequences(cfg)
+        self.jit_seconds = 0.0
+        if config.custom_operators:
+            self._register_custom(config.custom_operators)
+
+        lay, tcta, tsm, smem = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        N.check(self.lib.go_problem_occupancy(self.handle, config.team_size, config.teams_per_cta,
+                                              C.byref(lay), C.byref(tcta), C.byref(tsm),
+                                              C.byref(smem)))
+        self.layout, self.teams_per_sm, self.smem_bytes = lay.value, tsm.value, smem.value
+        info = N.device_info(dev)
+        self.device_info = info
+        if config.population is not None:
+            pop_size = config.population
+        elif config.resolved_concurrency_hint() is not None or \
+                config.resolved_cache_budget() is not None:
+            pop_size = adaptive_population_size(
+                config.resolved_concurrency_hint() or info.sm_count * self.teams_per_sm,
+                config.resolved_cache_budget() or info.l2_bytes,
+                config.working_set_bytes or estimate_working_set_bytes(problem),
+                config.fast_budget_bytes)
+        else:
+            pop_size = b200_population_size(info.sm_count, self.teams_per_sm, info.l2_bytes,
+                                            config.working_set_bytes or
+                                            estimate_working_set_bytes(problem),
+                                            self.layout < 6)
+        pop_size = max(pop_size, config.islands.count)
+        self.pop_size = pop_size
+
+        if initial_population is None:
+            pop = initialize_population(problem, pop_size, config.oversample_factor,
+                                        derived_rng(seed, _STREAM_INIT), dev)
+        else:
+            pop = [s.copy() for s in initial_population]
+            evaluate_many(problem, pop, dev)
+        self.initial_population = pop
+        if cfg.penalty_weight is not None:
+            pw = cfg.penalty_weight
+        else:
+            scale = float(np.mean([abs(s.objectives[0]) for s in pop]))
+            pw = 1000.0 * (scale if scale > 0 else 1.0)
+        self.penalty_weight = pw
+        gbest = pop[_best_index(pop, cfg)]
+        t0 = config.initial_temperature
+        if t0 is None:
+            t0 = max(1e-6, 0.05 * abs(scalar_fitness(gbest, cfg, pw)))
+        self.t0 = t0
+
+        ec = N.EngineConfig()
+        ec.population = pop_size
+        ec.team_size = config.team_size
+        ec.teams_per_cta = config.teams_per_cta
+        ec.seed = seed & _MASK64
+        ec.t0 = t0
+        ec.cooling_alpha = config.cooling_alpha
+        ec.penalty_weight = pw
+        a = config.aos
+        ec.aos_interval, ec.aos_alpha, ec.aos_floor = a.update_interval, a.ema_alpha, a.weight_floor
+        ec.aos_cap, ec.aos_eps, ec.stagnation_threshold = a.weight_cap, a.epsilon, a.stagnation_threshold
+        isl = config.islands
+        ec.islands, ec.migration = isl.count, N.MIG[isl.migration]
+        ec.migration_interval, ec.top_n = isl.interval, isl.top_n
+        ec.elite_interval = config.elite_injection_interval
+        ec.has_target = config.target_objective is not None
+        ec.target_objective = config.target_objective or 0.0
+        ec.evolver_offset = config.evolver_offset
+        od = cfg.obj_defs[0]
+        ec.maximize = od.direction is Direction.MAXIMIZE
+        ec.obj_weight = cfg.comparison_or_default().weights[0]
+        self.engine = C.c_void_p()
+        N.check(self.lib.go_engine_create(self.handle, C.byref(ec), C.byref(self.engine)))
+        reg = self.registry
+        ids = np.array(reg.ids(), dtype=np.int32)
+        w = np.array(reg.weights(), dtype=np.float64)
+        floors = np.array([e.floor for e in reg.entries], dtype=np.float64)
+        caps = np.array([e.cap for e in reg.entries], dtype=np.float64)
+        kw = np.array(DEFAULT_K_WEIGHTS, dtype=np.float64)
+        N.check(self.lib.go_engine_set_registry(self.engine, len(ids), N.iptr(ids), N.dptr(w),
+                                                N.dptr(floors), N.dptr(caps), reg.total(),
+                                                N.dptr(kw)))
+        genes, sizes = pack_solutions(pop, cfg)
+        obj = np.array([s.objectives[0] for s in pop], dtype=np.float64)
+        pen = np.array([s.penalty for s in pop], dtype=np.float64)
+        N.check(self.lib.go_engine_set_population(self.engine, N.iptr(genes), N.iptr(sizes),
+                                                  N.dptr(obj), N.dptr(pen)))
+        N.check(self.lib.go_engine_set_history(self.engine, int(config.record_history)))
+        self.generations = 0
+        self.stats = N.RunStats()
+
+    def _register_custom(self, ops):
+        cfg = self.cfg
+        probe = random_solution(cfg, derived_rng(self.seed, _STREAM_PROBE))
+        usable = []
+        for op in ops:
+            validate_custom_id(self.registry, op)
+            if any(op.id == u.id for u in usable):
+                raise ValueError(f"sequence id {op.id} already registered")
+            if not op.cuda:
+                warnings.warn(f"custom operator {op.name!r} (id {op.id}) excluded: no CUDA "
+                              "snippet (the device engine cannot run Python operators)",
+                              RuntimeWarning, stacklevel=3)
+                continue
+            usable.append(op)
+        if not usable:
+            return
+        t = time.perf_counter()
+        arr = (N.CustomOp * len(usable))()
+        keep = []
+        for i, op in enumerate(usable):
+            name, body = op.name.encode(), op.cuda.encode()
+            keep += [name, body]
+            arr[i] = N.CustomOp(op.id, name, body)
+        status = np.zeros(len(usable), dtype=np.int32)
+        msg_len = 512
+        msgs = C.create_string_buffer(msg_len * len(usable))
+        genes, sizes = pack_solutions([probe], cfg)
+        N.check(self.lib.go_problem_set_custom_ops(self.handle, arr, len(usable), N.iptr(genes),
+                                                   N.iptr(sizes), self.seed & _MASK64,
+                                                   N.iptr(status), msgs, msg_len))
+        for i, op in enumerate(usable):
+            if status[i]:
+                append_custom(self.registry, op)
+            else:
+                text = msgs.raw[i * msg_len:(i + 1) * msg_len].split(b"\0")[0].decode()
+                warnings.warn(f"custom operator {op.name!r} (id {op.id}) excluded: {text}",
+                              RuntimeWarning, stacklevel=3)
+        self.jit_seconds = time.perf_counter() - t
+
+    def run(self, max_generations: int, time_limit_s: float | None):
+        st = N.RunStats()
+        N.check(self.lib.go_engine_run(self.engine, int(max_generations),
+                                       float(time_limit_s or 0.0), C.byref(st)))
+        self.stats = st
+        self.generations = st.generations
+        return st
+
+    def best(self) -> Solution:
+        cfg = self.cfg
+        W = cfg.d1 * cfg.d2
+        genes = np.zeros(W, dtype=np.int32)
+        sizes = np.zeros(cfg.d1, dtype=np.int32)
+        obj, pen, gen = C.c_double(), C.c_double(), C.c_int64()
+        N.check(self.lib.go_engine_get_best(self.engine, N.iptr(genes), N.iptr(sizes),
+                                            C.byref(obj), C.byref(pen), C.byref(gen)))
+        s = Solution(genes.reshape(cfg.d1, cfg.d2), sizes, 1)
+        s.objectives[0] = obj.value
+        s.penalty = pen.value
+        return s
+
+    def population(self) -> list[Solution]:
+        cfg = self.cfg
+        P, W = self.pop_size, cfg.d1 * cfg.d2
+        genes = np.zeros((P, W), dtype=np.int32)
+        sizes = np.zeros((P, cfg.d1), dtype=np.int32)
+        obj = np.zeros(P)
+        pen = np.zeros(P)
+        N.check(self.lib.go_engine_get_population(self.engine, N.iptr(genes), N.iptr(sizes),
+                                                  N.dptr(obj), N.dptr(pen)))
+        out = []
+        for i in range(P):
+            s = Solution(genes[i].reshape(cfg.d1, cfg.d2), sizes[i], 1)
+            s.objectives[0] = obj[i]
+            s.penalty = pen[i]
+            out.append(s)
+        return out
+
+    def weights(self):
+        nseq = len(self.registry.entries)
+        w = np.zeros(nseq)
+        kw = np.zeros(3)
+        stall = C.c_int32()
+        N.check(self.lib.go_engine_get_registry(self.engine, N.dptr(w), N.dptr(kw),
+                                                C.byref(stall)))
+        return w, kw
+
+    def history(self, count: int):
+        buf = np.zeros(max(1, count))
+        got = C.c_int64()
+        N.check(self.lib.go_engine_get_history(self.engine, N.dptr(buf), len(buf), C.byref(got)))
+        return buf[:got.value]
+
+    def close(self):
+        if getattr(self, "engine", None) is not None and self.engine.value:
+            self.lib.go_engine_destroy(self.engine)
+            self.engine = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def _run_single(problem, config: EngineConfig, seed: int, best_known) -> RunResult:
+    dr = DeviceRun(problem, config, seed)
+    cfg = dr.cfg
+    try:
+        # the budget clock starts with the run (engine.py:619) minus JIT compile
+        # time, which the paper reports separately
+        limit = config.time_limit_seconds
+        remaining = None
+        if limit is not None:
+            remaining = limit - (time.perf_counter() - dr.t_start - dr.jit_seconds)
+        if remaining is not None and remaining <= 0:
+            st = N.RunStats()
+        else:
+            st = dr.run(config.max_generations, remaining if remaining is not None else 0.0)
+        best = dr.best()
+        w, kw = dr.weights()
+        hist = None
+        if config.record_history:
+            phi = dr.history(int(st.generations))
+            t0, a = dr.t0, config.cooling_alpha
+            hist = {"best_phi": [float(x) for x in phi],
+                    "temperature": [t0 * a ** (g - 1) for g in range(1, len(phi) + 1)]}
+        pop = dr.population()
+    finally:
+        dr.close()
+    elapsed = time.perf_counter() - dr.t_start - dr.jit_seconds
+    gap = None
+    if best_known is not None and cfg.obj_defs[0].direction is Direction.MINIMIZE and best_known:
+        gap = (float(best.objectives[0]) - best_known) / best_known * 100.0
+    gens = int(st.generations)
+    echo = config.as_dict()
+    echo["population_effective"] = dr.pop_size
+    return RunResult(
+        best=best, objectives=[float(v) for v in best.objectives], penalty=float(best.penalty),
+        feasible=best.penalty == 0.0, gap_pct=gap, generations_completed=gens,
+        elapsed_seconds=elapsed, gens_per_sec=gens / elapsed if elapsed > 0 else 0.0,
+        final_weights={"sequences": [{"id": e.id, "name": e.name, "weight": float(wi)}
+                                     for e, wi in zip(dr.registry.entries, w)],
+                       "k_steps": [float(x) for x in kw]},
+        profile=dr.profile.as_dict(), config=echo, seed=seed, history=hist,
+        device={"lane_evals": int(st.lane_evals), "kernel_launches": int(st.kernel_launches),
+                "device_ms": float(st.device_ms), "layout": dr.layout,
+                "teams_per_sm": dr.teams_per_sm, "smem_bytes": dr.smem_bytes,
+                "jit_seconds": dr.jit_seconds, "error_flags": int(st.error_flags),
+                "missing_operators": dr.missing_ops, "penalty_weight": dr.penalty_weight,
+                "t0": dr.t0},
+        population=pop)

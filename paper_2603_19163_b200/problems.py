@@ -1,0 +1,213 @@
+"""Problem definitions — API mirror of the reference's `problems.py` and
+`builtins.py`, backed by the device (no CPU objective path).
+
+`builtin_problem(name, InstanceData)` (builtins.py:42-50) returns a problem
+whose configuration matches the reference's exactly (encoding, d1, d2, n, row
+mode, objective definitions) and whose objective / penalty are evaluated by
+`libcugenopt.so` (go_eval_batch).  Python `compute_objective` callbacks of
+user subclasses cannot run on the device: the engine rejects them loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .core import (ComparisonMode, Direction, Encoding, ObjDef, ProblemConfig, RowModeKind,
+                   Solution, validate_solution)
+
+BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph_coloring",
+                 "bin_packing", "load_balancing", "jsp_int", "jsp_perm", "schedule_binary",
+                 "vrp_priority", "vrp_nonlinear")
+DEVICE_PROBLEMS = ("tsp",)
+
+
+@dataclass
+class InstanceData:
+    """problems.py:18-46 — numeric payload of one instance."""
+
+    distance_matrix: np.ndarray | None = None
+    weights: np.ndarray | None = None
+    values: np.ndarray | None = None
+    capacity: float | None = None
+    flow_matrix: np.ndarray | None = None
+    cost_matrix: np.ndarray | None = None
+    edges: list | None = None
+    num_colors: int | None = None
+    item_sizes: np.ndarray | None = None
+    bin_capacity: float | None = None
+    durations: np.ndarray | None = None
+    num_machines: int | None = None
+    jobs: list | None = None
+    demands: np.ndarray | None = None
+    vehicles: int | None = None
+    ready_times: np.ndarray | None = None
+    due_times: np.ndarray | None = None
+    service_times: np.ndarray | None = None
+    priorities: np.ndarray | None = None
+    requirements: np.ndarray | None = None
+    meta: dict = field(default_factory=dict)
+
+
+class ProblemDefinition:
+    """problems.py:49-74.  Device-backed problems implement `_native_desc`."""
+
+    def config(self) -> ProblemConfig:
+        raise NotImplementedError
+
+    def compute_objective(self, i: int, sol: Solution) -> float:
+        obj, _ = device_evaluate(self, [sol])
+        return float(obj[0, i])
+
+    def compute_penalty(self, sol: Solution) -> float:
+        _, pen = device_evaluate(self, [sol])
+        return float(pen[0])
+
+    def init_matrices(self) -> list[np.ndarray]:
+        return []
+
+    def init_candidates(self, rng) -> list[Solution] | None:
+        return None
+
+    def payload_nbytes(self) -> int:
+        return sum(m.nbytes for m in self.init_matrices())
+
+    # -- device plumbing -------------------------------------------------------
+    _handle = None
+    _handle_device = None
+
+    def _native_desc(self):
+        raise TypeError(
+            f"{type(self).__name__} has no device objective: the B200 engine evaluates "
+            "built-in problems (and NVRTC objectives) only; Python callbacks are not a "
+            "supported path")
+
+    def device_handle(self, device: int = 0):
+        if self._handle is not None and self._handle_device == device:
+            return self._handle
+        lib = N.load()
+        desc, keep = self._native_desc()
+        h = C.c_void_p()
+        N.check(lib.go_problem_create(C.byref(desc), device, C.byref(h)))
+        self._keepalive = keep
+        self._handle = h
+        self._handle_device = device
+        return h
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and N._lib is not None:
+            try:
+                N._lib.go_problem_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
+
+
+def check_distance_matrix(d, symmetric: bool = True) -> np.ndarray:
+    """problems.py:97-107."""
+    d = np.asarray(d, dtype=np.float64)
+    if d.ndim != 2 or d.shape[0] != d.shape[1]:
+        raise ValueError(f"distance matrix must be square, got shape {d.shape}")
+    if np.any(d < 0):
+        raise ValueError("distance matrix must be nonnegative")
+    if np.any(np.diag(d) != 0):
+        raise ValueError("distance matrix must have a zero diagonal")
+    if symmetric and not np.array_equal(d, d.T):
+        raise ValueError("distance matrix declared symmetric but is not")
+    return d
+
+
+def pack_solutions(sols, cfg: ProblemConfig):
+    """Solutions -> (genes[m][d1*d2] int32, sizes[m][d1] int32) for the C ABI."""
+    m = len(sols)
+    genes = np.zeros((m, cfg.d1 * cfg.d2), dtype=np.int32)
+    sizes = np.zeros((m, cfg.d1), dtype=np.int32)
+    for i, s in enumerate(sols):
+        genes[i] = s.data.reshape(-1)
+        sizes[i] = s.dim2_sizes
+    return genes, sizes
+
+
+def device_evaluate(problem: ProblemDefinition, sols, device: int = 0):
+    """Batch evaluate() on the device: objectives [m, 1], penalties [m]."""
+    cfg = problem.config()
+    lib = N.load()
+    h = problem.device_handle(device)
+    genes, sizes = pack_solutions(sols, cfg)
+    obj = np.zeros(len(sols), dtype=np.float64)
+    pen = np.zeros(len(sols), dtype=np.float64)
+    N.check(lib.go_eval_batch(h, N.iptr(genes), N.iptr(sizes), len(sols), N.dptr(obj),
+                              N.dptr(pen)))
+    return obj.reshape(-1, 1), pen
+
+
+def evaluate(problem: ProblemDefinition, sol: Solution, *, validate: bool = True):
+    """problems.py:77-94, evaluated on the device."""
+    cfg = problem.config()
+    if validate:
+        report = validate_solution(sol, cfg)
+        if not report.ok:
+            raise ValueError(f"refusing to evaluate invalid solution: {report.violations[:3]}")
+    obj, pen = device_evaluate(problem, [sol])
+    sol.objectives[:] = obj[0]
+    sol.penalty = float(pen[0])
+    if sol.penalty < 0:
+        raise ValueError(f"penalty must be nonnegative, got {sol.penalty}")
+    return sol.objectives, sol.penalty
+
+
+def evaluate_many(problem: ProblemDefinition, sols, device: int = 0):
+    """Evaluate a list of solutions in one device call (used by initialisation)."""
+    if not sols:
+        return
+    obj, pen = device_evaluate(problem, sols, device)
+    for s, o, p in zip(sols, obj, pen):
+        s.objectives[:] = o
+        s.penalty = float(p)
+
+
+class TspProblem(ProblemDefinition):
+    """builtins.py:53-77: cyclic tour length over a symmetric matrix."""
+
+    def __init__(self, dist):
+        self.dist = check_distance_matrix(dist)
+        self.n = self.dist.shape[0]
+        self._cfg = ProblemConfig(encoding=Encoding.permutation(), d1=1, d2=self.n, n=self.n,
+                                  row_mode=RowModeKind.SINGLE_SEQ,
+                                  obj_defs=(ObjDef("tour_length"),))
+
+    def config(self):
+        return self._cfg
+
+    def compute_penalty(self, sol):
+        return 0.0
+
+    def init_matrices(self):
+        return [self.dist]
+
+    def _native_desc(self):
+        d = N.f64(self.dist)
+        desc = N.ProblemDesc(kind=N.GO_TSP, n=self.n, d1=1, d2=self.n)
+        desc.dist = N.dptr(d)
+        return desc, (d,)
+
+
+def _need(instance: InstanceData, *names):
+    missing = [f for f in names if getattr(instance, f) is None]
+    if missing:
+        raise ValueError(f"instance payload missing fields: {', '.join(missing)}")
+
+
+def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
+    """builtins.py:42-50."""
+    if name not in BUILTIN_NAMES:
+        raise ValueError(f"unknown problem {name!r}; known problems: {', '.join(BUILTIN_NAMES)}")
+    if name == "tsp":
+        _need(instance, "distance_matrix")
+        return TspProblem(instance.distance_matrix)
+    raise NotImplementedError(
+        f"problem {name!r} has no B200 device path in this build "
+        f"(device problems: {', '.join(DEVICE_PROBLEMS)})")
