@@ -1,0 +1,340 @@
+"""Benchmark: move evaluations / s and % gap @30 s on the pcb442-shaped TSP
+(BASELINE.json metric; config C2: 26x17 lattice, known optimum 44,200, with
+the user-registered tsp-delta operators compiled by NVRTC).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W]          # our engine
+    python bench.py --impl reference [...]                         # CPU reference arm
+
+A step = one evolve chunk of --gens-per-step generations (one AOS interval)
+for the whole population, inputs resident in HBM; L2 is flushed (a 256 MiB
+write on the engine's stream) between timed steps.  `value` is device-timed
+(CUDA events on the engine stream, max over ranks); `e2e` is the same metric
+through the C ABI with host buffers (population H2D + run + population D2H
+per step).  Multi-GPU: one process per GPU, independent islands with
+disjoint Philox streams (weak scaling, no data-path collective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "move evals/sec and % gap @30s on TSP-442 shape at 1/2/4/8 B200 vs CPU ref"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), "measured", d
+    return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2603_19163_b200 as G
+    from paper_2603_19163_b200 import _native as N
+    from paper_2603_19163_b200 import instances as I
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl")
+    d, opt = I.tsp_lattice()
+    prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=d))
+    ops = G.tsp_delta_operators()
+    cfg = G.EngineConfig(team_size=args.team_size, seed=args.seed + 1000 * rank,
+                         custom_operators=ops, device=local,
+                         population=args.population or None,
+                         evolver_offset=rank * 1_000_000)
+    dr = G.DeviceRun(prob, cfg, cfg.seed)
+    P, T = dr.pop_size, cfg.team_size
+    gps = args.gens_per_step
+    stream = C.c_void_p()
+    N.check(dr.lib.go_engine_stream(dr.engine, C.byref(stream)))
+    tstream = torch.cuda.ExternalStream(stream.value, device=torch.device("cuda", local))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    done = 0
+    for _ in range(args.warmup):
+        done += gps
+        dr.run(done, None)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    dev_ms = evolve_ms = 0.0
+    launches = evolve_launches = reads_pos = reads_elem = 0
+    st = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(tstream):
+                flush.random_(0, 255)  # L2 flush outside the timed events
+            done += gps
+            st = dr.run(done, None)
+            dev_ms += st.device_ms
+            evolve_ms += st.evolve_ms
+            launches += st.kernel_launches
+            evolve_launches += st.evolve_launches
+            reads_pos += st.reads_pos
+            reads_elem += st.reads_elem
+    torch.cuda.synchronize()
+    gens_timed = args.steps * gps
+    evals_local = P * T * gens_timed
+    t_max = dev_ms
+    evals_all = evals_local
+    if world > 1:
+        tt = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+        ev = torch.tensor([evals_local], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(ev)
+        evals_all = float(ev.item())
+    value = evals_all / (t_max / 1e3)
+
+    # ---- e2e through the C ABI with host buffers -----------------------------
+    genes = np.zeros((P, dr.cfg.d2), dtype=np.int32)
+    sizes = np.zeros((P, 1), dtype=np.int32)
+    obj = np.zeros(P)
+    pen = np.zeros(P)
+    N.check(dr.lib.go_engine_get_population(dr.engine, N.iptr(genes), N.iptr(sizes),
+                                            N.dptr(obj), N.dptr(pen)))
+    if world > 1:
+        torch.distributed.barrier()
+    e2e_steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        N.check(dr.lib.go_engine_set_population(dr.engine, N.iptr(genes), N.iptr(sizes),
+                                                N.dptr(obj), N.dptr(pen)))
+        dr.run(gps, None)
+        N.check(dr.lib.go_engine_get_population(dr.engine, N.iptr(genes), N.iptr(sizes),
+                                                N.dptr(obj), N.dptr(pen)))
+    e2e_wall = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_wall], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_wall = float(tt.item())
+    e2e_value = world * P * T * gps * e2e_steps / e2e_wall
+    h2d = genes.nbytes + sizes.nbytes + obj.nbytes + pen.nbytes
+    dr.close()
+
+    # ---- % gap at the 30 s budget through the public run() ------------------------
+    gap = None
+    gap_info = {}
+    if args.gap_seconds > 0:
+        res = G.run(prob, G.EngineConfig(team_size=args.team_size, seed=args.seed + 7 * rank,
+                                         custom_operators=ops, device=local,
+                                         time_limit_seconds=args.gap_seconds,
+                                         max_generations=10 ** 9,
+                                         evolver_offset=rank * 1_000_000), best_known=opt)
+        gaps = [res.gap_pct]
+        if world > 1:
+            gt = torch.tensor([res.gap_pct], dtype=torch.float64, device=f"cuda:{local}")
+            allg = [torch.zeros_like(gt) for _ in range(world)]
+            torch.distributed.all_gather(allg, gt)
+            gaps = [float(x.item()) for x in allg]
+        gap = min(gaps)
+        gap_info = {"gap_pct_30s": gap, "gap_pct_30s_per_rank": gaps,
+                    "best_30s": res.objectives[0], "generations_30s": res.generations_completed,
+                    "move_evals_per_s_30s": res.device["lane_evals"] / res.elapsed_seconds,
+                    "elapsed_30s": res.elapsed_seconds}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    hbm, src, pk = peaks()
+    alg_bytes = reads_pos * 2 + reads_elem * (st.elem_bytes if st else 2)
+    achieved_gbs = alg_bytes / (evolve_ms / 1e3) / 1e9 if evolve_ms > 0 else 0.0
+    clocks = clk.summary()
+    info = N.device_info(local)
+    sm_mhz = clocks.get("sm_mhz") or pk.get("clocks_under_load", {}).get("sm_mhz_median", 1965.0)
+    smem_peak = info.sm_count * 128 * sm_mhz * 1e6 / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import cpu_bench
+        procs = cpu_cores() if args.cpu_procs == 0 else args.cpu_procs
+        cb = cpu_bench.throughput(d, procs, pop=8, team=128, gens=args.cpu_gens)
+        cpu = {"value": cb["value"], "unit": "move evals/s", "cores": procs, "kind": "port",
+               "sample": f"oracle engine (== reference run(), MT19937) on C2 with tsp-delta, full "
+                         f"reference registry: {procs} processes x P=8 x T=128 x "
+                         f"{args.cpu_gens} generations ({cb['evals']} evals in "
+                         f"{cb['wall_s']:.1f} s)"}
+    out = {
+        "metric": METRIC, "value": value, "unit": "move evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int16 genes / int16 distances, int64 deltas",
+        "data": "synthetic (seeded 26x17 lattice, permuted labels, TSPLIB nint)",
+        "config": {"workload": "C2 pcb442-shaped lattice TSP n=442 + user tsp-delta ops (NVRTC)",
+                   "population_per_gpu": P, "team_size": T, "generations_per_step": gps,
+                   "layout": "int16 packed triangle in shared memory",
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": f"islands x{world} (independent, disjoint streams)"},
+        "e2e": {"value": e2e_value, "unit": "move evals/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(h2d),
+                "path": "go_engine_set_population(host) + go_engine_run + "
+                        "go_engine_get_population(host) per step"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved_gbs / hbm, "traffic": None,
+                     "peak_source": src, "kernel": "go_evolve_tsp_jit",
+                     "evolve_ms": evolve_ms, "evolve_launches": int(evolve_launches),
+                     "algorithmic_bytes": int(alg_bytes),
+                     "note": "instance and solutions are shared-memory resident; see smem"},
+        "roofline_smem": {"achieved": achieved_gbs, "peak": smem_peak, "unit": "GB/s",
+                          "frac": achieved_gbs / smem_peak,
+                          "peak_formula": f"{info.sm_count} SM x 128 B/clk x {sm_mhz} MHz"},
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        **gap_info,
+    }
+    print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """The reference's own algorithm on the host cores: the oracle in MT mode
+    reproduces genopt.run() bit-for-bit (pinned by tests/golden)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import cpu_bench
+    from paper_2603_19163_b200 import instances as I
+    d, opt = I.tsp_lattice()
+    procs = cpu_cores() if args.cpu_procs == 0 else args.cpu_procs
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.warmup):
+        cpu_bench.throughput(d, procs, pop=4, team=128, gens=1)
+    for _ in range(args.steps):
+        vals.append(cpu_bench.throughput(d, procs, pop=8, team=128, gens=args.cpu_gens))
+    value = sum(v["evals"] for v in vals) / sum(v["wall_s"] for v in vals)
+    gap = {}
+    if args.gap_seconds > 0:
+        g = cpu_bench.gap_at(d, args.gap_seconds, procs, opt)
+        gap = {"gap_pct_30s": g["best_gap_pct"], "median_gap_pct_30s": g["median_gap_pct"],
+               "move_evals_per_s_30s": g["evals_per_s"]}
+    out = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "move evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(v["wall_s"] for v in vals) / max(1, len(vals)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded 26x17 lattice, permuted labels, TSPLIB nint)",
+        "config": {"workload": "C2 pcb442-shaped lattice TSP n=442 + user tsp-delta ops",
+                   "population_per_process": 8, "team_size": 128,
+                   "generations_per_step": args.cpu_gens},
+        "cpu_baseline": {"value": value, "unit": "move evals/s", "cores": procs, "kind": "port",
+                         "sample": f"{procs} processes x P=8 x T=128 x {args.cpu_gens} "
+                                   "generations per step, oracle MT mode == reference run()"},
+        "e2e": {"value": value, "unit": "move evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
+        **gap,
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gens-per-step", type=int, default=10)
+    ap.add_argument("--team-size", type=int, default=128)
+    ap.add_argument("--population", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--gap-seconds", type=float, default=30.0)
+    ap.add_argument("--cpu-gens", type=int, default=4)
+    ap.add_argument("--cpu-procs", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,12 @@ typedef struct go_run_stats {
   double device_ms;       /* CUDA-event time of the evolve+epilogue launches */
   int32_t stopped_by;     /* 0 max gens, 1 time, 2 target */
   int32_t error_flags;    /* sticky device error bits (custom-op misuse) */
+  int64_t reads_pos;      /* solution positions read by move evaluations */
+  int64_t reads_elem;     /* instance-matrix elements read by move evaluations */
+  int32_t elem_bytes;     /* bytes per matrix element in the chosen layout */
+  int32_t gene_bytes;     /* bytes per solution position (int16) */
+  double evolve_ms;       /* CUDA-event time of the evolve launches alone */
+  int64_t evolve_launches;
 } go_run_stats;
 
 /* ---- library / device ---------------------------------------------------- */

@@ -76,7 +76,10 @@ class EngineConfig(C.Structure):
 class RunStats(C.Structure):
     _fields_ = [("generations", C.c_int64), ("lane_evals", C.c_int64),
                 ("kernel_launches", C.c_int64), ("device_ms", C.c_double),
-                ("stopped_by", C.c_int32), ("error_flags", C.c_int32)]
+                ("stopped_by", C.c_int32), ("error_flags", C.c_int32),
+                ("reads_pos", C.c_int64), ("reads_elem", C.c_int64),
+                ("elem_bytes", C.c_int32), ("gene_bytes", C.c_int32),
+                ("evolve_ms", C.c_double), ("evolve_launches", C.c_int64)]
 
 
 _lib = None

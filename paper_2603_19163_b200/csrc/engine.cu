@@ -178,6 +178,8 @@ struct go_engine {
   int teams_per_sm = 0;
   static const int kDepth = 8;
   cudaEvent_t ring_ev[kDepth] = {};
+  cudaEvent_t k_beg[kDepth] = {}, k_end[kDepth] = {};  // evolve-kernel-only timing
+  bool k_pending[kDepth] = {};
   cudaEvent_t t_start = nullptr, t_stop = nullptr;
   long long launches = 0;
 };
@@ -639,6 +641,8 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   *e->h_stop = 0;
   CK(cudaHostGetDevicePointer((void**)&e->d_stop_map, e->h_stop, 0));
   for (auto& ev : e->ring_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  for (auto& ev : e->k_beg) CK(cudaEventCreate(&ev));
+  for (auto& ev : e->k_end) CK(cudaEventCreate(&ev));
   CK(cudaEventCreate(&e->t_start));
   CK(cudaEventCreate(&e->t_stop));
   go::GlobalState gs{};
@@ -662,6 +666,10 @@ int go_engine_destroy(go_engine* e) {
   if (e->h_stop) cudaFreeHost(e->h_stop);
   for (auto& ev : e->ring_ev)
     if (ev) cudaEventDestroy(ev);
+  for (int i = 0; i < go_engine::kDepth; ++i) {
+    if (e->k_beg[i]) cudaEventDestroy(e->k_beg[i]);
+    if (e->k_end[i]) cudaEventDestroy(e->k_end[i]);
+  }
   if (e->t_start) cudaEventDestroy(e->t_start);
   if (e->t_stop) cudaEventDestroy(e->t_stop);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -767,6 +775,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   go::GlobalState gs{};
   CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
   long long done = gs.gens_done;
+  const unsigned long long rp0 = gs.rd_pos, re0 = gs.rd_elem;
   if (gs.stop) {  // a previous run stopped; resume from the same state
     gs.stop = 0;
     *e->h_stop = 0;
@@ -858,6 +867,14 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   q.seed = c.seed;
   q.max_gens = max_generations;
 
+  double evolve_ms = 0.0;
+  long long evolve_launches = 0;
+  auto harvest = [&](int s) {
+    if (!e->k_pending[s]) return;
+    float kms = 0.f;
+    if (cudaEventElapsedTime(&kms, e->k_beg[s], e->k_end[s]) == cudaSuccess) evolve_ms += kms;
+    e->k_pending[s] = false;
+  };
   while (done < max_generations) {
     if (*(volatile int*)e->h_stop) break;
     long long end = std::min<long long>(max_generations, done + go::MAX_CHUNK);
@@ -867,6 +884,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     const int slot = (int)(chunk % go_engine::kDepth);
     if (chunk >= go_engine::kDepth) {
       CK(cudaEventSynchronize(e->ring_ev[slot]));
+      harvest(slot);
       if (*(volatile int*)e->h_stop) break;
     }
     double* ht = e->h_temps + (size_t)slot * go::MAX_CHUNK;
@@ -878,9 +896,13 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     a.gen0 = done + 1;
     a.ngen = (int)(end - done);
     void* args[] = {&a};
+    CK(cudaEventRecord(e->k_beg[slot], e->stream));
     int rc = launch_static_or_jit(e->k_evolve, e->k_evolve_jit, dim3(e->grid), dim3(e->E * e->TS),
                                   e->smem, e->stream, args);
     if (rc) return rc;
+    CK(cudaEventRecord(e->k_end[slot], e->stream));
+    e->k_pending[slot] = true;
+    ++evolve_launches;
     q.gen0 = a.gen0;
     q.ngen = a.ngen;
     go::go_epilogue_kernel<<<1, go::EPI_THREADS, 0, e->stream>>>(q);
@@ -892,6 +914,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   }
   CK(cudaEventRecord(e->t_stop, e->stream));
   CK(cudaStreamSynchronize(e->stream));
+  for (int s = 0; s < go_engine::kDepth; ++s) harvest(s);
   CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, e->t_start, e->t_stop));
@@ -903,6 +926,12 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     stats->device_ms = ms;
     stats->stopped_by = gs.stop == 1 ? 1 : (gs.stop == 2 ? 2 : 0);
     stats->error_flags = gs.err;
+    stats->reads_pos = (int64_t)(gs.rd_pos - rp0);
+    stats->reads_elem = (int64_t)(gs.rd_elem - re0);
+    stats->elem_bytes = (int32_t)elem_size(kLayouts[e->layout].elem);
+    stats->gene_bytes = 2;
+    stats->evolve_ms = evolve_ms;
+    stats->evolve_launches = evolve_launches;
   }
   return GO_OK;
 }

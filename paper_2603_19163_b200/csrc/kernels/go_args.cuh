@@ -30,6 +30,8 @@ struct GlobalState {
   int stop;               // 0 run, 1 time, 2 target, 3 max generations
   int err;                // sticky device error bits
   long long hist_count;
+  unsigned long long rd_pos;   // positions read by move evaluations (all lanes)
+  unsigned long long rd_elem;  // matrix elements read by move evaluations
 };
 
 struct EvolveArgs {

@@ -175,6 +175,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   const double* kw = s_misc;
   const double total = s_misc[3];
   int err = 0;
+  unsigned long long rd_pos = 0, rd_elem = 0;
 
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
@@ -193,6 +194,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       c.L = &L;
       c.pol = &pol;
       c.err = 0;
+      c.rd_pos = 0;
+      c.rd_elem = 0;
       k = sample_k(kw, rng);
       for (int s = 0; s < k; ++s) {
         const int si = sample_seq(s_cum, nseq, total, rng);
@@ -200,11 +203,13 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         c.out.kind = MV_NONE;
         run_perm_op<Policy, Custom>(s_kind[si], c);
         if (c.out.kind != MV_NONE) {
-          delta += pol.delta(L, c.out);
+          delta += pol.delta(L, c.out, c.rd_pos, c.rd_elem);
           L.push(c.out);
         }
       }
       err |= c.err;
+      rd_pos += c.rd_pos;
+      rd_elem += c.rd_elem;
     }
 
     // ---- team argmin over (delta, lane) ----------------------------------
@@ -301,6 +306,15 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     A.best_pen[ev] = bpen;
   }
   if (err) atomicOr(&A.gs->err, err);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    rd_pos += __shfl_xor_sync(0xffffffffu, rd_pos, off);
+    rd_elem += __shfl_xor_sync(0xffffffffu, rd_elem, off);
+  }
+  if ((lane & 31) == 0) {
+    atomicAdd(&A.gs->rd_pos, rd_pos);
+    atomicAdd(&A.gs->rd_elem, rd_elem);
+  }
 }
 
 }  // namespace go

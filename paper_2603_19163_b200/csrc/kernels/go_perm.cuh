@@ -122,11 +122,14 @@ __device__ __forceinline__ void move_slots(const Move& mv, int n, int* so, int& 
 // Φ(cand after mv) − Φ(cand) for the cyclic tour objective (builtins.py:67-71)
 template <class D>
 __device__ __forceinline__ typename D::Acc tsp_move_delta(const D& d, const Chain& L,
-                                                          const Move& mv) {
+                                                          const Move& mv, unsigned& rd_pos,
+                                                          unsigned& rd_elem) {
   typedef typename D::Acc Acc;
   const int n = L.n;
   int so[4], sn[4], no, nn;
   move_slots(mv, n, so, no, sn, nn);
+  rd_pos += 2 * (no + nn);
+  rd_elem += no + nn;
   Acc delta = 0;
   for (int i = 0; i < no; ++i) {
     const int p = so[i], q = p + 1 == n ? 0 : p + 1;
@@ -154,6 +157,7 @@ struct PermCtx {
   const Policy* pol;
   Move out;
   int err;
+  unsigned rd_pos, rd_elem;  // algorithmic reads (roofline accounting)
 
   __device__ __forceinline__ int size() const { return L->n; }
   __device__ __forceinline__ int at(int p) {
@@ -161,6 +165,7 @@ struct PermCtx {
       err |= ERR_OP_RANGE;
       return 0;
     }
+    ++rd_pos;
     return L->at(p);
   }
   __device__ __forceinline__ double dist(int a, int b) {
@@ -168,6 +173,7 @@ struct PermCtx {
       err |= ERR_OP_RANGE;
       return 0.0;
     }
+    ++rd_elem;
     return pol->cost(a, b);
   }
   __device__ __forceinline__ double random() { return rng->random(); }
@@ -262,8 +268,9 @@ struct TspPolicy {
   D d;
   __device__ __forceinline__ int n_items() const { return d.n; }
   __device__ __forceinline__ double cost(int a, int b) const { return (double)d(a, b); }
-  __device__ __forceinline__ Acc delta(const Chain& L, const Move& mv) const {
-    return tsp_move_delta(d, L, mv);
+  __device__ __forceinline__ Acc delta(const Chain& L, const Move& mv, unsigned& rp,
+                                       unsigned& re) const {
+    return tsp_move_delta(d, L, mv, rp, re);
   }
   // full tour length partial sum over slots [lo, hi) step `step` (team reduce)
   __device__ __forceinline__ Acc partial(const i16* t, int n, int lo, int step) const {

@@ -61,7 +61,8 @@ __device__ __forceinline__ void tsp_delta_entry(const void* inst, int n, const s
       m.b = mv[2];
       m.c = mv[3];
       if (m.kind == MV_NONE) continue;
-      d += pol.delta(L, m);
+      unsigned rp = 0, re = 0;
+      d += pol.delta(L, m, rp, re);
       L.push(m);
     }
     delta[blockIdx.x] = (double)d;
@@ -95,6 +96,8 @@ __device__ __forceinline__ void tsp_probe_entry(const void* inst, int n, int kin
     c.L = &L;
     c.pol = &pol;
     c.err = 0;
+    c.rd_pos = 0;
+    c.rd_elem = 0;
     c.out.kind = MV_NONE;
     run_perm_op<TspPolicy<D>, Custom>(kind, c);
     if (c.out.kind != MV_NONE) L.push(c.out);
