@@ -118,15 +118,16 @@ int query_device(int dev, DeviceInfo* di) {
   return GO_OK;
 }
 
-unsigned team_bytes_for(int elem, int n) {
-  return elem == E_F64 ? go::PermSmem::team_bytes<double>(n) : go::PermSmem::team_bytes<long long>(n);
+unsigned team_bytes_for(int elem, int n, int TS) {
+  return elem == E_F64 ? go::PermSmem::team_bytes<double>(n, TS)
+                       : go::PermSmem::team_bytes<long long>(n, TS);
 }
 
 // smem bytes needed by one CTA with E teams for a given layout
-size_t cta_smem(int layout, int n, int E, size_t inst_img_bytes) {
+size_t cta_smem(int layout, int n, int E, int TS, size_t inst_img_bytes) {
   const LayoutInfo& L = kLayouts[layout];
   const unsigned inst = L.global ? 0u : pad16(inst_img_bytes);
-  return go::PermSmem::team_off(inst) + (size_t)E * team_bytes_for(L.elem, n);
+  return go::PermSmem::team_off(inst) + (size_t)E * team_bytes_for(L.elem, n, TS);
 }
 
 }  // namespace
@@ -306,10 +307,9 @@ void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_o
   const int Emax = std::max(1, std::min(8, 512 / TS));
   const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
   const int full = p->elem * 2, tri = p->elem * 2 + 1;
-  for (int E = E0; E >= 1; E = E / 2) {
-    if (cta_smem(full, n, E, p->full_bytes) <= optin) { *layout = full; *E_out = E; return; }
-    if (n >= 2 && cta_smem(tri, n, E, p->tri_bytes) <= optin) { *layout = tri; *E_out = E; return; }
-    if (E == 1) break;
+  for (int E = E0; E >= 1; --E) {
+    if (cta_smem(full, n, E, TS, p->full_bytes) <= optin) { *layout = full; *E_out = E; return; }
+    if (n >= 2 && cta_smem(tri, n, E, TS, p->tri_bytes) <= optin) { *layout = tri; *E_out = E; return; }
   }
   *layout = global_layout(p->elem);
   *E_out = E0;
@@ -378,7 +378,7 @@ int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_
   const int TS = (team_size + 31) / 32 * 32;
   int L = 0, E = 0;
   choose_layout(p, TS, teams_per_cta, &L, &E);
-  const size_t smem = cta_smem(L, p->n, E, inst_img_bytes(p, L));
+  const size_t smem = cta_smem(L, p->n, E, TS, inst_img_bytes(p, L));
   CK(cudaFuncSetAttribute(kLayouts[L].evolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   int blocks = 0;
@@ -592,7 +592,7 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   const LayoutInfo& L = kLayouts[e->layout];
   e->inst = inst_ptr(p, e->layout);
   e->inst_bytes = L.global ? 0u : pad16(inst_img_bytes(p, e->layout));
-  e->smem = cta_smem(e->layout, e->n, e->E, inst_img_bytes(p, e->layout));
+  e->smem = cta_smem(e->layout, e->n, e->E, e->TS, inst_img_bytes(p, e->layout));
   e->grid = (e->P + e->E - 1) / e->E;
   if (!p->ops.empty()) {
     gohost::JitModule* m = nullptr;
@@ -680,8 +680,8 @@ int go_engine_destroy(go_engine* e) {
 int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const double* weights,
                            const double* floors, const double* caps, double total,
                            const double* k_weights) {
-  if (!e || nseq < 1 || nseq > 32 || !ids || !weights || !k_weights)
-    return fail(GO_E_INVALID, "registry needs 1..32 sequences");
+  if (!e || nseq < 1 || nseq > 31 || !ids || !weights || !k_weights)
+    return fail(GO_E_INVALID, "registry needs 1..31 sequences");
   go::RegistryDev r{};
   r.nseq = nseq;
   double acc = 0.0;
@@ -823,7 +823,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.E = e->E;
   a.ev_offset = c.evolver_offset;
   a.team_stride = e->TS;
-  a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n);
+  a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
   a.resync = kLayouts[e->layout].elem == E_F64;
   go::EpilogueArgs q{};
   q.P = e->P;

@@ -122,6 +122,18 @@ struct Stream {
     return (int)r;
   }
   __device__ __forceinline__ int randrange(int lo, int hi) { return lo + randbelow(hi - lo); }
+  // words consumed so far / resume at a word position (lane state hand-off)
+  __device__ __forceinline__ u32 tell() const { return ctr * 4u - (u32)avail; }
+  __device__ __forceinline__ void seek(u32 pos) {
+    ctr = pos >> 2;
+    avail = 0;
+    const int off = (int)(pos & 3u);
+    if (off) {
+      philox_block(ctr++, k0, k1, w0, w1, w2, w3);
+      avail = 4;
+      for (int i = 0; i < off; ++i) word();
+    }
+  }
 };
 
 // ---- barriers -------------------------------------------------------------

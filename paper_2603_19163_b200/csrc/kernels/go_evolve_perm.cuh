@@ -45,7 +45,47 @@ struct TeamShared {
   int impr[MAX_SEQ];
   int k_usage[3];
   int k_impr[3];
+  unsigned char cnt[16][MAX_SEQ];  // per-warp lane counts per sequence (lane sort)
 };
+
+// Per logical lane state handed between threads across chain steps
+// (structure of arrays after TeamShared; TS = lanes rounded up to 32).
+template <class Acc>
+struct LaneArrays {
+  u64* mv;         // [3][TS] packed moves
+  Acc* delta;      // [TS]
+  u32* pos;        // [TS] stream words consumed
+  u32* meta;       // [TS] k | nm | sq0 | sq1 | sq2
+  unsigned short* order;  // [TS] thread slot -> logical lane
+  static __host__ __device__ unsigned bytes(int TS) {
+    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2));
+  }
+  __device__ __forceinline__ void bind(unsigned char* p, int TS) {
+    mv = (u64*)p;
+    delta = (Acc*)(p + 3 * 8 * TS);
+    pos = (u32*)(p + (3 * 8 + sizeof(Acc)) * TS);
+    meta = pos + TS;
+    order = (unsigned short*)(meta + TS);
+  }
+};
+
+__device__ __forceinline__ u64 pack_move(const Move& m) {
+  return (u64)m.kind | ((u64)(u32)m.a << 2) | ((u64)(u32)m.b << 22) | ((u64)(u32)m.c << 42);
+}
+__device__ __forceinline__ Move unpack_move(u64 v) {
+  Move m;
+  m.kind = (int)(v & 3u);
+  m.a = (int)((v >> 2) & 0xFFFFFu);
+  m.b = (int)((v >> 22) & 0xFFFFFu);
+  m.c = (int)((v >> 42) & 0xFFFFFu);
+  return m;
+}
+__device__ __forceinline__ u32 pack_meta(int k, int nm, int q0, int q1, int q2) {
+  return (u32)k | ((u32)nm << 2) | ((u32)q0 << 4) | ((u32)q1 << 9) | ((u32)q2 << 14);
+}
+__device__ __forceinline__ int meta_k(u32 m) { return (int)(m & 3u); }
+__device__ __forceinline__ int meta_nm(u32 m) { return (int)((m >> 2) & 3u); }
+__device__ __forceinline__ int meta_sq(u32 m, int s) { return (int)((m >> (4 + 5 * s)) & 31u); }
 
 // sample_k (aos.py:147-154)
 __device__ __forceinline__ int sample_k(const double* kw, Stream& r) {
@@ -102,12 +142,18 @@ struct PermSmem {
   static __host__ __device__ unsigned inst_off() { return 0; }
   static __host__ __device__ unsigned reg_off(unsigned inst_bytes) { return align(inst_bytes, 128); }
   static __host__ __device__ unsigned team_off(unsigned inst_bytes) {
-    return reg_off(inst_bytes) + 640;
+    return reg_off(inst_bytes) + 768;
   }
   static __host__ __device__ unsigned row_bytes(int n) { return align(2u * n, 16); }
   template <class Acc>
-  static __host__ __device__ unsigned team_bytes(int n) {
-    return align(2 * row_bytes(n) + (unsigned)sizeof(TeamShared<Acc>), 16);
+  static __host__ __device__ unsigned shared_off(int n) { return 2 * row_bytes(n); }
+  template <class Acc>
+  static __host__ __device__ unsigned lanes_off(int n) {
+    return align(shared_off<Acc>(n) + (unsigned)sizeof(TeamShared<Acc>), 16);
+  }
+  template <class Acc>
+  static __host__ __device__ unsigned team_bytes(int n, int TS) {
+    return align(lanes_off<Acc>(n) + LaneArrays<Acc>::bytes(TS), 16);
   }
 };
 
@@ -120,9 +166,11 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   // ---- stage the instance and the registry --------------------------------
   const unsigned ro = PermSmem::reg_off(A.inst_bytes);
   u64* mbar = (u64*)(sm + ro);
-  double* s_cum = (double*)(sm + ro + 16);       // 32 doubles
-  double* s_misc = s_cum + 32;                    // kw[3], total
-  int* s_kind = (int*)(s_misc + 4);               // 32 ints
+  double* s_cum = (double*)(sm + ro + 16);  // 32 doubles
+  double* s_misc = s_cum + 32;               // kw[3], total
+  int* s_kind = (int*)(s_misc + 4);          // 32 ints: implementation per registry index
+  int* s_gord = s_kind + 32;                 // 32 ints: registry indices in sort order
+  int* s_grank = s_gord + 32;                // 32 ints: sort position of a registry index
   if (A.inst_bytes) {
     stage_to_smem(sm, A.inst, A.inst_bytes, mbar);
     pol.d.m = (const typename decltype(pol.d)::Elem*)sm;
@@ -135,10 +183,20 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   }
   if (threadIdx.x < 3) s_misc[threadIdx.x] = R->kw[threadIdx.x];
   if (threadIdx.x == 3) s_misc[3] = R->total;
+  if (threadIdx.x == 32) {  // lane-sort order: user operators first (long loops), then built-ins
+    int j = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i < nseq; ++i)
+        if ((R->kind[i] >= SEQ_CUSTOM_BASE) == (pass == 0)) {
+          s_gord[j] = i;
+          s_grank[i] = j++;
+        }
+  }
   __syncthreads();
 
   const int TS = A.team_stride, T = A.T, n = A.n;
   const int team = threadIdx.x / TS, lane = threadIdx.x - team * TS;
+  const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
   const int ev = blockIdx.x * A.E + team;
   if (ev >= A.P) return;  // idle team slot; no CTA-wide barrier follows
   const long long evg = (long long)A.ev_offset + ev;
@@ -146,7 +204,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   unsigned char* tb = sm + PermSmem::team_off(A.inst_bytes) + team * A.team_smem;
   i16* cur = (i16*)tb;
   i16* nxt = (i16*)(tb + PermSmem::row_bytes(n));
-  TeamShared<Acc>* ts = (TeamShared<Acc>*)(tb + 2 * PermSmem::row_bytes(n));
+  TeamShared<Acc>* ts = (TeamShared<Acc>*)(tb + PermSmem::shared_off<Acc>(n));
+  LaneArrays<Acc> la;
+  la.bind(tb + PermSmem::lanes_off<Acc>(n), TS);
 
   for (int p = lane; p < n; p += TS) cur[p] = A.genes[(size_t)ev * n + p];
   for (int i = lane; i < MAX_SEQ; i += TS) {
@@ -164,16 +224,17 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     Acc part = pol.partial(cur, n, lane, TS);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-    if ((lane & 31) == 0) ts->wd[lane >> 5] = part;
+    if (wl == 0) ts->wd[warp] = part;
     team_bar(team, TS);
     Acc tot = 0;
-    for (int w = 0; w < TS / 32; ++w) tot += ts->wd[w];
+    for (int w = 0; w < nwarps; ++w) tot += ts->wd[w];
     phi = (double)tot;
     team_bar(team, TS);
   }
   double bscal = A.best_scal[ev], bpen = A.best_pen[ev];
   const double* kw = s_misc;
   const double total = s_misc[3];
+  const unsigned lt_mask = (1u << wl) - 1u;
   int err = 0;
   unsigned long long rd_pos = 0, rd_elem = 0;
 
@@ -181,64 +242,112 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
 
-    // ---- lanes: sample, move, delta --------------------------------------
-    Acc delta = 0;
-    int k = 0, sq0 = 0, sq1 = 0, sq2 = 0;
-    Chain L;
-    L.reset(cur, n);
+    // ---- A: every lane draws k and its first sequence (identity mapping) ----
+    int hold_lane = -1, hold_seq = 31;  // 31 = no work
     if (lane < T) {
       Stream rng;
       rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)lane, 0));
-      PermCtx<Policy> c;
-      c.rng = &rng;
-      c.L = &L;
-      c.pol = &pol;
-      c.err = 0;
-      c.rd_pos = 0;
-      c.rd_elem = 0;
-      k = sample_k(kw, rng);
-      for (int s = 0; s < k; ++s) {
-        const int si = sample_seq(s_cum, nseq, total, rng);
-        if (s == 0) sq0 = si; else if (s == 1) sq1 = si; else sq2 = si;
-        c.out.kind = MV_NONE;
-        run_perm_op<Policy, Custom>(s_kind[si], c);
-        if (c.out.kind != MV_NONE) {
-          delta += pol.delta(L, c.out, c.rd_pos, c.rd_elem);
-          L.push(c.out);
-        }
-      }
-      err |= c.err;
-      rd_pos += c.rd_pos;
-      rd_elem += c.rd_elem;
+      const int k = sample_k(kw, rng);
+      const int s0 = sample_seq(s_cum, nseq, total, rng);
+      la.pos[lane] = rng.tell();
+      la.meta[lane] = pack_meta(k, 0, s0, 0, 0);
+      la.delta[lane] = (Acc)0;
+      hold_lane = lane;
+      hold_seq = s0;
     }
 
-    // ---- team argmin over (delta, lane) ----------------------------------
-    Acc bd = lane < T ? delta : AccMax<Acc>::value();  // padding lanes never win
+    // ---- B: chain steps; lanes are regrouped by sequence before each step so
+    //      a warp runs one operator at a time (counting sort over <= 32 ids) ----
+    for (int s = 0; s < MAX_CHAIN; ++s) {
+      const unsigned grp = __match_any_sync(0xffffffffu, hold_seq);
+      const int rank = __popc(grp & lt_mask);
+      ts->cnt[warp][wl] = 0;
+      __syncwarp();
+      if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
+      team_bar(team, TS);
+      // exclusive scan of per-sequence totals in sort order (each warp redundantly)
+      int tj = 0;
+      if (wl < nseq) {
+        const int q = s_gord[wl];
+        for (int w = 0; w < nwarps; ++w) tj += ts->cnt[w][q];
+      }
+      int incl = tj;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (wl >= off) incl += v;
+      }
+      const int active = __shfl_sync(0xffffffffu, incl, 31);
+      const int my_pos = hold_seq != 31 ? s_grank[hold_seq] : 0;
+      int base = __shfl_sync(0xffffffffu, incl - tj, my_pos);
+      if (hold_seq != 31) {
+        for (int w = 0; w < warp; ++w) base += ts->cnt[w][hold_seq];
+        la.order[base + rank] = (unsigned short)hold_lane;
+      }
+      team_bar(team, TS);
+      if (active == 0) break;  // uniform
+
+      hold_lane = -1;
+      hold_seq = 31;
+      if (lane < active) {
+        const int L = la.order[lane];
+        Stream rng;
+        rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+        rng.seek(la.pos[L]);
+        const u32 meta = la.meta[L];
+        const int k = meta_k(meta);
+        int nm = meta_nm(meta);
+        int q[3] = {meta_sq(meta, 0), meta_sq(meta, 1), meta_sq(meta, 2)};
+        Chain C;
+        C.reset(cur, n);
+        for (int i = 0; i < nm; ++i) C.push(unpack_move(la.mv[i * TS + L]));
+        Acc d = la.delta[L];
+        PermCtx<Policy> c;
+        c.rng = &rng;
+        c.L = &C;
+        c.pol = &pol;
+        c.err = 0;
+        c.rd_pos = 0;
+        c.rd_elem = 0;
+        c.out.kind = MV_NONE;
+        run_perm_op<Policy, Custom>(s_kind[q[s]], c);
+        if (c.out.kind != MV_NONE) {
+          d += pol.delta(C, c.out, c.rd_pos, c.rd_elem);
+          la.mv[nm * TS + L] = pack_move(c.out);
+          ++nm;
+        }
+        err |= c.err;
+        rd_pos += c.rd_pos;
+        rd_elem += c.rd_elem;
+        if (s + 1 < k) {
+          q[s + 1] = sample_seq(s_cum, nseq, total, rng);
+          hold_lane = L;
+          hold_seq = q[s + 1];
+        }
+        la.pos[L] = rng.tell();
+        la.meta[L] = pack_meta(k, nm, q[0], q[1], q[2]);
+        la.delta[L] = d;
+      }
+    }
+    team_bar(team, TS);
+
+    // ---- C: team argmin over (delta, lane) -------------------------------------
+    Acc bd = lane < T ? la.delta[lane] : AccMax<Acc>::value();  // padding lanes never win
     int bl = lane < T ? lane : 0x7fffffff;
     argmin_warp(bd, bl);
-    if ((lane & 31) == 0) {
-      ts->wd[lane >> 5] = bd;
-      ts->wl[lane >> 5] = bl;
+    if (wl == 0) {
+      ts->wd[warp] = bd;
+      ts->wl[warp] = bl;
     }
     team_bar(team, TS);
     bd = ts->wd[0];
     bl = ts->wl[0];
-    for (int w = 1; w < TS / 32; ++w) {
+    for (int w = 1; w < nwarps; ++w) {
       const Acc od = ts->wd[w];
       if (od < bd) {  // warps are in lane order: ties keep the lower lane
         bd = od;
         bl = ts->wl[w];
       }
-    }
-    if (lane == bl) {
-      ts->nm = L.nm;
-      ts->chain[0] = L.m0;
-      ts->chain[1] = L.m1;
-      ts->chain[2] = L.m2;
-      ts->k = k;
-      ts->sq[0] = sq0;
-      ts->sq[1] = sq1;
-      ts->sq[2] = sq2;
     }
     const double bdd = (double)bd;
     if (lane == 0) {
@@ -249,27 +358,27 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         acc = ar.random() < exp(-bdd / temp);
       }
       ts->accept = acc;
+      if (acc) {
+        const u32 meta = la.meta[bl];
+        const int kk = meta_k(meta);
+        const int improved = bdd < 0.0;
+        for (int s = 0; s < kk; ++s) {
+          const int si = meta_sq(meta, s);
+          ts->usage[si] += 1;
+          ts->impr[si] += improved;
+        }
+        ts->k_usage[kk - 1] += 1;
+        ts->k_impr[kk - 1] += improved;
+      }
     }
     team_bar(team, TS);
 
     if (ts->accept) {
       Chain W;
       W.reset(cur, n);
-      W.nm = ts->nm;
-      W.m0 = ts->chain[0];
-      W.m1 = ts->chain[1];
-      W.m2 = ts->chain[2];
+      const int nm = meta_nm(la.meta[bl]);
+      for (int i = 0; i < nm; ++i) W.push(unpack_move(la.mv[i * TS + bl]));
       for (int p = lane; p < n; p += TS) nxt[p] = cur[W.src_all(p)];
-      if (lane == 0) {
-        const int improved = bdd < 0.0;
-        const int kk = ts->k;
-        for (int s = 0; s < kk; ++s) {
-          ts->usage[ts->sq[s]] += 1;
-          ts->impr[ts->sq[s]] += improved;
-        }
-        ts->k_usage[kk - 1] += 1;
-        ts->k_impr[kk - 1] += improved;
-      }
       team_bar(team, TS);
       i16* t = cur;
       cur = nxt;
@@ -311,7 +420,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     rd_pos += __shfl_xor_sync(0xffffffffu, rd_pos, off);
     rd_elem += __shfl_xor_sync(0xffffffffu, rd_elem, off);
   }
-  if ((lane & 31) == 0) {
+  if (wl == 0) {
     atomicAdd(&A.gs->rd_pos, rd_pos);
     atomicAdd(&A.gs->rd_elem, rd_elem);
   }
