@@ -213,7 +213,10 @@ def run_ours(args):
         gap_info = {"gap_pct_30s": gap, "gap_pct_30s_per_rank": gaps,
                     "best_30s": res.objectives[0], "generations_30s": res.generations_completed,
                     "move_evals_per_s_30s": res.device["lane_evals"] / res.elapsed_seconds,
-                    "elapsed_30s": res.elapsed_seconds}
+                    "elapsed_30s": res.elapsed_seconds,
+                    "final_weights_30s": {e["name"]: round(e["weight"], 4)
+                                          for e in res.final_weights["sequences"]},
+                    "k_weights_30s": [round(x, 4) for x in res.final_weights["k_steps"]]}
 
     if rank != 0:
         if world > 1:

@@ -25,6 +25,32 @@ template <> struct AccOf<double> { typedef double T; };
 template <class E> struct ValOf { typedef int T; };
 template <> struct ValOf<double> { typedef double T; };
 
+// Explicit shared-space loads: the staged instance pointer travels through
+// operator contexts, where the compiler can no longer prove it is shared and
+// would emit generic LD instead of LDS.
+template <class E> struct LdShared;
+template <> struct LdShared<short> {
+  __device__ __forceinline__ static int load(unsigned addr) {
+    short v;
+    asm("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return (int)v;
+  }
+};
+template <> struct LdShared<int> {
+  __device__ __forceinline__ static int load(unsigned addr) {
+    int v;
+    asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+  }
+};
+template <> struct LdShared<double> {
+  __device__ __forceinline__ static double load(unsigned addr) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+  }
+};
+
 // row-major n x n
 template <class E, bool GLOBAL>
 struct MatFull {
@@ -35,8 +61,11 @@ struct MatFull {
   static constexpr bool kInSmem = !GLOBAL;
   const E* __restrict__ m;
   int n;
+  unsigned sbase;  // shared-space address of m (shared layouts, set when staged)
+  int use_s;       // 1: read through ld.shared at sbase
   __device__ __forceinline__ Val operator()(int a, int b) const {
     if (GLOBAL) return (Val)__ldg(m + a * n + b);
+    if (use_s) return (Val)LdShared<E>::load(sbase + (unsigned)(a * n + b) * (unsigned)sizeof(E));
     return (Val)m[a * n + b];
   }
   static __host__ __device__ long long bytes(int n) { return (long long)n * n * sizeof(E); }
@@ -52,10 +81,16 @@ struct MatTri {
   static constexpr bool kInSmem = true;
   const E* __restrict__ m;
   int n;
+  unsigned sbase;  // shared-space address of m (set when staged)
+  int use_s;       // 1: read through ld.shared at sbase
   __device__ __forceinline__ Val operator()(int a, int b) const {
-    if (a == b) return (Val)0;
     const int lo = a < b ? a : b, hi = a ^ b ^ lo;
-    return (Val)m[((lo * (2 * n - lo - 1)) >> 1) + (hi - lo - 1)];
+    // a == b would index slot "-1" of its row; read slot 0 and discard it
+    const int idx = ((lo * (2 * n - lo - 1)) >> 1) + (hi - lo - 1);
+    Val v;
+    if (use_s) v = (Val)LdShared<E>::load(sbase + (unsigned)(a == b ? 0 : idx) * (unsigned)sizeof(E));
+    else v = (Val)m[a == b ? 0 : idx];
+    return a == b ? (Val)0 : v;
   }
   static __host__ __device__ long long bytes(int n) {
     return (long long)n * (n - 1) / 2 * sizeof(E);

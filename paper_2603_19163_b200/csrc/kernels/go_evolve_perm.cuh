@@ -174,6 +174,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   if (A.inst_bytes) {
     stage_to_smem(sm, A.inst, A.inst_bytes, mbar);
     pol.d.m = (const typename decltype(pol.d)::Elem*)sm;
+    pol.d.sbase = smem_u32(sm);
+    pol.d.use_s = 1;
   }
   const RegistryDev* R = A.reg;
   const int nseq = R->nseq;

@@ -160,21 +160,20 @@ struct PermCtx {
   unsigned rd_pos, rd_elem;  // algorithmic reads (roofline accounting)
 
   __device__ __forceinline__ int size() const { return L->n; }
+  // branch-free range checks: an out-of-range index reads element 0 and
+  // raises the sticky error bit (probe exclusion), never faults
   __device__ __forceinline__ int at(int p) {
-    if ((unsigned)p >= (unsigned)L->n) {
-      err |= ERR_OP_RANGE;
-      return 0;
-    }
+    const bool ok = (unsigned)p < (unsigned)L->n;
+    err |= ok ? 0 : ERR_OP_RANGE;
     ++rd_pos;
-    return L->at(p);
+    return L->at(ok ? p : 0);
   }
   __device__ __forceinline__ double dist(int a, int b) {
-    if ((unsigned)a >= (unsigned)pol->n_items() || (unsigned)b >= (unsigned)pol->n_items()) {
-      err |= ERR_OP_RANGE;
-      return 0.0;
-    }
+    const unsigned ni = (unsigned)pol->n_items();
+    const bool ok = (unsigned)a < ni && (unsigned)b < ni;
+    err |= ok ? 0 : ERR_OP_RANGE;
     ++rd_elem;
-    return pol->cost(a, b);
+    return pol->cost(ok ? a : 0, ok ? b : 0);
   }
   __device__ __forceinline__ double random() { return rng->random(); }
   __device__ __forceinline__ int randbelow(int n) {

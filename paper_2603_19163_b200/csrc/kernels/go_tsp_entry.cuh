@@ -11,6 +11,8 @@ __device__ __forceinline__ void tsp_evolve_entry(const EvolveArgs& a) {
   TspPolicy<D> pol;
   pol.d.m = (const typename D::Elem*)a.inst;
   pol.d.n = a.n;
+  pol.d.sbase = 0;
+  pol.d.use_s = 0;
   evolve_perm<TspPolicy<D>, Custom>(a, pol);
 }
 
@@ -23,6 +25,8 @@ __device__ __forceinline__ void tsp_eval_entry(const void* inst, int n, const sh
   TspPolicy<D> pol;
   pol.d.m = (const typename D::Elem*)inst;
   pol.d.n = n;
+  pol.d.sbase = 0;
+  pol.d.use_s = 0;
   const short* t = genes + (size_t)blockIdx.x * n;
   Acc s = n < 2 ? (Acc)0 : pol.partial(t, n, threadIdx.x, blockDim.x);
 #pragma unroll
@@ -47,6 +51,8 @@ __device__ __forceinline__ void tsp_delta_entry(const void* inst, int n, const s
   TspPolicy<D> pol;
   pol.d.m = (const typename D::Elem*)inst;
   pol.d.n = n;
+  pol.d.sbase = 0;
+  pol.d.use_s = 0;
   for (int p = threadIdx.x; p < n; p += blockDim.x) row[p] = genes[(size_t)blockIdx.x * n + p];
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -87,6 +93,8 @@ __device__ __forceinline__ void tsp_probe_entry(const void* inst, int n, int kin
     TspPolicy<D> pol;
     pol.d.m = (const typename D::Elem*)inst;
     pol.d.n = n;
+    pol.d.sbase = 0;
+  pol.d.use_s = 0;
     Stream rng;
     rng.init(key);
     Chain L;

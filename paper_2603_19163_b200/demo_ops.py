@@ -52,7 +52,7 @@ DELTA_OR_OPT = r"""
   int bp = 0;
   for (int t = 0; t < 24; ++t) {
     const int pos = ctx.randbelow(m + 1);
-    const int qp = pos > 0 ? pos - 1 : m - 1, qn = pos % m;
+    const int qp = pos > 0 ? pos - 1 : m - 1, qn = pos == m ? 0 : pos;
     const int prev = ctx.at(qp < s ? qp : qp + L), nxt = ctx.at(qn < s ? qn : qn + L);
     const double delta = ctx.dist(prev, f) + ctx.dist(l, nxt) - ctx.dist(prev, nxt);
     if (!have || delta < bd) { have = true; bd = delta; bp = pos; }
@@ -69,15 +69,16 @@ DELTA_NODE_INSERT = r"""
   const int m = n - 1;                       // rest[q] = tour[q < i ? q : q + 1]
   int prev = ctx.at(m - 1 < i ? m - 1 : m);  // rest[-1]
   double dpc = ctx.dist(prev, city);
-  bool have = false;
   double bd = 0.0;
-  int bp = 0;
-  for (int pos = 0; pos <= m; ++pos) {
-    const int q = pos % m;
-    const int nxt = ctx.at(q < i ? q : q + 1);
+  int bp = -1;
+  // slot m (pos % m == 0) repeats slot 0's delta and can never win the
+  // strict '<' scan, so the reference's m + 1 slots reduce to m
+#pragma unroll 4
+  for (int pos = 0; pos < m; ++pos) {
+    const int nxt = ctx.at(pos + (pos >= i));
     const double dcn = ctx.dist(city, nxt);
     const double delta = dpc + dcn - ctx.dist(prev, nxt);
-    if (!have || delta < bd) { have = true; bd = delta; bp = pos; }
+    if (bp < 0 || delta < bd) { bd = delta; bp = pos; }
     prev = nxt;
     dpc = dcn;  // dist(prev', city) == dist(city, nxt): TSP matrices are symmetric
   }
