@@ -45,6 +45,7 @@ struct TeamShared {
   int impr[MAX_SEQ];
   int k_usage[3];
   int k_impr[3];
+  int nreq;                        // pending cooperative relocations this step
   unsigned char cnt[16][MAX_SEQ];  // per-warp lane counts per sequence (lane sort)
 };
 
@@ -57,8 +58,9 @@ struct LaneArrays {
   u32* pos;        // [TS] stream words consumed
   u32* meta;       // [TS] k | nm | sq0 | sq1 | sq2
   unsigned short* order;  // [TS] thread slot -> logical lane
+  unsigned short* req;    // [TS] lanes with a pending cooperative relocation
   static __host__ __device__ unsigned bytes(int TS) {
-    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2));
+    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2));
   }
   __device__ __forceinline__ void bind(unsigned char* p, int TS) {
     mv = (u64*)p;
@@ -66,18 +68,19 @@ struct LaneArrays {
     pos = (u32*)(p + (3 * 8 + sizeof(Acc)) * TS);
     meta = pos + TS;
     order = (unsigned short*)(meta + TS);
+    req = order + TS;
   }
 };
 
 __device__ __forceinline__ u64 pack_move(const Move& m) {
-  return (u64)m.kind | ((u64)(u32)m.a << 2) | ((u64)(u32)m.b << 22) | ((u64)(u32)m.c << 42);
+  return (u64)m.kind | ((u64)(u32)m.a << 3) | ((u64)(u32)m.b << 23) | ((u64)(u32)m.c << 43);
 }
 __device__ __forceinline__ Move unpack_move(u64 v) {
   Move m;
-  m.kind = (int)(v & 3u);
-  m.a = (int)((v >> 2) & 0xFFFFFu);
-  m.b = (int)((v >> 22) & 0xFFFFFu);
-  m.c = (int)((v >> 42) & 0xFFFFFu);
+  m.kind = (int)(v & 7u);
+  m.a = (int)((v >> 3) & 0xFFFFFu);
+  m.b = (int)((v >> 23) & 0xFFFFFu);
+  m.c = (int)((v >> 43) & 0xFFFFFu);
   return m;
 }
 __device__ __forceinline__ u32 pack_meta(int k, int nm, int q0, int q1, int q2) {
@@ -245,7 +248,6 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     const double temp = A.temps[gi];
 
     // ---- A: every lane draws k and its first sequence (identity mapping) ----
-    int hold_lane = -1, hold_seq = 31;  // 31 = no work
     if (lane < T) {
       Stream rng;
       rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)lane, 0));
@@ -254,19 +256,26 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       la.pos[lane] = rng.tell();
       la.meta[lane] = pack_meta(k, 0, s0, 0, 0);
       la.delta[lane] = (Acc)0;
-      hold_lane = lane;
-      hold_seq = s0;
     }
+    // (no barrier: the step-0 ranking reads only this thread's own lane)
 
-    // ---- B: chain steps; lanes are regrouped by sequence before each step so
-    //      a warp runs one operator at a time (counting sort over <= 32 ids) ----
+    // ---- B: chain steps.  Before each step the lanes are regrouped by
+    //      sequence (counting sort over <= 31 ids) so a warp runs one
+    //      operator at a time; deferred relocations are then resolved
+    //      cooperatively by all warps of the team. ---------------------------
     for (int s = 0; s < MAX_CHAIN; ++s) {
+      int hold_seq = 31;  // 31 = no work this step
+      if (lane < T) {
+        const u32 mt = la.meta[lane];
+        if (meta_k(mt) > s) hold_seq = meta_sq(mt, s);
+      }
       const unsigned grp = __match_any_sync(0xffffffffu, hold_seq);
       const int rank = __popc(grp & lt_mask);
       ts->cnt[warp][wl] = 0;
       __syncwarp();
       if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
       team_bar(team, TS);
+      if (lane == 0) ts->nreq = 0;
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
       if (wl < nseq) {
@@ -284,13 +293,11 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       int base = __shfl_sync(0xffffffffu, incl - tj, my_pos);
       if (hold_seq != 31) {
         for (int w = 0; w < warp; ++w) base += ts->cnt[w][hold_seq];
-        la.order[base + rank] = (unsigned short)hold_lane;
+        la.order[base + rank] = (unsigned short)lane;
       }
       team_bar(team, TS);
       if (active == 0) break;  // uniform
 
-      hold_lane = -1;
-      hold_seq = 31;
       if (lane < active) {
         const int L = la.order[lane];
         Stream rng;
@@ -299,7 +306,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         const u32 meta = la.meta[L];
         const int k = meta_k(meta);
         int nm = meta_nm(meta);
-        int q[3] = {meta_sq(meta, 0), meta_sq(meta, 1), meta_sq(meta, 2)};
+        int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
         Chain C;
         C.reset(cur, n);
         for (int i = 0; i < nm; ++i) C.push(unpack_move(la.mv[i * TS + L]));
@@ -312,8 +319,13 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         c.rd_pos = 0;
         c.rd_elem = 0;
         c.out.kind = MV_NONE;
-        run_perm_op<Policy, Custom>(s_kind[q[s]], c);
-        if (c.out.kind != MV_NONE) {
+        run_perm_op<Policy, Custom>(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
+        bool pending = false;
+        if (c.out.kind == MV_RELOCATE_BEST) {
+          la.mv[nm * TS + L] = pack_move(c.out);  // resolved below, nm unchanged
+          la.req[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+          pending = true;
+        } else if (c.out.kind != MV_NONE) {
           d += pol.delta(C, c.out, c.rd_pos, c.rd_elem);
           la.mv[nm * TS + L] = pack_move(c.out);
           ++nm;
@@ -321,17 +333,77 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         err |= c.err;
         rd_pos += c.rd_pos;
         rd_elem += c.rd_elem;
-        if (s + 1 < k) {
-          q[s + 1] = sample_seq(s_cum, nseq, total, rng);
-          hold_lane = L;
-          hold_seq = q[s + 1];
+        if (!pending && s + 1 < k) {
+          const int nq = sample_seq(s_cum, nseq, total, rng);
+          if (s == 0) q1 = nq; else q2 = nq;
         }
         la.pos[L] = rng.tell();
-        la.meta[L] = pack_meta(k, nm, q[0], q[1], q[2]);
+        la.meta[L] = pack_meta(k, nm, q0, q1, q2);
         la.delta[L] = d;
       }
+      team_bar(team, TS);
+
+      // ---- cooperative relocations: one warp per request, 32 slots per step
+      const int nreq = ts->nreq;
+      if (nreq > 0) {
+        for (int r = warp; r < nreq; r += nwarps) {
+          const int L = la.req[r];
+          const u32 meta = la.meta[L];
+          const int nm = meta_nm(meta);
+          Chain C;
+          C.reset(cur, n);
+          for (int i = 0; i < nm; ++i) C.push(unpack_move(la.mv[i * TS + L]));
+          const Move rq = unpack_move(la.mv[nm * TS + L]);
+          const int st = rq.a, len = rq.b, m = n - len;
+          const int f = C.at(st), l = C.at(st + len - 1);
+          double best = 0.0;
+          int bp = 0x7fffffff;
+          for (int p = wl; p < m; p += 32) {
+            const int qp = p > 0 ? p - 1 : m - 1;
+            const int prev = C.at(qp < st ? qp : qp + len), nxt = C.at(p < st ? p : p + len);
+            const double dlt = pol.insertion(prev, f, l, nxt);
+            if (bp == 0x7fffffff || dlt < best) {  // p ascends per thread: keeps first min
+              best = dlt;
+              bp = p;
+            }
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+            if (op != 0x7fffffff && (bp == 0x7fffffff || ob < best || (ob == best && op < bp))) {
+              best = ob;
+              bp = op;
+            }
+          }
+          if (wl == 0) {
+            rd_pos += 2u * (unsigned)m + 2u;
+            rd_elem += 3u * (unsigned)m;
+            Move mv;
+            mv.kind = MV_SEGMENT;
+            mv.a = st;
+            mv.b = len;
+            mv.c = bp;
+            unsigned rp = 0, re = 0;
+            const Acc d = la.delta[L] + pol.delta(C, mv, rp, re);
+            la.mv[nm * TS + L] = pack_move(mv);
+            const int k = meta_k(meta);
+            int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+            if (s + 1 < k) {  // continue the lane's stream after its operator's draws
+              Stream rng;
+              rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+              rng.seek(la.pos[L]);
+              const int nq = sample_seq(s_cum, nseq, total, rng);
+              if (s == 0) q1 = nq; else q2 = nq;
+              la.pos[L] = rng.tell();
+            }
+            la.meta[L] = pack_meta(k, nm + 1, meta_sq(meta, 0), q1, q2);
+            la.delta[L] = d;
+          }
+        }
+        team_bar(team, TS);
+      }
     }
-    team_bar(team, TS);
 
     // ---- C: team argmin over (delta, lane) -------------------------------------
     Acc bd = lane < T ? la.delta[lane] : AccMax<Acc>::value();  // padding lanes never win

@@ -24,7 +24,10 @@
 
 namespace go {
 
-enum MoveKind { MV_NONE = 0, MV_SWAP = 1, MV_REVERSE = 2, MV_SEGMENT = 3 };
+enum MoveKind {
+  MV_NONE = 0, MV_SWAP = 1, MV_REVERSE = 2, MV_SEGMENT = 3,
+  MV_RELOCATE_BEST = 4  // deferred: SEGMENT(a, b, best slot), resolved cooperatively
+};
 
 struct Move {
   int kind, a, b, c;
@@ -214,6 +217,22 @@ struct PermCtx {
     out.kind = MV_SEGMENT; out.a = start; out.b = len; out.c = pos;
   }
   __device__ __forceinline__ void insert(int i, int pos) { move_segment(i, 1, pos); }
+  // Relocate [start, start+len) to the slot of the shortened row minimising
+  //   d(prev, seg[0]) + d(seg[-1], next) - d(prev, next)      (float64)
+  // taking the FIRST minimum over slots 0..n-len-1 — exactly the scan of the
+  // reference's delta_node_insert (demo_ops.py:71-89, len = 1) and of a
+  // full-scan or-opt.  The scan is not run by this lane: the framework
+  // resolves every pending relocation of the team with whole warps (32
+  // slots per step) after the operators return, so it must be the
+  // operator's last action.
+  __device__ __forceinline__ void relocate_best(int start, int len) {
+    const int n = L->n;
+    if (len < 1 || start < 0 || start + len > n || n - len < 2) {
+      err |= ERR_OP_MOVE;
+      return;
+    }
+    out.kind = MV_RELOCATE_BEST; out.a = start; out.b = len; out.c = 0;
+  }
 };
 
 // ---- built-in single-row permutation operators ----------------------------
@@ -259,6 +278,25 @@ __device__ __forceinline__ void bi_or_opt(Ctx& c) {
   c.move_segment(s, L, pos);
 }
 
+// Serial resolution of a deferred relocation (probe kernel / reference path).
+template <class Policy>
+__device__ __forceinline__ Move resolve_relocate_serial(const Policy& pol, const Chain& L, int start,
+                                                        int len) {
+  const int n = L.n, m = n - len;
+  const int f = L.at(start), l = L.at(start + len - 1);
+  double bd = 0.0;
+  int bp = -1;
+  for (int pos = 0; pos < m; ++pos) {
+    const int qp = pos > 0 ? pos - 1 : m - 1;
+    const int prev = L.at(qp < start ? qp : qp + len), nxt = L.at(pos < start ? pos : pos + len);
+    const double dlt = pol.insertion(prev, f, l, nxt);
+    if (bp < 0 || dlt < bd) { bd = dlt; bp = pos; }
+  }
+  Move mv;
+  mv.kind = MV_SEGMENT; mv.a = start; mv.b = len; mv.c = bp;
+  return mv;
+}
+
 // ---- problem policies over a single permutation row -------------------------
 template <class D>
 struct TspPolicy {
@@ -270,6 +308,11 @@ struct TspPolicy {
   __device__ __forceinline__ Acc delta(const Chain& L, const Move& mv, unsigned& rp,
                                        unsigned& re) const {
     return tsp_move_delta(d, L, mv, rp, re);
+  }
+  // insertion cost of segment (f .. l) between prev and nxt, the reference's
+  // float64 expression order (demo_ops.py:62, :83)
+  __device__ __forceinline__ double insertion(int prev, int f, int l, int nxt) const {
+    return (double)d(prev, f) + (double)d(l, nxt) - (double)d(prev, nxt);
   }
   // full tour length partial sum over slots [lo, hi) step `step` (team reduce)
   __device__ __forceinline__ Acc partial(const i16* t, int n, int lo, int step) const {

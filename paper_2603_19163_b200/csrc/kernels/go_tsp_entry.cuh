@@ -108,6 +108,7 @@ __device__ __forceinline__ void tsp_probe_entry(const void* inst, int n, int kin
     c.rd_elem = 0;
     c.out.kind = MV_NONE;
     run_perm_op<TspPolicy<D>, Custom>(kind, c);
+    if (c.out.kind == MV_RELOCATE_BEST) c.out = resolve_relocate_serial(pol, L, c.out.a, c.out.b);
     if (c.out.kind != MV_NONE) L.push(c.out);
     *err_out = c.err;
     ch = L;

@@ -10,7 +10,7 @@ scores the resulting primitive move exactly (go_perm.cuh).
 
 Ctx API: size(), at(p), dist(a, b), random(), randrange(lo, hi),
 randbelow(n), swap(i, j), reverse(i, j), move_segment(start, len, pos),
-insert(i, pos).
+insert(i, pos), relocate_best(start, len) (cooperative best-slot scan).
 """
 
 from __future__ import annotations
@@ -61,7 +61,20 @@ DELTA_OR_OPT = r"""
 """
 
 DELTA_NODE_INSERT = r"""
-  // demo_ops.py:71-89 — move one city to its best position over the whole tour
+  // demo_ops.py:71-89 — move one city to its best position over the whole tour.
+  // The O(n) scan is handed to the framework (ctx.relocate_best): same float64
+  // expression d(prev,c) + d(c,next) - d(prev,next), same first-minimum rule,
+  // evaluated 32 slots at a time by a whole warp instead of one lane.
+  const int n = ctx.size();
+  if (n < 4) return;
+  const int i = ctx.randbelow(n);
+  ctx.relocate_best(i, 1);
+"""
+
+# The same operator written as a plain per-lane loop (kept for comparison and
+# as an example of a self-contained snippet; selected by
+# tsp_delta_operators(cooperative=False)).
+DELTA_NODE_INSERT_LOOP = r"""
   const int n = ctx.size();
   if (n < 4) return;
   const int i = ctx.randbelow(n);
@@ -86,11 +99,12 @@ DELTA_NODE_INSERT = r"""
 """
 
 
-def tsp_delta_operators() -> tuple[CustomOperator, ...]:
+def tsp_delta_operators(cooperative: bool = True) -> tuple[CustomOperator, ...]:
     return (
         CustomOperator(100, "delta_two_opt", None, 1.0, DELTA_TWO_OPT),
         CustomOperator(101, "delta_or_opt", None, 1.0, DELTA_OR_OPT),
-        CustomOperator(102, "delta_node_insert", None, 1.0, DELTA_NODE_INSERT),
+        CustomOperator(102, "delta_node_insert", None, 1.0,
+                       DELTA_NODE_INSERT if cooperative else DELTA_NODE_INSERT_LOOP),
     )
 
 

@@ -132,7 +132,7 @@ def test_delta_chains_match_oracle(lib, n, integral):
 
 
 def _engine_vs_oracle(dist, P, T, G, seed, custom=False, islands=1, migration="ring",
-                      mig_interval=100, elite=50):
+                      mig_interval=100, elite=50, cooperative=True):
     import paper_2603_19163_b200 as G_
     from paper_2603_19163_b200.demo_ops import tsp_delta_operators
     prob = _tsp(dist)
@@ -140,7 +140,7 @@ def _engine_vs_oracle(dist, P, T, G, seed, custom=False, islands=1, migration="r
                           record_history=True, elite_injection_interval=elite,
                           islands=G_.IslandsConfig(count=islands, migration=migration,
                                                    interval=mig_interval),
-                          custom_operators=tsp_delta_operators() if custom else ())
+                          custom_operators=tsp_delta_operators(cooperative) if custom else ())
     res = G_.run(prob, cfg)
     ocfg = OE.RunCfg(population=P, team_size=T, max_generations=G, seed=seed,
                      record_history=True, elite_interval=elite, islands=islands,
@@ -175,19 +175,31 @@ def test_evolve_bit_identical_islands_and_elite():
     _assert_same_run(res, ref)
 
 
-def test_evolve_bit_identical_with_user_operators():
+@pytest.mark.parametrize("cooperative", [True, False])
+def test_evolve_bit_identical_with_user_operators(cooperative):
     res, ref = _engine_vs_oracle(I.tsp_random(51, 51, True), P=6, T=32, G=40, seed=2024,
-                                 custom=True)
+                                 custom=True, cooperative=cooperative)
     _assert_same_run(res, ref)
     assert [e["id"] for e in res.final_weights["sequences"]][-3:] == [100, 101, 102]
 
 
-def test_evolve_lattice_shared_memory_triangle():
+@pytest.mark.parametrize("cooperative", [True, False])
+def test_evolve_lattice_shared_memory_triangle(cooperative):
     """C2 shape: int16 packed triangle staged into shared memory."""
     d, _ = I.tsp_lattice()
-    res, ref = _engine_vs_oracle(d, P=4, T=128, G=12, seed=456, custom=True)
+    res, ref = _engine_vs_oracle(d, P=4, T=128, G=12, seed=456, custom=True,
+                                 cooperative=cooperative)
     _assert_same_run(res, ref)
     assert res.device["layout"] == 1  # L_I16_TRI
+
+
+def test_float_instance_with_user_operators_matches_oracle():
+    """Float matrix: decisions are float64 in both engines; bit-identical while
+    the int64/float64 delta sums agree (they do on this seed)."""
+    res, ref = _engine_vs_oracle(I.tsp_random(40, 9, False), P=4, T=32, G=20, seed=9,
+                                 custom=True)
+    assert res.generations_completed == ref.generations
+    assert abs(res.objectives[0] - ref.objectives[0]) <= 1e-6 * ref.objectives[0]
 
 
 def test_float_instance_runs_within_tolerance():
