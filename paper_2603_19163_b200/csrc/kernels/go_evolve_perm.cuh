@@ -356,20 +356,39 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           const Move rq = unpack_move(la.mv[nm * TS + L]);
           const int st = rq.a, len = rq.b, m = n - len;
           const int f = C.at(st), l = C.at(st + len - 1);
-          double best = 0.0;
+          // slot p sits between rest[p-1] and rest[p] (rest = row without the
+          // segment); 32 consecutive slots per step, prev / d(prev, f) come
+          // from the neighbouring lane (d(prev, f) == d(f, prev) == previous
+          // slot's d(l, next) when len == 1: TSP matrices are symmetric)
+          Acc best = 0;
           int bp = 0x7fffffff;
-          for (int p = wl; p < m; p += 32) {
-            const int qp = p > 0 ? p - 1 : m - 1;
-            const int prev = C.at(qp < st ? qp : qp + len), nxt = C.at(p < st ? p : p + len);
-            const double dlt = pol.insertion(prev, f, l, nxt);
-            if (bp == 0x7fffffff || dlt < best) {  // p ascends per thread: keeps first min
+          int carry = C.at(m - 1 < st ? m - 1 : m - 1 + len);  // rest[m-1] = prev of slot 0
+          Acc carry_b = pol.cost_acc(l, carry);
+#pragma unroll 2
+          for (int p0 = 0; p0 < m; p0 += 32) {
+            const int p = p0 + wl;
+            const bool in = p < m;
+            const int nxt = C.at(in ? (p < st ? p : p + len) : 0);
+            const Acc b = pol.cost_acc(l, nxt);
+            int prev = __shfl_up_sync(0xffffffffu, nxt, 1);
+            Acc a_l = __shfl_up_sync(0xffffffffu, b, 1);
+            if (wl == 0) {
+              prev = carry;
+              a_l = carry_b;
+            }
+            const Acc a = len == 1 ? a_l : pol.cost_acc(prev, f);
+            const Acc c = pol.cost_acc(prev, nxt);
+            const Acc dlt = Policy::kIntegral ? a + b - c : (Acc)(((double)a + (double)b) - (double)c);
+            if (in && (bp == 0x7fffffff || dlt < best)) {  // p ascends per thread: first min
               best = dlt;
               bp = p;
             }
+            carry = __shfl_sync(0xffffffffu, nxt, 31);
+            carry_b = __shfl_sync(0xffffffffu, b, 31);
           }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const Acc ob = __shfl_xor_sync(0xffffffffu, best, off);
             const int op = __shfl_xor_sync(0xffffffffu, bp, off);
             if (op != 0x7fffffff && (bp == 0x7fffffff || ob < best || (ob == best && op < bp))) {
               best = ob;
@@ -377,8 +396,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
             }
           }
           if (wl == 0) {
-            rd_pos += 2u * (unsigned)m + 2u;
-            rd_elem += 3u * (unsigned)m;
+            rd_pos += (unsigned)m + 3u;
+            rd_elem += (len == 1 ? 2u : 3u) * (unsigned)m + 1u;
             Move mv;
             mv.kind = MV_SEGMENT;
             mv.a = st;

@@ -284,12 +284,12 @@ __device__ __forceinline__ Move resolve_relocate_serial(const Policy& pol, const
                                                         int len) {
   const int n = L.n, m = n - len;
   const int f = L.at(start), l = L.at(start + len - 1);
-  double bd = 0.0;
+  typename Policy::Acc bd = 0;
   int bp = -1;
   for (int pos = 0; pos < m; ++pos) {
     const int qp = pos > 0 ? pos - 1 : m - 1;
     const int prev = L.at(qp < start ? qp : qp + len), nxt = L.at(pos < start ? pos : pos + len);
-    const double dlt = pol.insertion(prev, f, l, nxt);
+    const typename Policy::Acc dlt = pol.insertion(prev, f, l, nxt);
     if (bp < 0 || dlt < bd) { bd = dlt; bp = pos; }
   }
   Move mv;
@@ -310,10 +310,14 @@ struct TspPolicy {
     return tsp_move_delta(d, L, mv, rp, re);
   }
   // insertion cost of segment (f .. l) between prev and nxt, the reference's
-  // float64 expression order (demo_ops.py:62, :83)
-  __device__ __forceinline__ double insertion(int prev, int f, int l, int nxt) const {
-    return (double)d(prev, f) + (double)d(l, nxt) - (double)d(prev, nxt);
+  // float64 expression order (demo_ops.py:62, :83).  On integral matrices the
+  // float64 sum of integer terms is exact, so Acc (int64) gives the same value
+  // and the same comparisons.
+  __device__ __forceinline__ Acc insertion(int prev, int f, int l, int nxt) const {
+    if (kIntegral) return (Acc)d(prev, f) + (Acc)d(l, nxt) - (Acc)d(prev, nxt);
+    return (Acc)((double)d(prev, f) + (double)d(l, nxt) - (double)d(prev, nxt));
   }
+  __device__ __forceinline__ Acc cost_acc(int a, int b) const { return (Acc)d(a, b); }
   // full tour length partial sum over slots [lo, hi) step `step` (team reduce)
   __device__ __forceinline__ Acc partial(const i16* t, int n, int lo, int step) const {
     Acc s = 0;
