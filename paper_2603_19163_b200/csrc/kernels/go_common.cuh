@@ -84,6 +84,15 @@ __device__ __forceinline__ void philox_block(u32 c0, u32 k0, u32 k1, u32& o0, u3
 }
 
 // One lane's stream: key = mix64(parts), words consumed w0..w3 per block.
+// The Philox refill is kept out of line (by value, so the stream stays in
+// registers): inlined at every draw site it made the evolve kernel several
+// times larger than the instruction cache.
+__device__ __noinline__ uint4 philox_refill(u32 c0, u32 k0, u32 k1) {
+  uint4 w;
+  philox_block(c0, k0, k1, w.x, w.y, w.z, w.w);
+  return w;
+}
+
 struct Stream {
   u32 k0, k1, ctr, w0, w1, w2, w3;
   int avail;
@@ -95,16 +104,21 @@ struct Stream {
     avail = 0;
   }
   __device__ __forceinline__ u32 word() {
-    if (avail == 0) {
-      philox_block(ctr++, k0, k1, w0, w1, w2, w3);
-      avail = 4;
-    }
+    if (avail == 0) refill();
     const u32 r = w0;
     w0 = w1;
     w1 = w2;
     w2 = w3;
     --avail;
     return r;
+  }
+  __device__ __forceinline__ void refill() {
+    const uint4 w = philox_refill(ctr++, k0, k1);
+    w0 = w.x;
+    w1 = w.y;
+    w2 = w.z;
+    w3 = w.w;
+    avail = 4;
   }
   // random.Random.random()
   __device__ __forceinline__ double random() {
@@ -129,8 +143,7 @@ struct Stream {
     avail = 0;
     const int off = (int)(pos & 3u);
     if (off) {
-      philox_block(ctr++, k0, k1, w0, w1, w2, w3);
-      avail = 4;
+      refill();
       for (int i = 0; i < off; ++i) word();
     }
   }

@@ -72,17 +72,8 @@ struct LaneArrays {
   }
 };
 
-__device__ __forceinline__ u64 pack_move(const Move& m) {
-  return (u64)m.kind | ((u64)(u32)m.a << 3) | ((u64)(u32)m.b << 23) | ((u64)(u32)m.c << 43);
-}
-__device__ __forceinline__ Move unpack_move(u64 v) {
-  Move m;
-  m.kind = (int)(v & 7u);
-  m.a = (int)((v >> 3) & 0xFFFFFu);
-  m.b = (int)((v >> 23) & 0xFFFFFu);
-  m.c = (int)((v >> 43) & 0xFFFFFu);
-  return m;
-}
+__device__ __forceinline__ u64 pack_move(const Move& m) { return pack_mv(m); }
+__device__ __forceinline__ Move unpack_move(u64 v) { return unpack_mv(v); }
 __device__ __forceinline__ u32 pack_meta(int k, int nm, int q0, int q1, int q2) {
   return (u32)k | ((u32)nm << 2) | ((u32)q0 << 4) | ((u32)q1 << 9) | ((u32)q2 << 14);
 }
@@ -263,6 +254,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     //      sequence (counting sort over <= 31 ids) so a warp runs one
     //      operator at a time; deferred relocations are then resolved
     //      cooperatively by all warps of the team. ---------------------------
+#pragma unroll 1
     for (int s = 0; s < MAX_CHAIN; ++s) {
       int hold_seq = 31;  // 31 = no work this step
       if (lane < T) {
@@ -309,7 +301,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
         Chain C;
         C.reset(cur, n);
-        for (int i = 0; i < nm; ++i) C.push(unpack_move(la.mv[i * TS + L]));
+        for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
         Acc d = la.delta[L];
         PermCtx<Policy> c;
         c.rng = &rng;
@@ -346,13 +338,14 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       // ---- cooperative relocations: one warp per request, 32 slots per step
       const int nreq = ts->nreq;
       if (nreq > 0) {
+#pragma unroll 1
         for (int r = warp; r < nreq; r += nwarps) {
           const int L = la.req[r];
           const u32 meta = la.meta[L];
           const int nm = meta_nm(meta);
           Chain C;
           C.reset(cur, n);
-          for (int i = 0; i < nm; ++i) C.push(unpack_move(la.mv[i * TS + L]));
+          for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
           const Move rq = unpack_move(la.mv[nm * TS + L]);
           const int st = rq.a, len = rq.b, m = n - len;
           const int f = C.at(st), l = C.at(st + len - 1);
@@ -470,7 +463,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       Chain W;
       W.reset(cur, n);
       const int nm = meta_nm(la.meta[bl]);
-      for (int i = 0; i < nm; ++i) W.push(unpack_move(la.mv[i * TS + bl]));
+      for (int i = 0; i < nm; ++i) W.push_packed(la.mv[i * TS + bl]);
       for (int p = lane; p < n; p += TS) nxt[p] = cur[W.src_all(p)];
       team_bar(team, TS);
       i16* t = cur;

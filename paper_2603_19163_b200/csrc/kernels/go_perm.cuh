@@ -49,11 +49,33 @@ __device__ __forceinline__ int move_src(const Move& m, int p) {
   }
 }
 
+__device__ __forceinline__ unsigned long long pack_mv(const Move& m) {
+  return (unsigned long long)m.kind | ((unsigned long long)(unsigned)m.a << 3) |
+         ((unsigned long long)(unsigned)m.b << 23) | ((unsigned long long)(unsigned)m.c << 43);
+}
+__device__ __forceinline__ Move unpack_mv(unsigned long long v) {
+  Move m;
+  m.kind = (int)(v & 7u);
+  m.a = (int)((v >> 3) & 0xFFFFFu);
+  m.b = (int)((v >> 23) & 0xFFFFFu);
+  m.c = (int)((v >> 43) & 0xFFFFFu);
+  return m;
+}
+
+// composed position map of 1..3 packed moves, latest first (out of line:
+// it sits behind every at() of a non-empty chain)
+__device__ __noinline__ int chain_src(int p, int nm, unsigned long long m0, unsigned long long m1,
+                                      unsigned long long m2) {
+  if (nm > 2) p = move_src(unpack_mv(m2), p);
+  if (nm > 1) p = move_src(unpack_mv(m1), p);
+  return move_src(unpack_mv(m0), p);
+}
+
 // The lane's candidate: base row (shared memory) composed with <= 3 moves.
 struct Chain {
   const i16* base;
   int n, nm;
-  Move m0, m1, m2;
+  unsigned long long pm0, pm1, pm2;  // packed moves
 
   __device__ __forceinline__ void reset(const i16* b, int n_) {
     base = b;
@@ -61,20 +83,18 @@ struct Chain {
     nm = 0;
   }
   __device__ __forceinline__ int src_all(int p) const {
-    if (nm > 2) p = move_src(m2, p);
-    if (nm > 1) p = move_src(m1, p);
-    if (nm > 0) p = move_src(m0, p);
-    return p;
+    return nm == 0 ? p : chain_src(p, nm, pm0, pm1, pm2);
   }
   __device__ __forceinline__ int at(int p) const { return base[src_all(p)]; }
   // element at p of the row AFTER applying `mv` on top of this chain
   __device__ __forceinline__ int at_after(const Move& mv, int p) const {
     return at(move_src(mv, p));
   }
-  __device__ __forceinline__ void push(const Move& mv) {
-    if (nm == 0) m0 = mv;
-    else if (nm == 1) m1 = mv;
-    else m2 = mv;
+  __device__ __forceinline__ void push(const Move& mv) { push_packed(pack_mv(mv)); }
+  __device__ __forceinline__ void push_packed(unsigned long long v) {
+    if (nm == 0) pm0 = v;
+    else if (nm == 1) pm1 = v;
+    else pm2 = v;
     ++nm;
   }
 };
@@ -122,17 +142,22 @@ __device__ __forceinline__ void move_slots(const Move& mv, int n, int* so, int& 
   }
 }
 
-// Φ(cand after mv) − Φ(cand) for the cyclic tour objective (builtins.py:67-71)
+template <class Acc>
+struct DeltaOut {
+  Acc delta;
+  int slots;  // old + new edge slots read (2 positions + 1 element each)
+};
+
+// Φ(cand after mv) − Φ(cand) for the cyclic tour objective (builtins.py:67-71).
+// Out of line and by value: it has ~16 map-composed reads, and inlining it at
+// each call site blew the kernel past the instruction cache.
 template <class D>
-__device__ __forceinline__ typename D::Acc tsp_move_delta(const D& d, const Chain& L,
-                                                          const Move& mv, unsigned& rd_pos,
-                                                          unsigned& rd_elem) {
+__device__ __noinline__ DeltaOut<typename D::Acc> tsp_move_delta_ool(const D d, const Chain L,
+                                                                     const Move mv) {
   typedef typename D::Acc Acc;
   const int n = L.n;
   int so[4], sn[4], no, nn;
   move_slots(mv, n, so, no, sn, nn);
-  rd_pos += 2 * (no + nn);
-  rd_elem += no + nn;
   Acc delta = 0;
   for (int i = 0; i < no; ++i) {
     const int p = so[i], q = p + 1 == n ? 0 : p + 1;
@@ -142,7 +167,20 @@ __device__ __forceinline__ typename D::Acc tsp_move_delta(const D& d, const Chai
     const int p = sn[i], q = p + 1 == n ? 0 : p + 1;
     delta += (Acc)d(L.at_after(mv, p), L.at_after(mv, q));
   }
-  return delta;
+  DeltaOut<Acc> o;
+  o.delta = delta;
+  o.slots = no + nn;
+  return o;
+}
+
+template <class D>
+__device__ __forceinline__ typename D::Acc tsp_move_delta(const D& d, const Chain& L,
+                                                          const Move& mv, unsigned& rd_pos,
+                                                          unsigned& rd_elem) {
+  const DeltaOut<typename D::Acc> o = tsp_move_delta_ool(d, L, mv);
+  rd_pos += 2u * (unsigned)o.slots;
+  rd_elem += (unsigned)o.slots;
+  return o.delta;
 }
 
 // ---- operator context (what built-in and user operators may touch) --------

@@ -26,6 +26,7 @@ DELTA_TWO_OPT = r"""
   bool have = false;
   double bd = 0.0;
   int bi = 0, bj = 0;
+#pragma unroll 1
   for (int s = 0; s < 24; ++s) {
     const int i = ctx.randrange(0, n - 1);
     const int j = ctx.randrange(i + 1, n);
@@ -50,6 +51,7 @@ DELTA_OR_OPT = r"""
   bool have = false;
   double bd = 0.0;
   int bp = 0;
+#pragma unroll 1
   for (int t = 0; t < 24; ++t) {
     const int pos = ctx.randbelow(m + 1);
     const int qp = pos > 0 ? pos - 1 : m - 1, qn = pos == m ? 0 : pos;
