@@ -134,7 +134,7 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
   for (size_t i = 0; i < ops.size(); ++i) {
     src << "// operator " << ops[i].id << " (" << ops[i].name << ")\n"
         << "template <class Ctx> __device__ __forceinline__ void op_slot" << i
-        << "(Ctx& ctx) {\n#line 1 \"" << ops[i].name << "\"\n"
+        << "(Ctx& ctx) {\n#line 1 \"@OPDIR@/" << ops[i].name << ".cuh\"\n"
         << ops[i].body << "\n}\n";
   }
   src << "}  // namespace user\nstruct UserOps {\n"
@@ -166,13 +166,32 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
   nvrtcVersion(&ver_major, &ver_minor);
   keyblob += std::to_string(ver_major) + "." + std::to_string(ver_minor);
   *key_out = sha256_hex(keyblob);
-  const std::string path = cache_dir() + "/" + *key_out + ".cubin";
+  const std::string cdir = cache_dir();
+  const std::string path = cdir + "/" + *key_out + ".cubin";
+  // The generated translation unit and each operator snippet are written next
+  // to the cubin and referenced by #line, so compiler errors name the operator
+  // and ncu's source page can import them.
+  const std::string opdir = cdir + "/" + *key_out + ".ops";
+  mkdir(opdir.c_str(), 0755);
+  std::string final_src = source;
+  for (size_t at = final_src.find("@OPDIR@"); at != std::string::npos;
+       at = final_src.find("@OPDIR@", at))
+    final_src.replace(at, 7, opdir);
+  for (const auto& op : ops) {
+    std::ofstream f(opdir + "/" + op.name + ".cuh");
+    f << op.body;
+  }
+  const std::string src_path = opdir + "/go_user_ops.cu";
+  {
+    std::ofstream f(src_path);
+    f << final_src;
+  }
 
   bool hit = false;
   std::string cubin = read_file(path, &hit);
   if (!hit || cubin.empty()) {
     nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, source.c_str(), "go_user_ops.cu", 0, nullptr, nullptr) !=
+    if (nvrtcCreateProgram(&prog, final_src.c_str(), src_path.c_str(), 0, nullptr, nullptr) !=
         NVRTC_SUCCESS) {
       *log = "nvrtcCreateProgram failed";
       return GO_E_COMPILE;
