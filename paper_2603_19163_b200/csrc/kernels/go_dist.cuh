@@ -25,6 +25,11 @@ template <> struct AccOf<double> { typedef double T; };
 template <class E> struct ValOf { typedef int T; };
 template <> struct ValOf<double> { typedef double T; };
 
+// narrowest exact type for a sum of three terms (insertion scans)
+template <class E> struct ScanOf { typedef int T; };
+template <> struct ScanOf<int> { typedef long long T; };
+template <> struct ScanOf<double> { typedef double T; };
+
 // Explicit shared-space loads: the staged instance pointer travels through
 // operator contexts, where the compiler can no longer prove it is shared and
 // would emit generic LD instead of LDS.
@@ -57,6 +62,7 @@ struct MatFull {
   typedef E Elem;
   typedef typename ValOf<E>::T Val;
   typedef typename AccOf<E>::T Acc;
+  typedef typename ScanOf<E>::T Scan;
   static constexpr bool kIntegral = !(sizeof(E) == 8);
   static constexpr bool kInSmem = !GLOBAL;
   const E* __restrict__ m;
@@ -77,6 +83,7 @@ struct MatTri {
   typedef E Elem;
   typedef typename ValOf<E>::T Val;
   typedef typename AccOf<E>::T Acc;
+  typedef typename ScanOf<E>::T Scan;
   static constexpr bool kIntegral = !(sizeof(E) == 8);
   static constexpr bool kInSmem = true;
   const E* __restrict__ m;

@@ -352,26 +352,34 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           // slot p sits between rest[p-1] and rest[p] (rest = row without the
           // segment); 32 consecutive slots per step, prev / d(prev, f) come
           // from the neighbouring lane (d(prev, f) == d(f, prev) == previous
-          // slot's d(l, next) when len == 1: TSP matrices are symmetric)
-          Acc best = 0;
+          // slot's d(l, next) when len == 1: TSP matrices are symmetric).
+          // Scan is the narrowest exact type (int32 for int16 matrices); the
+          // chain's moves are unpacked once and composed inline per slot.
+          typedef typename Policy::Scan Scan;
+          const Move c0 = unpack_mv(C.pm0), c1 = unpack_mv(C.pm1), c2 = unpack_mv(C.pm2);
+          Scan best = 0;
           int bp = 0x7fffffff;
           int carry = C.at(m - 1 < st ? m - 1 : m - 1 + len);  // rest[m-1] = prev of slot 0
-          Acc carry_b = pol.cost_acc(l, carry);
+          Scan carry_b = pol.cost_scan(l, carry);
 #pragma unroll 2
           for (int p0 = 0; p0 < m; p0 += 32) {
             const int p = p0 + wl;
             const bool in = p < m;
-            const int nxt = C.at(in ? (p < st ? p : p + len) : 0);
-            const Acc b = pol.cost_acc(l, nxt);
+            int q = in ? (p < st ? p : p + len) : 0;
+            if (nm > 2) q = move_src(c2, q);
+            if (nm > 1) q = move_src(c1, q);
+            if (nm > 0) q = move_src(c0, q);
+            const int nxt = cur[q];
+            const Scan b = pol.cost_scan(l, nxt);
             int prev = __shfl_up_sync(0xffffffffu, nxt, 1);
-            Acc a_l = __shfl_up_sync(0xffffffffu, b, 1);
+            Scan a_l = __shfl_up_sync(0xffffffffu, b, 1);
             if (wl == 0) {
               prev = carry;
               a_l = carry_b;
             }
-            const Acc a = len == 1 ? a_l : pol.cost_acc(prev, f);
-            const Acc c = pol.cost_acc(prev, nxt);
-            const Acc dlt = Policy::kIntegral ? a + b - c : (Acc)(((double)a + (double)b) - (double)c);
+            const Scan a = len == 1 ? a_l : pol.cost_scan(prev, f);
+            const Scan c = pol.cost_scan(prev, nxt);
+            const Scan dlt = Policy::kIntegral ? a + b - c : (Scan)(((double)a + (double)b) - (double)c);
             if (in && (bp == 0x7fffffff || dlt < best)) {  // p ascends per thread: first min
               best = dlt;
               bp = p;
@@ -381,7 +389,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) {
-            const Acc ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const Scan ob = __shfl_xor_sync(0xffffffffu, best, off);
             const int op = __shfl_xor_sync(0xffffffffu, bp, off);
             if (op != 0x7fffffff && (bp == 0x7fffffff || ob < best || (ob == best && op < bp))) {
               best = ob;

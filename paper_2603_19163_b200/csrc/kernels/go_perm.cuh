@@ -356,6 +356,8 @@ struct TspPolicy {
     return (Acc)((double)d(prev, f) + (double)d(l, nxt) - (double)d(prev, nxt));
   }
   __device__ __forceinline__ Acc cost_acc(int a, int b) const { return (Acc)d(a, b); }
+  typedef typename D::Scan Scan;
+  __device__ __forceinline__ Scan cost_scan(int a, int b) const { return (Scan)d(a, b); }
   // full tour length partial sum over slots [lo, hi) step `step` (team reduce)
   __device__ __forceinline__ Acc partial(const i16* t, int n, int lo, int step) const {
     Acc s = 0;
