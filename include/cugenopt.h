@@ -209,6 +209,9 @@ int go_elite_record_bytes(go_engine* e, int64_t* bytes);
 int go_engine_export_elites(go_engine* e, void* device_buf, int top_n);
 int go_engine_import_elites(go_engine* e, const void* device_buf, int n_ranks, int rank,
                             int top_n, int strategy, int64_t event_index);
+/* per-phase clock64 totals of the evolve kernel (only filled by builds with
+ * GO_PHASE_TIMING; zero otherwise): diagnostic, not part of the contract */
+int go_engine_debug_counters(go_engine* e, int64_t* out, int n);
 /* the CUDA stream the engine enqueues on (cudaStream_t as void*) */
 int go_engine_stream(go_engine* e, void** stream);
 int go_engine_sync(go_engine* e);

@@ -116,6 +116,7 @@ def _bind(lib):
         "go_engine_export_elites": ([V, V, C.c_int], C.c_int),
         "go_engine_import_elites": ([V, V, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64],
                                     C.c_int),
+        "go_engine_debug_counters": ([V, P(C.c_int64), C.c_int], C.c_int),
         "go_engine_stream": ([V, P(V)], C.c_int),
         "go_engine_sync": ([V], C.c_int),
     }

@@ -1031,6 +1031,16 @@ int go_engine_import_elites(go_engine* e, const void* device_buf, int n_ranks, i
   return fail(GO_E_UNSUPPORTED, "cross-GPU island exchange not built yet");
 }
 
+int go_engine_debug_counters(go_engine* e, int64_t* out, int n) {
+  if (!e || !out || n < 1) return fail(GO_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaStreamSynchronize(e->stream));
+  go::GlobalState gs{};
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < 16; ++i) out[i] = (int64_t)gs.prof[i];
+  return GO_OK;
+}
+
 int go_engine_stream(go_engine* e, void** stream) {
   if (!e || !stream) return fail(GO_E_INVALID, "bad arguments");
   *stream = (void*)e->stream;

@@ -157,8 +157,10 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
     }
   }
   const std::string inc = "-I" + kdir;
+  const char* extra = getenv("GO_JIT_DEFINE");  // e.g. GO_PHASE_TIMING (profiling builds)
+  const std::string extra_opt = std::string("-D") + (extra && *extra ? extra : "GO_JIT_DEFAULT=1");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
-                        "-default-device", "-DGO_JIT=1", inc.c_str()};
+                        "-default-device", "-DGO_JIT=1", extra_opt.c_str(), inc.c_str()};
   const int nopts = sizeof(opts) / sizeof(opts[0]);
   std::string keyblob = source + headers_blob;
   for (int i = 0; i < nopts - 1; ++i) keyblob += opts[i];

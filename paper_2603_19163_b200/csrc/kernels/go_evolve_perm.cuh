@@ -234,6 +234,12 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   int err = 0;
   unsigned long long rd_pos = 0, rd_elem = 0;
 
+#ifdef GO_PHASE_TIMING
+  unsigned long long prof[16] = {0}, t_last = clock64();
+#define GO_TICK(slot) do { const unsigned long long t_ = clock64(); prof[(slot)] += t_ - t_last; t_last = t_; } while (0)
+#else
+#define GO_TICK(slot) do { } while (0)
+#endif
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
@@ -267,6 +273,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       __syncwarp();
       if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
       team_bar(team, TS);
+      GO_TICK(1 + 4 * s);
       if (lane == 0) ts->nreq = 0;
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
@@ -288,6 +295,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         la.order[base + rank] = (unsigned short)lane;
       }
       team_bar(team, TS);
+      GO_TICK(2 + 4 * s);
       if (active == 0) break;  // uniform
 
       if (lane < active) {
@@ -334,6 +342,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         la.delta[L] = d;
       }
       team_bar(team, TS);
+      GO_TICK(3 + 4 * s);
 
       // ---- cooperative relocations: one warp per request, 32 slots per step
       const int nreq = ts->nreq;
@@ -422,6 +431,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           }
         }
         team_bar(team, TS);
+        GO_TICK(4 + 4 * s);
       }
     }
 
@@ -434,6 +444,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       ts->wl[warp] = bl;
     }
     team_bar(team, TS);
+    GO_TICK(13);
     bd = ts->wd[0];
     bl = ts->wl[0];
     for (int w = 1; w < nwarps; ++w) {
@@ -489,10 +500,15 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       bpen = 0.0;
       if (lane == 0) A.best_gen[ev] = g;
     }
+    GO_TICK(14);
   }
 
   // ---- write back ----------------------------------------------------------
   team_bar(team, TS);
+#ifdef GO_PHASE_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 16; ++i) atomicAdd(&A.gs->prof[i], prof[i]);
+#endif
   for (int p = lane; p < n; p += TS) A.genes[(size_t)ev * n + p] = cur[p];
   for (int i = lane; i < MAX_SEQ; i += TS) {
     A.usage[ev * MAX_SEQ + i] = ts->usage[i];
