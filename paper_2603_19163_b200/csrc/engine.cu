@@ -304,7 +304,8 @@ namespace {
 void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_out) {
   const int n = p->n;
   const size_t optin = (size_t)p->dev.smem_optin;
-  const int Emax = std::max(1, std::min(8, 512 / TS));
+  const int cap = p->ops.empty() ? 512 : gohost::jit_max_threads();
+  const int Emax = std::max(1, std::min(8, cap / TS));
   const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
   const int full = p->elem * 2, tri = p->elem * 2 + 1;
   for (int E = E0; E >= 1; --E) {

@@ -121,6 +121,12 @@ static std::string cache_dir() {
   return d;
 }
 
+int jit_max_threads() {
+  const char* e = getenv("GO_EVOLVE_MAX_THREADS");
+  const int v = e ? atoi(e) : 512;
+  return (v >= 128 && v <= 1024 && v % 32 == 0) ? v : 512;
+}
+
 static const char* kHeaders[] = {"go_common.cuh", "go_dist.cuh", "go_perm.cuh", "go_args.cuh",
                                  "go_evolve_perm.cuh", "go_tsp_entry.cuh"};
 
@@ -159,8 +165,10 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
   const std::string inc = "-I" + kdir;
   const char* extra = getenv("GO_JIT_DEFINE");  // e.g. GO_PHASE_TIMING (profiling builds)
   const std::string extra_opt = std::string("-D") + (extra && *extra ? extra : "GO_JIT_DEFAULT=1");
+  const std::string thr_opt = "-DGO_EVOLVE_MAX_THREADS=" + std::to_string(jit_max_threads());
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
-                        "-default-device", "-DGO_JIT=1", extra_opt.c_str(), inc.c_str()};
+                        "-default-device", "-DGO_JIT=1", extra_opt.c_str(), thr_opt.c_str(),
+                        inc.c_str()};
   const int nopts = sizeof(opts) / sizeof(opts[0]);
   std::string keyblob = source + headers_blob;
   for (int i = 0; i < nopts - 1; ++i) keyblob += opts[i];

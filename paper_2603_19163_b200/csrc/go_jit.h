@@ -23,6 +23,7 @@ struct JitModule {
 };
 
 std::string sha256_hex(const std::string& data);
+int jit_max_threads();  // CTA thread cap of JIT-built evolve kernels (GO_EVOLVE_MAX_THREADS)
 std::string kernel_dir();
 
 // Builds (or loads from the cubin cache) the evolve + probe kernels of the

@@ -120,8 +120,14 @@ __device__ __forceinline__ void tsp_probe_entry(const void* inst, int n, int kin
 }  // namespace go
 
 // Declares the extern "C" kernels of one (layout, custom-ops) instantiation.
+// GO_EVOLVE_MAX_THREADS bounds the CTA (teams x lanes) and so the register
+// budget per thread (65536 / max threads); the host reads the same value.
+#ifndef GO_EVOLVE_MAX_THREADS
+#define GO_EVOLVE_MAX_THREADS 512
+#endif
 #define GO_TSP_KERNELS(SUFFIX, D, CUSTOM)                                                     \
-  extern "C" __global__ void __launch_bounds__(512, 1) go_evolve_tsp_##SUFFIX(go::EvolveArgs a) { \
+  extern "C" __global__ void __launch_bounds__(GO_EVOLVE_MAX_THREADS, 1)                    \
+      go_evolve_tsp_##SUFFIX(go::EvolveArgs a) {                                              \
     go::tsp_evolve_entry<D, CUSTOM>(a);                                                       \
   }                                                                                           \
   extern "C" __global__ void go_probe_tsp_##SUFFIX(const void* inst, int n, int kind,        \
