@@ -365,7 +365,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           // Scan is the narrowest exact type (int32 for int16 matrices); the
           // chain's moves are unpacked once and composed inline per slot.
           typedef typename Policy::Scan Scan;
-          const Move c0 = C.m0, c1 = C.m1, c2 = C.m2;
+          const Move c0 = unpack_mv(C.pm0), c1 = unpack_mv(C.pm1), c2 = unpack_mv(C.pm2);
           Scan best = 0;
           int bp = 0x7fffffff;
           int carry = C.at(m - 1 < st ? m - 1 : m - 1 + len);  // rest[m-1] = prev of slot 0

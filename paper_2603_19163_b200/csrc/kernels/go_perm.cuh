@@ -62,37 +62,41 @@ __device__ __forceinline__ Move unpack_mv(unsigned long long v) {
   return m;
 }
 
-// The lane's candidate: base row (shared memory) composed with <= 3 moves,
-// kept unpacked in registers; src() composes the maps inline (latest first).
+// composed position map of 1..3 packed moves, latest first (out of line:
+// it sits behind every at() of a non-empty chain)
+__device__ __noinline__ int chain_src(int p, int nm, unsigned long long m0, unsigned long long m1,
+                                      unsigned long long m2) {
+  if (nm > 2) p = move_src(unpack_mv(m2), p);
+  if (nm > 1) p = move_src(unpack_mv(m1), p);
+  return move_src(unpack_mv(m0), p);
+}
+
+// The lane's candidate: base row (shared memory) composed with <= 3 moves.
 struct Chain {
   const i16* base;
   int n, nm;
-  Move m0, m1, m2;
+  unsigned long long pm0, pm1, pm2;  // packed moves
 
   __device__ __forceinline__ void reset(const i16* b, int n_) {
     base = b;
     n = n_;
     nm = 0;
-    m0.kind = m1.kind = m2.kind = MV_NONE;
   }
   __device__ __forceinline__ int src_all(int p) const {
-    if (nm > 2) p = move_src(m2, p);
-    if (nm > 1) p = move_src(m1, p);
-    if (nm > 0) p = move_src(m0, p);
-    return p;
+    return nm == 0 ? p : chain_src(p, nm, pm0, pm1, pm2);
   }
   __device__ __forceinline__ int at(int p) const { return base[src_all(p)]; }
   // element at p of the row AFTER applying `mv` on top of this chain
   __device__ __forceinline__ int at_after(const Move& mv, int p) const {
     return at(move_src(mv, p));
   }
-  __device__ __forceinline__ void push(const Move& mv) {
-    if (nm == 0) m0 = mv;
-    else if (nm == 1) m1 = mv;
-    else m2 = mv;
+  __device__ __forceinline__ void push(const Move& mv) { push_packed(pack_mv(mv)); }
+  __device__ __forceinline__ void push_packed(unsigned long long v) {
+    if (nm == 0) pm0 = v;
+    else if (nm == 1) pm1 = v;
+    else pm2 = v;
     ++nm;
   }
-  __device__ __forceinline__ void push_packed(unsigned long long v) { push(unpack_mv(v)); }
 };
 
 __device__ __forceinline__ int wrap_slot(int s, int n) { return s < 0 ? s + n : s; }
