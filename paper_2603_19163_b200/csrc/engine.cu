@@ -26,6 +26,7 @@
 #include "go_drv.h"
 #include "go_jit.h"
 #include "kernels/go_epilogue.cuh"
+#include "kernels/go_row_entry.cuh"
 #include "kernels/go_tsp_entry.cuh"
 
 // ---- static instantiations: built-in operators, every layout ----------------
@@ -51,6 +52,33 @@ GO_TSP_KERNELS(f64g, go::DistF64FullG, go::NoCustomOps)
 GO_EVAL_KERNELS(i16, go::DistI16FullG)
 GO_EVAL_KERNELS(i32, go::DistI32FullG)
 GO_EVAL_KERNELS(f64, go::DistF64FullG)
+
+// ---- row family: QAP / knapsack / JSP-int -------------------------------------
+GO_ROW_KERNEL(go_evolve_qap_i16, go::RK_QAP, short, short)
+GO_ROW_KERNEL(go_evolve_qap_i32, go::RK_QAP, int, short)
+GO_ROW_KERNEL(go_evolve_qap_f64, go::RK_QAP, double, short)
+GO_ROW_KERNEL(go_evolve_knap, go::RK_KNAP, double, unsigned char)
+GO_ROW_KERNEL(go_evolve_jsp, go::RK_JSP, int, short)
+extern "C" __global__ void go_eval_qap_i16(const void* inst, unsigned off1, int n, const short* g,
+                                           double* obj) {
+  go::qap_eval_entry<short>(inst, off1, n, g, obj);
+}
+extern "C" __global__ void go_eval_qap_i32(const void* inst, unsigned off1, int n, const short* g,
+                                           double* obj) {
+  go::qap_eval_entry<int>(inst, off1, n, g, obj);
+}
+extern "C" __global__ void go_eval_qap_f64(const void* inst, unsigned off1, int n, const short* g,
+                                           double* obj) {
+  go::qap_eval_entry<double>(inst, off1, n, g, obj);
+}
+extern "C" __global__ void go_eval_knap(const void* inst, unsigned off1, int n, double cap,
+                                        const short* g, double* obj, double* pen) {
+  go::knap_eval_entry(inst, off1, n, cap, g, obj, pen);
+}
+extern "C" __global__ void go_eval_jsp(const void* inst, unsigned off1, int n_jobs, int per_job,
+                                       int n_mach, const short* g, double* obj) {
+  go::jsp_eval_entry(inst, off1, n_jobs, per_job, n_mach, g, obj);
+}
 
 namespace {
 
@@ -135,6 +163,14 @@ size_t cta_smem(int layout, int n, int E, int TS, size_t inst_img_bytes) {
 // ---- handles -------------------------------------------------------------------
 struct go_problem {
   int kind = 0, n = 0, d1 = 1, d2 = 0, device = 0;
+  int family = 0;          // 0: TSP (chain kernel), 1: row kernel
+  // row family
+  int row_kind = 0;        // go::RowKind
+  void* d_img = nullptr;   // instance image
+  size_t img_bytes = 0;
+  unsigned off1 = 0;
+  double capacity = 0.0;
+  int n_jobs = 0, per_job = 0, n_mach = 0, lb = 0, ub = 0, scratch_ints = 0, gsize = 2;
   int elem = E_F64;
   bool integral = false;
   void* d_full = nullptr;  // n*n in elem type (global reads, eval kernels)
@@ -220,8 +256,12 @@ int go_device_query(int device, go_device_info* out) {
   return GO_OK;
 }
 
+static int create_row_problem(const go_problem_desc* d, int device, go_problem** out);
+
 int go_problem_create(const go_problem_desc* d, int device, go_problem** out) {
   if (!d || !out) return fail(GO_E_INVALID, "null argument");
+  if (d->kind == GO_QAP || d->kind == GO_KNAPSACK || d->kind == GO_JSP_INT)
+    return create_row_problem(d, device, out);
   if (d->kind != GO_TSP)
     return fail(GO_E_UNSUPPORTED, "problem kind " + std::to_string(d->kind) +
                                       " has no device path in this build");
@@ -284,9 +324,98 @@ int go_problem_create(const go_problem_desc* d, int device, go_problem** out) {
   return GO_OK;
 }
 
+static int create_row_problem(const go_problem_desc* d, int device, go_problem** out) {
+  std::unique_ptr<go_problem> p(new go_problem());
+  p->kind = d->kind;
+  p->family = 1;
+  p->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaFree(0));
+  int rc = query_device(device, &p->dev);
+  if (rc) return rc;
+  std::vector<unsigned char> img;
+  if (d->kind == GO_QAP) {  // builtins.py:265-290
+    const int n = d->n;
+    if (n < 1 || n > 32767 || !d->flow || !d->dist) return fail(GO_E_INVALID, "QAP needs n, flow, dist");
+    bool integral = true;
+    double maxv = 0;
+    for (size_t i = 0; i < (size_t)n * n; ++i) {
+      for (const double v : {d->flow[i], d->dist[i]}) {
+        if (!std::isfinite(v)) return fail(GO_E_INVALID, "QAP matrices must be finite");
+        if (v != std::floor(v)) integral = false;
+        maxv = std::max(maxv, std::fabs(v));
+      }
+    }
+    p->elem = !integral ? E_F64 : (maxv <= 32767.0 ? E_I16 : (maxv <= 2147483647.0 ? E_I32 : E_F64));
+    const size_t es = elem_size(p->elem), mb = (size_t)n * n * es;
+    p->off1 = pad16(mb);
+    img.assign(p->off1 + pad16(mb), 0);
+    for (size_t i = 0; i < (size_t)n * n; ++i) {
+      const double f = d->flow[i], v = d->dist[i];
+      if (p->elem == E_I16) {
+        ((short*)img.data())[i] = (short)f;
+        ((short*)(img.data() + p->off1))[i] = (short)v;
+      } else if (p->elem == E_I32) {
+        ((int*)img.data())[i] = (int)f;
+        ((int*)(img.data() + p->off1))[i] = (int)v;
+      } else {
+        ((double*)img.data())[i] = f;
+        ((double*)(img.data() + p->off1))[i] = v;
+      }
+    }
+    p->n = n;
+    p->row_kind = go::RK_QAP;
+    p->gsize = 2;
+  } else if (d->kind == GO_KNAPSACK) {  // builtins.py:240-262
+    const int n = d->n;
+    if (n < 1 || n > 32767 || !d->weights || !d->values) return fail(GO_E_INVALID, "knapsack needs n, weights, values");
+    p->off1 = pad16((size_t)n * 8);
+    img.assign(2 * (size_t)p->off1, 0);
+    memcpy(img.data(), d->weights, (size_t)n * 8);
+    memcpy(img.data() + p->off1, d->values, (size_t)n * 8);
+    p->capacity = d->capacity;
+    p->n = n;
+    p->row_kind = go::RK_KNAP;
+    p->gsize = 1;
+    p->ub = 1;
+  } else {  // GO_JSP_INT, builtins.py:408-456
+    const int nj = d->n_jobs, pj = d->ops_per_job;
+    if (nj < 1 || pj < 1 || nj > 255 * 4 || (long long)nj * pj > 32767 || !d->jsp_machine || !d->jsp_duration)
+      return fail(GO_E_INVALID, "JSP needs jobs x ops (<= 32767 operations)");
+    const int n = nj * pj;
+    int nm = 0;
+    for (int i = 0; i < n; ++i) {
+      if (d->jsp_machine[i] < 0 || d->jsp_duration[i] < 0) return fail(GO_E_INVALID, "negative JSP entry");
+      nm = std::max(nm, d->jsp_machine[i] + 1);
+    }
+    if (pj > 255) return fail(GO_E_UNSUPPORTED, "more than 255 operations per job");
+    p->off1 = pad16((size_t)n * 4);
+    img.assign(2 * (size_t)p->off1, 0);
+    memcpy(img.data(), d->jsp_machine, (size_t)n * 4);
+    memcpy(img.data() + p->off1, d->jsp_duration, (size_t)n * 4);
+    p->n = n;
+    p->n_jobs = nj;
+    p->per_job = pj;
+    p->n_mach = nm;
+    p->lb = 0;
+    p->ub = n - 1;
+    p->row_kind = go::RK_JSP;
+    p->gsize = 2;
+    p->scratch_ints = go::jsp_scratch_ints(nj, nm);
+  }
+  p->d1 = 1;
+  p->d2 = p->n;
+  p->img_bytes = img.size();
+  CK(cudaMalloc(&p->d_img, img.size()));
+  CK(cudaMemcpy(p->d_img, img.data(), img.size(), cudaMemcpyHostToDevice));
+  *out = p.release();
+  return GO_OK;
+}
+
 int go_problem_destroy(go_problem* p) {
   if (!p) return GO_OK;
   cudaSetDevice(p->device);
+  cudaFree(p->d_img);
   for (auto& kv : p->jit)
     if (kv.second.mod && gohost::drv()) gohost::drv()->ModuleUnload(kv.second.mod);
   cudaFree(p->d_full);
@@ -314,6 +443,51 @@ void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_o
   }
   *layout = global_layout(p->elem);
   *E_out = E0;
+}
+
+// ---- row family helpers ----------------------------------------------------------
+void* row_kernel(const go_problem* p) {
+  if (p->row_kind == go::RK_QAP)
+    return p->elem == E_I16 ? (void*)go_evolve_qap_i16
+                            : (p->elem == E_I32 ? (void*)go_evolve_qap_i32 : (void*)go_evolve_qap_f64);
+  if (p->row_kind == go::RK_KNAP) return (void*)go_evolve_knap;
+  return (void*)go_evolve_jsp;
+}
+
+unsigned row_team_bytes(const go_problem* p, int TS) {
+  return go::RowSmem::team_bytes(p->n, p->gsize, TS, p->scratch_ints * 4);
+}
+
+// layout codes for the row family: 10 = instance staged in shared memory, 11 = global
+bool choose_row(const go_problem* p, int TS, int E_req, int* layout, int* E_out, size_t* smem) {
+  const size_t optin = (size_t)p->dev.smem_optin;
+  const int Emax = std::max(1, std::min(8, 512 / TS));
+  const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
+  const unsigned tb = row_team_bytes(p, TS);
+  for (int pass = 0; pass < 2; ++pass) {
+    const unsigned inst = pass == 0 ? pad16(p->img_bytes) : 0u;
+    for (int E = E0; E >= 1; --E) {
+      const size_t need = go::PermSmem::team_off(inst) + (size_t)E * tb;
+      if (need <= optin) {
+        *layout = pass == 0 ? 10 : 11;
+        *E_out = E;
+        *smem = need;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+bool seq_supported(const go_problem* p, int id) {
+  if (p->family == 0) return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
+                             id == go::SEQ_OR_OPT;
+  if (id == go::SEQ_SEG_SHUFFLE || id == go::SEQ_SCATTER_SHUFFLE) return true;
+  if (p->row_kind == go::RK_QAP)
+    return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
+           id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT;
+  if (p->row_kind == go::RK_KNAP) return id == go::SEQ_FLIP || id == go::SEQ_SEG_FLIP;
+  return id == go::SEQ_RANDOM_RESET || id == go::SEQ_SEG_RESET;
 }
 
 int launch_static_or_jit(void* fn, CUfunction jf, dim3 grid, dim3 block, size_t smem,
@@ -377,6 +551,21 @@ int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_
   if (!p || team_size < 1 || team_size > 512) return fail(GO_E_INVALID, "bad arguments");
   CK(cudaSetDevice(p->device));
   const int TS = (team_size + 31) / 32 * 32;
+  if (p->family == 1) {
+    int L = 0, E = 0;
+    size_t smem = 0;
+    if (!choose_row(p, TS, teams_per_cta, &L, &E, &smem))
+      return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
+    void* fn = row_kernel(p);
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int blocks = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, E * TS, smem));
+    if (layout) *layout = L;
+    if (teams_cta) *teams_cta = E;
+    if (teams_per_sm) *teams_per_sm = blocks * E;
+    if (smem_bytes) *smem_bytes = (int64_t)smem;
+    return GO_OK;
+  }
   int L = 0, E = 0;
   choose_layout(p, TS, teams_per_cta, &L, &E);
   const size_t smem = cta_smem(L, p->n, E, TS, inst_img_bytes(p, L));
@@ -397,6 +586,41 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
   if (m == 0) return GO_OK;
   CK(cudaSetDevice(p->device));
   const int n = p->n;
+  if (p->family == 1) {
+    std::vector<short> h((size_t)m * n);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = (short)genes[i];
+    short* d_g = nullptr;
+    double *d_o = nullptr, *d_p = nullptr;
+    CK(cudaMalloc(&d_g, h.size() * 2));
+    CK(cudaMalloc(&d_o, (size_t)m * 8));
+    CK(cudaMalloc(&d_p, (size_t)m * 8));
+    CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d_p, 0, (size_t)m * 8));
+    const void* inst = p->d_img;
+    unsigned off1 = p->off1;
+    int nn = n;
+    if (p->row_kind == go::RK_QAP) {
+      void* fn = p->elem == E_I16 ? (void*)go_eval_qap_i16
+                                  : (p->elem == E_I32 ? (void*)go_eval_qap_i32 : (void*)go_eval_qap_f64);
+      void* args[] = {(void*)&inst, &off1, &nn, &d_g, &d_o};
+      CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
+    } else if (p->row_kind == go::RK_KNAP) {
+      double cap = p->capacity;
+      void* args[] = {(void*)&inst, &off1, &nn, &cap, &d_g, &d_o, &d_p};
+      CK(cudaLaunchKernel((void*)go_eval_knap, dim3(m), dim3(128), args, 0, 0));
+    } else {
+      int nj = p->n_jobs, pj = p->per_job, nmach = p->n_mach;
+      void* args[] = {(void*)&inst, &off1, &nj, &pj, &nmach, &d_g, &d_o};
+      CK(cudaLaunchKernel((void*)go_eval_jsp, dim3(m), dim3(32), args, (size_t)p->scratch_ints * 4, 0));
+    }
+    CK(cudaMemcpy(obj_out, d_o, (size_t)m * 8, cudaMemcpyDeviceToHost));
+    if (pen_out) CK(cudaMemcpy(pen_out, d_p, (size_t)m * 8, cudaMemcpyDeviceToHost));
+    cudaFree(d_g);
+    cudaFree(d_o);
+    cudaFree(d_p);
+    (void)sizes;
+    return GO_OK;
+  }
   std::vector<short> h((size_t)m * n);
   for (size_t i = 0; i < h.size(); ++i) h[i] = (short)genes[i];
   short* d_g = nullptr;
@@ -589,19 +813,28 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   e->TS = (c->team_size + 31) / 32 * 32;
   e->n = p->n;
   e->W = p->n;
+  if (p->family == 1) {
+    if (!p->ops.empty()) return fail(GO_E_UNSUPPORTED, "user operators run on the TSP path only");
+    if (!choose_row(p, e->TS, c->teams_per_cta, &e->layout, &e->E, &e->smem))
+      return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
+    e->inst = p->d_img;
+    e->inst_bytes = e->layout == 10 ? pad16(p->img_bytes) : 0u;
+    e->k_evolve = row_kernel(p);
+  } else {
   choose_layout(p, e->TS, c->teams_per_cta, &e->layout, &e->E);
   const LayoutInfo& L = kLayouts[e->layout];
   e->inst = inst_ptr(p, e->layout);
   e->inst_bytes = L.global ? 0u : pad16(inst_img_bytes(p, e->layout));
   e->smem = cta_smem(e->layout, e->n, e->E, e->TS, inst_img_bytes(p, e->layout));
+  }
   e->grid = (e->P + e->E - 1) / e->E;
-  if (!p->ops.empty()) {
+  if (p->family == 0 && !p->ops.empty()) {
     gohost::JitModule* m = nullptr;
     int rc = ensure_jit(p, e->layout, &m);
     if (rc) return rc;
     e->k_evolve_jit = m->evolve;
-  } else {
-    e->k_evolve = L.evolve;
+  } else if (p->family == 0) {
+    e->k_evolve = kLayouts[e->layout].evolve;
   }
   int rc = set_smem_attr(e->k_evolve, e->k_evolve_jit, e->smem);
   if (rc) return rc;
@@ -689,7 +922,7 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
   for (int i = 0; i < nseq; ++i) {
     const int id = ids[i];
     int kind = -1;
-    if (id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE || id == go::SEQ_OR_OPT) {
+    if (id >= 0 && id < 32 && seq_supported(e->prob, id)) {
       kind = id;
     } else if (id >= 100) {
       for (size_t s = 0; s < e->prob->ops.size(); ++s)
@@ -824,8 +1057,26 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.E = e->E;
   a.ev_offset = c.evolver_offset;
   a.team_stride = e->TS;
-  a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
-  a.resync = kLayouts[e->layout].elem == E_F64;
+  go::RowArgs x{};
+  if (e->prob->family == 1) {
+    const go_problem* p = e->prob;
+    a.team_smem = (int)row_team_bytes(p, e->TS);
+    a.resync = 0;
+    x.off1 = p->off1;
+    x.capacity = p->capacity;
+    x.penalty_weight = c.penalty_weight;
+    x.obj_weight = c.obj_weight > 0 ? c.obj_weight : 1.0;
+    x.n_jobs = p->n_jobs;
+    x.per_job = p->per_job;
+    x.n_mach = p->n_mach;
+    x.n_cfg = p->n;
+    x.lb = p->lb;
+    x.ub = p->ub;
+    x.scratch_ints = p->scratch_ints;
+  } else {
+    a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
+    a.resync = kLayouts[e->layout].elem == E_F64;
+  }
   go::EpilogueArgs q{};
   q.P = e->P;
   q.W = e->W;
@@ -896,7 +1147,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     a.temps = dt;
     a.gen0 = done + 1;
     a.ngen = (int)(end - done);
-    void* args[] = {&a};
+    void* args[] = {&a, &x};
     CK(cudaEventRecord(e->k_beg[slot], e->stream));
     int rc = launch_static_or_jit(e->k_evolve, e->k_evolve_jit, dim3(e->grid), dim3(e->E * e->TS),
                                   e->smem, e->stream, args);
@@ -929,7 +1180,8 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     stats->error_flags = gs.err;
     stats->reads_pos = (int64_t)(gs.rd_pos - rp0);
     stats->reads_elem = (int64_t)(gs.rd_elem - re0);
-    stats->elem_bytes = (int32_t)elem_size(kLayouts[e->layout].elem);
+    stats->elem_bytes = e->prob->family == 1 ? (e->prob->row_kind == go::RK_QAP ? (int32_t)elem_size(e->prob->elem) : (e->prob->row_kind == go::RK_KNAP ? 8 : 4))
+                                             : (int32_t)elem_size(kLayouts[e->layout].elem);
     stats->gene_bytes = 2;
     stats->evolve_ms = evolve_ms;
     stats->evolve_launches = evolve_launches;

@@ -65,6 +65,18 @@ struct EvolveArgs {
   int resync;            // recompute Φ at chunk start (float matrices)
 };
 
+// Problem-specific extras of the row kernel (go_evolve_row.cuh).
+struct RowArgs {
+  unsigned off1;         // byte offset of the second instance array (QAP D, knapsack v, JSP durations)
+  double capacity;       // knapsack capacity (builtins.py:258-262)
+  double penalty_weight; // engine.py:651-655
+  double obj_weight;     // Weighted scalarisation weight (Maximize negated inside)
+  int n_jobs, per_job, n_mach;  // JSP-int
+  int n_cfg;             // ProblemConfig.n (lns_scope)
+  int lb, ub;            // integer encoding bounds
+  int scratch_ints;      // per-lane int scratch (JSP decode)
+};
+
 struct EpilogueArgs {
   int P, W;              // evolvers, genes per solution
   short* genes;

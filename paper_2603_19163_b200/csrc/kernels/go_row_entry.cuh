@@ -1,0 +1,84 @@
+// go_row_entry.cuh — kernels of the row family (QAP / knapsack / JSP-int).
+#pragma once
+#include "go_evolve_row.cuh"
+
+namespace go {
+
+// evaluate() for m QAP permutations (builtins.py:282-284), one block each
+template <class E>
+__device__ __forceinline__ void qap_eval_entry(const void* inst, unsigned off1, int n,
+                                               const short* genes, double* obj) {
+  typedef typename AccOf<E>::T A;
+  __shared__ A red[32];
+  const E* f = (const E*)inst;
+  const E* d = (const E*)((const unsigned char*)inst + off1);
+  const short* p = genes + (size_t)blockIdx.x * n;
+  A s = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    for (int j = 0; j < n; ++j) s += (A)f[i * n + j] * (A)d[p[i] * n + p[j]];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    A t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    obj[blockIdx.x] = (double)t;
+  }
+}
+
+// knapsack value / weight excess (builtins.py:258-262)
+__device__ __forceinline__ void knap_eval_entry(const void* inst, unsigned off1, int n,
+                                                double cap, const short* genes, double* obj,
+                                                double* pen) {
+  __shared__ double rv[32], rw[32];
+  const double* w = (const double*)inst;
+  const double* v = (const double*)((const unsigned char*)inst + off1);
+  const short* x = genes + (size_t)blockIdx.x * n;
+  double sv = 0.0, sw = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sv += v[i] * (double)x[i];
+    sw += w[i] * (double)x[i];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sv += __shfl_xor_sync(0xffffffffu, sv, off);
+    sw += __shfl_xor_sync(0xffffffffu, sw, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rv[threadIdx.x >> 5] = sv;
+    rw[threadIdx.x >> 5] = sw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tv = 0.0, tw = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      tv += rv[q];
+      tw += rw[q];
+    }
+    obj[blockIdx.x] = tv;
+    const double over = tw - cap;
+    pen[blockIdx.x] = over > 0.0 ? over : 0.0;
+  }
+}
+
+__device__ __forceinline__ void jsp_eval_entry(const void* inst, unsigned off1, int n_jobs,
+                                               int per_job, int n_mach, const short* genes,
+                                               double* obj) {
+  extern __shared__ int jscr[];
+  if (threadIdx.x != 0) return;
+  JspView J;
+  J.mach = (const int*)inst;
+  J.dur = (const int*)((const unsigned char*)inst + off1);
+  J.n_jobs = n_jobs;
+  J.per_job = per_job;
+  J.n_mach = n_mach;
+  obj[blockIdx.x] = (double)jsp_decode(J, genes + (size_t)blockIdx.x * n_jobs * per_job, jscr);
+}
+
+}  // namespace go
+
+#define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \
+  extern "C" __global__ void __launch_bounds__(512, 1) NAME(go::EvolveArgs a, go::RowArgs x) { \
+    go::evolve_row<KIND, E, G>(a, x);                                                         \
+  }

@@ -369,9 +369,10 @@ class DeviceRun:
         dev = config.device
         self.handle = problem.device_handle(dev)
         self.profile = classify(cfg)
-        self.registry = build_registry(cfg)
+        dev_seqs = problem.device_sequences()
+        self.registry = build_registry(cfg, dev_seqs)
         apply_preset(self.registry, self.profile)
-        self.missing_ops = missing_device_sequences(cfg)
+        self.missing_ops = missing_device_sequences(cfg, dev_seqs)
         self.jit_seconds = 0.0
         if config.custom_operators:
             self._register_custom(config.custom_operators)
@@ -396,7 +397,7 @@ class DeviceRun:
             pop_size = b200_population_size(info.sm_count, self.teams_per_sm, info.l2_bytes,
                                             config.working_set_bytes or
                                             estimate_working_set_bytes(problem),
-                                            self.layout < 6)
+                                            self.layout < 6 or self.layout == 10)
         pop_size = max(pop_size, config.islands.count)
         self.pop_size = pop_size
 

@@ -35,11 +35,6 @@ BUILTIN_NAMES = {
     SEQ_SCATTER_SHUFFLE: "scatter_shuffle", SEQ_GUIDED_REBUILD: "guided_rebuild",
 }
 
-# Built-in sequences with a device implementation, per (encoding, row mode).
-DEVICE_SEQUENCES = {
-    (EncodingKind.PERMUTATION, RowModeKind.SINGLE_SEQ): (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE,
-                                                         SEQ_OR_OPT),
-}
 
 
 @dataclass
@@ -138,26 +133,20 @@ def sequence_applicable(seq_id: int, cfg: ProblemConfig) -> bool:
     raise KeyError(f"unknown built-in sequence id {seq_id}")
 
 
-def device_sequences(cfg: ProblemConfig) -> tuple[int, ...]:
-    return DEVICE_SEQUENCES.get((cfg.encoding.kind, cfg.row_mode), ())
-
-
 def build_registry(cfg: ProblemConfig, allowed=None) -> SequenceRegistry:
-    """Applicable built-ins (operators.py:618-624) restricted to those with a
-    device implementation (`allowed` narrows further)."""
-    dev = set(device_sequences(cfg))
+    """Applicable built-ins in id order (operators.py:618-624).  The engine
+    passes `allowed` = the problem's device sequences (problem.device_sequences()),
+    so the registry holds exactly the operators the device kernel runs."""
     entries = [SequenceEntry(sid, name) for sid, name in BUILTIN_NAMES.items()
-               if sequence_applicable(sid, cfg) and sid in dev
-               and (allowed is None or sid in allowed)]
+               if sequence_applicable(sid, cfg) and (allowed is None or sid in allowed)]
     if not entries:
         raise NotImplementedError("no device operators for this encoding / row mode")
     return SequenceRegistry(entries)
 
 
-def missing_device_sequences(cfg: ProblemConfig) -> list[int]:
+def missing_device_sequences(cfg: ProblemConfig, device: tuple) -> list[int]:
     """Reference sequences for this layout that the device does not run yet."""
-    dev = set(device_sequences(cfg))
-    return [sid for sid in BUILTIN_NAMES if sequence_applicable(sid, cfg) and sid not in dev]
+    return [sid for sid in BUILTIN_NAMES if sequence_applicable(sid, cfg) and sid not in device]
 
 
 def validate_custom_id(registry: SequenceRegistry, op: CustomOperator):

@@ -18,11 +18,14 @@ import numpy as np
 from . import _native as N
 from .core import (ComparisonMode, Direction, Encoding, ObjDef, ProblemConfig, RowModeKind,
                    Solution, validate_solution)
+from .operators import (SEQ_FLIP, SEQ_INSERT, SEQ_OR_OPT, SEQ_RANDOM_RESET, SEQ_REVERSE,
+                        SEQ_SCATTER_SHUFFLE, SEQ_SEG_FLIP, SEQ_SEG_RESET, SEQ_SEG_SHUFFLE, SEQ_SWAP,
+                        SEQ_THREE_OPT)
 
 BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph_coloring",
                  "bin_packing", "load_balancing", "jsp_int", "jsp_perm", "schedule_binary",
                  "vrp_priority", "vrp_nonlinear")
-DEVICE_PROBLEMS = ("tsp",)
+DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int")
 
 
 @dataclass
@@ -78,6 +81,11 @@ class ProblemDefinition:
     # -- device plumbing -------------------------------------------------------
     _handle = None
     _handle_device = None
+    #: built-in sequence ids the device kernel for this problem implements
+    DEVICE_SEQUENCES: tuple = ()
+
+    def device_sequences(self) -> tuple:
+        return self.DEVICE_SEQUENCES
 
     def _native_desc(self):
         raise TypeError(
@@ -172,6 +180,8 @@ def evaluate_many(problem: ProblemDefinition, sols, device: int = 0):
 class TspProblem(ProblemDefinition):
     """builtins.py:53-77: cyclic tour length over a symmetric matrix."""
 
+    DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT)
+
     def __init__(self, dist):
         self.dist = check_distance_matrix(dist)
         self.n = self.dist.shape[0]
@@ -195,6 +205,102 @@ class TspProblem(ProblemDefinition):
         return desc, (d,)
 
 
+class QapProblem(ProblemDefinition):
+    """builtins.py:265-290: Σ_ij F_ij D[π_i, π_j] (matrices not symmetry-checked)."""
+
+    DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT,
+                        SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE)
+
+    def __init__(self, flow, dist):
+        self.flow = np.asarray(flow, dtype=np.float64)
+        self.dist = np.asarray(dist, dtype=np.float64)
+        if self.flow.shape != self.dist.shape or self.flow.ndim != 2 or \
+                self.flow.shape[0] != self.flow.shape[1]:
+            raise ValueError("flow and distance matrices must be square and equal-shaped")
+        self.n = self.flow.shape[0]
+        self._cfg = ProblemConfig(encoding=Encoding.permutation(), d1=1, d2=self.n, n=self.n,
+                                  row_mode=RowModeKind.SINGLE_SEQ,
+                                  obj_defs=(ObjDef("total_cost"),))
+
+    def config(self):
+        return self._cfg
+
+    def compute_penalty(self, sol):
+        return 0.0
+
+    def init_matrices(self):
+        return [self.flow, self.dist]
+
+    def _native_desc(self):
+        f, d = N.f64(self.flow), N.f64(self.dist)
+        desc = N.ProblemDesc(kind=N.GO_QAP, n=self.n, d1=1, d2=self.n)
+        desc.flow, desc.dist = N.dptr(f), N.dptr(d)
+        return desc, (f, d)
+
+
+class KnapsackProblem(ProblemDefinition):
+    """builtins.py:240-262: maximise v·x, penalty max(0, w·x - capacity)."""
+
+    DEVICE_SEQUENCES = (SEQ_FLIP, SEQ_SEG_FLIP, SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE)
+
+    def __init__(self, weights, values, capacity):
+        self.weights = np.asarray(weights, dtype=np.float64)
+        self.values = np.asarray(values, dtype=np.float64)
+        self.capacity = float(capacity)
+        if len(self.weights) != len(self.values):
+            raise ValueError("weights and values must have equal length")
+        self.n = len(self.weights)
+        self._cfg = ProblemConfig(encoding=Encoding.binary(), d1=1, d2=self.n, n=self.n,
+                                  row_mode=RowModeKind.SINGLE_SEQ,
+                                  obj_defs=(ObjDef("total_value", Direction.MAXIMIZE),))
+
+    def config(self):
+        return self._cfg
+
+    def _native_desc(self):
+        w, v = N.f64(self.weights), N.f64(self.values)
+        desc = N.ProblemDesc(kind=N.GO_KNAPSACK, n=self.n, d1=1, d2=self.n,
+                             capacity=self.capacity)
+        desc.weights, desc.values = N.dptr(w), N.dptr(v)
+        return desc, (w, v)
+
+
+class JspIntProblem(ProblemDefinition):
+    """builtins.py:408-456: priority-decoded serial schedule generator."""
+
+    DEVICE_SEQUENCES = (SEQ_RANDOM_RESET, SEQ_SEG_RESET, SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE)
+
+    def __init__(self, jobs):
+        self.jobs = [[(int(m), int(d)) for m, d in ops] for ops in jobs]
+        if not self.jobs:
+            raise ValueError("at least one job required")
+        self.ops_per_job = len(self.jobs[0])
+        for j, ops in enumerate(self.jobs):
+            if len(ops) != self.ops_per_job:
+                raise ValueError(f"job {j} has {len(ops)} operations, expected {self.ops_per_job}")
+        self.n_jobs = len(self.jobs)
+        self.n_machines = 1 + max(m for ops in self.jobs for m, _ in ops)
+        self.n_ops = self.n_jobs * self.ops_per_job
+        self._cfg = ProblemConfig(encoding=Encoding.integer(0, self.n_ops - 1), d1=1,
+                                  d2=self.n_ops, n=self.n_ops, row_mode=RowModeKind.SINGLE_SEQ,
+                                  obj_defs=(ObjDef("makespan"),))
+
+    def config(self):
+        return self._cfg
+
+    def compute_penalty(self, sol):
+        return 0.0
+
+    def _native_desc(self):
+        mach = np.array([m for ops in self.jobs for m, _ in ops], dtype=np.int32)
+        dur = np.array([d for ops in self.jobs for _, d in ops], dtype=np.int32)
+        desc = N.ProblemDesc(kind=N.GO_JSP_INT, n=self.n_ops, d1=1, d2=self.n_ops,
+                             n_jobs=self.n_jobs, n_machines=self.n_machines,
+                             ops_per_job=self.ops_per_job, lb=0, ub=self.n_ops - 1)
+        desc.jsp_machine, desc.jsp_duration = N.iptr(mach), N.iptr(dur)
+        return desc, (mach, dur)
+
+
 def _need(instance: InstanceData, *names):
     missing = [f for f in names if getattr(instance, f) is None]
     if missing:
@@ -208,6 +314,15 @@ def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
     if name == "tsp":
         _need(instance, "distance_matrix")
         return TspProblem(instance.distance_matrix)
+    if name == "qap":
+        _need(instance, "flow_matrix", "distance_matrix")
+        return QapProblem(instance.flow_matrix, instance.distance_matrix)
+    if name == "knapsack":
+        _need(instance, "weights", "values", "capacity")
+        return KnapsackProblem(instance.weights, instance.values, instance.capacity)
+    if name == "jsp_int":
+        _need(instance, "jobs")
+        return JspIntProblem(instance.jobs)
     raise NotImplementedError(
         f"problem {name!r} has no B200 device path in this build "
         f"(device problems: {', '.join(DEVICE_PROBLEMS)})")

@@ -67,7 +67,7 @@ def test_registry_and_presets_match_oracle():
     for dist in (I.tsp_random(51, 51), I.tsp_lattice()[0]):
         prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=dist))
         cfg = prob.config()
-        reg = G.build_registry(cfg)
+        reg = G.build_registry(cfg, prob.device_sequences())
         G.apply_preset(reg, G.classify(cfg))
         oreg = OA.build_registry(OP.Tsp(dist).spec, (0, 1, 2, 3))
         OA.apply_preset(oreg, OA.scale_of(OP.Tsp(dist).spec))
