@@ -59,6 +59,11 @@ GO_ROW_KERNEL(go_evolve_qap_i32, go::RK_QAP, int, short)
 GO_ROW_KERNEL(go_evolve_qap_f64, go::RK_QAP, double, short)
 GO_ROW_KERNEL(go_evolve_knap, go::RK_KNAP, double, unsigned char)
 GO_ROW_KERNEL(go_evolve_jsp, go::RK_JSP, int, short)
+GO_ROW_KERNEL(go_evolve_part, go::RK_PART, double, short)
+extern "C" __global__ void go_eval_part(const void* inst, go::RowArgs x, const short* g, double* obj,
+                                        double* pen) {
+  go::part_eval_entry(inst, x, g, obj, pen);
+}
 extern "C" __global__ void go_eval_qap_i16(const void* inst, unsigned off1, int n, const short* g,
                                            double* obj) {
   go::qap_eval_entry<short>(inst, off1, n, g, obj);
@@ -171,6 +176,9 @@ struct go_problem {
   unsigned off1 = 0;
   double capacity = 0.0;
   int n_jobs = 0, per_job = 0, n_mach = 0, lb = 0, ub = 0, scratch_ints = 0, gsize = 2;
+  // partition problems: stored compactly as cells[n_cells] + sizes[d1] (n = n_cells + d1)
+  int n_cells = 0, tw = 0;
+  unsigned off2 = 0, off3 = 0, off4 = 0;
   int elem = E_F64;
   bool integral = false;
   void* d_full = nullptr;  // n*n in elem type (global reads, eval kernels)
@@ -260,7 +268,8 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
 
 int go_problem_create(const go_problem_desc* d, int device, go_problem** out) {
   if (!d || !out) return fail(GO_E_INVALID, "null argument");
-  if (d->kind == GO_QAP || d->kind == GO_KNAPSACK || d->kind == GO_JSP_INT)
+  if (d->kind == GO_QAP || d->kind == GO_KNAPSACK || d->kind == GO_JSP_INT ||
+      d->kind == GO_VRPTW || d->kind == GO_CVRP)
     return create_row_problem(d, device, out);
   if (d->kind != GO_TSP)
     return fail(GO_E_UNSUPPORTED, "problem kind " + std::to_string(d->kind) +
@@ -378,6 +387,33 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
     p->row_kind = go::RK_KNAP;
     p->gsize = 1;
     p->ub = 1;
+  } else if (d->kind == GO_VRPTW || d->kind == GO_CVRP) {  // builtins.py:80-190
+    const int n = d->n, v = d->d1;
+    if (n < 1 || n > 30000 || v < 1 || v > 2000 || !d->dist || !d->demands)
+      return fail(GO_E_INVALID, "routing needs n customers, vehicles, dist (n+1)^2, demands");
+    const bool tw = d->kind == GO_VRPTW;
+    if (tw && (!d->ready || !d->due || !d->service)) return fail(GO_E_INVALID, "VRPTW needs ready/due/service");
+    const size_t n1 = (size_t)n + 1;
+    p->off1 = pad16(n1 * n1 * 8);
+    p->off2 = p->off1 + pad16((size_t)n * 8);
+    p->off3 = p->off2 + pad16(n1 * 8);
+    p->off4 = p->off3 + pad16(n1 * 8);
+    img.assign(p->off4 + pad16(n1 * 8), 0);
+    memcpy(img.data(), d->dist, n1 * n1 * 8);
+    memcpy(img.data() + p->off1, d->demands, (size_t)n * 8);
+    if (tw) {
+      memcpy(img.data() + p->off2, d->ready, n1 * 8);
+      memcpy(img.data() + p->off3, d->due, n1 * 8);
+      memcpy(img.data() + p->off4, d->service, n1 * 8);
+    }
+    p->capacity = d->capacity;
+    p->tw = tw;
+    p->n_cells = n;
+    p->row_kind = go::RK_PART;
+    p->gsize = 2;
+    p->n = n + v;  // compact row length
+    p->d1 = v;
+    p->d2 = d->d2 > 0 ? d->d2 : n;
   } else {  // GO_JSP_INT, builtins.py:408-456
     const int nj = d->n_jobs, pj = d->ops_per_job;
     if (nj < 1 || pj < 1 || nj > 255 * 4 || (long long)nj * pj > 32767 || !d->jsp_machine || !d->jsp_duration)
@@ -403,8 +439,10 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
     p->gsize = 2;
     p->scratch_ints = go::jsp_scratch_ints(nj, nm);
   }
-  p->d1 = 1;
-  p->d2 = p->n;
+  if (p->row_kind != go::RK_PART) {
+    p->d1 = 1;
+    p->d2 = p->n;
+  }
   p->img_bytes = img.size();
   CK(cudaMalloc(&p->d_img, img.size()));
   CK(cudaMemcpy(p->d_img, img.data(), img.size(), cudaMemcpyHostToDevice));
@@ -445,12 +483,78 @@ void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_o
   *E_out = E0;
 }
 
+// ---- solution layout at the ABI (genes[m][d1*d2] + sizes[m][d1]) <-> device rows --
+void to_device_rows(const go_problem* p, const int32_t* genes, const int32_t* sizes, int m,
+                    std::vector<short>& out) {
+  out.assign((size_t)m * p->n, 0);
+  if (p->family == 1 && p->row_kind == go::RK_PART) {
+    for (int s = 0; s < m; ++s) {
+      short* o = out.data() + (size_t)s * p->n;
+      int at = 0;
+      for (int r = 0; r < p->d1; ++r) {
+        const int len = sizes ? sizes[(size_t)s * p->d1 + r] : 0;
+        for (int q = 0; q < len && at < p->n_cells; ++q)
+          o[at++] = (short)genes[(size_t)s * p->d1 * p->d2 + (size_t)r * p->d2 + q];
+        o[p->n_cells + r] = (short)len;
+      }
+    }
+    return;
+  }
+  for (size_t i = 0; i < out.size(); ++i) out[i] = (short)genes[i];
+}
+
+void from_device_rows(const go_problem* p, const short* rows, int m, int32_t* genes,
+                      int32_t* sizes) {
+  if (p->family == 1 && p->row_kind == go::RK_PART) {
+    for (int s = 0; s < m; ++s) {
+      const short* o = rows + (size_t)s * p->n;
+      int at = 0;
+      for (int r = 0; r < p->d1; ++r) {
+        const int len = o[p->n_cells + r];
+        if (sizes) sizes[(size_t)s * p->d1 + r] = len;
+        for (int q = 0; q < p->d2; ++q)
+          if (genes) genes[(size_t)s * p->d1 * p->d2 + (size_t)r * p->d2 + q] = q < len ? o[at + q] : 0;
+        at += len;
+      }
+    }
+    return;
+  }
+  for (int s = 0; s < m; ++s) {
+    if (genes)
+      for (int q = 0; q < p->n; ++q) genes[(size_t)s * p->n + q] = rows[(size_t)s * p->n + q];
+    if (sizes) sizes[s] = p->n;
+  }
+}
+
+go::RowArgs row_args(const go_problem* p) {
+  go::RowArgs x{};
+  x.off1 = p->off1;
+  x.off2 = p->off2;
+  x.off3 = p->off3;
+  x.off4 = p->off4;
+  x.capacity = p->capacity;
+  x.n_jobs = p->n_jobs;
+  x.per_job = p->per_job;
+  x.n_mach = p->n_mach;
+  x.n_cfg = p->row_kind == go::RK_PART ? p->n_cells : p->n;
+  x.lb = p->lb;
+  x.ub = p->ub;
+  x.scratch_ints = p->scratch_ints;
+  x.n_cells = p->n_cells;
+  x.d1 = p->d1;
+  x.d2 = p->d2;
+  x.tw = p->tw;
+  x.obj_weight = 1.0;
+  return x;
+}
+
 // ---- row family helpers ----------------------------------------------------------
 void* row_kernel(const go_problem* p) {
   if (p->row_kind == go::RK_QAP)
     return p->elem == E_I16 ? (void*)go_evolve_qap_i16
                             : (p->elem == E_I32 ? (void*)go_evolve_qap_i32 : (void*)go_evolve_qap_f64);
   if (p->row_kind == go::RK_KNAP) return (void*)go_evolve_knap;
+  if (p->row_kind == go::RK_PART) return (void*)go_evolve_part;
   return (void*)go_evolve_jsp;
 }
 
@@ -487,6 +591,10 @@ bool seq_supported(const go_problem* p, int id) {
     return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
            id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT;
   if (p->row_kind == go::RK_KNAP) return id == go::SEQ_FLIP || id == go::SEQ_SEG_FLIP;
+  if (p->row_kind == go::RK_PART)
+    return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
+           id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_ROW_SWAP ||
+           id == go::SEQ_ROW_SPLIT || id == go::SEQ_ROW_MERGE;
   return id == go::SEQ_RANDOM_RESET || id == go::SEQ_SEG_RESET;
 }
 
@@ -587,8 +695,8 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
   CK(cudaSetDevice(p->device));
   const int n = p->n;
   if (p->family == 1) {
-    std::vector<short> h((size_t)m * n);
-    for (size_t i = 0; i < h.size(); ++i) h[i] = (short)genes[i];
+    std::vector<short> h;
+    to_device_rows(p, genes, sizes, m, h);
     short* d_g = nullptr;
     double *d_o = nullptr, *d_p = nullptr;
     CK(cudaMalloc(&d_g, h.size() * 2));
@@ -604,6 +712,10 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
                                   : (p->elem == E_I32 ? (void*)go_eval_qap_i32 : (void*)go_eval_qap_f64);
       void* args[] = {(void*)&inst, &off1, &nn, &d_g, &d_o};
       CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
+    } else if (p->row_kind == go::RK_PART) {
+      go::RowArgs x = row_args(p);
+      void* args[] = {(void*)&inst, &x, &d_g, &d_o, &d_p};
+      CK(cudaLaunchKernel((void*)go_eval_part, dim3(m), dim3(32), args, 0, 0));
     } else if (p->row_kind == go::RK_KNAP) {
       double cap = p->capacity;
       void* args[] = {(void*)&inst, &off1, &nn, &cap, &d_g, &d_o, &d_p};
@@ -952,12 +1064,11 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
 
 int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* sizes,
                              const double* obj, const double* pen) {
-  (void)sizes;
   if (!e || !genes || !obj) return fail(GO_E_INVALID, "bad arguments");
   CK(cudaSetDevice(e->prob->device));
   const size_t P = e->P, W = e->W;
-  std::vector<short> g(P * W);
-  for (size_t i = 0; i < g.size(); ++i) g[i] = (short)genes[i];
+  std::vector<short> g;
+  to_device_rows(e->prob, genes, sizes, (int)P, g);
   std::vector<double> sc(P), pe(P);
   const double w = e->cfg.obj_weight > 0 ? e->cfg.obj_weight : 1.0;
   int best = 0;
@@ -1062,17 +1173,9 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     const go_problem* p = e->prob;
     a.team_smem = (int)row_team_bytes(p, e->TS);
     a.resync = 0;
-    x.off1 = p->off1;
-    x.capacity = p->capacity;
+    x = row_args(p);
     x.penalty_weight = c.penalty_weight;
     x.obj_weight = c.obj_weight > 0 ? c.obj_weight : 1.0;
-    x.n_jobs = p->n_jobs;
-    x.per_job = p->per_job;
-    x.n_mach = p->n_mach;
-    x.n_cfg = p->n;
-    x.lb = p->lb;
-    x.ub = p->ub;
-    x.scratch_ints = p->scratch_ints;
   } else {
     a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
     a.resync = kLayouts[e->layout].elem == E_F64;
@@ -1195,13 +1298,11 @@ int go_engine_get_population(go_engine* e, int32_t* genes, int32_t* sizes, doubl
   CK(cudaSetDevice(e->prob->device));
   CK(cudaStreamSynchronize(e->stream));
   const size_t P = e->P, W = e->W;
-  if (genes) {
+  if (genes || sizes) {
     std::vector<short> g(P * W);
     CK(cudaMemcpy(g.data(), e->genes, P * W * 2, cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < g.size(); ++i) genes[i] = g[i];
+    from_device_rows(e->prob, g.data(), (int)P, genes, sizes);
   }
-  if (sizes)
-    for (size_t i = 0; i < P; ++i) sizes[i] = e->n;
   std::vector<double> sc(P);
   CK(cudaMemcpy(sc.data(), e->scal, P * 8, cudaMemcpyDeviceToHost));
   if (obj)
@@ -1220,9 +1321,7 @@ int go_engine_get_best(go_engine* e, int32_t* genes, int32_t* sizes, double* obj
   std::vector<short> g(e->W);
   const short* src = gs.gev >= 0 ? e->best_genes + (size_t)gs.gev * e->W : e->gbest_genes;
   CK(cudaMemcpy(g.data(), src, (size_t)e->W * 2, cudaMemcpyDeviceToHost));
-  if (genes)
-    for (int i = 0; i < e->W; ++i) genes[i] = g[i];
-  if (sizes) sizes[0] = e->n;
+  from_device_rows(e->prob, g.data(), 1, genes, sizes);
   if (obj) *obj = gs.gscal * e->obj_sign_over_w;
   if (pen) *pen = gs.gpen;
   if (found_gen) *found_gen = gs.ggen;

@@ -75,6 +75,9 @@ struct RowArgs {
   int n_cfg;             // ProblemConfig.n (lns_scope)
   int lb, ub;            // integer encoding bounds
   int scratch_ints;      // per-lane int scratch (JSP decode)
+  // partition problems (VRPTW / CVRP): compact row = cells[n_cells] + sizes[d1]
+  unsigned off2, off3, off4;  // ready, due, service offsets (off1 = demands)
+  int n_cells, d1, d2, tw;
 };
 
 struct EpilogueArgs {

@@ -16,11 +16,12 @@
 #include "go_common.cuh"
 #include "go_dist.cuh"
 #include "go_evolve_perm.cuh"
+#include "go_part.cuh"
 #include "go_row.cuh"
 
 namespace go {
 
-enum RowKind { RK_QAP = 0, RK_KNAP = 1, RK_JSP = 2 };
+enum RowKind { RK_QAP = 0, RK_KNAP = 1, RK_JSP = 2, RK_PART = 3 };
 
 // Instance views (all in shared memory once staged; `use_s` reads via ld.shared).
 template <class E>
@@ -268,7 +269,19 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   QapView<E> qv;
   KnapView kv;
   JspView jv;
-  if (KIND == RK_QAP) {
+  PartView pv;
+  if (KIND == RK_PART) {
+    pv.dist = (const double*)inst;
+    pv.demand = (const double*)(inst + X.off1);
+    pv.ready = (const double*)(inst + X.off2);
+    pv.due = (const double*)(inst + X.off3);
+    pv.service = (const double*)(inst + X.off4);
+    pv.n = X.n_cells;
+    pv.d1 = X.d1;
+    pv.d2 = X.d2;
+    pv.cap = X.capacity;
+    pv.tw = X.tw;
+  } else if (KIND == RK_QAP) {
     qv.f = (const E*)inst;
     qv.d = (const E*)(inst + X.off1);
     qv.n = n;
@@ -430,27 +443,42 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         const u32 meta = la.meta[L];
         const int k = meta_k(meta);
         int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
-        RowCtx<G> c;
-        c.rng = &rng;
-        c.row = (G*)(rows + (size_t)L * rs);
-        c.n = n;
-        c.n_cfg = X.n_cfg;
-        c.lb = X.lb;
-        c.ub = X.ub;
-        c.err = 0;
-        c.nr = la.nr[L];
-        c.rlo = la.rlo + L;
-        c.rhi = la.rhi + L;
-        c.rstride = TS;
-        run_row_op(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
-        err |= c.err;
+        if (KIND == RK_PART) {
+          PartCtx c;
+          c.rng = &rng;
+          c.cells = (short*)(rows + (size_t)L * rs);
+          c.sz = c.cells + X.n_cells;
+          c.n = X.n_cells;
+          c.d1 = X.d1;
+          c.d2 = X.d2;
+          c.n_cfg = X.n_cfg;
+          c.total = X.n_cells;
+          c.err = 0;
+          run_part_op(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
+          err |= c.err;
+        } else {
+          RowCtx<G> c;
+          c.rng = &rng;
+          c.row = (G*)(rows + (size_t)L * rs);
+          c.n = n;
+          c.n_cfg = X.n_cfg;
+          c.lb = X.lb;
+          c.ub = X.ub;
+          c.err = 0;
+          c.nr = la.nr[L];
+          c.rlo = la.rlo + L;
+          c.rhi = la.rhi + L;
+          c.rstride = TS;
+          run_row_op(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
+          err |= c.err;
+          la.nr[L] = (unsigned char)(c.nr > MAX_RANGES ? MAX_RANGES + 1 : c.nr);
+        }
         if (s + 1 < k) {
           const int nq = sample_seq(s_cum, nseq, total, rng);
           if (s == 0) q1 = nq; else q2 = nq;
         }
         la.pos[L] = rng.tell();
         la.meta[L] = pack_meta(k, 0, q0, q1, q2);
-        la.nr[L] = (unsigned char)(c.nr > MAX_RANGES ? MAX_RANGES + 1 : c.nr);
       }
       team_bar(team, TS);
     }
@@ -467,7 +495,16 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       }
       const int nm = merge_ranges(nr, l_in, h_in, n, lo, hi);
       double nscal = scal, npen = pen, a0 = 0.0, a1 = 0.0, dl;
-      if (KIND == RK_QAP) {
+      if (KIND == RK_PART) {
+        double dist, pn;
+        part_eval(pv, (const short*)row, (const short*)row + X.n_cells, dist, pn);
+        nscal = __dadd_rn(0.0, __dmul_rn(X.obj_weight, dist));
+        npen = pn;
+        const double phi_c = __dadd_rn(nscal, __dmul_rn(pwt, npen));
+        const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
+        dl = __dsub_rn(phi_c, phi0);
+        rd_elem += 6u * (unsigned)X.n_cells;
+      } else if (KIND == RK_QAP) {
         unsigned rd = 0;
         const double dq = qap_delta(qv, cur, row, nm, lo, hi, rd);
         rd_elem += rd;

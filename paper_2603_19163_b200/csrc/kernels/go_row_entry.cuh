@@ -76,6 +76,28 @@ __device__ __forceinline__ void jsp_eval_entry(const void* inst, unsigned off1, 
   obj[blockIdx.x] = (double)jsp_decode(J, genes + (size_t)blockIdx.x * n_jobs * per_job, jscr);
 }
 
+__device__ __forceinline__ void part_eval_entry(const void* inst, go::RowArgs x, const short* genes,
+                                                double* obj, double* pen) {
+  if (threadIdx.x != 0) return;
+  const unsigned char* b = (const unsigned char*)inst;
+  PartView v;
+  v.dist = (const double*)b;
+  v.demand = (const double*)(b + x.off1);
+  v.ready = (const double*)(b + x.off2);
+  v.due = (const double*)(b + x.off3);
+  v.service = (const double*)(b + x.off4);
+  v.n = x.n_cells;
+  v.d1 = x.d1;
+  v.d2 = x.d2;
+  v.cap = x.capacity;
+  v.tw = x.tw;
+  const short* row = genes + (size_t)blockIdx.x * (x.n_cells + x.d1);
+  double d, p;
+  part_eval(v, row, row + x.n_cells, d, p);
+  obj[blockIdx.x] = d;
+  pen[blockIdx.x] = p;
+}
+
 }  // namespace go
 
 #define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \

@@ -19,13 +19,13 @@ from . import _native as N
 from .core import (ComparisonMode, Direction, Encoding, ObjDef, ProblemConfig, RowModeKind,
                    Solution, validate_solution)
 from .operators import (SEQ_FLIP, SEQ_INSERT, SEQ_OR_OPT, SEQ_RANDOM_RESET, SEQ_REVERSE,
-                        SEQ_SCATTER_SHUFFLE, SEQ_SEG_FLIP, SEQ_SEG_RESET, SEQ_SEG_SHUFFLE, SEQ_SWAP,
-                        SEQ_THREE_OPT)
+                        SEQ_ROW_MERGE, SEQ_ROW_SPLIT, SEQ_ROW_SWAP, SEQ_SCATTER_SHUFFLE,
+                        SEQ_SEG_FLIP, SEQ_SEG_RESET, SEQ_SEG_SHUFFLE, SEQ_SWAP, SEQ_THREE_OPT)
 
 BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph_coloring",
                  "bin_packing", "load_balancing", "jsp_int", "jsp_perm", "schedule_binary",
                  "vrp_priority", "vrp_nonlinear")
-DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int")
+DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int", "vrptw", "cvrp")
 
 
 @dataclass
@@ -301,6 +301,96 @@ class JspIntProblem(ProblemDefinition):
         return desc, (mach, dur)
 
 
+class RoutingProblem(ProblemDefinition):
+    """builtins.py:80-152 (CVRP): Σ route lengths, penalty Σ max(0, load - cap).
+    Customers are values 0..n-1 at matrix index c + 1 (index 0 = depot)."""
+
+    DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT,
+                        SEQ_ROW_SWAP, SEQ_ROW_SPLIT, SEQ_ROW_MERGE, SEQ_SEG_SHUFFLE,
+                        SEQ_SCATTER_SHUFFLE)
+    _KIND = N.GO_CVRP
+
+    def __init__(self, dist, demands, capacity, vehicles, objectives=("distance",),
+                 comparison=None):
+        self.dist = check_distance_matrix(dist)
+        self.demands = np.asarray(demands, dtype=np.float64)
+        self.capacity = float(capacity)
+        self.vehicles = int(vehicles)
+        self.n = len(self.demands)
+        if self.dist.shape[0] != self.n + 1:
+            raise ValueError(f"distance matrix has {self.dist.shape[0]} nodes, expected "
+                             f"{self.n + 1} (depot + {self.n} customers)")
+        if self.vehicles < 1:
+            raise ValueError("at least one vehicle required")
+        self.objective_names = tuple(objectives)
+        for name in self.objective_names:
+            if name not in ("distance", "vehicles"):
+                raise ValueError(f"unknown routing objective {name!r}")
+        self._cfg = ProblemConfig(encoding=Encoding.permutation(), d1=self.vehicles, d2=self.n,
+                                  n=self.n, row_mode=RowModeKind.MULTI_PARTITION,
+                                  obj_defs=tuple(ObjDef(nm) for nm in self.objective_names),
+                                  comparison=comparison)
+
+    def config(self):
+        return self._cfg
+
+    def init_matrices(self):
+        return [self.dist[1:, 1:]]
+
+    def payload_nbytes(self):
+        return self.dist.nbytes + self.demands.nbytes
+
+    def _arrays(self):
+        n1 = self.n + 1
+        z = np.zeros(n1)
+        return z, z, z
+
+    def _native_desc(self):
+        if self.objective_names != ("distance",):
+            raise TypeError("the device routing path optimises the single 'distance' objective")
+        d, dem = N.f64(self.dist), N.f64(self.demands)
+        ready, due, service = (N.f64(a) for a in self._arrays())
+        desc = N.ProblemDesc(kind=self._KIND, n=self.n, d1=self.vehicles, d2=self.n,
+                             capacity=self.capacity)
+        desc.dist, desc.demands = N.dptr(d), N.dptr(dem)
+        desc.ready, desc.due, desc.service = N.dptr(ready), N.dptr(due), N.dptr(service)
+        return desc, (d, dem, ready, due, service)
+
+
+class VrptwProblem(RoutingProblem):
+    """builtins.py:155-190: CVRP + sequential lateness (arrival = max(ready, t + d))."""
+
+    _KIND = N.GO_VRPTW
+
+    def __init__(self, dist, demands, capacity, vehicles, ready, due, service,
+                 objectives=("distance",), comparison=None):
+        super().__init__(dist, demands, capacity, vehicles, objectives=objectives,
+                         comparison=comparison)
+        self.ready = np.asarray(ready, dtype=np.float64)
+        self.due = np.asarray(due, dtype=np.float64)
+        self.service = np.asarray(service, dtype=np.float64)
+        for arr, label in ((self.ready, "ready"), (self.due, "due"), (self.service, "service")):
+            if len(arr) != self.n + 1:
+                raise ValueError(f"{label} times must cover depot + {self.n} customers")
+
+    def _arrays(self):
+        return self.ready, self.due, self.service
+
+    def payload_nbytes(self):
+        return super().payload_nbytes() + self.ready.nbytes + self.due.nbytes + \
+            self.service.nbytes
+
+
+def _routing_kwargs(instance: InstanceData) -> dict:
+    kwargs = {}
+    meta = instance.meta or {}
+    if "objectives" in meta:
+        kwargs["objectives"] = tuple(meta["objectives"])
+    if "comparison" in meta:
+        kwargs["comparison"] = meta["comparison"]
+    return kwargs
+
+
 def _need(instance: InstanceData, *names):
     missing = [f for f in names if getattr(instance, f) is None]
     if missing:
@@ -323,6 +413,16 @@ def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
     if name == "jsp_int":
         _need(instance, "jobs")
         return JspIntProblem(instance.jobs)
+    if name == "cvrp":
+        _need(instance, "distance_matrix", "demands", "capacity", "vehicles")
+        return RoutingProblem(instance.distance_matrix, instance.demands, instance.capacity,
+                              instance.vehicles, **_routing_kwargs(instance))
+    if name == "vrptw":
+        _need(instance, "distance_matrix", "demands", "capacity", "vehicles", "ready_times",
+              "due_times", "service_times")
+        return VrptwProblem(instance.distance_matrix, instance.demands, instance.capacity,
+                            instance.vehicles, instance.ready_times, instance.due_times,
+                            instance.service_times, **_routing_kwargs(instance))
     raise NotImplementedError(
         f"problem {name!r} has no B200 device path in this build "
         f"(device problems: {', '.join(DEVICE_PROBLEMS)})")

@@ -86,3 +86,46 @@ def test_knapsack_islands_and_migration():
     assert res.history["best_phi"] == out.history["best_phi"]
     assert [s.row(0).tolist() for s in res.population] == \
         [s.row(0).tolist() for s in out.population]
+
+
+def _vrptw_pair(n=None, vehicles=None, tw=True):
+    vd = I.vrptw_solomon_like() if n is None else I.vrptw_solomon_like(n=n, vehicles=vehicles,
+                                                                       seed=7)
+    if tw:
+        g = G.builtin_problem("vrptw", G.InstanceData(
+            distance_matrix=vd.dist, demands=vd.demands, capacity=vd.capacity,
+            vehicles=vd.vehicles, ready_times=vd.ready, due_times=vd.due,
+            service_times=vd.service))
+        return g, OP.Vrptw(vd.dist, vd.demands, vd.capacity, vd.vehicles, vd.ready, vd.due,
+                           vd.service)
+    g = G.builtin_problem("cvrp", G.InstanceData(distance_matrix=vd.dist, demands=vd.demands,
+                                                 capacity=vd.capacity, vehicles=vd.vehicles))
+    return g, OP.Routing(vd.dist, vd.demands, vd.capacity, vd.vehicles)
+
+
+def test_vrptw_eval_bit_exact_against_reference_golden(golden):
+    prob, ref = _vrptw_pair()
+    rows = golden["evaluate"]["vrptw100"]
+    sols = [sol_from_json(ref, row) for row in rows]
+    obj, pen = G.problems.device_evaluate(prob, [G.Solution(s.data, s.sizes, 1) for s in sols])
+    for o, p, row in zip(obj[:, 0], pen, rows):
+        assert [o] == row["obj"] and p == row["pen"]  # float64 bit-for-bit (numpy pairwise)
+
+
+@pytest.mark.parametrize("tw,n,veh,P,T,Gn,seed", [(True, 30, 6, 4, 32, 20, 21),
+                                                  (False, 30, 6, 4, 32, 20, 22),
+                                                  (True, None, None, 2, 16, 4, 42)])
+def test_routing_evolve_bit_identical_to_oracle(tw, n, veh, P, T, Gn, seed):
+    prob, ref = _vrptw_pair(n, veh, tw)
+    res = G.run(prob, G.EngineConfig(population=P, team_size=T, max_generations=Gn, seed=seed,
+                                     record_history=True))
+    out = OE.run(ref, OE.RunCfg(population=P, team_size=T, max_generations=Gn, seed=seed,
+                                record_history=True, allowed_ops=prob.device_sequences()),
+                 device_stream="philox")
+    assert res.device["error_flags"] == 0
+    assert res.history["best_phi"] == out.history["best_phi"]
+    assert res.objectives == out.objectives and res.penalty == out.penalty
+    assert [e["weight"] for e in res.final_weights["sequences"]] == [float(w) for w in out.weights]
+    got = [([int(x) for x in s.row(r)] for r in range(s.d1)) for s in res.population]
+    exp = [([int(x) for x in s.row(r)] for r in range(s.d1)) for s in out.population]
+    assert [list(map(list, g)) for g in got] == [list(map(list, e)) for e in exp]
