@@ -100,6 +100,45 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def other_configs(G, I, local, steps=5, gps=10):
+    """Device throughput on the other BASELINE shapes (C1, C3, C4, C5a, C5b):
+    a few 10-generation steps each with the B200 population rule."""
+    vd = I.vrptw_solomon_like()
+    f, dq = I.qap_random(100, 100)
+    w, v, cap = I.knapsack_random(1000, 1000)
+    probs = {
+        "C1 TSP n=51 (nint)": G.builtin_problem("tsp", G.InstanceData(
+            distance_matrix=I.tsp_random(51, 51))),
+        "C3 VRPTW n=100, 25 vehicles": G.builtin_problem("vrptw", G.InstanceData(
+            distance_matrix=vd.dist, demands=vd.demands, capacity=vd.capacity,
+            vehicles=vd.vehicles, ready_times=vd.ready, due_times=vd.due,
+            service_times=vd.service)),
+        "C4 QAP n=100": G.builtin_problem("qap", G.InstanceData(flow_matrix=f,
+                                                                distance_matrix=dq)),
+        "C5a JSP-int 20x15": G.builtin_problem("jsp_int", G.InstanceData(
+            jobs=I.jsp_random(20, 15, 2015))),
+        "C5b knapsack n=1000": G.builtin_problem("knapsack", G.InstanceData(
+            weights=w, values=v, capacity=cap)),
+    }
+    out = {}
+    for name, prob in probs.items():
+        dr = G.DeviceRun(prob, G.EngineConfig(device=local), 42)
+        done = 0
+        for _ in range(2):
+            done += gps
+            dr.run(done, None)
+        ms = 0.0
+        for _ in range(steps):
+            done += gps
+            ms += dr.run(done, None).device_ms
+        evals = dr.pop_size * 128 * gps * steps
+        out[name] = {"move_evals_per_s": evals / (ms / 1e3), "population": dr.pop_size,
+                     "ms_per_step": ms / steps, "smem_bytes": dr.smem_bytes,
+                     "layout": dr.layout, "best_after": float(dr.best().objectives[0])}
+        dr.close()
+    return out
+
+
 # ---------------------------------------------------------------------------
 def run_ours(args):
     import ctypes as C
@@ -218,6 +257,7 @@ def run_ours(args):
                                           for e in res.final_weights["sequences"]},
                     "k_weights_30s": [round(x, 4) for x in res.final_weights["k_steps"]]}
 
+    extra = other_configs(G, I, local) if (args.other_configs and world == 1) else None
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -267,6 +307,7 @@ def run_ours(args):
         "clocks": clocks,
         "cpu_baseline": cpu,
         **gap_info,
+        "other_configs": extra,
     }
     print(json.dumps(out))
     if world > 1:
@@ -330,6 +371,8 @@ def main():
     ap.add_argument("--cpu-gens", type=int, default=4)
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--other-configs", type=int, default=1,
+                    help="also measure C1/C3/C4/C5 device throughput (N=1 only)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
