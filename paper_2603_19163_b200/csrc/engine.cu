@@ -26,6 +26,7 @@
 #include "go_drv.h"
 #include "go_jit.h"
 #include "kernels/go_epilogue.cuh"
+#include "kernels/go_islands.cuh"
 #include "kernels/go_row_entry.cuh"
 #include "kernels/go_tsp_entry.cuh"
 
@@ -1364,23 +1365,47 @@ int go_elite_record_bytes(go_engine* e, int64_t* bytes) {
   return GO_OK;
 }
 
+static go::IslandArgs island_args(go_engine* e, void* buf, int top_n) {
+  go::IslandArgs a{};
+  a.P = e->P;
+  a.W = e->W;
+  a.genes = e->genes;
+  a.scal = e->scal;
+  a.pen = e->pen;
+  a.gbest_genes = e->gbest_genes;
+  a.gs = e->gs;
+  a.buf = (unsigned char*)buf;
+  int64_t rb = 0;
+  go_elite_record_bytes(e, &rb);
+  a.rec_bytes = (int)rb;
+  a.top_n = top_n;
+  a.seed = e->cfg.seed;
+  return a;
+}
+
 int go_engine_export_elites(go_engine* e, void* device_buf, int top_n) {
-  (void)e;
-  (void)device_buf;
-  (void)top_n;
-  return fail(GO_E_UNSUPPORTED, "cross-GPU island exchange not built yet");
+  if (!e || !device_buf || top_n < 1 || top_n > 64) return fail(GO_E_INVALID, "bad arguments");
+  CK(cudaSetDevice(e->prob->device));
+  go::IslandArgs a = island_args(e, device_buf, top_n);
+  go::go_export_elites_kernel<<<1, go::EPI_THREADS, 0, e->stream>>>(a);
+  CK(cudaGetLastError());
+  return GO_OK;
 }
 
 int go_engine_import_elites(go_engine* e, const void* device_buf, int n_ranks, int rank,
                             int top_n, int strategy, int64_t event_index) {
-  (void)e;
-  (void)device_buf;
-  (void)n_ranks;
-  (void)rank;
-  (void)top_n;
-  (void)strategy;
-  (void)event_index;
-  return fail(GO_E_UNSUPPORTED, "cross-GPU island exchange not built yet");
+  if (!e || !device_buf || n_ranks < 1 || rank < 0 || rank >= n_ranks || top_n < 1 || top_n > 64)
+    return fail(GO_E_INVALID, "bad arguments");
+  if (strategy == GO_MIG_HYBRID) strategy = event_index % 2 == 0 ? GO_MIG_RING : GO_MIG_GLOBAL_TOP_N;
+  CK(cudaSetDevice(e->prob->device));
+  go::IslandArgs a = island_args(e, (void*)device_buf, top_n);
+  a.n_ranks = n_ranks;
+  a.rank = rank;
+  a.strategy = strategy;
+  a.event = event_index;
+  go::go_import_elites_kernel<<<1, go::EPI_THREADS, 0, e->stream>>>(a);
+  CK(cudaGetLastError());
+  return GO_OK;
 }
 
 int go_engine_debug_counters(go_engine* e, int64_t* out, int n) {

@@ -109,6 +109,16 @@ __device__ __forceinline__ void island_range(int P, int islands, int i, int& lo,
   hi = lo + base + (i < extra ? 1 : 0);
 }
 
+__device__ __forceinline__ void put_solution_raw(short* genes, double* scal_a, double* pen_a, int W,
+                                                 int dst, const short* src, double pen,
+                                                 double scal) {
+  copy_genes(genes + (size_t)dst * W, src, W);
+  if (threadIdx.x == 0) {
+    pen_a[dst] = pen;
+    scal_a[dst] = scal;
+  }
+}
+
 __device__ __forceinline__ void put_solution(const EpilogueArgs& A, int dst, const short* src,
                                              double pen, double scal) {
   copy_genes(A.genes + (size_t)dst * A.W, src, A.W);

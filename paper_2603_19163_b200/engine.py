@@ -101,6 +101,7 @@ class EngineConfig:
     device: int = 0
     teams_per_cta: int = 0          # evolver teams sharing one CTA's staged instance (0 = auto)
     evolver_offset: int = 0         # global index of local evolver 0 (multi-GPU islands)
+    distributed: bool = False       # ranks of the torch.distributed group are islands (islands.py)
 
     def __post_init__(self):
         if self.team_size < 1:
@@ -340,6 +341,9 @@ def run(problem: ProblemDefinition, config: EngineConfig,
         best_known: float | None = None) -> RunResult:
     """engine.py:601-614: replicas run the whole pipeline with seed + i and
     the comparison-best result is returned."""
+    if config.distributed:
+        from .islands import run_distributed
+        return run_distributed(problem, config, best_known)
     if config.replicas == 1:
         return _run_single(problem, config, config.seed, best_known)
     results = [_run_single(problem, config, config.seed + i, best_known)
@@ -358,7 +362,8 @@ class DeviceRun:
     use it directly to keep the engine resident between calls."""
 
     def __init__(self, problem: ProblemDefinition, config: EngineConfig, seed: int,
-                 initial_population: list[Solution] | None = None):
+                 initial_population: list[Solution] | None = None,
+                 init_rng: random.Random | None = None):
         self.t_start = time.perf_counter()
         self.problem, self.config, self.seed = problem, config, seed
         cfg = problem.config()
@@ -403,7 +408,7 @@ class DeviceRun:
 
         if initial_population is None:
             pop = initialize_population(problem, pop_size, config.oversample_factor,
-                                        derived_rng(seed, _STREAM_INIT), dev)
+                                        init_rng or derived_rng(seed, _STREAM_INIT), dev)
         else:
             pop = [s.copy() for s in initial_population]
             evaluate_many(problem, pop, dev)
