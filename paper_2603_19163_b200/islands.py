@@ -81,18 +81,27 @@ class DeviceIsland:
 
 
 def exchange_round(island, world, rank, top_n, strategy, event, dist, send, recv):
-    """One migration event: export -> all_gather -> import."""
+    """One migration event: export -> all_gather -> import.  Device buffers
+    go straight to NCCL; a gloo group (CPU tests, several ranks sharing one
+    GPU) stages the few-KB records through host memory."""
+    import torch
     island.export(send, top_n)
     with island.collective_stream():
-        parts = list(recv.chunk(world))
-        dist.all_gather(parts, send)
-        if parts[0].data_ptr() != recv.data_ptr():  # all_gather may not write in place
-            recv.copy_(__import__("torch").cat(parts))
+        staged = send.is_cuda and dist.get_backend() != "nccl"
+        src = send.cpu() if staged else send
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(parts, src)
+        recv.copy_(torch.cat(parts))
     island.import_(recv, world, rank, top_n, strategy, event)
+
+
+def _coll_device(dist, device):
+    return device if dist.get_backend() == "nccl" else "cpu"
 
 
 def agree_stop(local_stop, dist, device):
     import torch
+    device = _coll_device(dist, device)
     t = torch.tensor([1 if local_stop else 0], dtype=torch.int32, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return bool(t.item())
@@ -128,6 +137,7 @@ def best_over_ranks(problem, best, dist, world, device="cpu"):
     (penalty, objective, rank) then of the winner's genes."""
     import torch
     cfg = problem.config()
+    device = _coll_device(dist, device)
     row = torch.tensor([best.penalty, float(best.objectives[0])], dtype=torch.float64,
                        device=device)
     rows = [torch.zeros_like(row) for _ in range(world)]

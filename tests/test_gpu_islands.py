@@ -66,3 +66,42 @@ def test_import_matches_reference_migration(strategy, event, top_n):
     for dr, b0 in zip(drs, before):  # gathered bests refresh the global best (elite source)
         assert dr.best().objectives[0] == min(b0, cur_best)
         dr.close()
+
+
+def _rank_main(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # ranks share cuda:0
+    d = I.tsp_random(40, 5)
+    prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=d))
+    res = G.run(prob, G.EngineConfig(population=8, team_size=32, max_generations=250, seed=3,
+                                     distributed=True, device=0,
+                                     islands=G.IslandsConfig(count=world, migration="hybrid",
+                                                             interval=50, top_n=2)))
+    o = OP.Tsp(d)
+    phi = o.objective(0, OP.Sol(res.best.data, res.best.dim2_sizes))
+    q.put((rank, res.generations_completed, res.device["migration_events"], res.objectives[0],
+           phi, res.device["winner_rank"]))
+    dist.destroy_process_group()
+
+
+def test_run_distributed_two_ranks_one_gpu():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, g0, e0, b0, phi0, w0), (_, g1, e1, b1, phi1, w1) = out
+    assert g0 == g1 == 250 and e0 == e1 == 5
+    assert b0 == b1 == phi0 == phi1 and w0 == w1
