@@ -121,14 +121,18 @@ def run_island_loop(island, config, dist, rank, world, t_start, device="cpu"):
         remaining = None
         if config.time_limit_seconds is not None:
             remaining = config.time_limit_seconds - (time.perf_counter() - t_start)
-        stop = remaining is not None and remaining <= 0
-        if not stop:
+        timed_out = remaining is not None and remaining <= 0
+        if not timed_out:
             gens, stopped, _ = island.run(target, remaining)
-            stop = stopped or gens >= config.max_generations
-        if agree_stop(stop, dist, device):
+            timed_out = stopped and gens < target
+        # a deadline on any rank ends the run for all (same collective count)
+        if agree_stop(timed_out, dist, device):
             break
-        exchange_round(island, world, rank, top_n, strategy, events, dist, send, recv)
-        events += 1
+        if gens % isl.interval == 0:  # migration at the end of generation g (engine.py:730)
+            exchange_round(island, world, rank, top_n, strategy, events, dist, send, recv)
+            events += 1
+        if gens >= config.max_generations:
+            break
     return gens, events
 
 

@@ -135,7 +135,7 @@ def test_two_rank_island_exchange_over_gloo(strategy):
         p.join(timeout=60)
         assert p.exitcode == 0
     (r0, g0, e0, n0, b0, best0, w0, genes0), (r1, g1, e1, n1, b1, best1, w1, genes1) = res
-    assert g0 == g1 == 450 and e0 == e1 == 4          # exchanges at 100, 200, 300, 400
+    assert g0 == g1 == 450 and e0 == e1 == 4          # exchanges after gens 100..400
     assert n0 > 0 and n1 > 0                           # both islands received migrants
     assert best0 == best1 == min(b0)                   # comparison-best over ranks, agreed
     assert w0 == w1 and genes0 == genes1 == list(range(12))
