@@ -53,8 +53,10 @@ enum go_move_kind {
   GO_MOVE_NONE = 0,
   GO_MOVE_SWAP = 1,    /* a,b: swap positions a != b                     (op_swap)    */
   GO_MOVE_REVERSE = 2, /* a<b: reverse positions [a, b]                  (op_reverse) */
-  GO_MOVE_SEGMENT = 3  /* a=start, b=len, c=pos: remove [a,a+b), reinsert
+  GO_MOVE_SEGMENT = 3, /* a=start, b=len, c=pos: remove [a,a+b), reinsert
                           at c of the shortened row (op_insert: b=1; op_or_opt) */
+  GO_MOVE_THREE_OPT = 8 /* + variant 0..6; a<b<c = cuts i<j<k in (0, n): row a|b|c|d
+                          reconnected as op_three_opt's variant (operators.py:289-315) */
 };
 
 typedef struct go_move { int32_t kind, a, b, c; } go_move;

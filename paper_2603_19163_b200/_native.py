@@ -19,6 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libcugenopt.so"
 GO_OK, GO_E_INVALID, GO_E_CUDA, GO_E_UNSUPPORTED, GO_E_COMPILE, GO_E_NODEVICE = 0, -1, -2, -3, -4, -5
 GO_TSP, GO_VRPTW, GO_QAP, GO_JSP_INT, GO_KNAPSACK, GO_CVRP = range(6)
 MOVE_NONE, MOVE_SWAP, MOVE_REVERSE, MOVE_SEGMENT = range(4)
+MOVE_THREE_OPT = 8  # + variant 0..6
 MIG = {"ring": 0, "global_top_n": 1, "hybrid": 2}
 
 

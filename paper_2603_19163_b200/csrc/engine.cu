@@ -222,6 +222,12 @@ struct go_engine {
   double obj_sign_over_w = 1.0;
   int nseq = 0;
   int teams_per_sm = 0;
+  // crossover snapshot (EvolveArgs::snap): allocated when the registry holds
+  // OX / uniform crossover; `coop` = the grid fits one co-resident wave, so a
+  // chunk may span generations (grid barrier), else chunks are 1 generation
+  short* snap = nullptr;
+  unsigned* gbar = nullptr;
+  bool xover = false, coop = false;
   static const int kDepth = 8;
   cudaEvent_t ring_ev[kDepth] = {};
   cudaEvent_t k_beg[kDepth] = {}, k_end[kDepth] = {};  // evolve-kernel-only timing
@@ -586,21 +592,31 @@ bool choose_row(const go_problem* p, int TS, int E_req, int* layout, int* E_out,
 
 bool seq_supported(const go_problem* p, int id) {
   if (p->family == 0) return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
-                             id == go::SEQ_OR_OPT;
+                             id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT;
   if (id == go::SEQ_SEG_SHUFFLE || id == go::SEQ_SCATTER_SHUFFLE) return true;
   if (p->row_kind == go::RK_QAP)
     return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
-           id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT;
-  if (p->row_kind == go::RK_KNAP) return id == go::SEQ_FLIP || id == go::SEQ_SEG_FLIP;
+           id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_OX;
+  if (p->row_kind == go::RK_KNAP)
+    return id == go::SEQ_FLIP || id == go::SEQ_SEG_FLIP || id == go::SEQ_UNIFORM_X;
   if (p->row_kind == go::RK_PART)
     return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
            id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_ROW_SWAP ||
-           id == go::SEQ_ROW_SPLIT || id == go::SEQ_ROW_MERGE;
-  return id == go::SEQ_RANDOM_RESET || id == go::SEQ_SEG_RESET;
+           id == go::SEQ_ROW_SPLIT || id == go::SEQ_ROW_MERGE || id == go::SEQ_OX;
+  return id == go::SEQ_RANDOM_RESET || id == go::SEQ_SEG_RESET || id == go::SEQ_UNIFORM_X;
 }
 
 int launch_static_or_jit(void* fn, CUfunction jf, dim3 grid, dim3 block, size_t smem,
-                         cudaStream_t st, void** args) {
+                         cudaStream_t st, void** args, bool coop = false) {
+  if (coop) {  // all CTAs co-resident (grid barrier inside the kernel)
+    if (jf) {
+      CU(gohost::drv()->LaunchCooperativeKernel(jf, grid.x, grid.y, grid.z, block.x, block.y,
+                                                block.z, (unsigned)smem, (CUstream)st, args));
+    } else {
+      CK(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, st));
+    }
+    return GO_OK;
+  }
   if (jf) {
     CU(gohost::drv()->LaunchKernel(jf, grid.x, grid.y, grid.z, block.x, block.y, block.z, (unsigned)smem,
                       (CUstream)st, args, nullptr));
@@ -772,6 +788,8 @@ int go_delta_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, in
     else if (mv.kind == GO_MOVE_REVERSE) ok = mv.a >= 0 && mv.a < mv.b && mv.b < n;
     else if (mv.kind == GO_MOVE_SEGMENT)
       ok = mv.b >= 1 && mv.a >= 0 && mv.a + mv.b <= n && mv.c >= 0 && mv.c <= n - mv.b;
+    else if (mv.kind >= GO_MOVE_THREE_OPT && mv.kind < GO_MOVE_THREE_OPT + 7)
+      ok = 0 < mv.a && mv.a < mv.b && mv.b < mv.c && mv.c < n;
     else ok = mv.kind == GO_MOVE_NONE;
     if (!ok) return fail(GO_E_INVALID, "malformed move at index " + std::to_string(i));
   }
@@ -960,6 +978,7 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   }
   e->teams_per_sm = blocks * e->E;
   if (blocks < 1) return fail(GO_E_UNSUPPORTED, "evolve kernel does not fit on an SM");
+  e->coop = (long long)blocks * p->dev.sm >= e->grid;
 
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   const size_t P = e->P, W = e->W;
@@ -1006,7 +1025,7 @@ int go_engine_destroy(go_engine* e) {
   void* bufs[] = {e->genes, e->best_genes, e->gbest_genes, e->scratch, e->scal, e->pen,
                   e->best_scal, e->best_pen, e->best_gen, e->usage, e->impr, e->k_usage,
                   e->k_impr, e->agg, e->rec_scal, e->rec_pen, e->temps, e->reg, e->gs,
-                  e->history};
+                  e->history, e->snap, e->gbar};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_temps) cudaFreeHost(e->h_temps);
@@ -1058,6 +1077,12 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
   for (int j = 0; j < 3; ++j) r.kw[j] = k_weights[j];
   e->nseq = nseq;
   CK(cudaSetDevice(e->prob->device));
+  e->xover = false;
+  for (int i = 0; i < nseq; ++i) e->xover |= ids[i] == go::SEQ_OX || ids[i] == go::SEQ_UNIFORM_X;
+  if (e->xover && !e->snap) {
+    CK(cudaMalloc(&e->snap, (size_t)2 * e->P * e->W * 2));
+    CK(cudaMalloc(&e->gbar, 16));
+  }
   CK(cudaMemcpyAsync(e->reg, &r, sizeof(r), cudaMemcpyHostToDevice, e->stream));
   CK(cudaStreamSynchronize(e->stream));
   return GO_OK;
@@ -1169,6 +1194,9 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.E = e->E;
   a.ev_offset = c.evolver_offset;
   a.team_stride = e->TS;
+  a.snap = e->xover ? e->snap : nullptr;
+  a.gbar = e->gbar;
+  a.islands = c.islands;
   go::RowArgs x{};
   if (e->prob->family == 1) {
     const go_problem* p = e->prob;
@@ -1237,6 +1265,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     end = std::min(end, next_mult(done, I));
     end = std::min(end, next_mult(done, EI));
     if (c.islands >= 2) end = std::min(end, next_mult(done, MI));
+    if (e->xover && !e->coop) end = done + 1;  // launch boundary = snapshot barrier
     const int slot = (int)(chunk % go_engine::kDepth);
     if (chunk >= go_engine::kDepth) {
       CK(cudaEventSynchronize(e->ring_ev[slot]));
@@ -1251,10 +1280,15 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     a.temps = dt;
     a.gen0 = done + 1;
     a.ngen = (int)(end - done);
+    if (e->xover) {  // snapshot of generation gen0 = the population at launch
+      CK(cudaMemcpyAsync(e->snap + (size_t)(a.gen0 & 1) * e->P * e->W, e->genes,
+                         (size_t)e->P * e->W * 2, cudaMemcpyDeviceToDevice, e->stream));
+      CK(cudaMemsetAsync(e->gbar, 0, 16, e->stream));
+    }
     void* args[] = {&a, &x};
     CK(cudaEventRecord(e->k_beg[slot], e->stream));
     int rc = launch_static_or_jit(e->k_evolve, e->k_evolve_jit, dim3(e->grid), dim3(e->E * e->TS),
-                                  e->smem, e->stream, args);
+                                  e->smem, e->stream, args, e->xover && a.ngen > 1);
     if (rc) return rc;
     CK(cudaEventRecord(e->k_end[slot], e->stream));
     e->k_pending[slot] = true;

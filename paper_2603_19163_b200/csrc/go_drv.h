@@ -14,6 +14,8 @@ struct Drv {
   CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**) = nullptr;
+  CUresult (*LaunchCooperativeKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                      unsigned, unsigned, CUstream, void**) = nullptr;
   CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
@@ -35,6 +37,7 @@ inline const Drv* drv() {
     GO_RESOLVE(ModuleUnload, "cuModuleUnload");
     GO_RESOLVE(ModuleGetFunction, "cuModuleGetFunction");
     GO_RESOLVE(LaunchKernel, "cuLaunchKernel");
+    GO_RESOLVE(LaunchCooperativeKernel, "cuLaunchCooperativeKernel");
     GO_RESOLVE(FuncSetAttribute, "cuFuncSetAttribute");
     GO_RESOLVE(OccupancyMaxActiveBlocksPerMultiprocessor,
                "cuOccupancyMaxActiveBlocksPerMultiprocessor");

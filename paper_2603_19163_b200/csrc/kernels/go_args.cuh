@@ -63,6 +63,15 @@ struct EvolveArgs {
   int team_stride;       // threads per team (T rounded up to 32)
   int team_smem;         // bytes of shared memory per team
   int resync;            // recompute Φ at chunk start (float matrices)
+  // crossover mates (engine.py:553-559): the island snapshot of generation g
+  // is snap[g & 1] ([2][P][n]); the host copies genes into snap[gen0 & 1]
+  // before the launch, teams write their row into snap[(g+1) & 1] after
+  // generation g and meet at a grid barrier (gbar, zeroed per launch) before
+  // generation g+1 reads it.  snap == null: no crossover in the registry.
+  short* snap;
+  unsigned* gbar;
+  int islands;           // island count (engine.py:790-798 contiguous partition)
+  int pad_x;
 };
 
 // Problem-specific extras of the row kernel (go_evolve_row.cuh).

@@ -149,10 +149,173 @@ struct Stream {
   }
 };
 
+// ---- CPython sampling helpers shared by the operator families ---------------
+// CPython random.sample's table-size rule: set method iff n > setsize
+__device__ __forceinline__ int sample_setsize(int k) {
+  int s = 21;
+  if (k > 5) {
+    long long p = 1;
+    while (p < 3LL * k) p *= 4;  // 4 ** ceil(log(3k, 4)); 3k is never a power of 4
+    s += (int)p;
+  }
+  return s;
+}
+
+// lns_scope (operators.py:130-134): max(2, ceil(min(0.1 n, 30)))
+__device__ __forceinline__ int lns_scope(int n) {
+  const double x = fmin(0.1 * (double)n, 30.0);
+  const int c = (int)ceil(x);
+  return c < 2 ? 2 : c;
+}
+
+// random.sample(range(total), m) for m <= 30: CPython's pool method (a
+// virtual pool of overrides) when total <= setsize(m), else the set method
+template <class C>
+__device__ __forceinline__ void sample_range(C& c, int total, int m, int* picks) {
+  if (total <= sample_setsize(m)) {
+    int ovi[30], ovv[30], no = 0;
+    for (int t = 0; t < m; ++t) {
+      const int jj = c.randbelow(total - t);
+      int val = jj;
+      for (int q = 0; q < no; ++q)
+        if (ovi[q] == jj) val = ovv[q];
+      picks[t] = val;
+      const int src = total - t - 1;
+      int sval = src;
+      for (int q = 0; q < no; ++q)
+        if (ovi[q] == src) sval = ovv[q];
+      bool found = false;
+      for (int q = 0; q < no; ++q)
+        if (ovi[q] == jj) {
+          ovv[q] = sval;
+          found = true;
+        }
+      if (!found) {
+        ovi[no] = jj;
+        ovv[no] = sval;
+        ++no;
+      }
+    }
+  } else {
+    for (int t = 0; t < m; ++t) {
+      int jj;
+      bool dup;
+      do {
+        jj = c.randbelow(total);
+        dup = false;
+        for (int q = 0; q < t; ++q) dup |= picks[q] == jj;
+      } while (dup);
+      picks[t] = jj;
+    }
+  }
+}
+
+// sample(range(1, n), 3) sorted (operators.py:300)
+template <class C>
+__device__ __forceinline__ void sample3_sorted(C& c, int n, int& i, int& j, int& k) {
+  const int N = n - 1;  // population 1..n-1
+  int out[3];
+  if (N <= sample_setsize(3)) {  // pool method with a virtual pool
+    int ovi[3], ovv[3], no = 0;
+    for (int t = 0; t < 3; ++t) {
+      const int jj = c.randbelow(N - t);
+      int val = jj + 1;
+      for (int q = 0; q < no; ++q)
+        if (ovi[q] == jj) val = ovv[q];
+      out[t] = val;
+      // pool[jj] = pool[N - t - 1]
+      const int src = N - t - 1;
+      int sval = src + 1;
+      for (int q = 0; q < no; ++q)
+        if (ovi[q] == src) sval = ovv[q];
+      bool found = false;
+      for (int q = 0; q < no; ++q)
+        if (ovi[q] == jj) {
+          ovv[q] = sval;
+          found = true;
+        }
+      if (!found) {
+        ovi[no] = jj;
+        ovv[no] = sval;
+        ++no;
+      }
+    }
+  } else {  // set method
+    for (int t = 0; t < 3; ++t) {
+      int jj;
+      bool dup;
+      do {
+        jj = c.randbelow(N);
+        dup = false;
+        for (int q = 0; q < t; ++q) dup |= (out[q] == jj + 1);
+      } while (dup);
+      out[t] = jj + 1;
+    }
+  }
+  // sort three
+  int a = out[0], b = out[1], d = out[2], t;
+  if (a > b) { t = a; a = b; b = t; }
+  if (b > d) { t = b; b = d; d = t; }
+  if (a > b) { t = a; a = b; b = t; }
+  i = a;
+  j = b;
+  k = d;
+}
+
 // ---- barriers -------------------------------------------------------------
 __device__ __forceinline__ void team_bar(int team, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(nthreads) : "memory");
 }
+
+// ---- grid barrier (crossover snapshots) -------------------------------------
+// Every team's lane 0 arrives once per epoch; the launch is cooperative (all
+// teams co-resident), the counter is zeroed by the host before the launch.
+__device__ __forceinline__ void grid_team_barrier(unsigned* ctr, unsigned target, int lane,
+                                                  int team, int nthreads) {
+  team_bar(team, nthreads);  // the team's snapshot writes are issued
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  team_bar(team, nthreads);
+}
+
+// Island membership of evolver `ev` among P (engine.py:790-798) and the mate
+// draw of pick_mate (engine.py:553-559): None (no draw) for a 1-member island.
+struct MateSel {
+  const short* rows;  // snapshot of this generation, [P][n]
+  int start, size, pos, n;
+  __device__ __forceinline__ void init(const short* snap_g, int ev, int P, int islands, int n_) {
+    rows = snap_g;
+    n = n_;
+    const int base = P / islands, extra = P - base * islands;
+    int isl;
+    if (ev < extra * (base + 1)) {
+      isl = ev / (base + 1);
+      start = isl * (base + 1);
+      size = base + 1;
+    } else {
+      isl = extra + (ev - extra * (base + 1)) / base;
+      start = extra * (base + 1) + (isl - extra) * base;
+      size = base;
+    }
+    pos = ev - start;
+  }
+  template <class R>
+  __device__ __forceinline__ const short* pick(R& rng) const {
+    if (rows == nullptr || size <= 1) return nullptr;
+    int j = rng.randbelow(size - 1);
+    j += j >= pos;
+    return rows + (size_t)(start + j) * n;
+  }
+};
 
 // ---- cp.async.bulk staging (global -> shared, one elected thread) ---------
 __device__ __forceinline__ u32 smem_u32(const void* p) {

@@ -124,6 +124,7 @@ __device__ __forceinline__ void run_perm_op(int kind, PermCtx<Policy>& c) {
     case SEQ_INSERT: bi_insert(c); break;
     case SEQ_REVERSE: bi_reverse(c); break;
     case SEQ_OR_OPT: bi_or_opt(c); break;
+    case SEQ_THREE_OPT: bi_three_opt(c); break;
     default:
       if (kind >= SEQ_CUSTOM_BASE) Custom::run(kind - SEQ_CUSTOM_BASE, c);
       else c.err |= ERR_UNKNOWN_SEQ;

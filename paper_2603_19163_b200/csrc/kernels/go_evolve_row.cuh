@@ -229,6 +229,217 @@ __device__ __forceinline__ int jsp_decode(const JspView& J, const G* prio, int* 
   return span;
 }
 
+// ---- op_guided_rebuild (operators.py:501-571) on a lane row ---------------------
+// Every trial is scored with the run's scalar fitness (phi_fn, engine.py:548-550).
+// QAP and JSP-int are integer-valued: QAP trial scores are exact int64 offsets
+// (adjacent-swap deltas walking the value from the row end to position 0) and
+// JSP scores are makespans, so first-minimum choices equal the reference's
+// full re-evaluations.  Knapsack and partition scores are float64 in the
+// reference's expression order (partitions: a full part_eval per trial).
+
+// sorted descending (the single-row order of sorted(cells, key=(r, -p)))
+__device__ __forceinline__ void sort_desc(int* a, int m) {
+  for (int i = 1; i < m; ++i) {
+    const int v = a[i];
+    int j = i;
+    while (j > 0 && a[j - 1] < v) {
+      a[j] = a[j - 1];
+      --j;
+    }
+    a[j] = v;
+  }
+}
+
+template <class G>
+__device__ __forceinline__ void row_pop(G* r, int size, int p) {
+  for (int q = p; q < size - 1; ++q) r[q] = r[q + 1];
+}
+
+// QAP swap delta of positions (r, s) of permutation row (general F, D)
+template <class E, class G>
+__device__ __forceinline__ typename AccOf<E>::T qap_swap_delta(const QapView<E>& q, const G* row,
+                                                               int n, int r, int s) {
+  typedef typename AccOf<E>::T A;
+  const int pr = row[r], ps = row[s];
+  A d = (q.F(r, r) - q.F(s, s)) * (q.D(ps, ps) - q.D(pr, pr)) +
+        (q.F(r, s) - q.F(s, r)) * (q.D(ps, pr) - q.D(pr, ps));
+  for (int k = 0; k < n; ++k) {
+    if (k == r || k == s) continue;
+    const int pk = row[k];
+    d += (q.F(r, k) - q.F(s, k)) * (q.D(ps, pk) - q.D(pr, pk)) +
+         (q.F(k, r) - q.F(k, s)) * (q.D(pk, ps) - q.D(pk, pr));
+  }
+  return d;
+}
+
+template <class E, class G, class R>
+__device__ void gr_qap(const QapView<E>& q, G* row, int n, int n_cfg, R& rng) {
+  typedef typename AccOf<E>::T A;
+  if (n < 3) return;
+  const int ls = lns_scope(n_cfg);
+  const int m = ls < n - 1 ? ls : n - 1;
+  int picks[30];
+  G taken[30];
+  sample_range(rng, n, m, picks);
+  sort_desc(picks, m);
+  int size = n;
+  for (int t = 0; t < m; ++t) {  // _row_remove in (r, -p) order
+    taken[t] = row[picks[t]];
+    row_pop(row, size, picks[t]);
+    --size;
+  }
+  for (int t = 0; t < m; ++t) row[size++] = taken[t];  // park at the row end
+  for (int t = 0; t < m; ++t) {
+    const G v = taken[t];
+    int q0 = 0;
+    while (row[q0] != v) ++q0;
+    row_pop(row, n, q0);
+    row[n - 1] = v;  // trial n-1 (score offset 0), then walk down to 0
+    A sc = 0, best = 0;
+    int bp = n - 1;
+    for (int p = n - 1; p >= 1; --p) {
+      sc += qap_swap_delta(q, row, n, p - 1, p);
+      const G tmp = row[p - 1];
+      row[p - 1] = row[p];
+      row[p] = tmp;
+      if (sc <= best) {  // lower positions win ties: first minimum in 0..n-1
+        best = sc;
+        bp = p - 1;
+      }
+    }
+    for (int p = 0; p < bp; ++p) row[p] = row[p + 1];  // v from 0 to bp
+    row[bp] = v;
+  }
+}
+
+// binary / integer: coordinate-greedy reset of a scatter of cells
+template <int KIND, class G, class R>
+__device__ void gr_cells(const KnapView& kv, const JspView& jv, G* row, int n, int n_cfg, int lb,
+                         int ub, double wobj, double pw, int* scratch, R& rng) {
+  if (n == 0) return;
+  const int ls = lns_scope(n_cfg);
+  const int m = ls < n ? ls : n;
+  int cells[30];
+  sample_range(rng, n, m, cells);
+  if (KIND == RK_KNAP) {
+    lb = 0;
+    ub = 1;
+  }
+  const int D = ub - lb + 1;
+  int dom[16];
+  int nd = D;
+  if (D > 16) {  // sorted(rng.sample(domain, 16))
+    sample_range(rng, D, 16, dom);
+    for (int i = 1; i < 16; ++i) {
+      const int v = dom[i];
+      int j = i;
+      while (j > 0 && dom[j - 1] > v) {
+        dom[j] = dom[j - 1];
+        --j;
+      }
+      dom[j] = v;
+    }
+    nd = 16;
+    for (int i = 0; i < 16; ++i) dom[i] += lb;
+  } else {
+    for (int i = 0; i < D; ++i) dom[i] = lb + i;
+  }
+  double V = 0.0, W = 0.0;
+  if (KIND == RK_KNAP)
+    for (int p = 0; p < n; ++p) {
+      const double x = (double)row[p];
+      V += kv.v[p] * x;
+      W += kv.w[p] * x;
+    }
+  for (int t = 0; t < m; ++t) {
+    const int p = cells[t];
+    const G old = row[p];
+    int bv = (int)old;
+    double bs = 0.0;
+    bool have = false;
+    for (int i = 0; i < nd; ++i) {
+      const int v = dom[i];
+      double sc;
+      if (KIND == RK_KNAP) {
+        const double dx = (double)(v - (int)old);
+        const double nv = V + kv.v[p] * dx, nw = W + kv.w[p] * dx;
+        const double over = __dsub_rn(nw, kv.cap);
+        sc = __dadd_rn(__dadd_rn(0.0, __dmul_rn(wobj, -nv)), __dmul_rn(pw, over > 0.0 ? over : 0.0));
+      } else {
+        row[p] = (G)v;
+        sc = (double)jsp_decode(jv, row, scratch);
+      }
+      if (!have || sc < bs) {
+        have = true;
+        bs = sc;
+        bv = v;
+      }
+    }
+    row[p] = (G)bv;
+    if (KIND == RK_KNAP) {
+      const double dx = (double)(bv - (int)old);
+      V += kv.v[p] * dx;
+      W += kv.w[p] * dx;
+    }
+  }
+}
+
+// partitions (VRPTW / CVRP): operators.py:520-546 with a full evaluation per trial
+__device__ void gr_part(const PartView& pv, PartCtx& c, double wobj, double pw) {
+  const int total = c.total;
+  if (total < 3) return;
+  const int ls = lns_scope(c.n_cfg);
+  const int m = ls < total - 1 ? ls : total - 1;
+  int picks[30], rr[30], pp[30];
+  short taken[30];
+  sample_range(c, total, m, picks);
+  for (int t = 0; t < m; ++t) c.cell_at(picks[t], rr[t], pp[t]);
+  for (int i = 1; i < m; ++i) {  // sorted by (r, -p)
+    const int r0 = rr[i], p0 = pp[i];
+    int j = i;
+    while (j > 0 && (rr[j - 1] > r0 || (rr[j - 1] == r0 && pp[j - 1] < p0))) {
+      rr[j] = rr[j - 1];
+      pp[j] = pp[j - 1];
+      --j;
+    }
+    rr[j] = r0;
+    pp[j] = p0;
+  }
+  for (int t = 0; t < m; ++t) taken[t] = c.remove(rr[t], pp[t]);
+  for (int t = 0; t < m; ++t) {  // park at the end of the first open row
+    int r = 0;
+    while (r < c.d1 - 1 && c.sz[r] >= c.d2) ++r;
+    c.insert(r, c.sz[r], taken[t]);
+  }
+  for (int t = 0; t < m; ++t) {
+    const short v = taken[t];
+    int g = 0;
+    while (c.cells[g] != v) ++g;
+    int r0, p0;
+    c.cell_at(g, r0, p0);
+    c.remove(r0, p0);
+    double bs = 0.0;
+    int br = -1, bp = 0;
+    for (int r = 0; r < c.d1; ++r) {
+      if (c.sz[r] >= c.d2) continue;
+      const int lim = c.sz[r];
+      for (int pos = 0; pos <= lim; ++pos) {
+        c.insert(r, pos, v);
+        double dist, pen;
+        part_eval(pv, c.cells, c.sz, dist, pen);
+        const double sc = __dadd_rn(__dadd_rn(0.0, __dmul_rn(wobj, dist)), __dmul_rn(pw, pen));
+        c.remove(r, pos);
+        if (br < 0 || sc < bs) {
+          bs = sc;
+          br = r;
+          bp = pos;
+        }
+      }
+    }
+    c.insert(br, bp, v);
+  }
+}
+
 template <int KIND, class E, class G>
 __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X) {
   extern __shared__ __align__(128) unsigned char sm[];
@@ -376,9 +587,13 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   unsigned long long rd_pos = 0, rd_elem = 0;
   const double pwt = X.penalty_weight;
 
+  MateSel ms;
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
+    // crossover snapshot of this generation (see EvolveArgs::snap)
+    if (A.snap && gi > 0) grid_team_barrier(A.gbar, (unsigned)(gi * A.P), lane, team, TS);
+    ms.init(A.snap ? A.snap + (size_t)(g & 1) * A.P * n : nullptr, ev, A.P, A.islands, n);
 
     // ---- A: copy the current row into every lane row; draw k and sequence 0
     {
@@ -454,7 +669,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           c.n_cfg = X.n_cfg;
           c.total = X.n_cells;
           c.err = 0;
-          run_part_op(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
+          c.mates = &ms;
+          const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
+          if (kind == SEQ_GUIDED_REBUILD) gr_part(pv, c, X.obj_weight, pwt);
+          else run_part_op(kind, c);
           err |= c.err;
         } else {
           RowCtx<G> c;
@@ -469,7 +687,16 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           c.rlo = la.rlo + L;
           c.rhi = la.rhi + L;
           c.rstride = TS;
-          run_row_op(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
+          c.mates = &ms;
+          const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
+          if (kind == SEQ_GUIDED_REBUILD) {
+            if (KIND == RK_QAP) gr_qap(qv, c.row, n, X.n_cfg, c);
+            else gr_cells<KIND>(kv, jv, c.row, n, X.n_cfg, X.lb, X.ub, X.obj_weight, pwt,
+                                scratch + L * X.scratch_ints, c);
+            c.mark_all();
+          } else {
+            run_row_op(kind, c);
+          }
           err |= c.err;
           la.nr[L] = (unsigned char)(c.nr > MAX_RANGES ? MAX_RANGES + 1 : c.nr);
         }
@@ -589,6 +816,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     if (lane == 0) {
       A.rec_scal[(size_t)gi * A.P + ev] = scal;
       A.rec_pen[(size_t)gi * A.P + ev] = pen;
+    }
+    if (A.snap && gi + 1 < A.ngen) {
+      short* sn = A.snap + ((size_t)((g + 1) & 1) * A.P + ev) * n;
+      for (int p = lane; p < n; p += TS) sn[p] = (short)cur[p];
     }
     if (strictly_better(pen, scal, bpen, bscal)) {
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = (short)cur[p];

@@ -32,6 +32,7 @@ struct PartCtx {
   int n, d1, d2, n_cfg;
   int total;     // cells currently stored (n except inside an op)
   int err;
+  const MateSel* mates;  // crossover mates (engine.py:553-559); rows = cells + sizes
   __device__ __forceinline__ int randbelow(int m) { return rng->randbelow(m); }
   __device__ __forceinline__ int randrange(int lo, int hi) { return rng->randrange(lo, hi); }
   __device__ __forceinline__ int start(int r) const {
@@ -306,6 +307,16 @@ __device__ __forceinline__ void pop_scatter_shuffle(PartCtx& c) {
   rop_scatter_shuffle(rc);
 }
 
+// op_ox_crossover, MULTI_PARTITION branch (operators.py:437-448): OX over the
+// flattened active values, written back with the row sizes unchanged.  The
+// compact cells ARE the flattened values, and every mate holds all n cells.
+__device__ __forceinline__ void pop_ox(PartCtx& c) {
+  const short* mate = c.mates->pick(c);
+  if (mate == nullptr) return;
+  if (c.total < 2) return;
+  ox_in_place(c.cells, mate, c.total, c);
+}
+
 __device__ __forceinline__ void run_part_op(int kind, PartCtx& c) {
   switch (kind) {
     case SEQ_SWAP: pop_swap(c); break;
@@ -318,6 +329,7 @@ __device__ __forceinline__ void run_part_op(int kind, PartCtx& c) {
     case SEQ_ROW_MERGE: pop_row_merge(c); break;
     case SEQ_SEG_SHUFFLE: pop_seg_shuffle(c); break;
     case SEQ_SCATTER_SHUFFLE: pop_scatter_shuffle(c); break;
+    case SEQ_OX: pop_ox(c); break;
     default: c.err |= ERR_UNKNOWN_SEQ;
   }
 }

@@ -10,6 +10,10 @@
 //   SEGMENT(s,L,pos)   remove [s,s+L), reinsert at pos of the shortened row:
 //                      op_insert (L=1, :228-251), op_or_opt (L=2,3, :264-283),
 //                      demo or-opt / node-insert (demo_ops.py:48-89)
+//   THREE_OPT(i,j,k,v) row = a b c d with a=[0,i) b=[i,j) c=[j,k) d=[k,n),
+//                      reconnected as variant v of op_three_opt (:289-315):
+//                      0 a b^r c d, 1 a b c^r d, 2 a b^r c^r d, 3 a c b d,
+//                      4 a c b^r d, 5 a c^r b d, 6 a c^r b^r d
 //
 // Delta evaluation (TSP): a move rewires only the slots (p, p+1 mod n) at its
 // cut points; with the symmetric matrices the reference enforces
@@ -26,8 +30,25 @@ namespace go {
 
 enum MoveKind {
   MV_NONE = 0, MV_SWAP = 1, MV_REVERSE = 2, MV_SEGMENT = 3,
-  MV_RELOCATE_BEST = 4  // deferred: SEGMENT(a, b, best slot), resolved cooperatively
+  MV_RELOCATE_BEST = 4,  // deferred: SEGMENT(a, b, best slot), resolved cooperatively
+  MV_3OPT = 8            // 8 + variant (0..6): THREE_OPT(a=i, b=j, c=k)
 };
+
+__device__ __forceinline__ bool is_3opt(int kind) { return kind >= MV_3OPT && kind < MV_3OPT + 7; }
+
+// source position inside [i, k) of three-opt variant v (see header)
+__device__ __forceinline__ int three_opt_src(int v, int i, int j, int k, int p) {
+  const int lc = k - j, q = p - i;
+  switch (v) {
+    case 0: return p < j ? i + j - 1 - p : p;
+    case 1: return p < j ? p : j + k - 1 - p;
+    case 2: return p < j ? i + j - 1 - p : j + k - 1 - p;
+    case 3: return q < lc ? j + q : i + (q - lc);
+    case 4: return q < lc ? j + q : (j - 1) - (q - lc);
+    case 5: return q < lc ? (k - 1) - q : i + (q - lc);
+    default: return i + k - 1 - p;
+  }
+}
 
 struct Move {
   int kind, a, b, c;
@@ -45,20 +66,22 @@ __device__ __forceinline__ int move_src(const Move& m, int p) {
       return q < m.a ? q : q + m.b;
     }
     default:
+      if (is_3opt(m.kind) && p >= m.a && p < m.c) return three_opt_src(m.kind - MV_3OPT, m.a, m.b, m.c, p);
       return p;
   }
 }
 
+// packed: kind 4 bits | a, b, c 20 bits each (rows up to 2^20 positions)
 __device__ __forceinline__ unsigned long long pack_mv(const Move& m) {
-  return (unsigned long long)m.kind | ((unsigned long long)(unsigned)m.a << 3) |
-         ((unsigned long long)(unsigned)m.b << 23) | ((unsigned long long)(unsigned)m.c << 43);
+  return (unsigned long long)m.kind | ((unsigned long long)(unsigned)m.a << 4) |
+         ((unsigned long long)(unsigned)m.b << 24) | ((unsigned long long)(unsigned)m.c << 44);
 }
 __device__ __forceinline__ Move unpack_mv(unsigned long long v) {
   Move m;
-  m.kind = (int)(v & 7u);
-  m.a = (int)((v >> 3) & 0xFFFFFu);
-  m.b = (int)((v >> 23) & 0xFFFFFu);
-  m.c = (int)((v >> 43) & 0xFFFFFu);
+  m.kind = (int)(v & 15u);
+  m.a = (int)((v >> 4) & 0xFFFFFu);
+  m.b = (int)((v >> 24) & 0xFFFFFu);
+  m.c = (int)((v >> 44) & 0xFFFFFu);
   return m;
 }
 
@@ -126,6 +149,11 @@ __device__ __forceinline__ void move_slots(const Move& mv, int n, int* so, int& 
       o[0] = c - 1; o[1] = a - 1;     o[2] = a + b - 1;
       w[0] = c - 1; w[1] = c + b - 1; w[2] = a + b - 1;
     }
+    co = cw = 3;
+  } else if (is_3opt(mv.kind)) {  // cuts i-1, j-1, k-1 -> junctions i-1, i+|first|-1, k-1
+    const int first = mv.kind - MV_3OPT < 3 ? b - a : c - b;
+    o[0] = a - 1; o[1] = b - 1;         o[2] = c - 1;
+    w[0] = a - 1; w[1] = a + first - 1; w[2] = c - 1;
     co = cw = 3;
   }
   for (int i = 0; i < co; ++i) {
@@ -255,6 +283,14 @@ struct PermCtx {
     out.kind = MV_SEGMENT; out.a = start; out.b = len; out.c = pos;
   }
   __device__ __forceinline__ void insert(int i, int pos) { move_segment(i, 1, pos); }
+  // three-opt reconnection of cuts 0 < i < j < k < n, variant 0..6 (header)
+  __device__ __forceinline__ void three_opt(int i, int j, int k, int variant) {
+    if (!(0 < i && i < j && j < k && k < L->n) || variant < 0 || variant > 6) {
+      err |= ERR_OP_MOVE;
+      return;
+    }
+    out.kind = MV_3OPT + variant; out.a = i; out.b = j; out.c = k;
+  }
   // Relocate [start, start+len) to the slot of the shortened row minimising
   //   d(prev, seg[0]) + d(seg[-1], next) - d(prev, next)      (float64)
   // taking the FIRST minimum over slots 0..n-len-1 — exactly the scan of the
@@ -314,6 +350,23 @@ __device__ __forceinline__ void bi_or_opt(Ctx& c) {
   const int s = c.randbelow(n - L + 1);
   const int pos = c.randbelow(n - L + 1);
   c.move_segment(s, L, pos);
+}
+
+// op_three_opt (operators.py:289-315): _pick_row(sol, rng, 4) over the single
+// row, sorted sample(range(1, n), 3), variant randrange(7); rows shorter than
+// 4 fall back to op_reverse
+template <class Ctx>
+__device__ __forceinline__ void bi_three_opt(Ctx& c) {
+  const int n = c.size();
+  if (n < 4) {
+    bi_reverse(c);
+    return;
+  }
+  c.randbelow(1);
+  int i, j, k;
+  sample3_sorted(c, n, i, j, k);
+  const int variant = c.randbelow(7);
+  c.three_opt(i, j, k, variant);
 }
 
 // Serial resolution of a deferred relocation (probe kernel / reference path).

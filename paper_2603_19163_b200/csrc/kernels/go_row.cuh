@@ -25,6 +25,7 @@ struct RowCtx {
   short* rhi;
   int rstride;
   int err;
+  const MateSel* mates;  // crossover mates (engine.py:553-559)
 
   __device__ __forceinline__ void mark(int lo, int hi) {
     if (nr < MAX_RANGES) {
@@ -37,24 +38,6 @@ struct RowCtx {
   __device__ __forceinline__ int randbelow(int m) { return rng->randbelow(m); }
   __device__ __forceinline__ int randrange(int lo, int hi) { return rng->randrange(lo, hi); }
 };
-
-// CPython random.sample's table-size rule: set method iff n > setsize
-__device__ __forceinline__ int sample_setsize(int k) {
-  int s = 21;
-  if (k > 5) {
-    long long p = 1;
-    while (p < 3LL * k) p *= 4;  // 4 ** ceil(log(3k, 4)); 3k is never a power of 4
-    s += (int)p;
-  }
-  return s;
-}
-
-// lns_scope (operators.py:130-134): max(2, ceil(min(0.1 n, 30)))
-__device__ __forceinline__ int lns_scope(int n) {
-  const double x = fmin(0.1 * (double)n, 30.0);
-  const int c = (int)ceil(x);
-  return c < 2 ? 2 : c;
-}
 
 template <class G>
 __device__ __forceinline__ void row_reverse_range(G* r, int i, int j) {  // [i, j]
@@ -133,58 +116,6 @@ __device__ __forceinline__ void rop_or_opt(RowCtx<G>& c) {
   c.mark(s < pos ? s : pos, (s < pos ? pos : s) + L);
 }
 
-// sample(range(1, n), 3) sorted (operators.py:300)
-template <class G>
-__device__ __forceinline__ void sample3_sorted(RowCtx<G>& c, int n, int& i, int& j, int& k) {
-  const int N = n - 1;  // population 1..n-1
-  int out[3];
-  if (N <= sample_setsize(3)) {  // pool method with a virtual pool
-    int ovi[3], ovv[3], no = 0;
-    for (int t = 0; t < 3; ++t) {
-      const int jj = c.randbelow(N - t);
-      int val = jj + 1;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == jj) val = ovv[q];
-      out[t] = val;
-      // pool[jj] = pool[N - t - 1]
-      const int src = N - t - 1;
-      int sval = src + 1;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == src) sval = ovv[q];
-      bool found = false;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == jj) {
-          ovv[q] = sval;
-          found = true;
-        }
-      if (!found) {
-        ovi[no] = jj;
-        ovv[no] = sval;
-        ++no;
-      }
-    }
-  } else {  // set method
-    for (int t = 0; t < 3; ++t) {
-      int jj;
-      bool dup;
-      do {
-        jj = c.randbelow(N);
-        dup = false;
-        for (int q = 0; q < t; ++q) dup |= (out[q] == jj + 1);
-      } while (dup);
-      out[t] = jj + 1;
-    }
-  }
-  // sort three
-  int a = out[0], b = out[1], d = out[2], t;
-  if (a > b) { t = a; a = b; b = t; }
-  if (b > d) { t = b; b = d; d = t; }
-  if (a > b) { t = a; a = b; b = t; }
-  i = a;
-  j = b;
-  k = d;
-}
-
 template <class G>
 __device__ __forceinline__ void rop_three_opt(RowCtx<G>& c) {
   const int n = c.n;
@@ -257,6 +188,56 @@ __device__ __forceinline__ void rop_seg_reset(RowCtx<G>& c) {
   c.mark(i, j + 1);
 }
 
+// ---- crossover (operators.py:412-462) -------------------------------------------
+// _ox_sequence in place: the kept slice [c1, c2] stays, the other positions are
+// refilled in cyclic order from c2+1 with the mate's values (rotated to start
+// after c2) that are not in the slice.  Mate rows are read from the snapshot
+// with ld.global.cg (written by other SMs during this launch).
+template <class G, class R>
+__device__ __forceinline__ void ox_in_place(G* row, const short* mate, int n, R& rng) {
+  int c1 = rng.randbelow(n), c2 = rng.randbelow(n);
+  if (c1 > c2) {
+    const int t = c1;
+    c1 = c2;
+    c2 = t;
+  }
+  int w = c2 + 1 == n ? 0 : c2 + 1;  // next free position
+  int src = w;
+  for (int t = 0; t < n; ++t) {
+    const G v = (G)__ldcg(mate + src);
+    src = src + 1 == n ? 0 : src + 1;
+    bool kept = false;
+    for (int q = c1; q <= c2; ++q) kept |= row[q] == v;
+    if (kept) continue;
+    row[w] = v;
+    w = w + 1 == n ? 0 : w + 1;
+    if (w == c1) w = c2 + 1 == n ? 0 : c2 + 1;  // never lands inside the slice
+  }
+}
+
+template <class G>
+__device__ __forceinline__ void rop_ox(RowCtx<G>& c) {
+  const short* mate = c.mates->pick(c);
+  if (mate == nullptr) return;
+  if (c.n < 2) return;  // SINGLE_SEQ: row 0, equal sizes
+  ox_in_place(c.row, mate, c.n, c);
+  c.mark_all();
+}
+
+template <class G>
+__device__ __forceinline__ void rop_uniform_x(RowCtx<G>& c) {
+  const short* mate = c.mates->pick(c);
+  if (mate == nullptr) return;
+  int lo = c.n, hi = 0;
+  for (int p = 0; p < c.n; ++p)
+    if (c.rng->random() < 0.5) {
+      c.row[p] = (G)__ldcg(mate + p);
+      lo = p < lo ? p : lo;
+      hi = p + 1;
+    }
+  if (hi > lo) c.mark(lo, hi);
+}
+
 // ---- LNS shuffles (operators.py:468-499) -----------------------------------------
 template <class G>
 __device__ __forceinline__ void rop_seg_shuffle(RowCtx<G>& c) {
@@ -283,43 +264,7 @@ __device__ __forceinline__ void rop_scatter_shuffle(RowCtx<G>& c) {
   if (m > total) m = total;
   int picks[30];
   G vals[30];
-  // random.sample(range(total), m)
-  if (total <= sample_setsize(m)) {
-    int ovi[30], ovv[30], no = 0;
-    for (int t = 0; t < m; ++t) {
-      const int jj = c.randbelow(total - t);
-      int val = jj;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == jj) val = ovv[q];
-      picks[t] = val;
-      const int src = total - t - 1;
-      int sval = src;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == src) sval = ovv[q];
-      bool found = false;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == jj) {
-          ovv[q] = sval;
-          found = true;
-        }
-      if (!found) {
-        ovi[no] = jj;
-        ovv[no] = sval;
-        ++no;
-      }
-    }
-  } else {
-    for (int t = 0; t < m; ++t) {
-      int jj;
-      bool dup;
-      do {
-        jj = c.randbelow(total);
-        dup = false;
-        for (int q = 0; q < t; ++q) dup |= picks[q] == jj;
-      } while (dup);
-      picks[t] = jj;
-    }
-  }
+  sample_range(c, total, m, picks);  // random.sample(range(total), m)
   for (int t = 0; t < m; ++t) vals[t] = c.row[picks[t]];
   for (int i = m - 1; i >= 1; --i) {
     const int j = c.randbelow(i + 1);
@@ -345,6 +290,8 @@ __device__ __forceinline__ void run_row_op(int kind, RowCtx<G>& c) {
     case SEQ_SEG_RESET: rop_seg_reset(c); break;
     case SEQ_SEG_SHUFFLE: rop_seg_shuffle(c); break;
     case SEQ_SCATTER_SHUFFLE: rop_scatter_shuffle(c); break;
+    case SEQ_OX: rop_ox(c); break;
+    case SEQ_UNIFORM_X: rop_uniform_x(c); break;
     default: c.err |= ERR_UNKNOWN_SEQ;
   }
 }

@@ -129,3 +129,22 @@ def test_routing_evolve_bit_identical_to_oracle(tw, n, veh, P, T, Gn, seed):
     got = [([int(x) for x in s.row(r)] for r in range(s.d1)) for s in res.population]
     exp = [([int(x) for x in s.row(r)] for r in range(s.d1)) for s in out.population]
     assert [list(map(list, g)) for g in got] == [list(map(list, e)) for e in exp]
+
+
+def test_qap_ox_crossover_uneven_islands():
+    """OX mates come from the evolver's own island of the generation snapshot
+    (engine.py:553-559, :687-689); 7 evolvers over 3 islands = sizes 3/2/2."""
+    prob, ref = _pair("qap", True)
+    kw = dict(population=7, team_size=32, max_generations=24, seed=77, record_history=True,
+              elite_injection_interval=9)
+    res = G.run(prob, G.EngineConfig(islands=G.IslandsConfig(count=3, migration="ring",
+                                                             interval=8), **kw))
+    out = OE.run(ref, OE.RunCfg(islands=3, migration="ring", migration_interval=8,
+                                elite_interval=9, allowed_ops=prob.device_sequences(),
+                                population=7, team_size=32, max_generations=24, seed=77,
+                                record_history=True), device_stream="philox")
+    assert 12 in [e["id"] for e in res.final_weights["sequences"]]
+    assert res.history["best_phi"] == out.history["best_phi"]
+    assert [e["weight"] for e in res.final_weights["sequences"]] == [float(w) for w in out.weights]
+    assert [s.row(0).tolist() for s in res.population] == \
+        [s.row(0).tolist() for s in out.population]

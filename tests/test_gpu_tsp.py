@@ -73,11 +73,21 @@ def _apply(t, mv):
         seg = t[a:a + b]
         rest = t[:a] + t[a + b:]
         t = rest[:c] + seg + rest[c:]
+    elif kind >= N.MOVE_THREE_OPT:  # operators.py:289-315 reconnection variants
+        A, B, C, D = t[:a], t[a:b], t[b:c], t[c:]
+        v = kind - N.MOVE_THREE_OPT
+        parts = [(A, B[::-1], C, D), (A, B, C[::-1], D), (A, B[::-1], C[::-1], D), (A, C, B, D),
+                 (A, C, B[::-1], D), (A, C[::-1], B, D), (A, C[::-1], B[::-1], D)][v]
+        t = [x for part in parts for x in part]
     return t
 
 
 def _random_move(rng, n):
-    kind = rng.choice([N.MOVE_SWAP, N.MOVE_REVERSE, N.MOVE_SEGMENT])
+    kind = rng.choice([N.MOVE_SWAP, N.MOVE_REVERSE, N.MOVE_SEGMENT] +
+                      ([N.MOVE_THREE_OPT] if n >= 4 else []))
+    if kind == N.MOVE_THREE_OPT:
+        i, j, k = sorted(rng.sample(range(1, n), 3))
+        return (kind + rng.randrange(7), i, j, k)
     if kind == N.MOVE_SWAP:
         a = rng.randrange(n)
         b = rng.randrange(n - 1)
@@ -108,7 +118,9 @@ def test_delta_chains_match_oracle(lib, n, integral):
         if n >= 4 and rng.random() < 0.3:  # force the wrap / adjacency edge cases
             chain[0] = rng.choice([(N.MOVE_SWAP, 0, n - 1, 0), (N.MOVE_REVERSE, 0, n - 1, 0),
                                    (N.MOVE_SWAP, 1, 2, 0), (N.MOVE_SEGMENT, 0, 2, n - 2),
-                                   (N.MOVE_SEGMENT, n - 2, 2, 0), (N.MOVE_SEGMENT, 1, 1, 1)])
+                                   (N.MOVE_SEGMENT, n - 2, 2, 0), (N.MOVE_SEGMENT, 1, 1, 1),
+                                   (N.MOVE_THREE_OPT + 3, 1, 2, n - 1),
+                                   (N.MOVE_THREE_OPT + 6, 1, n - 2, n - 1)])
         tours.append(t)
         moves.append(chain)
     g = np.array(tours, dtype=np.int32)
@@ -145,7 +157,7 @@ def _engine_vs_oracle(dist, P, T, G, seed, custom=False, islands=1, migration="r
     ocfg = OE.RunCfg(population=P, team_size=T, max_generations=G, seed=seed,
                      record_history=True, elite_interval=elite, islands=islands,
                      migration=migration, migration_interval=mig_interval,
-                     allowed_ops=(0, 1, 2, 3),
+                     allowed_ops=prob.device_sequences(),
                      custom_ops=tuple((i, nm, f, 1.0) for i, nm, f in OM.TSP_DELTA) if custom else ())
     ref = OE.run(OP.Tsp(dist), ocfg, device_stream="philox")
     return res, ref
