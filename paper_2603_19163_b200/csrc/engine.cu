@@ -166,6 +166,8 @@ size_t cta_smem(int layout, int n, int E, int TS, size_t inst_img_bytes) {
 
 }  // namespace
 
+constexpr size_t kStackBytes = 4096;
+
 // ---- handles -------------------------------------------------------------------
 struct go_problem {
   int kind = 0, n = 0, d1 = 1, d2 = 0, device = 0;
@@ -227,6 +229,7 @@ struct go_engine {
   // chunk may span generations (grid barrier), else chunks are 1 generation
   short* snap = nullptr;
   unsigned* gbar = nullptr;
+  short* lane_rows = nullptr;  // TSP whole-row operators: [P][T][2][n]
   bool xover = false, coop = false;
   static const int kDepth = 8;
   cudaEvent_t ring_ev[kDepth] = {};
@@ -591,9 +594,13 @@ bool choose_row(const go_problem* p, int TS, int E_req, int* layout, int* E_out,
 }
 
 bool seq_supported(const go_problem* p, int id) {
-  if (p->family == 0) return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
-                             id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT;
-  if (id == go::SEQ_SEG_SHUFFLE || id == go::SEQ_SCATTER_SHUFFLE) return true;
+  if (p->family == 0)
+    return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
+           id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_OX ||
+           id == go::SEQ_SEG_SHUFFLE || id == go::SEQ_SCATTER_SHUFFLE ||
+           id == go::SEQ_GUIDED_REBUILD;
+  if (id == go::SEQ_SEG_SHUFFLE || id == go::SEQ_SCATTER_SHUFFLE || id == go::SEQ_GUIDED_REBUILD)
+    return true;
   if (p->row_kind == go::RK_QAP)
     return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
            id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_OX;
@@ -980,6 +987,11 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   if (blocks < 1) return fail(GO_E_UNSUPPORTED, "evolve kernel does not fit on an SM");
   e->coop = (long long)blocks * p->dev.sm >= e->grid;
 
+  // per-thread stack: the row kernels' guided rebuild nests numpy's recursive
+  // pairwise sum (go_part.cuh) below ~1 KB of frames; the default limit is 1 KB
+  size_t stack = 0;
+  CK(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+  if (stack < kStackBytes) CK(cudaDeviceSetLimit(cudaLimitStackSize, kStackBytes));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   const size_t P = e->P, W = e->W;
   CK(cudaMalloc(&e->genes, P * W * 2));
@@ -1025,7 +1037,7 @@ int go_engine_destroy(go_engine* e) {
   void* bufs[] = {e->genes, e->best_genes, e->gbest_genes, e->scratch, e->scal, e->pen,
                   e->best_scal, e->best_pen, e->best_gen, e->usage, e->impr, e->k_usage,
                   e->k_impr, e->agg, e->rec_scal, e->rec_pen, e->temps, e->reg, e->gs,
-                  e->history, e->snap, e->gbar};
+                  e->history, e->snap, e->gbar, e->lane_rows};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_temps) cudaFreeHost(e->h_temps);
@@ -1083,6 +1095,12 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
     CK(cudaMalloc(&e->snap, (size_t)2 * e->P * e->W * 2));
     CK(cudaMalloc(&e->gbar, 16));
   }
+  bool whole_row = false;
+  for (int i = 0; i < nseq; ++i)
+    whole_row |= ids[i] == go::SEQ_OX || ids[i] == go::SEQ_SEG_SHUFFLE ||
+                 ids[i] == go::SEQ_SCATTER_SHUFFLE || ids[i] == go::SEQ_GUIDED_REBUILD;
+  if (e->prob->family == 0 && whole_row && !e->lane_rows)
+    CK(cudaMalloc(&e->lane_rows, (size_t)e->P * e->T * 2 * e->n * 2));
   CK(cudaMemcpyAsync(e->reg, &r, sizeof(r), cudaMemcpyHostToDevice, e->stream));
   CK(cudaStreamSynchronize(e->stream));
   return GO_OK;
@@ -1195,6 +1213,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.ev_offset = c.evolver_offset;
   a.team_stride = e->TS;
   a.snap = e->xover ? e->snap : nullptr;
+  a.lane_rows = e->lane_rows;
   a.gbar = e->gbar;
   a.islands = c.islands;
   go::RowArgs x{};

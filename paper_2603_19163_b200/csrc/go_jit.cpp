@@ -127,7 +127,7 @@ int jit_max_threads() {
   return (v >= 128 && v <= 1024 && v % 32 == 0) ? v : 512;
 }
 
-static const char* kHeaders[] = {"go_common.cuh", "go_dist.cuh", "go_perm.cuh", "go_args.cuh",
+static const char* kHeaders[] = {"go_common.cuh", "go_dist.cuh", "go_perm.cuh", "go_perm_lns.cuh", "go_args.cuh",
                                  "go_evolve_perm.cuh", "go_tsp_entry.cuh"};
 
 int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,

@@ -72,6 +72,7 @@ struct EvolveArgs {
   unsigned* gbar;
   int islands;           // island count (engine.py:790-798 contiguous partition)
   int pad_x;
+  short* lane_rows;      // permutation kernel: [P][T][2][n] rows of deferred whole-row ops
 };
 
 // Problem-specific extras of the row kernel (go_evolve_row.cuh).

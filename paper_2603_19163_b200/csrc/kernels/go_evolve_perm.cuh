@@ -23,6 +23,7 @@
 #include "go_args.cuh"
 #include "go_common.cuh"
 #include "go_perm.cuh"
+#include "go_perm_lns.cuh"
 
 namespace go {
 
@@ -46,6 +47,7 @@ struct TeamShared {
   int k_usage[3];
   int k_impr[3];
   int nreq;                        // pending cooperative relocations this step
+  int ndreq;                       // pending deferred whole-row operators this step
   unsigned char cnt[16][MAX_SEQ];  // per-warp lane counts per sequence (lane sort)
 };
 
@@ -59,8 +61,9 @@ struct LaneArrays {
   u32* meta;       // [TS] k | nm | sq0 | sq1 | sq2
   unsigned short* order;  // [TS] thread slot -> logical lane
   unsigned short* req;    // [TS] lanes with a pending cooperative relocation
+  unsigned short* dreq;   // [TS] lanes with a pending deferred whole-row operator
   static __host__ __device__ unsigned bytes(int TS) {
-    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2));
+    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2 + 2));
   }
   __device__ __forceinline__ void bind(unsigned char* p, int TS) {
     mv = (u64*)p;
@@ -69,6 +72,7 @@ struct LaneArrays {
     meta = pos + TS;
     order = (unsigned short*)(meta + TS);
     req = order + TS;
+    dreq = req + TS;
   }
 };
 
@@ -80,6 +84,9 @@ __device__ __forceinline__ u32 pack_meta(int k, int nm, int q0, int q1, int q2) 
 __device__ __forceinline__ int meta_k(u32 m) { return (int)(m & 3u); }
 __device__ __forceinline__ int meta_nm(u32 m) { return (int)((m >> 2) & 3u); }
 __device__ __forceinline__ int meta_sq(u32 m, int s) { return (int)((m >> (4 + 5 * s)) & 31u); }
+// permutation kernel: the lane's chain base is its own materialised global row
+// (bit 19) number `sel` (bit 20) instead of the team's current tour
+enum : u32 { META_MAT = 1u << 19, META_SEL = 1u << 20, META_BASE = META_MAT | META_SEL };
 
 // sample_k (aos.py:147-154)
 __device__ __forceinline__ int sample_k(const double* kw, Stream& r) {
@@ -206,6 +213,11 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   la.bind(tb + PermSmem::lanes_off<Acc>(n), TS);
 
   for (int p = lane; p < n; p += TS) cur[p] = A.genes[(size_t)ev * n + p];
+  // lane-private global rows of deferred whole-row operators (2 per lane)
+  i16* const lrow = A.lane_rows ? A.lane_rows + (size_t)ev * T * 2 * n : nullptr;
+  auto lane_base = [&](int L, u32 meta) -> const i16* {
+    return (meta & META_MAT) ? lrow + ((size_t)L * 2 + ((meta & META_SEL) ? 1 : 0)) * n : cur;
+  };
   for (int i = lane; i < MAX_SEQ; i += TS) {
     ts->usage[i] = 0;
     ts->impr[i] = 0;
@@ -241,9 +253,13 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
 #else
 #define GO_TICK(slot) do { } while (0)
 #endif
+  MateSel ms;
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
+    // crossover snapshot of this generation (see EvolveArgs::snap)
+    if (A.snap && gi > 0) grid_team_barrier(A.gbar, (unsigned)(gi * A.P), lane, team, TS);
+    ms.init(A.snap ? A.snap + (size_t)(g & 1) * A.P * n : nullptr, ev, A.P, A.islands, n);
 
     // ---- A: every lane draws k and its first sequence (identity mapping) ----
     if (lane < T) {
@@ -275,7 +291,10 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
       team_bar(team, TS);
       GO_TICK(1 + 4 * s);
-      if (lane == 0) ts->nreq = 0;
+      if (lane == 0) {
+        ts->nreq = 0;
+        ts->ndreq = 0;
+      }
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
       if (wl < nseq) {
@@ -309,7 +328,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         int nm = meta_nm(meta);
         int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
         Chain C;
-        C.reset(cur, n);
+        C.reset(lane_base(L, meta), n);
         for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
         Acc d = la.delta[L];
         PermCtx<Policy> c;
@@ -320,16 +339,22 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         c.rd_pos = 0;
         c.rd_elem = 0;
         c.out.kind = MV_NONE;
-        run_perm_op<Policy, Custom>(s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)], c);
+        const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
         bool pending = false;
-        if (c.out.kind == MV_RELOCATE_BEST) {
-          la.mv[nm * TS + L] = pack_move(c.out);  // resolved below, nm unchanged
-          la.req[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+        if (perm_deferred(kind)) {  // whole-row operator: resolved by a warp below
+          la.dreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
           pending = true;
-        } else if (c.out.kind != MV_NONE) {
-          d += pol.delta(C, c.out, c.rd_pos, c.rd_elem);
-          la.mv[nm * TS + L] = pack_move(c.out);
-          ++nm;
+        } else {
+          run_perm_op<Policy, Custom>(kind, c);
+          if (c.out.kind == MV_RELOCATE_BEST) {
+            la.mv[nm * TS + L] = pack_move(c.out);  // resolved below, nm unchanged
+            la.req[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+            pending = true;
+          } else if (c.out.kind != MV_NONE) {
+            d += pol.delta(C, c.out, c.rd_pos, c.rd_elem);
+            la.mv[nm * TS + L] = pack_move(c.out);
+            ++nm;
+          }
         }
         err |= c.err;
         rd_pos += c.rd_pos;
@@ -339,7 +364,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           if (s == 0) q1 = nq; else q2 = nq;
         }
         la.pos[L] = rng.tell();
-        la.meta[L] = pack_meta(k, nm, q0, q1, q2);
+        la.meta[L] = pack_meta(k, nm, q0, q1, q2) | (meta & META_BASE);
         la.delta[L] = d;
       }
       team_bar(team, TS);
@@ -354,7 +379,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           const u32 meta = la.meta[L];
           const int nm = meta_nm(meta);
           Chain C;
-          C.reset(cur, n);
+          const i16* bse = lane_base(L, meta);
+          C.reset(bse, n);
           for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
           const Move rq = unpack_move(la.mv[nm * TS + L]);
           const int st = rq.a, len = rq.b, m = n - len;
@@ -379,7 +405,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
             if (nm > 2) q = move_src(c2, q);
             if (nm > 1) q = move_src(c1, q);
             if (nm > 0) q = move_src(c0, q);
-            const int nxt = cur[q];
+            const int nxt = bse[q];
             const Scan b = pol.cost_scan(l, nxt);
             int prev = __shfl_up_sync(0xffffffffu, nxt, 1);
             Scan a_l = __shfl_up_sync(0xffffffffu, b, 1);
@@ -427,12 +453,55 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
               if (s == 0) q1 = nq; else q2 = nq;
               la.pos[L] = rng.tell();
             }
-            la.meta[L] = pack_meta(k, nm + 1, meta_sq(meta, 0), q1, q2);
+            la.meta[L] = pack_meta(k, nm + 1, meta_sq(meta, 0), q1, q2) | (meta & META_BASE);
             la.delta[L] = d;
           }
         }
         team_bar(team, TS);
         GO_TICK(4 + 4 * s);
+      }
+
+      // ---- deferred whole-row operators (go_perm_lns.cuh): one warp per lane
+      const int ndreq = ts->ndreq;
+      if (ndreq > 0) {
+#pragma unroll 1
+        for (int r = warp; r < ndreq; r += nwarps) {
+          const int L = la.dreq[r];
+          const u32 meta = la.meta[L];
+          const int nm = meta_nm(meta), k = meta_k(meta);
+          int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+          const int kind = s_kind[meta_sq(meta, s)];
+          Chain C;
+          C.reset(lane_base(L, meta), n);
+          for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
+          const int nsel = (meta & META_MAT) && !(meta & META_SEL) ? 1 : 0;
+          i16* dst = lrow + ((size_t)L * 2 + nsel) * n;
+          i16* aux = lrow + ((size_t)L * 2 + (1 - nsel)) * n;
+          Stream rng;
+          rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+          rng.seek(la.pos[L]);
+          const int changed = perm_defer_run(pol, C, kind, dst, aux, &rng, &ms, n, wl);
+          Acc nd = la.delta[L];
+          u32 bits = meta & META_BASE;
+          int nm2 = nm;
+          if (changed) {
+            nd = perm_row_length(pol, dst, n, wl) - (Acc)phi;
+            bits = META_MAT | (nsel ? META_SEL : 0u);
+            nm2 = 0;
+          }
+          if (wl == 0) {
+            if (s + 1 < k) {
+              const int nq = sample_seq(s_cum, nseq, total, rng);
+              if (s == 0) q1 = nq; else q2 = nq;
+            }
+            la.pos[L] = rng.tell();
+            la.meta[L] = pack_meta(k, nm2, meta_sq(meta, 0), q1, q2) | bits;
+            la.delta[L] = nd;
+            rd_pos += 2u * (unsigned)n;
+            rd_elem += (unsigned)n;
+          }
+        }
+        team_bar(team, TS);
       }
     }
 
@@ -481,7 +550,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
 
     if (ts->accept) {
       Chain W;
-      W.reset(cur, n);
+      W.reset(lane_base(bl, la.meta[bl]), n);
       const int nm = meta_nm(la.meta[bl]);
       for (int i = 0; i < nm; ++i) W.push_packed(la.mv[i * TS + bl]);
       for (int p = lane; p < n; p += TS) nxt[p] = cur[W.src_all(p)];
@@ -494,6 +563,10 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     if (lane == 0) {
       A.rec_scal[(size_t)gi * A.P + ev] = phi;
       A.rec_pen[(size_t)gi * A.P + ev] = 0.0;
+    }
+    if (A.snap && gi + 1 < A.ngen) {
+      short* sn = A.snap + ((size_t)((g + 1) & 1) * A.P + ev) * n;
+      for (int p = lane; p < n; p += TS) sn[p] = cur[p];
     }
     if (strictly_better(0.0, phi, bpen, bscal)) {  // team best-ever, first occurrence
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = cur[p];

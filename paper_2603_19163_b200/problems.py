@@ -21,7 +21,7 @@ from .core import (ComparisonMode, Direction, Encoding, ObjDef, ProblemConfig, R
 from .operators import (SEQ_FLIP, SEQ_INSERT, SEQ_OR_OPT, SEQ_RANDOM_RESET, SEQ_REVERSE,
                         SEQ_ROW_MERGE, SEQ_ROW_SPLIT, SEQ_ROW_SWAP, SEQ_SCATTER_SHUFFLE,
                         SEQ_SEG_FLIP, SEQ_SEG_RESET, SEQ_SEG_SHUFFLE, SEQ_SWAP, SEQ_THREE_OPT,
-                        SEQ_OX_CROSSOVER, SEQ_UNIFORM_CROSSOVER)
+                        SEQ_OX_CROSSOVER, SEQ_UNIFORM_CROSSOVER, SEQ_GUIDED_REBUILD)
 
 BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph_coloring",
                  "bin_packing", "load_balancing", "jsp_int", "jsp_perm", "schedule_binary",
@@ -181,7 +181,8 @@ def evaluate_many(problem: ProblemDefinition, sols, device: int = 0):
 class TspProblem(ProblemDefinition):
     """builtins.py:53-77: cyclic tour length over a symmetric matrix."""
 
-    DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT)
+    DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT,
+                        SEQ_OX_CROSSOVER, SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD)
 
     def __init__(self, dist):
         self.dist = check_distance_matrix(dist)
@@ -210,7 +211,7 @@ class QapProblem(ProblemDefinition):
     """builtins.py:265-290: Σ_ij F_ij D[π_i, π_j] (matrices not symmetry-checked)."""
 
     DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT,
-                        SEQ_OX_CROSSOVER, SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE)
+                        SEQ_OX_CROSSOVER, SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD)
 
     def __init__(self, flow, dist):
         self.flow = np.asarray(flow, dtype=np.float64)
@@ -243,7 +244,7 @@ class KnapsackProblem(ProblemDefinition):
     """builtins.py:240-262: maximise v·x, penalty max(0, w·x - capacity)."""
 
     DEVICE_SEQUENCES = (SEQ_FLIP, SEQ_SEG_FLIP, SEQ_UNIFORM_CROSSOVER, SEQ_SEG_SHUFFLE,
-                        SEQ_SCATTER_SHUFFLE)
+                        SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD)
 
     def __init__(self, weights, values, capacity):
         self.weights = np.asarray(weights, dtype=np.float64)
@@ -271,7 +272,7 @@ class JspIntProblem(ProblemDefinition):
     """builtins.py:408-456: priority-decoded serial schedule generator."""
 
     DEVICE_SEQUENCES = (SEQ_RANDOM_RESET, SEQ_SEG_RESET, SEQ_UNIFORM_CROSSOVER, SEQ_SEG_SHUFFLE,
-                        SEQ_SCATTER_SHUFFLE)
+                        SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD)
 
     def __init__(self, jobs):
         self.jobs = [[(int(m), int(d)) for m, d in ops] for ops in jobs]
@@ -310,7 +311,7 @@ class RoutingProblem(ProblemDefinition):
 
     DEVICE_SEQUENCES = (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT,
                         SEQ_ROW_SWAP, SEQ_ROW_SPLIT, SEQ_ROW_MERGE, SEQ_OX_CROSSOVER,
-                        SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE)
+                        SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD)
     _KIND = N.GO_CVRP
 
     def __init__(self, dist, demands, capacity, vehicles, objectives=("distance",),

@@ -148,3 +148,28 @@ def test_qap_ox_crossover_uneven_islands():
     assert [e["weight"] for e in res.final_weights["sequences"]] == [float(w) for w in out.weights]
     assert [s.row(0).tolist() for s in res.population] == \
         [s.row(0).tolist() for s in out.population]
+
+
+@pytest.mark.parametrize("name,extra,P,T,Gn,seed", [
+    ("qap", 12, 3, 32, 6, 31), ("knap", 13, 3, 32, 6, 32), ("jsp", 13, 3, 16, 4, 33),
+    ("vrptw", 12, 3, 16, 4, 34), ("cvrp", 12, 3, 16, 4, 35)])
+def test_guided_rebuild_dominant_registry(name, extra, P, T, Gn, seed):
+    """Registry restricted to guided_rebuild (+ the family's crossover), so most
+    lanes run op_guided_rebuild (operators.py:501-571) with its phi-scored trials."""
+    if name in ("vrptw", "cvrp"):
+        prob, ref = _vrptw_pair(30, 6, name == "vrptw")
+    else:
+        prob, ref = _pair(name, True)
+    ops = (16, extra)
+    prob.device_sequences = lambda: ops
+    res = G.run(prob, G.EngineConfig(population=P, team_size=T, max_generations=Gn, seed=seed,
+                                     record_history=True))
+    out = OE.run(ref, OE.RunCfg(population=P, team_size=T, max_generations=Gn, seed=seed,
+                                record_history=True, allowed_ops=ops), device_stream="philox")
+    assert res.device["error_flags"] == 0
+    assert [e["id"] for e in res.final_weights["sequences"]] == out.ids
+    assert res.history["best_phi"] == out.history["best_phi"]
+    assert res.objectives == out.objectives and res.penalty == out.penalty
+    got = [[[int(x) for x in s.row(r)] for r in range(s.d1)] for s in res.population]
+    exp = [[[int(x) for x in s.row(r)] for r in range(s.d1)] for s in out.population]
+    assert got == exp
