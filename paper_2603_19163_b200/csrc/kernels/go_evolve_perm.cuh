@@ -553,7 +553,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       W.reset(lane_base(bl, la.meta[bl]), n);
       const int nm = meta_nm(la.meta[bl]);
       for (int i = 0; i < nm; ++i) W.push_packed(la.mv[i * TS + bl]);
-      for (int p = lane; p < n; p += TS) nxt[p] = cur[W.src_all(p)];
+      for (int p = lane; p < n; p += TS) nxt[p] = W.at(p);
       team_bar(team, TS);
       i16* t = cur;
       cur = nxt;

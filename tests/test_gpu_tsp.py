@@ -235,3 +235,24 @@ def test_time_limit_and_throughput_c2():
     o = OP.Tsp(d)
     assert res.objectives[0] == o.objective(0, OP.Sol(res.best.data, res.best.dim2_sizes))
     assert res.gap_pct is not None and res.gap_pct < 50
+
+
+@pytest.mark.parametrize("ops", [(12, 2), (14,), (15,), (16,), (4,), (12, 0), (16, 101), (14, 102)])
+def test_whole_row_operators_match_oracle(ops):
+    """OX / seg_shuffle / scatter_shuffle / guided_rebuild (go_perm_lns.cuh) and
+    3-opt, alone and chained with position-map moves and user operators."""
+    import paper_2603_19163_b200 as G_
+    from paper_2603_19163_b200.demo_ops import tsp_delta_operators
+    dist = I.tsp_random(51, 51, True)
+    prob = _tsp(dist)
+    builtin = tuple(o for o in ops if o < 100)
+    prob.device_sequences = lambda: builtin
+    custom = [o for o in tsp_delta_operators() if o.id in ops]
+    cfg = G_.EngineConfig(population=4, team_size=32, max_generations=12, seed=5,
+                          record_history=True, custom_operators=custom)
+    res = G_.run(prob, cfg)
+    ocfg = OE.RunCfg(population=4, team_size=32, max_generations=12, seed=5,
+                     record_history=True, allowed_ops=builtin,
+                     custom_ops=tuple((i, nm, f, 1.0) for i, nm, f in OM.TSP_DELTA if i in ops))
+    ref = OE.run(OP.Tsp(dist), ocfg, device_stream="philox")
+    _assert_same_run(res, ref)
