@@ -227,8 +227,8 @@ struct go_engine {
   // crossover snapshot (EvolveArgs::snap): allocated when the registry holds
   // OX / uniform crossover; `coop` = the grid fits one co-resident wave, so a
   // chunk may span generations (grid barrier), else chunks are 1 generation
-  short* snap = nullptr;
-  unsigned* gbar = nullptr;
+  short* snap = nullptr;  // [SNAP_DEPTH][P][W]
+  int* prog = nullptr;     // [P] published snapshot generation per team
   short* lane_rows = nullptr;  // TSP whole-row operators: [P][T][2][n]
   bool xover = false, coop = false;
   static const int kDepth = 8;
@@ -1037,7 +1037,7 @@ int go_engine_destroy(go_engine* e) {
   void* bufs[] = {e->genes, e->best_genes, e->gbest_genes, e->scratch, e->scal, e->pen,
                   e->best_scal, e->best_pen, e->best_gen, e->usage, e->impr, e->k_usage,
                   e->k_impr, e->agg, e->rec_scal, e->rec_pen, e->temps, e->reg, e->gs,
-                  e->history, e->snap, e->gbar, e->lane_rows};
+                  e->history, e->snap, e->prog, e->lane_rows};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_temps) cudaFreeHost(e->h_temps);
@@ -1092,8 +1092,8 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
   e->xover = false;
   for (int i = 0; i < nseq; ++i) e->xover |= ids[i] == go::SEQ_OX || ids[i] == go::SEQ_UNIFORM_X;
   if (e->xover && !e->snap) {
-    CK(cudaMalloc(&e->snap, (size_t)2 * e->P * e->W * 2));
-    CK(cudaMalloc(&e->gbar, 16));
+    CK(cudaMalloc(&e->snap, (size_t)go::SNAP_DEPTH * e->P * e->W * 2));
+    CK(cudaMalloc(&e->prog, (size_t)e->P * 4));
   }
   bool whole_row = false;
   for (int i = 0; i < nseq; ++i)
@@ -1214,7 +1214,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.team_stride = e->TS;
   a.snap = e->xover ? e->snap : nullptr;
   a.lane_rows = e->lane_rows;
-  a.gbar = e->gbar;
+  a.prog = e->prog;
   a.islands = c.islands;
   go::RowArgs x{};
   if (e->prob->family == 1) {
@@ -1300,9 +1300,11 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     a.gen0 = done + 1;
     a.ngen = (int)(end - done);
     if (e->xover) {  // snapshot of generation gen0 = the population at launch
-      CK(cudaMemcpyAsync(e->snap + (size_t)(a.gen0 & 1) * e->P * e->W, e->genes,
+      CK(cudaMemcpyAsync(e->snap + (size_t)(a.gen0 % go::SNAP_DEPTH) * e->P * e->W, e->genes,
                          (size_t)e->P * e->W * 2, cudaMemcpyDeviceToDevice, e->stream));
-      CK(cudaMemsetAsync(e->gbar, 0, 16, e->stream));
+      go::go_fill_i32_kernel<<<(e->P + 255) / 256, 256, 0, e->stream>>>(e->prog, e->P,
+                                                                        (int)a.gen0);
+      CK(cudaGetLastError());
     }
     void* args[] = {&a, &x};
     CK(cudaEventRecord(e->k_beg[slot], e->stream));

@@ -64,12 +64,16 @@ struct EvolveArgs {
   int team_smem;         // bytes of shared memory per team
   int resync;            // recompute Φ at chunk start (float matrices)
   // crossover mates (engine.py:553-559): the island snapshot of generation g
-  // is snap[g & 1] ([2][P][n]); the host copies genes into snap[gen0 & 1]
-  // before the launch, teams write their row into snap[(g+1) & 1] after
-  // generation g and meet at a grid barrier (gbar, zeroed per launch) before
-  // generation g+1 reads it.  snap == null: no crossover in the registry.
+  // is snap[g % SNAP_DEPTH] ([SNAP_DEPTH][P][n]).  The host copies genes into
+  // the slot of gen0 and sets prog[*] = gen0 before the launch; after
+  // generation g a team publishes its row in slot g+1 and then prog[ev] = g+1.
+  // A lane reading mate j's generation-g row waits for prog[j] >= g; a team
+  // overwriting slot g+1 first waits until every prog >= g+2-SNAP_DEPTH (no
+  // reader of that slot's previous generation remains).  Teams thus drift up
+  // to SNAP_DEPTH-2 generations apart instead of meeting every generation.
+  // snap == null: no crossover in the registry.
   short* snap;
-  unsigned* gbar;
+  int* prog;
   int islands;           // island count (engine.py:790-798 contiguous partition)
   int pad_x;
   short* lane_rows;      // permutation kernel: [P][T][2][n] rows of deferred whole-row ops

@@ -93,6 +93,19 @@ __device__ __noinline__ uint4 philox_refill(u32 c0, u32 k0, u32 k1) {
   return w;
 }
 
+// Counter-based access: word t of a stream is word t % 4 of Philox block t / 4,
+// so draws at known word positions can be computed by any thread in parallel.
+__device__ __forceinline__ u32 word_of(const uint4& w, u32 i) {
+  return i == 0 ? w.x : (i == 1 ? w.y : (i == 2 ? w.z : w.w));
+}
+// random.Random.random() consuming words t, t+1
+__device__ __forceinline__ double random_at(u32 k0, u32 k1, u32 t) {
+  const uint4 w = philox_refill(t >> 2, k0, k1);
+  const u32 a = word_of(w, t & 3);
+  const u32 b = (t & 3) == 3 ? philox_refill((t >> 2) + 1, k0, k1).x : word_of(w, (t & 3) + 1);
+  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
+}
+
 struct Stream {
   u32 k0, k1, ctr, w0, w1, w2, w3;
   int avail;
@@ -267,33 +280,60 @@ __device__ __forceinline__ void team_bar(int team, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(nthreads) : "memory");
 }
 
-// ---- grid barrier (crossover snapshots) -------------------------------------
-// Every team's lane 0 arrives once per epoch; the launch is cooperative (all
-// teams co-resident), the counter is zeroed by the host before the launch.
-__device__ __forceinline__ void grid_team_barrier(unsigned* ctr, unsigned target, int lane,
-                                                  int team, int nthreads) {
-  team_bar(team, nthreads);  // the team's snapshot writes are issued
-  if (lane == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    unsigned v;
+// ---- crossover snapshots: per-team progress instead of a grid barrier ---------
+enum { SNAP_DEPTH = 8 };
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// team: wait until every team has published generation >= target (one warp
+// polls prog[0..P)), then publish this team's snapshot row of generation gnext
+template <class G>
+__device__ __forceinline__ void snap_publish(short* snap, int* prog, int P, int ev, int n,
+                                             int gnext, const G* cur, int lane, int team,
+                                             int nthreads) {
+  const int target = gnext + 1 - SNAP_DEPTH;  // readers of the slot's old generation are done
+  if (lane < 32) {
     for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-      if (v >= target) break;
-      __nanosleep(64);
+      int mn = 0x7fffffff;
+      for (int t = lane; t < P; t += 32) {
+        const int v = ld_acquire(prog + t);
+        mn = v < mn ? v : mn;
+      }
+      mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+      if (mn >= target) break;
+      __nanosleep(128);
     }
-    __threadfence();
   }
   team_bar(team, nthreads);
+  short* dst = snap + ((size_t)(gnext % SNAP_DEPTH) * P + ev) * n;
+  for (int p = lane; p < n; p += nthreads) dst[p] = (short)cur[p];
+  team_bar(team, nthreads);
+  if (lane == 0) {
+    __threadfence();
+    st_release(prog + ev, gnext);
+  }
 }
 
 // Island membership of evolver `ev` among P (engine.py:790-798) and the mate
 // draw of pick_mate (engine.py:553-559): None (no draw) for a 1-member island.
+// The returned row is mate j's snapshot of generation `gen`, after waiting for
+// team j to have published it.
 struct MateSel {
   const short* rows;  // snapshot of this generation, [P][n]
-  int start, size, pos, n;
-  __device__ __forceinline__ void init(const short* snap_g, int ev, int P, int islands, int n_) {
-    rows = snap_g;
+  const int* prog;
+  int start, size, pos, n, gen;
+  __device__ __forceinline__ void init(const short* snap, const int* prog_, int g, int ev, int P,
+                                       int islands, int n_) {
+    rows = snap ? snap + (size_t)(g % SNAP_DEPTH) * P * n_ : nullptr;
+    prog = prog_;
+    gen = g;
     n = n_;
     const int base = P / islands, extra = P - base * islands;
     int isl;
@@ -313,7 +353,9 @@ struct MateSel {
     if (rows == nullptr || size <= 1) return nullptr;
     int j = rng.randbelow(size - 1);
     j += j >= pos;
-    return rows + (size_t)(start + j) * n;
+    j += start;
+    while (ld_acquire(prog + j) < gen) __nanosleep(64);
+    return rows + (size_t)j * n;
   }
 };
 

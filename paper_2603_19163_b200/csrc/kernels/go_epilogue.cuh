@@ -326,4 +326,10 @@ __global__ void go_arm_deadline_kernel(GlobalState* gs, long long budget_ns) {
   gs->deadline_ns = budget_ns > 0 ? (long long)globaltimer() + budget_ns : 0;
 }
 
+// snapshot progress of every team := the launch's first generation (EvolveArgs::prog)
+__global__ void go_fill_i32_kernel(int* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
 }  // namespace go

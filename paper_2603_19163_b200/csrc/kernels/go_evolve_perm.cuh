@@ -258,8 +258,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
     // crossover snapshot of this generation (see EvolveArgs::snap)
-    if (A.snap && gi > 0) grid_team_barrier(A.gbar, (unsigned)(gi * A.P), lane, team, TS);
-    ms.init(A.snap ? A.snap + (size_t)(g & 1) * A.P * n : nullptr, ev, A.P, A.islands, n);
+    ms.init(A.snap, A.prog, (int)g, ev, A.P, A.islands, n);
 
     // ---- A: every lane draws k and its first sequence (identity mapping) ----
     if (lane < T) {
@@ -564,10 +563,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       A.rec_scal[(size_t)gi * A.P + ev] = phi;
       A.rec_pen[(size_t)gi * A.P + ev] = 0.0;
     }
-    if (A.snap && gi + 1 < A.ngen) {
-      short* sn = A.snap + ((size_t)((g + 1) & 1) * A.P + ev) * n;
-      for (int p = lane; p < n; p += TS) sn[p] = cur[p];
-    }
+    if (A.snap && gi + 1 < A.ngen)
+      snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, lane, team, TS);
     if (strictly_better(0.0, phi, bpen, bscal)) {  // team best-ever, first occurrence
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = cur[p];
       bscal = phi;

@@ -67,8 +67,10 @@ struct RowLaneState {
   unsigned char* nr;
   short* rlo;  // [MAX_RANGES][TS]
   short* rhi;
+  unsigned short* greq;   // [TS] lanes with a deferred guided rebuild this step
+  unsigned short* uxreq;  // [TS] lanes with a deferred uniform crossover this step
   static __host__ __device__ unsigned bytes(int TS) {
-    return (unsigned)(TS * (4 + 4 + 8 * 5 + 2 + 1 + 4 * MAX_RANGES) + 16);
+    return (unsigned)(TS * (4 + 4 + 8 * 5 + 2 + 1 + 4 * MAX_RANGES + 2 + 2) + 16);
   }
   __device__ __forceinline__ void bind(unsigned char* p, int TS) {
     delta = (double*)p;
@@ -82,6 +84,8 @@ struct RowLaneState {
     rhi = rlo + MAX_RANGES * TS;
     order = (unsigned short*)(rhi + MAX_RANGES * TS);
     nr = (unsigned char*)(order + TS);
+    greq = (unsigned short*)(nr + TS);
+    uxreq = greq + TS;
   }
 };
 
@@ -272,49 +276,9 @@ __device__ __forceinline__ typename AccOf<E>::T qap_swap_delta(const QapView<E>&
   return d;
 }
 
-template <class E, class G, class R>
-__device__ void gr_qap(const QapView<E>& q, G* row, int n, int n_cfg, R& rng) {
-  typedef typename AccOf<E>::T A;
-  if (n < 3) return;
-  const int ls = lns_scope(n_cfg);
-  const int m = ls < n - 1 ? ls : n - 1;
-  int picks[30];
-  G taken[30];
-  sample_range(rng, n, m, picks);
-  sort_desc(picks, m);
-  int size = n;
-  for (int t = 0; t < m; ++t) {  // _row_remove in (r, -p) order
-    taken[t] = row[picks[t]];
-    row_pop(row, size, picks[t]);
-    --size;
-  }
-  for (int t = 0; t < m; ++t) row[size++] = taken[t];  // park at the row end
-  for (int t = 0; t < m; ++t) {
-    const G v = taken[t];
-    int q0 = 0;
-    while (row[q0] != v) ++q0;
-    row_pop(row, n, q0);
-    row[n - 1] = v;  // trial n-1 (score offset 0), then walk down to 0
-    A sc = 0, best = 0;
-    int bp = n - 1;
-    for (int p = n - 1; p >= 1; --p) {
-      sc += qap_swap_delta(q, row, n, p - 1, p);
-      const G tmp = row[p - 1];
-      row[p - 1] = row[p];
-      row[p] = tmp;
-      if (sc <= best) {  // lower positions win ties: first minimum in 0..n-1
-        best = sc;
-        bp = p - 1;
-      }
-    }
-    for (int p = 0; p < bp; ++p) row[p] = row[p + 1];  // v from 0 to bp
-    row[bp] = v;
-  }
-}
-
 // binary / integer: coordinate-greedy reset of a scatter of cells
 template <int KIND, class G, class R>
-__device__ void gr_cells(const KnapView& kv, const JspView& jv, G* row, int n, int n_cfg, int lb,
+__device__ __forceinline__ void gr_cells(const KnapView& kv, const JspView& jv, G* row, int n, int n_cfg, int lb,
                          int ub, double wobj, double pw, int* scratch, R& rng) {
   if (n == 0) return;
   const int ls = lns_scope(n_cfg);
@@ -384,60 +348,515 @@ __device__ void gr_cells(const KnapView& kv, const JspView& jv, G* row, int n, i
   }
 }
 
-// partitions (VRPTW / CVRP): operators.py:520-546 with a full evaluation per trial
-__device__ void gr_part(const PartView& pv, PartCtx& c, double wobj, double pw) {
-  const int total = c.total;
-  if (total < 3) return;
-  const int ls = lns_scope(c.n_cfg);
-  const int m = ls < total - 1 ? ls : total - 1;
-  int picks[30], rr[30], pp[30];
-  short taken[30];
-  sample_range(c, total, m, picks);
-  for (int t = 0; t < m; ++t) c.cell_at(picks[t], rr[t], pp[t]);
-  for (int i = 1; i < m; ++i) {  // sorted by (r, -p)
-    const int r0 = rr[i], p0 = pp[i];
-    int j = i;
-    while (j > 0 && (rr[j - 1] > r0 || (rr[j - 1] == r0 && pp[j - 1] < p0))) {
-      rr[j] = rr[j - 1];
-      pp[j] = pp[j - 1];
-      --j;
-    }
-    rr[j] = r0;
-    pp[j] = p0;
-  }
-  for (int t = 0; t < m; ++t) taken[t] = c.remove(rr[t], pp[t]);
-  for (int t = 0; t < m; ++t) {  // park at the end of the first open row
-    int r = 0;
-    while (r < c.d1 - 1 && c.sz[r] >= c.d2) ++r;
-    c.insert(r, c.sz[r], taken[t]);
-  }
-  for (int t = 0; t < m; ++t) {
-    const short v = taken[t];
-    int g = 0;
-    while (c.cells[g] != v) ++g;
-    int r0, p0;
-    c.cell_at(g, r0, p0);
-    c.remove(r0, p0);
-    double bs = 0.0;
-    int br = -1, bp = 0;
-    for (int r = 0; r < c.d1; ++r) {
-      if (c.sz[r] >= c.d2) continue;
-      const int lim = c.sz[r];
-      for (int pos = 0; pos <= lim; ++pos) {
-        c.insert(r, pos, v);
-        double dist, pen;
-        part_eval(pv, c.cells, c.sz, dist, pen);
-        const double sc = __dadd_rn(__dadd_rn(0.0, __dmul_rn(wobj, dist)), __dmul_rn(pw, pen));
-        c.remove(r, pos);
-        if (br < 0 || sc < bs) {
-          bs = sc;
-          br = r;
-          bp = pos;
+// ---- team-cooperative guided rebuild (QAP / JSP-int / partitions) --------------
+// A lane that draws guided_rebuild is deferred; after the chain step the whole
+// team resolves the deferred lanes one at a time.  Thread 0 replays the lane's
+// stream (all of the operator's draws come first: cells, domain sample) and
+// publishes them in `gx` (team scratch); the trials of each rebuilt value are
+// then scored in parallel and the first minimum is applied.
+struct GrShared {  // views into the team scratch (TeamShared::cnt, 128 ints)
+  int* gx;
+  __device__ __forceinline__ int& m() const { return gx[0]; }
+  __device__ __forceinline__ int& nd() const { return gx[1]; }
+  __device__ __forceinline__ int& res() const { return gx[2]; }
+  __device__ __forceinline__ int& aux() const { return gx[3]; }
+  __device__ __forceinline__ int* picks() const { return gx + 8; }   // [30]
+  __device__ __forceinline__ int* taken() const { return gx + 40; }  // [30]
+  __device__ __forceinline__ int* dom() const { return gx + 72; }    // [16]
+  __device__ __forceinline__ int* score() const { return gx + 88; }  // [16] JSP makespans
+};
+
+// Thread 0: the draws of op_guided_rebuild for the lane (operators.py:501-571).
+template <int KIND>
+__device__ __forceinline__ void gr_draw(Stream& rng, const GrShared& g, int n, int n_cfg, int lb,
+                                        int ub, const short* sz, int d1) {
+  const int ls = lns_scope(n_cfg);
+  int m = 0;
+  if (KIND == RK_JSP) {
+    if (n > 0) {
+      m = ls < n ? ls : n;
+      sample_range(rng, n, m, g.picks());
+      const int D = ub - lb + 1;
+      int nd = D;
+      if (D > 16) {  // sorted(rng.sample(domain, 16))
+        int* dm = g.dom();
+        sample_range(rng, D, 16, dm);
+        for (int i = 1; i < 16; ++i) {
+          const int v = dm[i];
+          int j = i;
+          while (j > 0 && dm[j - 1] > v) {
+            dm[j] = dm[j - 1];
+            --j;
+          }
+          dm[j] = v;
         }
+        nd = 16;
+        for (int i = 0; i < 16; ++i) dm[i] += lb;
+      } else {
+        for (int i = 0; i < D; ++i) g.dom()[i] = lb + i;
+      }
+      g.nd() = nd;
+    }
+  } else if (n >= 3) {  // permutation cells (single row or partitions)
+    m = ls < n - 1 ? ls : n - 1;
+    int* pk = g.picks();
+    sample_range(rng, n, m, pk);
+    if (KIND == RK_QAP) {  // sorted by (r, -p): descending positions
+      for (int i = 1; i < m; ++i) {
+        const int v = pk[i];
+        int j = i;
+        while (j > 0 && pk[j - 1] < v) {
+          pk[j] = pk[j - 1];
+          --j;
+        }
+        pk[j] = v;
+      }
+    } else {  // partitions: global cell -> (r, p), sorted by (r, -p), packed r << 16 | p
+      for (int t = 0; t < m; ++t) {
+        int gi = pk[t], r = 0;
+        while (gi >= sz[r]) {
+          gi -= sz[r];
+          ++r;
+        }
+        pk[t] = (r << 16) | (0xFFFF - gi);  // ascending key == (r asc, p desc)
+      }
+      for (int i = 1; i < m; ++i) {
+        const int v = pk[i];
+        int j = i;
+        while (j > 0 && pk[j - 1] > v) {
+          pk[j] = pk[j - 1];
+          --j;
+        }
+        pk[j] = v;
+      }
+      for (int t = 0; t < m; ++t) pk[t] = (pk[t] & 0xFFFF0000) | (0xFFFF - (pk[t] & 0xFFFF));
+    }
+  }
+  g.m() = m;
+  (void)d1;
+}
+
+// QAP swap delta of positions (a, a+1) in the row r (size n-1, without v) with v
+// inserted at a+1 (= the walk step moving v from a+1 to a).  r(k) is virtual:
+// r[k] = row[k < q0 ? k : k + 1] (row still holds v at q0).
+template <class E, class G>
+__device__ __forceinline__ typename AccOf<E>::T qap_walk_delta(const QapView<E>& q, const G* row,
+                                                               int n, int q0, int v, int a) {
+  typedef typename AccOf<E>::T A;
+  const int b = a + 1;
+  auto rr = [&](int k) -> int { return row[k < q0 ? k : k + 1]; };
+  const int pa = rr(a), pb = v;  // before the swap: r[a] at a, v at b
+  A d = (q.F(a, a) - q.F(b, b)) * (q.D(pb, pb) - q.D(pa, pa)) +
+        (q.F(a, b) - q.F(b, a)) * (q.D(pb, pa) - q.D(pa, pb));
+  for (int k = 0; k < n; ++k) {
+    if (k == a || k == b) continue;
+    const int pk = rr(k < a ? k : k - 1);
+    d += (q.F(a, k) - q.F(b, k)) * (q.D(pb, pk) - q.D(pa, pk)) +
+         (q.F(k, a) - q.F(k, b)) * (q.D(pk, pb) - q.D(pk, pa));
+  }
+  return d;
+}
+
+// rewrite row so that element at old position `src(t)` lands at t (team, two phases)
+template <class G, class F>
+__device__ __forceinline__ void team_permute(G* row, int n, const F& src, int lane, int team,
+                                             int TS) {
+  G v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int t = lane + i * TS;
+    if (t < n) v[i] = row[src(t)];
+  }
+  team_bar(team, TS);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int t = lane + i * TS;
+    if (t < n) row[t] = v[i];
+  }
+  team_bar(team, TS);
+}
+
+template <class E, class G>
+__device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& g, double* sbuf,
+                            int lane, int team, int TS) {
+  typedef typename AccOf<E>::T A;
+  const int m = g.m();
+  if (m == 0) return;
+  const int* pk = g.picks();
+  // pop the picks (descending positions) and park them at the end, in pick order
+  if (lane == 0)
+    for (int t = 0; t < m; ++t) g.taken()[t] = row[pk[t]];
+  if (n > 8 * TS) {  // rows longer than the register staging: serial moves by thread 0
+    if (lane == 0) {
+      int size = n;
+      for (int t = 0; t < m; ++t) {
+        row_pop(row, size, pk[t]);
+        --size;
+      }
+      for (int t = 0; t < m; ++t) row[size++] = (G)g.taken()[t];
+    }
+    team_bar(team, TS);
+  } else team_permute(row, n, [&](int t) -> int {
+    if (t >= n - m) return pk[t - (n - m)];
+    int p = t;  // t-th survivor: skip picked positions in ascending order
+    for (int j = m - 1; j >= 0; --j) p += pk[j] <= p;
+    return p;
+  }, lane, team, TS);
+  for (int t = 0; t < m; ++t) {
+    const int v = g.taken()[t];
+    for (int p = lane; p < n; p += TS)
+      if (row[p] == v) g.res() = p;
+    team_bar(team, TS);
+    const int q0 = g.res();
+    // walk v from n-1 down to 0: sd[a] = delta of the step a+1 -> a, computed in
+    // parallel chunks of `cap` steps; thread 0 accumulates the scores (relative
+    // to v at n-1) from the top, lower positions winning ties
+    A* sd = (A*)sbuf;
+    const int cap = 5 * TS;
+    A sc = 0, best = 0;
+    int bp = n - 1;
+    for (int hi = n - 1; hi > 0; hi -= cap) {
+      const int lo = hi - cap > 0 ? hi - cap : 0;
+      for (int a = lo + lane; a < hi; a += TS) sd[a - lo] = qap_walk_delta(q, row, n, q0, v, a);
+      team_bar(team, TS);
+      if (lane == 0)
+        for (int a = hi - 1; a >= lo; --a) {
+          sc += sd[a - lo];
+          if (sc <= best) {
+            best = sc;
+            bp = a;
+          }
+        }
+      team_bar(team, TS);
+    }
+    if (lane == 0) g.aux() = bp;
+    team_bar(team, TS);
+    const int b = g.aux();
+    if (n > 8 * TS) {
+      if (lane == 0) {
+        row_pop(row, n, q0);
+        for (int p = n - 1; p > b; --p) row[p] = row[p - 1];
+        row[b] = (G)v;
+      }
+      team_bar(team, TS);
+    } else {
+      team_permute(row, n, [&](int x) -> int {
+        if (x == b) return q0;
+        const int r = x < b ? x : x - 1;  // index in the row without v
+        return r < q0 ? r : r + 1;
+      }, lane, team, TS);
+    }
+  }
+}
+
+// warp-cooperative serial schedule generator (builtins.py:429-453) with one
+// priority overridden (position ovp := ovv); lanes own jobs wl + 32 s.
+// Fast path (n_jobs, n_machines <= 32, <= 255 operations per job): lane j owns
+// job j and machine j in registers; key = (priority, job, index) orders exactly
+// like (priority, op) since op = job * per_job + index.
+template <class G>
+__device__ __forceinline__ int jsp_decode_warp32(const JspView& J, const G* prio, int ovp, int ovv,
+                                                 int wl) {
+  const int pj = J.per_job;
+  const bool mine = wl < J.n_jobs;
+  int nx = 0, jf = 0, mfr = 0, span = 0;
+  int op0 = wl * pj;
+  int pr = mine ? (op0 == ovp ? ovv : (int)prio[op0]) : 0;
+  const int n_ops = J.n_jobs * pj;
+  for (int step = 0; step < n_ops; ++step) {
+    const unsigned key = mine && nx < pj
+                             ? ((unsigned)pr << 16) | ((unsigned)wl << 8) | (unsigned)nx
+                             : 0xFFFFFFFFu;
+    const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
+    const int j = (int)((kmin >> 8) & 0xFFu);
+    const int op = j * pj + (int)(kmin & 0xFFu);
+    const int m = J.mach[op], du = J.dur[op];
+    const int mfm = __shfl_sync(0xffffffffu, mfr, m);
+    const int jfo = __shfl_sync(0xffffffffu, jf, j);
+    const int done = (jfo > mfm ? jfo : mfm) + du;
+    if (wl == m) mfr = done;
+    if (wl == j) {
+      jf = done;
+      ++nx;
+      if (nx < pj) {
+        const int o = op + 1;
+        pr = o == ovp ? ovv : (int)prio[o];
       }
     }
-    c.insert(br, bp, v);
+    span = done > span ? done : span;
   }
+  return span;
+}
+
+template <class G>
+__device__ __forceinline__ int jsp_decode_warp(const JspView& J, const G* prio, int ovp, int ovv,
+                                               int* mf, int wl) {
+  if (J.n_jobs <= 32 && J.n_mach <= 32 && J.per_job < 256 && J.n_jobs * J.per_job < 32768)
+    return jsp_decode_warp32(J, prio, ovp, ovv, wl);
+  int nx[4], jf[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    nx[s] = 0;
+    jf[s] = 0;
+  }
+  for (int m = wl; m < J.n_mach; m += 32) mf[m] = 0;
+  __syncwarp();
+  int span = 0;
+  const int n_ops = J.n_jobs * J.per_job;
+  for (int step = 0; step < n_ops; ++step) {
+    unsigned key = 0xFFFFFFFFu;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int j = wl + 32 * s;
+      if (j < J.n_jobs && nx[s] < J.per_job) {
+        const int op = j * J.per_job + nx[s];
+        const int pr = op == ovp ? ovv : (int)prio[op];
+        const unsigned k2 = ((unsigned)pr << 16) | (unsigned)op;
+        key = k2 < key ? k2 : key;
+      }
+    }
+    key = __reduce_min_sync(0xFFFFFFFFu, key);
+    const int op = (int)(key & 0xFFFFu);
+    const int j = op / J.per_job;
+    if ((j & 31) == wl) {
+      const int s = j >> 5;
+      const int m = J.mach[op];
+      int jfs = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) jfs = t == s ? jf[t] : jfs;
+      const int mfm = mf[m];
+      const int done = (jfs > mfm ? jfs : mfm) + J.dur[op];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t == s) {
+          jf[t] = done;
+          nx[t] += 1;
+        }
+      mf[m] = done;
+      span = done > span ? done : span;
+    }
+    __syncwarp();
+  }
+  return __reduce_max_sync(0xFFFFFFFFu, (unsigned)span);
+}
+
+template <class G>
+__device__ void team_gr_jsp(const JspView& J, G* row, const GrShared& g, int* scratch,
+                            int scratch_ints, int lane, int team, int TS) {
+  const int m = g.m(), nd = g.nd();
+  const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
+  int* mf = scratch + warp * scratch_ints;
+  for (int t = 0; t < m; ++t) {
+    const int p = g.picks()[t];
+    for (int i = warp; i < nd; i += nwarps) {
+      const int sp = jsp_decode_warp(J, row, p, g.dom()[i], mf, wl);
+      if (wl == 0) g.score()[i] = sp;
+    }
+    team_bar(team, TS);
+    if (lane == 0) {  // first minimum in domain order
+      int bi = 0;
+      for (int i = 1; i < nd; ++i)
+        if (g.score()[i] < g.score()[bi]) bi = i;
+      row[p] = (G)g.dom()[bi];
+    }
+    team_bar(team, TS);
+  }
+}
+
+// a route of a compact partition row with one value virtually inserted
+struct RouteIns {
+  const short* base;
+  int ins, v;  // ins < 0: no insertion
+  __device__ __forceinline__ int operator[](int q) const {
+    return ins < 0 || q < ins ? base[q] : (q == ins ? v : base[q - 1]);
+  }
+};
+struct EdgeV {
+  const double* d;
+  RouteIns r;
+  int n1;
+  __device__ __forceinline__ double operator()(int i) const {
+    return d[(r[i] + 1) * n1 + r[i + 1] + 1];
+  }
+};
+struct DemV {
+  const double* dem;
+  RouteIns r;
+  __device__ __forceinline__ double operator()(int i) const { return dem[r[i]]; }
+};
+
+// part_eval (go_part.cuh) of the row with v inserted at (ri, pi): the same
+// arithmetic in the same order, element access through RouteIns
+__device__ __forceinline__ void part_eval_ins(const PartView& v, const short* cells, const short* sz,
+                                              int ri, int pi, int val, double& distance,
+                                              double& penalty) {
+  const int n1 = v.n + 1;
+  PySum dsum;
+  dsum.init();
+  double cap_pen = 0.0, late = 0.0;
+  int at = 0;
+  for (int r = 0; r < v.d1; ++r) {
+    const int len0 = sz[r];
+    RouteIns route{cells + at, r == ri ? pi : -1, val};
+    const int len = len0 + (r == ri);
+    double rd = 0.0;
+    if (len > 0) {
+      rd = __dadd_rn(v.dist[route[0] + 1], v.dist[(route[len - 1] + 1) * n1]);
+      if (len > 1) {
+        EdgeV e{v.dist, route, n1};
+        rd = __dadd_rn(rd, np_pairwise(e, 0, len - 1));
+      }
+    }
+    dsum.add(rd);
+    DemV dm{v.demand, route};
+    const double load = np_pairwise(dm, 0, len);
+    const double over = __dsub_rn(load, v.cap);
+    cap_pen = __dadd_rn(cap_pen, over > 0.0 ? over : 0.0);
+    if (v.tw && len > 0) {
+      double t = v.ready[0];
+      int prev = 0;
+      for (int q = 0; q < len; ++q) {
+        const int node = route[q] + 1;
+        const double arr0 = __dadd_rn(t, v.dist[prev * n1 + node]);
+        const double arrival = v.ready[node] >= arr0 ? v.ready[node] : arr0;
+        const double lt = __dsub_rn(arrival, v.due[node]);
+        late = __dadd_rn(late, lt > 0.0 ? lt : 0.0);
+        t = __dadd_rn(arrival, v.service[node]);
+        prev = node;
+      }
+      const double back = __dsub_rn(__dadd_rn(t, v.dist[prev * n1]), v.due[0]);
+      late = __dadd_rn(late, back > 0.0 ? back : 0.0);
+    }
+    at += len0;
+  }
+  distance = dsum.result();
+  penalty = v.tw ? __dadd_rn(cap_pen, late) : cap_pen;
+}
+
+// partitions (operators.py:520-546): thread 0 pops / parks / re-inserts, the
+// team scores every trial slot of every open row in parallel (full evaluation)
+__device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_cells, int d1,
+                             int d2, double wobj, double pw, const GrShared& g, double* sbuf,
+                             TeamShared<double>* ts, int lane, int team, int TS) {
+  const int m = g.m();
+  if (m == 0) return;
+  const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
+  PartCtx c;
+  c.cells = cells;
+  c.sz = sz;
+  c.n = n_cells;
+  c.d1 = d1;
+  c.d2 = d2;
+  c.total = n_cells;
+  if (lane == 0) {
+    for (int t = 0; t < m; ++t) {
+      const int rp = g.picks()[t];
+      g.taken()[t] = c.remove(rp >> 16, rp & 0xFFFF);
+    }
+    for (int t = 0; t < m; ++t) {  // park at the end of the first open row
+      int r = 0;
+      while (r < d1 - 1 && sz[r] >= d2) ++r;
+      c.insert(r, sz[r], (short)g.taken()[t]);
+    }
+  }
+  team_bar(team, TS);
+  for (int t = 0; t < m; ++t) {
+    const short v = (short)g.taken()[t];
+    if (lane == 0) {
+      c.total = n_cells;
+      int gi = 0;
+      while (cells[gi] != v) ++gi;
+      int r0, p0;
+      c.cell_at(gi, r0, p0);
+      c.remove(r0, p0);
+    }
+    team_bar(team, TS);
+    int ntr = 0;  // trial slots: open rows in order, positions 0..sz[r]
+    for (int r = 0; r < d1; ++r) ntr += sz[r] < d2 ? sz[r] + 1 : 0;
+    double bs = 0.0;
+    int bi = 0x7fffffff;
+    for (int i = lane; i < ntr; i += TS) {
+      int r = 0, k = i;
+      for (; r < d1; ++r) {
+        if (sz[r] >= d2) continue;
+        if (k <= sz[r]) break;
+        k -= sz[r] + 1;
+      }
+      double dist, pen;
+      part_eval_ins(pv, cells, sz, r, k, v, dist, pen);
+      const double sc = __dadd_rn(__dadd_rn(0.0, __dmul_rn(wobj, dist)), __dmul_rn(pw, pen));
+      if (bi == 0x7fffffff || sc < bs) {
+        bs = sc;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, bs, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || ob < bs || (ob == bs && oi < bi))) {
+        bs = ob;
+        bi = oi;
+      }
+    }
+    if (wl == 0) {
+      sbuf[warp] = bs;
+      ts->wl[warp] = bi;
+    }
+    team_bar(team, TS);
+    if (lane == 0) {
+      double b = 0.0;
+      int ib = 0x7fffffff;
+      for (int w = 0; w < nwarps; ++w) {
+        const int oi = ts->wl[w];
+        if (oi != 0x7fffffff && (ib == 0x7fffffff || sbuf[w] < b || (sbuf[w] == b && oi < ib))) {
+          b = sbuf[w];
+          ib = oi;
+        }
+      }
+      int r = 0, k = ib;
+      for (; r < d1; ++r) {
+        if (sz[r] >= d2) continue;
+        if (k <= sz[r]) break;
+        k -= sz[r] + 1;
+      }
+      c.total = n_cells - 1;
+      c.insert(r, k, v);
+    }
+    team_bar(team, TS);
+  }
+}
+
+// op_uniform_crossover (operators.py:451-462) resolved by one warp: lane 0 draws
+// the mate (pick_mate may reject), then every cell's random() sits at a known
+// word position (2 words each, no rejection), so the warp evaluates them in
+// parallel from the counter-based stream.  Returns the stream position after
+// the operator; lo/hi = touched range (hi <= lo: none).
+template <class G>
+__device__ __forceinline__ u32 warp_uniform_x(G* row, int n, const MateSel& ms, Stream& rng,
+                                              int wl, int& lo, int& hi) {
+  int mate = -1;
+  u32 pos0 = 0;
+  if (wl == 0) {
+    const short* mp = ms.pick(rng);
+    mate = mp ? (int)((mp - ms.rows) / n) : -1;
+    pos0 = rng.tell();
+  }
+  mate = __shfl_sync(0xffffffffu, mate, 0);
+  pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+  lo = n;
+  hi = 0;
+  if (mate < 0) return pos0;
+  const short* mrow = ms.rows + (size_t)mate * n;
+  for (int p = wl; p < n; p += 32)
+    if (random_at(rng.k0, rng.k1, pos0 + 2u * (u32)p) < 0.5) {
+      row[p] = (G)__ldcg(mrow + p);
+      lo = p < lo ? p : lo;
+      hi = p + 1;
+    }
+  lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
+  hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)hi);
+  return pos0 + 2u * (u32)n;
 }
 
 template <int KIND, class E, class G>
@@ -592,8 +1011,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
     // crossover snapshot of this generation (see EvolveArgs::snap)
-    if (A.snap && gi > 0) grid_team_barrier(A.gbar, (unsigned)(gi * A.P), lane, team, TS);
-    ms.init(A.snap ? A.snap + (size_t)(g & 1) * A.P * n : nullptr, ev, A.P, A.islands, n);
+    ms.init(A.snap, A.prog, (int)g, ev, A.P, A.islands, n);
 
     // ---- A: copy the current row into every lane row; draw k and sequence 0
     {
@@ -628,6 +1046,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       ts->cnt[warp][wl] = 0;
       __syncwarp();
       if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
+      if (lane == 0) {
+        ts->nreq = 0;
+        ts->ndreq = 0;
+      }
       team_bar(team, TS);
       int tj = 0;
       if (wl < nseq) {
@@ -658,9 +1080,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         const u32 meta = la.meta[L];
         const int k = meta_k(meta);
         int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+        bool pending = false;
         if (KIND == RK_PART) {
           PartCtx c;
-          c.rng = &rng;
+          c.rng = rng;
           c.cells = (short*)(rows + (size_t)L * rs);
           c.sz = c.cells + X.n_cells;
           c.n = X.n_cells;
@@ -671,12 +1094,17 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           c.err = 0;
           c.mates = &ms;
           const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
-          if (kind == SEQ_GUIDED_REBUILD) gr_part(pv, c, X.obj_weight, pwt);
-          else run_part_op(kind, c);
+          if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
+            la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+            pending = true;
+          } else {
+            run_part_op(kind, c);
+          }
+          rng = c.rng;
           err |= c.err;
         } else {
           RowCtx<G> c;
-          c.rng = &rng;
+          c.rng = rng;
           c.row = (G*)(rows + (size_t)L * rs);
           c.n = n;
           c.n_cfg = X.n_cfg;
@@ -689,25 +1117,106 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           c.rstride = TS;
           c.mates = &ms;
           const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
-          if (kind == SEQ_GUIDED_REBUILD) {
-            if (KIND == RK_QAP) gr_qap(qv, c.row, n, X.n_cfg, c);
-            else gr_cells<KIND>(kv, jv, c.row, n, X.n_cfg, X.lb, X.ub, X.obj_weight, pwt,
-                                scratch + L * X.scratch_ints, c);
+          if (kind == SEQ_GUIDED_REBUILD && KIND == RK_KNAP) {  // O(1) trials: inline
+            gr_cells<KIND>(kv, jv, c.row, n, X.n_cfg, X.lb, X.ub, X.obj_weight, pwt,
+                           scratch + L * X.scratch_ints, c);
             c.mark_all();
+          } else if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
+            la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+            pending = true;
+          } else if (kind == SEQ_UNIFORM_X) {  // warp-resolved below
+            la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
+            pending = true;
           } else {
             run_row_op(kind, c);
           }
+          rng = c.rng;
           err |= c.err;
           la.nr[L] = (unsigned char)(c.nr > MAX_RANGES ? MAX_RANGES + 1 : c.nr);
         }
-        if (s + 1 < k) {
-          const int nq = sample_seq(s_cum, nseq, total, rng);
-          if (s == 0) q1 = nq; else q2 = nq;
+        if (!pending) {
+          if (s + 1 < k) {
+            const int nq = sample_seq(s_cum, nseq, total, rng);
+            if (s == 0) q1 = nq; else q2 = nq;
+          }
+          la.pos[L] = rng.tell();
+          la.meta[L] = pack_meta(k, 0, q0, q1, q2);
         }
-        la.pos[L] = rng.tell();
-        la.meta[L] = pack_meta(k, 0, q0, q1, q2);
       }
       team_bar(team, TS);
+
+      // ---- deferred uniform crossovers: one warp per lane -------------------------
+      const int nux = ts->ndreq;
+      if (nux > 0) {
+#pragma unroll 1
+        for (int r = warp; r < nux; r += nwarps) {
+          const int L = la.uxreq[r];
+          Stream rng;
+          rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+          rng.seek(la.pos[L]);
+          int lo, hi;
+          const u32 pend = warp_uniform_x((G*)(rows + (size_t)L * rs), n, ms, rng, wl, lo, hi);
+          if (wl == 0) {
+            rng.seek(pend);
+            const u32 meta = la.meta[L];
+            const int k = meta_k(meta);
+            int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+            if (s + 1 < k) {
+              const int nq = sample_seq(s_cum, nseq, total, rng);
+              if (s == 0) q1 = nq; else q2 = nq;
+            }
+            la.pos[L] = rng.tell();
+            la.meta[L] = pack_meta(k, 0, meta_sq(meta, 0), q1, q2);
+            if (hi > lo) {  // RowCtx::mark
+              const int nr = la.nr[L];
+              if (nr < MAX_RANGES) {
+                la.rlo[nr * TS + L] = (short)lo;
+                la.rhi[nr * TS + L] = (short)hi;
+              }
+              la.nr[L] = (unsigned char)(nr + 1 > MAX_RANGES ? MAX_RANGES + 1 : nr + 1);
+            }
+          }
+        }
+        team_bar(team, TS);
+      }
+
+      // ---- deferred guided rebuilds: the whole team, one lane at a time ------------
+      const int ngr = ts->nreq;
+      if (ngr > 0) {
+        const GrShared gsh{(int*)&ts->cnt[0][0]};
+#pragma unroll 1
+        for (int r = 0; r < ngr; ++r) {
+          const int L = la.greq[r];
+          G* lrow = (G*)(rows + (size_t)L * rs);
+          if (lane == 0) {
+            Stream rng;
+            rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+            rng.seek(la.pos[L]);
+            gr_draw<KIND>(rng, gsh, KIND == RK_PART ? X.n_cells : n, X.n_cfg, X.lb, X.ub,
+                          (const short*)lrow + X.n_cells, X.d1);
+            const u32 meta = la.meta[L];
+            const int k = meta_k(meta);
+            int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+            if (s + 1 < k) {
+              const int nq = sample_seq(s_cum, nseq, total, rng);
+              if (s == 0) q1 = nq; else q2 = nq;
+            }
+            la.pos[L] = rng.tell();
+            la.meta[L] = pack_meta(k, 0, meta_sq(meta, 0), q1, q2);
+            la.nr[L] = (unsigned char)(MAX_RANGES + 1);  // whole row re-evaluated
+          }
+          team_bar(team, TS);
+          if (KIND == RK_QAP) {
+            team_gr_qap(qv, lrow, n, gsh, la.delta, lane, team, TS);
+          } else if (KIND == RK_JSP) {
+            team_gr_jsp(jv, lrow, gsh, scratch, X.scratch_ints, lane, team, TS);
+          } else if (KIND == RK_PART) {
+            team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2,
+                         X.obj_weight, pwt, gsh, la.delta, ts, lane, team, TS);
+          }
+          team_bar(team, TS);
+        }
+      }
     }
 
     // ---- C: evaluate every lane (identity mapping) --------------------------------
@@ -817,10 +1326,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       A.rec_scal[(size_t)gi * A.P + ev] = scal;
       A.rec_pen[(size_t)gi * A.P + ev] = pen;
     }
-    if (A.snap && gi + 1 < A.ngen) {
-      short* sn = A.snap + ((size_t)((g + 1) & 1) * A.P + ev) * n;
-      for (int p = lane; p < n; p += TS) sn[p] = (short)cur[p];
-    }
+    if (A.snap && gi + 1 < A.ngen)
+      snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, lane, team, TS);
     if (strictly_better(pen, scal, bpen, bscal)) {
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = (short)cur[p];
       bscal = scal;

@@ -26,15 +26,15 @@ struct PartView {  // instance (float64 arrays, customer c at matrix index c + 1
 };
 
 struct PartCtx {
-  Stream* rng;
+  Stream rng;  // by value (see RowCtx)
   short* cells;  // [n]
   short* sz;     // [d1]
   int n, d1, d2, n_cfg;
   int total;     // cells currently stored (n except inside an op)
   int err;
   const MateSel* mates;  // crossover mates (engine.py:553-559); rows = cells + sizes
-  __device__ __forceinline__ int randbelow(int m) { return rng->randbelow(m); }
-  __device__ __forceinline__ int randrange(int lo, int hi) { return rng->randrange(lo, hi); }
+  __device__ __forceinline__ int randbelow(int m) { return rng.randbelow(m); }
+  __device__ __forceinline__ int randrange(int lo, int hi) { return rng.randrange(lo, hi); }
   __device__ __forceinline__ int start(int r) const {
     int s = 0;
     for (int q = 0; q < r; ++q) s += sz[q];
@@ -169,11 +169,8 @@ __device__ __forceinline__ void pop_three_opt(PartCtx& c) {
     return;
   }
   const int size = c.sz[r];
-  // sample(range(1, size), 3), sorted — reuse the row helper through a shim
-  RowCtx<short> rc;
-  rc.rng = c.rng;
   int i, j, k;
-  sample3_sorted(rc, size, i, j, k);
+  sample3_sorted(c, size, i, j, k);  // sample(range(1, size), 3), sorted
   const int variant = c.randbelow(7);
   short* a = c.cells + c.start(r);
   switch (variant) {
@@ -305,6 +302,7 @@ __device__ __forceinline__ void pop_scatter_shuffle(PartCtx& c) {
   rc.nr = 0;
   rc.err = 0;
   rop_scatter_shuffle(rc);
+  c.rng = rc.rng;
 }
 
 // op_ox_crossover, MULTI_PARTITION branch (operators.py:437-448): OX over the

@@ -15,7 +15,7 @@ enum { MAX_RANGES = 6 };
 
 template <class G>
 struct RowCtx {
-  Stream* rng;
+  Stream rng;  // by value: a pointer would pin the stream to (L2-backed) local memory
   G* row;
   int n;         // active length (== d2 for single-row problems)
   int n_cfg;     // ProblemConfig.n (lns_scope argument)
@@ -35,8 +35,8 @@ struct RowCtx {
     ++nr;
   }
   __device__ __forceinline__ void mark_all() { nr = MAX_RANGES + 1; }
-  __device__ __forceinline__ int randbelow(int m) { return rng->randbelow(m); }
-  __device__ __forceinline__ int randrange(int lo, int hi) { return rng->randrange(lo, hi); }
+  __device__ __forceinline__ int randbelow(int m) { return rng.randbelow(m); }
+  __device__ __forceinline__ int randrange(int lo, int hi) { return rng.randrange(lo, hi); }
 };
 
 template <class G>
@@ -203,15 +203,24 @@ __device__ __forceinline__ void ox_in_place(G* row, const short* mate, int n, R&
   }
   int w = c2 + 1 == n ? 0 : c2 + 1;  // next free position
   int src = w;
-  for (int t = 0; t < n; ++t) {
-    const G v = (G)__ldcg(mate + src);
-    src = src + 1 == n ? 0 : src + 1;
-    bool kept = false;
-    for (int q = c1; q <= c2; ++q) kept |= row[q] == v;
-    if (kept) continue;
-    row[w] = v;
-    w = w + 1 == n ? 0 : w + 1;
-    if (w == c1) w = c2 + 1 == n ? 0 : c2 + 1;  // never lands inside the slice
+  for (int t0 = 0; t0 < n; t0 += 8) {  // 8 mate loads in flight per batch
+    G mv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (t0 + i < n) mv[i] = (G)__ldcg(mate + src);
+      src = src + 1 == n ? 0 : src + 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (t0 + i >= n) break;
+      const G v = mv[i];
+      bool kept = false;
+      for (int q = c1; q <= c2; ++q) kept |= row[q] == v;
+      if (kept) continue;
+      row[w] = v;
+      w = w + 1 == n ? 0 : w + 1;
+      if (w == c1) w = c2 + 1 == n ? 0 : c2 + 1;  // never lands inside the slice
+    }
   }
 }
 
@@ -229,12 +238,21 @@ __device__ __forceinline__ void rop_uniform_x(RowCtx<G>& c) {
   const short* mate = c.mates->pick(c);
   if (mate == nullptr) return;
   int lo = c.n, hi = 0;
-  for (int p = 0; p < c.n; ++p)
-    if (c.rng->random() < 0.5) {
-      c.row[p] = (G)__ldcg(mate + p);
-      lo = p < lo ? p : lo;
-      hi = p + 1;
-    }
+  for (int p0 = 0; p0 < c.n; p0 += 8) {  // draws first, then 8 mate loads in flight
+    unsigned take = 0;
+    for (int i = 0; i < 8 && p0 + i < c.n; ++i) take |= (c.rng.random() < 0.5 ? 1u : 0u) << i;
+    G mv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (take >> i & 1u) mv[i] = (G)__ldcg(mate + p0 + i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (take >> i & 1u) {
+        c.row[p0 + i] = mv[i];
+        lo = p0 + i < lo ? p0 + i : lo;
+        hi = p0 + i + 1;
+      }
+  }
   if (hi > lo) c.mark(lo, hi);
 }
 

@@ -31,7 +31,7 @@ def problems():
     }
 
 
-def time_cfg(make, ops, steps=3, gps=10):
+def time_cfg(make, ops, steps=6, gps=10):
     prob = make()
     if ops is not None:
         prob.device_sequences = lambda: ops
@@ -39,23 +39,29 @@ def time_cfg(make, ops, steps=3, gps=10):
     done = gps
     dr.run(done, None)
     ms = 0.0
+    per = []
     for _ in range(steps):
         done += gps
-        ms += dr.run(done, None).device_ms
-    w = {e["name"]: round(e["weight"], 4) for e in dr.registry_weights()["sequences"]} \
-        if hasattr(dr, "registry_weights") else None
+        t = dr.run(done, None).device_ms
+        per.append(round(t, 2))
+        ms += t
+    w, kw = dr.weights()
+    w = {e.id: round(float(x), 4) for e, x in zip(dr.registry.entries, w)}
     dr.close()
-    return ms / steps, w
+    return ms / steps, (w, [round(float(x), 3) for x in kw], per)
 
 
 def main():
-    sel = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5a", "C5b"]
+    sel = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5a", "C5b"]
     P = problems()
     for name in sel:
         make = P[name]
         full = make().device_sequences()
         t_full, w = time_cfg(make, None)
         print(f"{name}: full registry {t_full:.2f} ms/chunk  ops={full}", flush=True)
+        print(f"   weights {w[0]} k {w[1]} per-chunk {w[2]}", flush=True)
+        if "--full" in sys.argv:
+            continue
         for op in full:
             rest = tuple(o for o in full if o != op)
             try:
