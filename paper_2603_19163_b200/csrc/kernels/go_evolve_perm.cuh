@@ -479,12 +479,12 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           Stream rng;
           rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
-          const int changed = perm_defer_run(pol, C, kind, dst, aux, &rng, &ms, n, wl);
+          const DeferRes<Acc> dr = perm_defer(pol, C, kind, dst, aux, &rng, &ms, n, wl);
           Acc nd = la.delta[L];
           u32 bits = meta & META_BASE;
           int nm2 = nm;
-          if (changed) {
-            nd = perm_row_length(pol, dst, n, wl) - (Acc)phi;
+          if (dr.changed) {
+            nd = dr.len - (Acc)phi;
             bits = META_MAT | (nsel ? META_SEL : 0u);
             nm2 = 0;
           }

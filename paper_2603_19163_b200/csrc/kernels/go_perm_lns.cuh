@@ -244,4 +244,25 @@ __device__ __forceinline__ typename Policy::Acc perm_row_length(const Policy& po
   return s;
 }
 
+
+template <class Acc>
+struct DeferRes {
+  int changed;
+  Acc len;  // exact tour length of the new row (valid when changed)
+};
+
+// Runs the deferred operator and measures the new row.  (A register-resident
+// variant of OX / guided rebuild was measured 2x slower end to end on C2: its
+// unrolled shuffle code evicted the evolve loop from the instruction cache.)
+template <class Policy>
+__device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(const Policy pol, const Chain C,
+                                                                  int kind, i16* dst, i16* aux,
+                                                                  Stream* rng, const MateSel* ms,
+                                                                  int n_cfg, int wl) {
+  DeferRes<typename Policy::Acc> out;
+  out.changed = perm_defer_run(pol, C, kind, dst, aux, rng, ms, n_cfg, wl);
+  out.len = out.changed ? perm_row_length(pol, dst, C.n, wl) : 0;
+  return out;
+}
+
 }  // namespace go

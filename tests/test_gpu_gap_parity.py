@@ -1,0 +1,52 @@
+"""Equal-budget search-quality parity with the unmodified reference (north star:
+"final solution gap at an equal evaluation budget must be statistically no
+worse than the reference over at least 10 seeds").
+
+The reference side was run in the build container by
+tests/golden/make_gap_golden.py (genopt.run(), full built-in registry, with and
+without the user-registered tsp-delta operators) and frozen in
+tests/golden/gap_c1.json.  Here the device engine runs the same instance,
+population, team size, generation budget and seeds.  Trajectories differ by
+design (Philox lane streams vs MT19937), so the comparison is statistical: a
+one-sided Mann-Whitney U test must not find the device results worse
+(p > 0.05).  Device runs are deterministic, so the test is too."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2603_19163_b200 as G
+from paper_2603_19163_b200 import instances as I
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).with_name("golden") / "gap_c1.json"
+
+
+@pytest.mark.parametrize("variant", ["builtin", "tsp_delta"])
+def test_equal_budget_gap_no_worse_than_reference(variant):
+    from scipy.stats import mannwhitneyu
+    data = json.loads(GOLD.read_text())
+    cfg = data["config"]
+    d = I.tsp_random(51, 51, True)
+    prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=d))
+    ops = G.tsp_delta_operators() if variant == "tsp_delta" else ()
+    ours = []
+    for seed in data["seeds"]:
+        res = G.run(prob, G.EngineConfig(population=cfg["population"], team_size=cfg["team_size"],
+                                         max_generations=cfg["max_generations"], seed=seed,
+                                         custom_operators=ops))
+        assert res.generations_completed == cfg["max_generations"]
+        ours.append(float(res.objectives[0]))
+    ref = [data["runs"][variant][str(s)] for s in data["seeds"]]
+    best = min(ours + ref)
+    p = mannwhitneyu(ours, ref, alternative="greater").pvalue
+    summary = {"variant": variant, "ours": ours, "reference": ref,
+               "mean_gap_ours_pct": 100 * (np.mean(ours) - best) / best,
+               "mean_gap_reference_pct": 100 * (np.mean(ref) - best) / best, "p_worse": p}
+    out = Path("gpurun_out")
+    if out.is_dir():
+        (out / f"gap_parity_{variant}.json").write_text(json.dumps(summary, indent=1))
+    assert p > 0.05, summary

@@ -35,7 +35,8 @@ def time_cfg(make, ops, steps=6, gps=10):
     prob = make()
     if ops is not None:
         prob.device_sequences = lambda: ops
-    dr = G.DeviceRun(prob, G.EngineConfig(seed=42), 42)
+    custom = G.tsp_delta_operators() if CUSTOM else ()
+    dr = G.DeviceRun(prob, G.EngineConfig(seed=42, custom_operators=custom), 42)
     done = gps
     dr.run(done, None)
     ms = 0.0
@@ -49,6 +50,9 @@ def time_cfg(make, ops, steps=6, gps=10):
     w = {e.id: round(float(x), 4) for e, x in zip(dr.registry.entries, w)}
     dr.close()
     return ms / steps, (w, [round(float(x), 3) for x in kw], per)
+
+
+CUSTOM = "--custom" in sys.argv
 
 
 def main():
