@@ -296,10 +296,10 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // polls prog[0..P)), then publish this team's snapshot row of generation gnext
 template <class G>
 __device__ __forceinline__ void snap_publish(short* snap, int* prog, int P, int ev, int n,
-                                             int gnext, const G* cur, int lane, int team,
-                                             int nthreads) {
+                                             int gnext, const G* cur, int& gmin, int lane,
+                                             int team, int nthreads) {
   const int target = gnext + 1 - SNAP_DEPTH;  // readers of the slot's old generation are done
-  if (lane < 32) {
+  if (lane < 32 && target > gmin) {  // gmin: last observed minimum (progress only grows)
     for (;;) {
       int mn = 0x7fffffff;
       for (int t = lane; t < P; t += 32) {
@@ -307,8 +307,9 @@ __device__ __forceinline__ void snap_publish(short* snap, int* prog, int P, int 
         mn = v < mn ? v : mn;
       }
       mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+      gmin = mn;
       if (mn >= target) break;
-      __nanosleep(128);
+      __nanosleep(256);
     }
   }
   team_bar(team, nthreads);
@@ -354,7 +355,7 @@ struct MateSel {
     int j = rng.randbelow(size - 1);
     j += j >= pos;
     j += start;
-    while (ld_acquire(prog + j) < gen) __nanosleep(64);
+    while (ld_acquire(prog + j) < gen) __nanosleep(256);
     return rows + (size_t)j * n;
   }
 };

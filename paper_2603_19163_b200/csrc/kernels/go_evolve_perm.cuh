@@ -254,6 +254,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
 #define GO_TICK(slot) do { } while (0)
 #endif
   MateSel ms;
+  int snap_min = (int)A.gen0;  // every team has published gen0 (host)
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
@@ -564,7 +565,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       A.rec_pen[(size_t)gi * A.P + ev] = 0.0;
     }
     if (A.snap && gi + 1 < A.ngen)
-      snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, lane, team, TS);
+      snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, snap_min, lane, team, TS);
     if (strictly_better(0.0, phi, bpen, bscal)) {  // team best-ever, first occurrence
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = cur[p];
       bscal = phi;

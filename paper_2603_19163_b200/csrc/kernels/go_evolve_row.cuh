@@ -1007,6 +1007,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   const double pwt = X.penalty_weight;
 
   MateSel ms;
+  int snap_min = (int)A.gen0;  // every team has published gen0 (host)
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
@@ -1327,7 +1328,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       A.rec_pen[(size_t)gi * A.P + ev] = pen;
     }
     if (A.snap && gi + 1 < A.ngen)
-      snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, lane, team, TS);
+      snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, snap_min, lane, team, TS);
     if (strictly_better(pen, scal, bpen, bscal)) {
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = (short)cur[p];
       bscal = scal;

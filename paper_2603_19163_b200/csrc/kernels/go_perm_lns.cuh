@@ -28,30 +28,6 @@ __device__ __forceinline__ bool perm_deferred(int kind) {
          kind == SEQ_GUIDED_REBUILD;
 }
 
-// row[p .. size-2] = row[p+1 .. size-1]   (whole warp)
-__device__ __forceinline__ void warp_pop(i16* row, int size, int p, int wl) {
-  for (int b = p; b < size - 1; b += 32) {
-    const int q = b + wl;
-    const i16 v = q < size - 1 ? row[q + 1] : (i16)0;
-    __syncwarp();
-    if (q < size - 1) row[q] = v;
-    __syncwarp();
-  }
-}
-
-// row[p+1 .. size] = row[p .. size-1]; row[p] = v   (whole warp)
-__device__ __forceinline__ void warp_insert(i16* row, int size, int p, int v, int wl) {
-  for (int hi = size; hi > p; hi -= 32) {
-    const int q = hi - 1 - wl;
-    const i16 x = q >= p ? row[q] : (i16)0;
-    __syncwarp();
-    if (q >= p) row[q + 1] = x;
-    __syncwarp();
-  }
-  if (wl == 0) row[p] = (i16)v;
-  __syncwarp();
-}
-
 struct DeferOut {
   int changed;  // 0: the operator was a no-op (no materialisation kept)
 };
@@ -162,11 +138,15 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
     return 1;
   }
   // ---- guided rebuild (operators.py:501-546), single row, home = None -----------
+  // One gather builds the parked row (survivors in order, then the taken
+  // values in pick order) in `aux`; every re-insertion is then one insertion
+  // scan of the row without the value (read through an index skip, two chunks
+  // in flight) plus one rotation of the span between its old and new slot.
+  // Lane t tracks the position of taken value t, so no search pass is needed.
   const int ls = lns_scope(n_cfg);
   const int m = ls < n - 1 ? ls : n - 1;
-  int mypick = 0;
+  int picks[30];
   if (wl == 0) {
-    int picks[30];
     sample_range(*rng, n, m, picks);
     for (int i = 1; i < m; ++i) {  // sorted by (r, -p): descending positions
       const int v = picks[i];
@@ -177,44 +157,57 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
       }
       picks[j] = v;
     }
-    for (int t = 0; t < m; ++t) aux[t] = (i16)picks[t];  // hand the picks to the warp
   }
-  __syncwarp();
-  if (wl < m) mypick = aux[wl];
-  int mytaken = 0, size = n;
-  for (int t = 0; t < m; ++t) {  // _row_remove in that order
-    const int p = __shfl_sync(0xffffffffu, mypick, t);
-    const int v = dst[p];
-    if (wl == t) mytaken = v;
-    warp_pop(dst, size, p, wl);
-    --size;
+  int mypick = 0;
+  for (int t = 0; t < m; ++t) {
+    const int x = __shfl_sync(0xffffffffu, wl == 0 ? picks[t] : 0, 0);
+    if (wl == t) mypick = x;
   }
-  if (wl < m) dst[size + wl] = (i16)mytaken;  // park at the row end
+  const int mytaken = wl < m ? dst[mypick] : 0;
+  const int keep = n - m;
+  for (int b = 0; b < n; b += 32) {  // gather the parked row into aux
+    const int d = b + wl;
+    int src = d;  // d-th survivor: skip picked positions in ascending order
+    for (int j = m - 1; j >= 0; --j) src += __shfl_sync(0xffffffffu, mypick, j) <= src;
+    const int pk = __shfl_sync(0xffffffffu, mypick, d >= keep && d < n ? d - keep : 0);
+    if (d < n) aux[d] = d < keep ? dst[src] : dst[pk];
+  }
   __syncwarp();
   typedef typename Policy::Acc Acc;
+  int mypos = keep + wl;  // current slot of taken value wl
+  const int sz = n - 1;  // trials pos = 0 .. n-1 of the (n-1)-row without v (cyclic tour)
   for (int t = 0; t < m; ++t) {
     const int v = __shfl_sync(0xffffffffu, mytaken, t);
-    int q0 = 0x7fffffff;  // _locate_value: first occurrence
-    for (int b = 0; b < n; b += 32) {
-      const unsigned hit = __ballot_sync(0xffffffffu, b + wl < n && dst[b + wl] == v);
-      if (hit) {
-        q0 = b + __ffs(hit) - 1;
-        break;
-      }
-    }
-    warp_pop(dst, n, q0, wl);
-    const int sz = n - 1;  // trials pos = 0 .. n-1 of the (n-1)-row (cyclic tour)
+    const int q0 = __shfl_sync(0xffffffffu, mypos, t);
+    auto rv = [&](int i) -> int { return aux[i < q0 ? i : i + 1]; };  // row without v
+    const int first = rv(0), last = rv(sz - 1);
     Acc best = 0;
     int bp = 0x7fffffff;
-    for (int b = 0; b < n; b += 32) {
-      const int pos = b + wl;
-      if (pos < n) {
-        const int pv = dst[pos == 0 ? sz - 1 : pos - 1];
-        const int nx = dst[pos >= sz ? pos - sz : pos];
-        const Acc sc = pol.insertion(pv, v, v, nx);
+    int carry = last;  // element before slot 0 (cyclic)
+    for (int b = 0; b < n; b += 64) {  // two chunks in flight
+      const int p0 = b + wl, p1 = b + 32 + wl;
+      const int e0 = p0 < sz ? rv(p0) : first;
+      const int e1 = p1 < sz ? rv(p1) : first;
+      int pv0 = __shfl_up_sync(0xffffffffu, e0, 1);
+      int pv1 = __shfl_up_sync(0xffffffffu, e1, 1);
+      const int e0_31 = __shfl_sync(0xffffffffu, e0, 31);
+      if (wl == 0) {
+        pv0 = carry;
+        pv1 = e0_31;
+      }
+      carry = __shfl_sync(0xffffffffu, e1, 31);
+      if (p0 < n) {
+        const Acc sc = pol.insertion(pv0, v, v, e0);
         if (bp == 0x7fffffff || sc < best) {
           best = sc;
-          bp = pos;
+          bp = p0;
+        }
+      }
+      if (p1 < n) {
+        const Acc sc = pol.insertion(pv1, v, v, e1);
+        if (bp == 0x7fffffff || sc < best) {
+          best = sc;
+          bp = p1;
         }
       }
     }
@@ -227,8 +220,36 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
         bp = op;
       }
     }
-    warp_insert(dst, sz, bp, v, wl);
+    // move v from slot q0 to slot bp (the row keeps n slots)
+    if (bp < q0) {  // aux[bp+1 .. q0] = aux[bp .. q0-1], high chunks first
+      for (int hi = q0; hi > bp; hi -= 64) {
+        const int qa = hi - wl, qb = hi - 32 - wl;
+        const int xa = qa > bp ? aux[qa - 1] : 0;
+        const int xb = qb > bp ? aux[qb - 1] : 0;
+        __syncwarp();
+        if (qa > bp) aux[qa] = (i16)xa;
+        if (qb > bp) aux[qb] = (i16)xb;
+        __syncwarp();
+      }
+      if (mypos >= bp && mypos < q0) ++mypos;
+    } else if (bp > q0) {  // aux[q0 .. bp-1] = aux[q0+1 .. bp], low chunks first
+      for (int lo = q0; lo < bp; lo += 64) {
+        const int qa = lo + wl, qb = lo + 32 + wl;
+        const int xa = qa < bp ? aux[qa + 1] : 0;
+        const int xb = qb < bp ? aux[qb + 1] : 0;
+        __syncwarp();
+        if (qa < bp) aux[qa] = (i16)xa;
+        if (qb < bp) aux[qb] = (i16)xb;
+        __syncwarp();
+      }
+      if (mypos > q0 && mypos <= bp) --mypos;
+    }
+    if (wl == 0) aux[bp] = (i16)v;
+    if (wl == t) mypos = bp;
+    __syncwarp();
   }
+  for (int p = wl; p < n; p += 32) dst[p] = aux[p];
+  __syncwarp();
   return 1;
 }
 
