@@ -41,7 +41,8 @@ enum go_kind {
   GO_QAP = 2,       /* builtins.py:265-290 */
   GO_JSP_INT = 3,   /* builtins.py:408-456 */
   GO_KNAPSACK = 4,  /* builtins.py:240-262 */
-  GO_CVRP = 5       /* builtins.py:80-152 */
+  GO_CVRP = 5,      /* builtins.py:80-152 */
+  GO_USER = 6       /* NVRTC objective (go_problem_create_user) */
 };
 
 /* migration strategies (engine.py:483-521, :731-733) */
@@ -87,6 +88,26 @@ typedef struct go_problem_desc {
   const int32_t* jsp_duration;
   int32_t lb, ub;        /* integer encoding bounds */
 } go_problem_desc;
+
+/* A user-defined single-row problem whose objective and penalty are CUDA
+ * snippets compiled by NVRTC for sm_100a (the paper's solve_custom, PAPER.md:858-868;
+ * the reference's ProblemDefinition callbacks, problems.py:49-74).  The snippets are
+ * the bodies of
+ *     template <class Sol> double compute_obj(const Sol& sol, const Data& data)
+ *     template <class Sol> double compute_penalty(const Sol& sol, const Data& data)
+ * reading genes as sol[i] (0 <= i < sol.n) and each named array as data.<name>
+ * (const double*, length data.<name>_len).  Data arrays are copied at creation. */
+typedef struct go_user_problem_desc {
+  int32_t encoding;               /* 0 permutation, 1 binary, 2 integer (core.py:18-66) */
+  int32_t n;                      /* genes of the single row (dim2) */
+  int32_t lb, ub;                 /* integer encoding bounds (ignored otherwise) */
+  const char* compute_obj;        /* snippet body (required) */
+  const char* compute_penalty;    /* snippet body or NULL: penalty 0 */
+  int32_t n_data;
+  const char* const* data_names;  /* C identifiers */
+  const double* const* data;
+  const int64_t* data_lens;
+} go_user_problem_desc;
 
 typedef struct go_problem go_problem;
 typedef struct go_engine go_engine;
@@ -142,6 +163,10 @@ int go_device_query(int device, go_device_info* out);
 
 /* ---- problems: builtin_problem(name, InstanceData) (builtins.py:42-50) ---- */
 int go_problem_create(const go_problem_desc* desc, int device, go_problem** out);
+/* user problem: NVRTC compile (cached by SHA-256); a compile error returns
+ * GO_E_COMPILE with the NVRTC log in `log` (replaces ProblemDefinition, problems.py:49-74) */
+int go_problem_create_user(const go_user_problem_desc* desc, int device, go_problem** out,
+                           char* log, int log_len);
 int go_problem_destroy(go_problem* p);
 /* bytes of shared memory the instance needs when staged per CTA, 0 if it stays
  * in global/L2 (paper §4.3 auto-extension), and the representation chosen */

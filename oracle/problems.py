@@ -315,3 +315,25 @@ def validate(problem: Problem, sol: Sol) -> bool:
     if s.kind == BINARY:
         return all(set(sol.row(r).tolist()) <= {0, 1} for r in range(s.d1))
     return all(((sol.row(r) >= s.lb) & (sol.row(r) <= s.ub)).all() for r in range(s.d1))
+
+
+class Custom(Problem):
+    """A user-defined single-row problem (the CUDA-snippet path of
+    `solve_custom`; reference ProblemDefinition callbacks,
+    problems.py:49-74).  `obj(row)` / `pen(row)` restate the test's CUDA snippet
+    in Python with the same arithmetic order (test infrastructure only)."""
+
+    def __init__(self, kind, n, obj, pen=None, lb=0, ub=0, maximize=False, mats=()):
+        self.n = n
+        self.spec = Spec(kind, 1, n, n, SINGLE, directions=(MAX if maximize else MIN,),
+                         lb=lb, ub=ub)
+        self._obj, self._pen, self._mats = obj, pen, [np.asarray(m, np.float64) for m in mats]
+
+    def objective(self, i, sol):
+        return float(self._obj(sol.row(0)))
+
+    def penalty(self, sol):
+        return float(self._pen(sol.row(0))) if self._pen is not None else 0.0
+
+    def matrices(self):
+        return list(self._mats)

@@ -20,8 +20,8 @@ from .engine import (DeviceRun, EngineConfig, EvolverState, IslandsConfig, RunRe
                      initialize_population, random_solution, run, scalar_fitness)
 from .operators import (CustomOperator, SequenceEntry, SequenceRegistry, build_registry,
                         lns_scope)
-from .problems import (BUILTIN_NAMES, InstanceData, ProblemDefinition, builtin_problem,
-                       evaluate)
+from .problems import (BUILTIN_NAMES, CudaProblem, InstanceData, ProblemDefinition,
+                       builtin_problem, evaluate)
 from .profiles import PRESETS, ProblemProfile, Scale, WeightPreset, apply_preset, classify
 
 
@@ -30,6 +30,33 @@ def solve_tsp(dist_matrix, time_limit=30.0, **kw) -> RunResult:
     cfg = EngineConfig(time_limit_seconds=time_limit,
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
     return run(builtin_problem("tsp", InstanceData(distance_matrix=dist_matrix)), cfg)
+
+
+def solve_knapsack(weights, values, capacity, time_limit=30.0, **kw) -> RunResult:
+    """PAPER.md:850-856 `cugenopt.solve_knapsack(weights, values, cap)`."""
+    cfg = EngineConfig(time_limit_seconds=time_limit,
+                       max_generations=kw.pop("max_generations", 10 ** 9), **kw)
+    return run(builtin_problem("knapsack", InstanceData(weights=weights, values=values,
+                                                        capacity=capacity)), cfg)
+
+
+def solve_custom(encoding, dim2, n=None, compute_obj=None, compute_penalty=None, data=None,
+                 custom_operators=(), time_limit=30.0, lb=0, ub=None, maximize=False,
+                 best_known=None, **kw) -> RunResult:
+    """PAPER.md:858-868 `cugenopt.solve_custom(encoding=, dim2=, n=, compute_obj=,
+    compute_penalty=, data=, custom_operators=, time_limit=)`: a single-row
+    problem whose objective / penalty are CUDA snippets (see CudaProblem),
+    compiled by NVRTC into the device evolve kernel."""
+    if custom_operators:
+        raise ValueError("user operators are supported on the TSP path only; custom problems "
+                         "run every built-in operator applicable to their encoding")
+    if n is not None and int(n) != int(dim2):
+        raise ValueError("single-row custom problems need n == dim2")
+    prob = CudaProblem(encoding, int(dim2), compute_obj, compute_penalty, data, lb=lb, ub=ub,
+                       maximize=maximize)
+    cfg = EngineConfig(time_limit_seconds=time_limit,
+                       max_generations=kw.pop("max_generations", 10 ** 9), **kw)
+    return run(prob, cfg, best_known=best_known)
 
 
 __all__ = [name for name in dir() if not name.startswith("_")]

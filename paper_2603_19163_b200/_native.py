@@ -17,7 +17,8 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libcugenopt.so"
 
 GO_OK, GO_E_INVALID, GO_E_CUDA, GO_E_UNSUPPORTED, GO_E_COMPILE, GO_E_NODEVICE = 0, -1, -2, -3, -4, -5
-GO_TSP, GO_VRPTW, GO_QAP, GO_JSP_INT, GO_KNAPSACK, GO_CVRP = range(6)
+GO_TSP, GO_VRPTW, GO_QAP, GO_JSP_INT, GO_KNAPSACK, GO_CVRP, GO_USER = range(7)
+ENC_PERM, ENC_BINARY, ENC_INTEGER = range(3)
 MOVE_NONE, MOVE_SWAP, MOVE_REVERSE, MOVE_SEGMENT = range(4)
 MOVE_THREE_OPT = 8  # + variant 0..6
 MIG = {"ring": 0, "global_top_n": 1, "hybrid": 2}
@@ -54,6 +55,13 @@ class ProblemDesc(C.Structure):
                 ("capacity", C.c_double), ("n_jobs", C.c_int32), ("n_machines", C.c_int32),
                 ("ops_per_job", C.c_int32), ("jsp_machine", _PI), ("jsp_duration", _PI),
                 ("lb", C.c_int32), ("ub", C.c_int32)]
+
+
+class UserProblemDesc(C.Structure):  # go_user_problem_desc
+    _fields_ = [("encoding", C.c_int32), ("n", C.c_int32), ("lb", C.c_int32), ("ub", C.c_int32),
+                ("compute_obj", C.c_char_p), ("compute_penalty", C.c_char_p),
+                ("n_data", C.c_int32), ("data_names", C.POINTER(C.c_char_p)),
+                ("data", C.POINTER(_PD)), ("data_lens", C.POINTER(C.c_int64))]
 
 
 class CustomOp(C.Structure):
@@ -94,6 +102,8 @@ def _bind(lib):
         "go_device_count": ([P(C.c_int)], C.c_int),
         "go_device_query": ([C.c_int, P(DeviceInfo)], C.c_int),
         "go_problem_create": ([P(ProblemDesc), C.c_int, P(V)], C.c_int),
+        "go_problem_create_user": ([P(UserProblemDesc), C.c_int, P(V), C.c_char_p, C.c_int],
+                                   C.c_int),
         "go_problem_destroy": ([V], C.c_int),
         "go_problem_layout": ([V, P(C.c_int64), P(C.c_int32)], C.c_int),
         "go_problem_occupancy": ([V, C.c_int, C.c_int, _PI, _PI, _PI, P(C.c_int64)], C.c_int),

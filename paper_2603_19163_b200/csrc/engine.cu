@@ -188,6 +188,9 @@ struct go_problem {
   void* d_tri = nullptr;   // packed strict upper triangle (smem image)
   size_t full_bytes = 0, tri_bytes = 0;
   DeviceInfo dev;
+  // user problems (RK_USER): NVRTC objective module, encoding
+  gohost::JitModule user_mod;
+  int enc = 0;
   // user operators
   std::vector<gohost::UserOpSrc> ops;  // registered (compiled and probed)
   std::map<int, gohost::JitModule> jit;  // per layout
@@ -460,12 +463,78 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
   return GO_OK;
 }
 
+static bool c_identifier(const char* s) {
+  if (!s || !*s || !(std::isalpha((unsigned char)*s) || *s == '_')) return false;
+  for (const char* c = s; *c; ++c)
+    if (!(std::isalnum((unsigned char)*c) || *c == '_')) return false;
+  return std::strlen(s) < 64;
+}
+
+int go_problem_create_user(const go_user_problem_desc* d, int device, go_problem** out, char* log,
+                           int log_len) {
+  if (!d || !out || !d->compute_obj) return fail(GO_E_INVALID, "user problem needs compute_obj");
+  if (d->encoding < 0 || d->encoding > 2) return fail(GO_E_INVALID, "encoding must be 0, 1 or 2");
+  if (d->n < 1 || d->n > 32767) return fail(GO_E_INVALID, "n must be in [1, 32767]");
+  if (d->encoding == 2 && (d->lb > d->ub || d->lb < 0 || d->ub > 32767))
+    return fail(GO_E_INVALID, "integer bounds must satisfy 0 <= lb <= ub <= 32767");
+  if (d->n_data < 0 || (d->n_data > 0 && (!d->data_names || !d->data || !d->data_lens)))
+    return fail(GO_E_INVALID, "data arrays need names, pointers and lengths");
+  std::unique_ptr<go_problem> p(new go_problem());
+  p->kind = GO_USER;
+  p->family = 1;
+  p->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaFree(0));
+  int rc = query_device(device, &p->dev);
+  if (rc) return rc;
+  gohost::UserProblemSrc up;
+  up.obj = d->compute_obj;
+  up.pen = d->compute_penalty ? d->compute_penalty : "";
+  std::vector<unsigned char> img;
+  for (int i = 0; i < d->n_data; ++i) {
+    if (!c_identifier(d->data_names[i]) || d->data_lens[i] < 0 ||
+        (d->data_lens[i] > 0 && !d->data[i]))
+      return fail(GO_E_INVALID, std::string("bad data array #") + std::to_string(i));
+    for (int j = 0; j < i; ++j)
+      if (std::strcmp(d->data_names[i], d->data_names[j]) == 0)
+        return fail(GO_E_INVALID, std::string("duplicate data name ") + d->data_names[i]);
+    const size_t off = img.size(), bytes = (size_t)d->data_lens[i] * 8;
+    img.resize(off + pad16(bytes), 0);
+    if (bytes) memcpy(img.data() + off, d->data[i], bytes);
+    up.names.push_back(d->data_names[i]);
+    up.offsets.push_back(off);
+    up.lens.push_back(d->data_lens[i]);
+  }
+  if (img.empty()) img.assign(16, 0);
+  p->n = d->n;
+  p->d1 = 1;
+  p->d2 = d->n;
+  p->enc = d->encoding;
+  p->lb = d->encoding == 0 ? 0 : (d->encoding == 1 ? 0 : d->lb);
+  p->ub = d->encoding == 0 ? d->n - 1 : (d->encoding == 1 ? 1 : d->ub);
+  p->row_kind = go::RK_USER;
+  p->gsize = 2;
+  p->img_bytes = img.size();
+  std::string jlog;
+  rc = gohost::jit_build_user(up, &p->user_mod, &jlog);
+  if (log && log_len > 0) {
+    std::strncpy(log, jlog.c_str(), (size_t)log_len - 1);
+    log[log_len - 1] = 0;
+  }
+  if (rc) return fail(rc, "NVRTC build of the user problem failed: " + jlog.substr(0, 2000));
+  CK(cudaMalloc(&p->d_img, img.size()));
+  CK(cudaMemcpy(p->d_img, img.data(), img.size(), cudaMemcpyHostToDevice));
+  *out = p.release();
+  return GO_OK;
+}
+
 int go_problem_destroy(go_problem* p) {
   if (!p) return GO_OK;
   cudaSetDevice(p->device);
   cudaFree(p->d_img);
   for (auto& kv : p->jit)
     if (kv.second.mod && gohost::drv()) gohost::drv()->ModuleUnload(kv.second.mod);
+  if (p->user_mod.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod.mod);
   cudaFree(p->d_full);
   cudaFree(p->d_tri);
   delete p;
@@ -555,11 +624,13 @@ go::RowArgs row_args(const go_problem* p) {
   x.d2 = p->d2;
   x.tw = p->tw;
   x.obj_weight = 1.0;
+  x.enc = p->enc;
   return x;
 }
 
 // ---- row family helpers ----------------------------------------------------------
 void* row_kernel(const go_problem* p) {
+  if (p->row_kind == go::RK_USER) return nullptr;  // JIT (p->user_mod.evolve)
   if (p->row_kind == go::RK_QAP)
     return p->elem == E_I16 ? (void*)go_evolve_qap_i16
                             : (p->elem == E_I32 ? (void*)go_evolve_qap_i32 : (void*)go_evolve_qap_f64);
@@ -606,6 +677,14 @@ bool seq_supported(const go_problem* p, int id) {
            id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_OX;
   if (p->row_kind == go::RK_KNAP)
     return id == go::SEQ_FLIP || id == go::SEQ_SEG_FLIP || id == go::SEQ_UNIFORM_X;
+  if (p->row_kind == go::RK_USER) {  // sequence_applicable (operators.py:597-615)
+    if (p->enc == go::ENC_PERM)
+      return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
+             id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_OX;
+    if (p->enc == go::ENC_BINARY)
+      return id == go::SEQ_FLIP || id == go::SEQ_SEG_FLIP || id == go::SEQ_UNIFORM_X;
+    return id == go::SEQ_RANDOM_RESET || id == go::SEQ_SEG_RESET || id == go::SEQ_UNIFORM_X;
+  }
   if (p->row_kind == go::RK_PART)
     return id == go::SEQ_SWAP || id == go::SEQ_INSERT || id == go::SEQ_REVERSE ||
            id == go::SEQ_OR_OPT || id == go::SEQ_THREE_OPT || id == go::SEQ_ROW_SWAP ||
@@ -689,9 +768,15 @@ int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_
     if (!choose_row(p, TS, teams_per_cta, &L, &E, &smem))
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
     void* fn = row_kernel(p);
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUfunction jf = p->row_kind == go::RK_USER ? p->user_mod.evolve : nullptr;
+    int rc = set_smem_attr(fn, jf, smem);
+    if (rc) return rc;
     int blocks = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, E * TS, smem));
+    if (jf) {
+      CU(gohost::drv()->OccupancyMaxActiveBlocksPerMultiprocessor(&blocks, jf, E * TS, smem));
+    } else {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, E * TS, smem));
+    }
     if (layout) *layout = L;
     if (teams_cta) *teams_cta = E;
     if (teams_per_sm) *teams_per_sm = blocks * E;
@@ -744,6 +829,12 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
       double cap = p->capacity;
       void* args[] = {(void*)&inst, &off1, &nn, &cap, &d_g, &d_o, &d_p};
       CK(cudaLaunchKernel((void*)go_eval_knap, dim3(m), dim3(128), args, 0, 0));
+    } else if (p->row_kind == go::RK_USER) {
+      int mm = m;
+      void* args[] = {(void*)&inst, &nn, &mm, &d_g, &d_o, &d_p};
+      CU(gohost::drv()->LaunchKernel(p->user_mod.probe, (unsigned)((m + 127) / 128), 1, 1, 128, 1,
+                                     1, 0, nullptr, args, nullptr));
+      CK(cudaDeviceSynchronize());
     } else {
       int nj = p->n_jobs, pj = p->per_job, nmach = p->n_mach;
       void* args[] = {(void*)&inst, &off1, &nj, &pj, &nmach, &d_g, &d_o};
@@ -958,6 +1049,7 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
     e->inst = p->d_img;
     e->inst_bytes = e->layout == 10 ? pad16(p->img_bytes) : 0u;
     e->k_evolve = row_kernel(p);
+    if (p->row_kind == go::RK_USER) e->k_evolve_jit = p->user_mod.evolve;
   } else {
   choose_layout(p, e->TS, c->teams_per_cta, &e->layout, &e->E);
   const LayoutInfo& L = kLayouts[e->layout];
@@ -1224,6 +1316,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     x = row_args(p);
     x.penalty_weight = c.penalty_weight;
     x.obj_weight = c.obj_weight > 0 ? c.obj_weight : 1.0;
+    x.maximize = c.maximize;
   } else {
     a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
     a.resync = kLayouts[e->layout].elem == E_F64;

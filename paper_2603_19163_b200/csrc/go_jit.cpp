@@ -127,30 +127,16 @@ int jit_max_threads() {
   return (v >= 128 && v <= 1024 && v % 32 == 0) ? v : 512;
 }
 
-static const char* kHeaders[] = {"go_common.cuh", "go_dist.cuh", "go_perm.cuh", "go_perm_lns.cuh", "go_args.cuh",
-                                 "go_evolve_perm.cuh", "go_tsp_entry.cuh"};
+static const char* kHeaders[] = {"go_common.cuh",      "go_dist.cuh",      "go_perm.cuh",
+                                 "go_perm_lns.cuh",    "go_args.cuh",      "go_evolve_perm.cuh",
+                                 "go_tsp_entry.cuh",   "go_row.cuh",       "go_part.cuh",
+                                 "go_evolve_row.cuh",  "go_row_entry.cuh"};
 
-int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
-                    std::string* cubin_out, std::string* key_out, bool* hit_out,
-                    std::string* log) {
-  std::ostringstream src;
-  src << "// generated by go_jit.cpp — user operators for the TSP evolve kernel\n"
-      << "#include \"go_tsp_entry.cuh\"\n"
-      << "namespace go { namespace user {\n";
-  for (size_t i = 0; i < ops.size(); ++i) {
-    src << "// operator " << ops[i].id << " (" << ops[i].name << ")\n"
-        << "template <class Ctx> __device__ __forceinline__ void op_slot" << i
-        << "(Ctx& ctx) {\n#line 1 \"@OPDIR@/" << ops[i].name << ".cuh\"\n"
-        << ops[i].body << "\n}\n";
-  }
-  src << "}  // namespace user\nstruct UserOps {\n"
-      << "  template <class Ctx> __device__ __forceinline__ static void run(int slot, Ctx& ctx) {\n"
-      << "    switch (slot) {\n";
-  for (size_t i = 0; i < ops.size(); ++i)
-    src << "      case " << i << ": user::op_slot" << i << "(ctx); break;\n";
-  src << "      default: ctx.err |= ERR_UNKNOWN_SEQ;\n    }\n  }\n};\n}  // namespace go\n"
-      << "GO_TSP_KERNELS(jit, " << dist_type << ", go::UserOps)\n";
-  const std::string source = src.str();
+// NVRTC compile of a generated translation unit (plus the user snippets it
+// #line-references) with the SHA-256 cubin cache.
+static int jit_compile_source(const std::string& source, const std::vector<UserOpSrc>& ops,
+                              std::string* cubin_out, std::string* key_out, bool* hit_out,
+                              std::string* log) {
 
   const std::string kdir = kernel_dir();
   std::string headers_blob;
@@ -232,6 +218,29 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
   return GO_OK;
 }
 
+int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
+                    std::string* cubin_out, std::string* key_out, bool* hit_out,
+                    std::string* log) {
+  std::ostringstream src;
+  src << "// generated by go_jit.cpp — user operators for the TSP evolve kernel\n"
+      << "#include \"go_tsp_entry.cuh\"\n"
+      << "namespace go { namespace user {\n";
+  for (size_t i = 0; i < ops.size(); ++i) {
+    src << "// operator " << ops[i].id << " (" << ops[i].name << ")\n"
+        << "template <class Ctx> __device__ __forceinline__ void op_slot" << i
+        << "(Ctx& ctx) {\n#line 1 \"@OPDIR@/" << ops[i].name << ".cuh\"\n"
+        << ops[i].body << "\n}\n";
+  }
+  src << "}  // namespace user\nstruct UserOps {\n"
+      << "  template <class Ctx> __device__ __forceinline__ static void run(int slot, Ctx& ctx) {\n"
+      << "    switch (slot) {\n";
+  for (size_t i = 0; i < ops.size(); ++i)
+    src << "      case " << i << ": user::op_slot" << i << "(ctx); break;\n";
+  src << "      default: ctx.err |= ERR_UNKNOWN_SEQ;\n    }\n  }\n};\n}  // namespace go\n"
+      << "GO_TSP_KERNELS(jit, " << dist_type << ", go::UserOps)\n";
+  return jit_compile_source(src.str(), ops, cubin_out, key_out, hit_out, log);
+}
+
 int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
                   JitModule* out, std::string* log) {
   const auto t0 = std::chrono::steady_clock::now();
@@ -254,6 +263,64 @@ int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& op
   if (d->ModuleGetFunction(&out->evolve, out->mod, "go_evolve_tsp_jit") != CUDA_SUCCESS ||
       d->ModuleGetFunction(&out->probe, out->mod, "go_probe_tsp_jit") != CUDA_SUCCESS) {
     *log = "JIT module lacks go_evolve_tsp_jit / go_probe_tsp_jit";
+    return GO_E_COMPILE;
+  }
+  out->cache_hit = hit;
+  out->compile_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return GO_OK;
+}
+
+// ---- user problems: NVRTC-compiled objective / penalty ----------
+int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::ostringstream src;
+  src << "// generated by go_jit.cpp — user problem (objective + penalty snippets)\n"
+      << "#include \"go_row_entry.cuh\"\n"
+      << "namespace go { namespace user {\n"
+      << "struct Data {\n";
+  for (size_t i = 0; i < up.names.size(); ++i)
+    src << "  const double* " << up.names[i] << ";\n  int " << up.names[i] << "_len;\n";
+  src << "  int _unused;\n};\n"
+      << "__device__ __forceinline__ Data make_data(const unsigned char* b) {\n  Data d;\n";
+  for (size_t i = 0; i < up.names.size(); ++i)
+    src << "  d." << up.names[i] << " = (const double*)(b + " << up.offsets[i] << "ull);\n"
+        << "  d." << up.names[i] << "_len = " << up.lens[i] << ";\n";
+  src << "  d._unused = 0;\n  return d;\n}\n"
+      << "template <class Sol> __device__ __forceinline__ double compute_obj(const Sol& sol, "
+         "const Data& data) {\n#line 1 \"@OPDIR@/compute_obj.cuh\"\n"
+      << up.obj << "\n}\n"
+      << "template <class Sol> __device__ __forceinline__ double compute_penalty(const Sol& sol, "
+         "const Data& data) {\n#line 1 \"@OPDIR@/compute_penalty.cuh\"\n"
+      << (up.pen.empty() ? std::string("return 0.0;") : up.pen) << "\n}\n"
+      << "}  // namespace user\n"
+      << "struct UserProblem {\n"
+      << "  template <class S> __device__ __forceinline__ static double obj(const S& s, "
+         "const unsigned char* b) { return user::compute_obj(s, user::make_data(b)); }\n"
+      << "  template <class S> __device__ __forceinline__ static double pen(const S& s, "
+         "const unsigned char* b) { return user::compute_penalty(s, user::make_data(b)); }\n"
+      << "};\n}  // namespace go\nGO_USER_KERNELS(go::UserProblem)\n";
+  std::vector<UserOpSrc> files = {{0, "compute_obj", up.obj},
+                                  {1, "compute_penalty", up.pen.empty() ? "return 0.0;" : up.pen}};
+  std::string cubin;
+  bool hit = false;
+  int rc = jit_compile_source(src.str(), files, &cubin, &out->key, &hit, log);
+  if (rc) return rc;
+  const Drv* d = drv();
+  if (!d) {
+    *log = "CUDA driver API unavailable";
+    return GO_E_NODEVICE;
+  }
+  CUresult cr = d->ModuleLoadData(&out->mod, cubin.data());
+  if (cr != CUDA_SUCCESS) {
+    const char* s = nullptr;
+    d->GetErrorString(cr, &s);
+    *log = std::string("cuModuleLoadData: ") + (s ? s : "?");
+    return GO_E_CUDA;
+  }
+  if (d->ModuleGetFunction(&out->evolve, out->mod, "go_evolve_user") != CUDA_SUCCESS ||
+      d->ModuleGetFunction(&out->probe, out->mod, "go_eval_user") != CUDA_SUCCESS) {
+    *log = "JIT module lacks go_evolve_user / go_eval_user";
     return GO_E_COMPILE;
   }
   out->cache_hit = hit;

@@ -36,4 +36,15 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
 int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
                   JitModule* out, std::string* log);
 
+// A user problem: objective / penalty snippet bodies and the named float64
+// data arrays they read (byte offsets into the instance image).
+struct UserProblemSrc {
+  std::string obj, pen;
+  std::vector<std::string> names;
+  std::vector<unsigned long long> offsets;
+  std::vector<long long> lens;
+};
+// Builds go_evolve_user (JitModule::evolve) and go_eval_user (JitModule::probe).
+int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log);
+
 }  // namespace gohost

@@ -92,6 +92,8 @@ struct RowArgs {
   // partition problems (VRPTW / CVRP): compact row = cells[n_cells] + sizes[d1]
   unsigned off2, off3, off4;  // ready, due, service offsets (off1 = demands)
   int n_cells, d1, d2, tw;
+  // user problems (NVRTC objective): encoding 0 permutation, 1 binary, 2 integer
+  int enc, maximize;
 };
 
 struct EpilogueArgs {

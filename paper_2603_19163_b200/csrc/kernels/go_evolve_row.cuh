@@ -21,7 +21,51 @@
 
 namespace go {
 
-enum RowKind { RK_QAP = 0, RK_KNAP = 1, RK_JSP = 2, RK_PART = 3 };
+enum RowKind { RK_QAP = 0, RK_KNAP = 1, RK_JSP = 2, RK_PART = 3, RK_USER = 4 };
+enum UserEnc { ENC_PERM = 0, ENC_BINARY = 1, ENC_INTEGER = 2 };
+
+// ---- solution views handed to NVRTC-compiled user objectives ----------------------
+// A user objective is `template <class Sol> double compute_obj(const Sol& sol,
+// const Data& data)` reading genes as sol[i] (i < sol.n).  The views let trial
+// evaluations run without copying the row.
+template <class G>
+struct RowSol {  // the row itself
+  const G* r;
+  int n;
+  __device__ __forceinline__ int operator[](int i) const { return r[i]; }
+  __device__ __forceinline__ int size() const { return n; }
+};
+template <class G>
+struct OvSol {  // gene p replaced by v (binary / integer trials)
+  const G* r;
+  int n, p, v;
+  __device__ __forceinline__ int operator[](int i) const { return i == p ? v : (int)r[i]; }
+  __device__ __forceinline__ int size() const { return n; }
+};
+template <class G>
+struct InsSol {  // v moved from slot q0 to slot pos (permutation insertion trials)
+  const G* r;
+  int n, q0, pos, v;
+  __device__ __forceinline__ int operator[](int i) const {
+    if (i == pos) return v;
+    const int j = i < pos ? i : i - 1;  // index in the row without v
+    return r[j < q0 ? j : j + 1];
+  }
+  __device__ __forceinline__ int size() const { return n; }
+};
+
+struct NoUser {  // built-in kinds: never called
+  template <class S>
+  __device__ __forceinline__ static double obj(const S&, const unsigned char*) { return 0.0; }
+  template <class S>
+  __device__ __forceinline__ static double pen(const S&, const unsigned char*) { return 0.0; }
+};
+
+// scalar_fitness (engine.py:215-222) of one objective + penalty, rounding each product
+__device__ __forceinline__ double user_phi(double obj, double pen, double w, int maximize,
+                                           double pw) {
+  return __dadd_rn(__dadd_rn(0.0, __dmul_rn(w, maximize ? -obj : obj)), __dmul_rn(pw, pen));
+}
 
 // Instance views (all in shared memory once staged; `use_s` reads via ld.shared).
 template <class E>
@@ -367,12 +411,13 @@ struct GrShared {  // views into the team scratch (TeamShared::cnt, 128 ints)
 };
 
 // Thread 0: the draws of op_guided_rebuild for the lane (operators.py:501-571).
+// `cells`: binary / integer encodings (coordinate-greedy branch).
 template <int KIND>
 __device__ __forceinline__ void gr_draw(Stream& rng, const GrShared& g, int n, int n_cfg, int lb,
-                                        int ub, const short* sz, int d1) {
+                                        int ub, const short* sz, int d1, bool cells) {
   const int ls = lns_scope(n_cfg);
   int m = 0;
-  if (KIND == RK_JSP) {
+  if (cells) {
     if (n > 0) {
       m = ls < n ? ls : n;
       sample_range(rng, n, m, g.picks());
@@ -401,7 +446,7 @@ __device__ __forceinline__ void gr_draw(Stream& rng, const GrShared& g, int n, i
     m = ls < n - 1 ? ls : n - 1;
     int* pk = g.picks();
     sample_range(rng, n, m, pk);
-    if (KIND == RK_QAP) {  // sorted by (r, -p): descending positions
+    if (KIND != RK_PART) {  // sorted by (r, -p): descending positions
       for (int i = 1; i < m; ++i) {
         const int v = pk[i];
         int j = i;
@@ -476,14 +521,12 @@ __device__ __forceinline__ void team_permute(G* row, int n, const F& src, int la
   team_bar(team, TS);
 }
 
-template <class E, class G>
-__device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& g, double* sbuf,
-                            int lane, int team, int TS) {
-  typedef typename AccOf<E>::T A;
+// pop the picks (descending positions) and park them at the row end in pick
+// order (operators.py:527-533); taken values published in g.taken()
+template <class G>
+__device__ void team_pop_park(G* row, int n, const GrShared& g, int lane, int team, int TS) {
   const int m = g.m();
-  if (m == 0) return;
   const int* pk = g.picks();
-  // pop the picks (descending positions) and park them at the end, in pick order
   if (lane == 0)
     for (int t = 0; t < m; ++t) g.taken()[t] = row[pk[t]];
   if (n > 8 * TS) {  // rows longer than the register staging: serial moves by thread 0
@@ -496,12 +539,42 @@ __device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& 
       for (int t = 0; t < m; ++t) row[size++] = (G)g.taken()[t];
     }
     team_bar(team, TS);
-  } else team_permute(row, n, [&](int t) -> int {
-    if (t >= n - m) return pk[t - (n - m)];
-    int p = t;  // t-th survivor: skip picked positions in ascending order
-    for (int j = m - 1; j >= 0; --j) p += pk[j] <= p;
-    return p;
-  }, lane, team, TS);
+  } else {
+    team_permute(row, n, [&](int t) -> int {
+      if (t >= n - m) return pk[t - (n - m)];
+      int p = t;  // t-th survivor: skip picked positions in ascending order
+      for (int j = m - 1; j >= 0; --j) p += pk[j] <= p;
+      return p;
+    }, lane, team, TS);
+  }
+}
+
+// move the value at slot q0 to slot b (the row keeps n slots)
+template <class G>
+__device__ void team_move(G* row, int n, int q0, int b, int v, int lane, int team, int TS) {
+  if (n > 8 * TS) {
+    if (lane == 0) {
+      row_pop(row, n, q0);
+      for (int p = n - 1; p > b; --p) row[p] = row[p - 1];
+      row[b] = (G)v;
+    }
+    team_bar(team, TS);
+  } else {
+    team_permute(row, n, [&](int x) -> int {
+      if (x == b) return q0;
+      const int r = x < b ? x : x - 1;  // index in the row without v
+      return r < q0 ? r : r + 1;
+    }, lane, team, TS);
+  }
+}
+
+template <class E, class G>
+__device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& g, double* sbuf,
+                            int lane, int team, int TS) {
+  typedef typename AccOf<E>::T A;
+  const int m = g.m();
+  if (m == 0) return;
+  team_pop_park(row, n, g, lane, team, TS);
   for (int t = 0; t < m; ++t) {
     const int v = g.taken()[t];
     for (int p = lane; p < n; p += TS)
@@ -531,21 +604,92 @@ __device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& 
     }
     if (lane == 0) g.aux() = bp;
     team_bar(team, TS);
-    const int b = g.aux();
-    if (n > 8 * TS) {
-      if (lane == 0) {
-        row_pop(row, n, q0);
-        for (int p = n - 1; p > b; --p) row[p] = row[p - 1];
-        row[b] = (G)v;
+    team_move(row, n, q0, g.aux(), v, lane, team, TS);
+  }
+}
+
+// user objectives: guided rebuild trials scored by the NVRTC-compiled objective
+// on virtual rows (no copies), in parallel over the team
+struct UserScore {
+  const unsigned char* inst;
+  double w, pw;
+  int maximize;
+};
+
+template <class U, class G>
+__device__ void team_gr_user_perm(G* row, int n, const GrShared& g, const UserScore& us,
+                                  double* sbuf, TeamShared<double>* ts, int lane, int team,
+                                  int TS) {
+  const int m = g.m();
+  if (m == 0) return;
+  const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
+  team_pop_park(row, n, g, lane, team, TS);
+  for (int t = 0; t < m; ++t) {
+    const int v = g.taken()[t];
+    for (int p = lane; p < n; p += TS)
+      if (row[p] == v) g.res() = p;
+    team_bar(team, TS);
+    const int q0 = g.res();
+    double bs = 0.0;
+    int bi = 0x7fffffff;
+    for (int pos = lane; pos < n; pos += TS) {  // ascending per thread: first minimum
+      const InsSol<G> sol{row, n, q0, pos, v};
+      const double sc = user_phi(U::obj(sol, us.inst), U::pen(sol, us.inst), us.w, us.maximize,
+                                 us.pw);
+      if (bi == 0x7fffffff || sc < bs) {
+        bs = sc;
+        bi = pos;
       }
-      team_bar(team, TS);
-    } else {
-      team_permute(row, n, [&](int x) -> int {
-        if (x == b) return q0;
-        const int r = x < b ? x : x - 1;  // index in the row without v
-        return r < q0 ? r : r + 1;
-      }, lane, team, TS);
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, bs, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || ob < bs || (ob == bs && oi < bi))) {
+        bs = ob;
+        bi = oi;
+      }
+    }
+    if (wl == 0) {
+      sbuf[warp] = bs;
+      ts->wl[warp] = bi;
+    }
+    team_bar(team, TS);
+    if (lane == 0) {
+      double b = 0.0;
+      int ib = 0x7fffffff;
+      for (int w = 0; w < nwarps; ++w) {
+        const int oi = ts->wl[w];
+        if (oi != 0x7fffffff && (ib == 0x7fffffff || sbuf[w] < b || (sbuf[w] == b && oi < ib))) {
+          b = sbuf[w];
+          ib = oi;
+        }
+      }
+      g.aux() = ib;
+    }
+    team_bar(team, TS);
+    team_move(row, n, q0, g.aux(), v, lane, team, TS);
+  }
+}
+
+template <class U, class G>
+__device__ void team_gr_user_cells(G* row, int n, const GrShared& g, const UserScore& us,
+                                   double* sbuf, int lane, int team, int TS) {
+  const int m = g.m(), nd = g.nd();
+  for (int t = 0; t < m; ++t) {
+    const int p = g.picks()[t];
+    for (int i = lane; i < nd; i += TS) {
+      const OvSol<G> sol{row, n, p, g.dom()[i]};
+      sbuf[i] = user_phi(U::obj(sol, us.inst), U::pen(sol, us.inst), us.w, us.maximize, us.pw);
+    }
+    team_bar(team, TS);
+    if (lane == 0) {  // first minimum in domain order
+      int bi = 0;
+      for (int i = 1; i < nd; ++i)
+        if (sbuf[i] < sbuf[bi]) bi = i;
+      row[p] = (G)g.dom()[bi];
+    }
+    team_bar(team, TS);
   }
 }
 
@@ -859,7 +1003,7 @@ __device__ __forceinline__ u32 warp_uniform_x(G* row, int n, const MateSel& ms, 
   return pos0 + 2u * (u32)n;
 }
 
-template <int KIND, class E, class G>
+template <int KIND, class E, class G, class U = NoUser>
 __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X) {
   extern __shared__ __align__(128) unsigned char sm[];
   if (A.gs->stop) return;
@@ -1194,7 +1338,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
             rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
             rng.seek(la.pos[L]);
             gr_draw<KIND>(rng, gsh, KIND == RK_PART ? X.n_cells : n, X.n_cfg, X.lb, X.ub,
-                          (const short*)lrow + X.n_cells, X.d1);
+                          (const short*)lrow + X.n_cells, X.d1,
+                          KIND == RK_JSP || (KIND == RK_USER && X.enc != ENC_PERM));
             const u32 meta = la.meta[L];
             const int k = meta_k(meta);
             int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
@@ -1214,6 +1359,12 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           } else if (KIND == RK_PART) {
             team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2,
                          X.obj_weight, pwt, gsh, la.delta, ts, lane, team, TS);
+          } else if (KIND == RK_USER) {
+            const UserScore us{inst, X.obj_weight, pwt, X.maximize};
+            if (X.enc == ENC_PERM)
+              team_gr_user_perm<U>(lrow, n, gsh, us, la.delta, ts, lane, team, TS);
+            else
+              team_gr_user_cells<U>(lrow, n, gsh, us, la.delta, lane, team, TS);
           }
           team_bar(team, TS);
         }
@@ -1241,6 +1392,15 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
         dl = __dsub_rn(phi_c, phi0);
         rd_elem += 6u * (unsigned)X.n_cells;
+      } else if (KIND == RK_USER) {  // NVRTC objective, full evaluation
+        const RowSol<G> sol{row, n};
+        nscal = __dadd_rn(0.0, __dmul_rn(X.obj_weight, X.maximize ? -U::obj(sol, inst)
+                                                                   : U::obj(sol, inst)));
+        npen = U::pen(sol, inst);
+        const double phi_c = __dadd_rn(nscal, __dmul_rn(pwt, npen));
+        const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
+        dl = __dsub_rn(phi_c, phi0);
+        rd_pos += 0u;
       } else if (KIND == RK_QAP) {
         unsigned rd = 0;
         const double dq = qap_delta(qv, cur, row, nm, lo, hi, rd);

@@ -98,7 +98,30 @@ __device__ __forceinline__ void part_eval_entry(const void* inst, go::RowArgs x,
   pen[blockIdx.x] = p;
 }
 
+// evaluate() of m user-problem rows: one thread per solution (the user objective
+// is serial code)
+template <class U>
+__device__ __forceinline__ void user_eval_entry(const void* inst, int n, int m,
+                                                const short* genes, double* obj, double* pen) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const RowSol<short> sol{genes + (size_t)i * n, n};
+  obj[i] = U::obj(sol, (const unsigned char*)inst);
+  pen[i] = U::pen(sol, (const unsigned char*)inst);
+}
+
 }  // namespace go
+
+// Kernels of one NVRTC user problem (go_jit.cpp generates `U`).
+#define GO_USER_KERNELS(U)                                                                    \
+  extern "C" __global__ void __launch_bounds__(512, 1) go_evolve_user(go::EvolveArgs a,        \
+                                                                      go::RowArgs x) {        \
+    go::evolve_row<go::RK_USER, double, short, U>(a, x);                                      \
+  }                                                                                           \
+  extern "C" __global__ void go_eval_user(const void* inst, int n, int m, const short* g,     \
+                                          double* obj, double* pen) {                          \
+    go::user_eval_entry<U>(inst, n, m, g, obj, pen);                                          \
+  }
 
 #define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \
   extern "C" __global__ void __launch_bounds__(512, 1) NAME(go::EvolveArgs a, go::RowArgs x) { \

@@ -430,3 +430,91 @@ def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
     raise NotImplementedError(
         f"problem {name!r} has no B200 device path in this build "
         f"(device problems: {', '.join(DEVICE_PROBLEMS)})")
+
+
+class CudaProblem(ProblemDefinition):
+    """A user-defined single-row problem whose objective and penalty are CUDA
+    snippets, compiled by NVRTC for sm_100a into the row evolve kernel (the
+    paper's `solve_custom`).  It stands in for a reference
+    `ProblemDefinition` subclass (problems.py:49-74): the reference's Python
+    `compute_objective` / `compute_penalty` callbacks become the bodies of
+
+        template <class Sol> double compute_obj(const Sol& sol, const Data& data)
+        template <class Sol> double compute_penalty(const Sol& sol, const Data& data)
+
+    reading genes as `sol[i]` (0 <= i < sol.n) and every entry of `data` as
+    `data.<name>` (const double*, length `data.<name>_len`).  All built-in
+    operators applicable to the encoding run on the device, including
+    crossovers and guided rebuild (whose trials call the snippet)."""
+
+    JIT = True  # device_handle compiles (reported as jit_seconds, outside the budget)
+    _ENC = {"permutation": N.ENC_PERM, "binary": N.ENC_BINARY, "integer": N.ENC_INTEGER}
+    _SEQS = {
+        "permutation": (SEQ_SWAP, SEQ_INSERT, SEQ_REVERSE, SEQ_OR_OPT, SEQ_THREE_OPT,
+                        SEQ_OX_CROSSOVER, SEQ_SEG_SHUFFLE, SEQ_SCATTER_SHUFFLE,
+                        SEQ_GUIDED_REBUILD),
+        "binary": (SEQ_FLIP, SEQ_SEG_FLIP, SEQ_UNIFORM_CROSSOVER, SEQ_SEG_SHUFFLE,
+                   SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD),
+        "integer": (SEQ_RANDOM_RESET, SEQ_SEG_RESET, SEQ_UNIFORM_CROSSOVER, SEQ_SEG_SHUFFLE,
+                    SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD),
+    }
+
+    def __init__(self, encoding: str, n: int, compute_obj: str, compute_penalty: str | None = None,
+                 data: dict | None = None, lb: int = 0, ub: int | None = None,
+                 maximize: bool = False, name: str = "objective",
+                 init_matrices: list | None = None):
+        if encoding not in self._ENC:
+            raise ValueError(f"encoding must be one of {sorted(self._ENC)}, got {encoding!r}")
+        if not isinstance(compute_obj, str) or not compute_obj.strip():
+            raise ValueError("compute_obj must be a CUDA snippet (function body)")
+        self.encoding, self.n = encoding, int(n)
+        self.compute_obj_src, self.compute_penalty_src = compute_obj, compute_penalty
+        self.data = {k: np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
+                     for k, v in (data or {}).items()}
+        if encoding == "permutation":
+            enc = Encoding.permutation()
+        elif encoding == "binary":
+            enc = Encoding.binary()
+        else:
+            if ub is None:
+                raise ValueError("integer encoding needs ub")
+            enc = Encoding.integer(int(lb), int(ub))
+        self.lb, self.ub = (int(lb), int(ub)) if encoding == "integer" else (0, 0)
+        self._matrices = [np.asarray(m, dtype=np.float64) for m in (init_matrices or [])]
+        self._cfg = ProblemConfig(
+            encoding=enc, d1=1, d2=self.n, n=self.n, row_mode=RowModeKind.SINGLE_SEQ,
+            obj_defs=(ObjDef(name, Direction.MAXIMIZE if maximize else Direction.MINIMIZE),))
+
+    def config(self):
+        return self._cfg
+
+    def init_matrices(self):
+        return self._matrices
+
+    def payload_nbytes(self) -> int:
+        return sum(a.nbytes for a in self.data.values())
+
+    def device_sequences(self):
+        return self._SEQS[self.encoding]
+
+    def device_handle(self, device: int = 0):
+        if self._handle is not None and self._handle_device == device:
+            return self._handle
+        lib = N.load()
+        names = list(self.data)
+        arrays = [self.data[k] for k in names]
+        c_names = (C.c_char_p * max(1, len(names)))(*[k.encode() for k in names])
+        c_ptrs = (C.POINTER(C.c_double) * max(1, len(names)))(*[N.dptr(a) for a in arrays])
+        c_lens = (C.c_int64 * max(1, len(names)))(*[len(a) for a in arrays])
+        desc = N.UserProblemDesc(
+            encoding=self._ENC[self.encoding], n=self.n, lb=self.lb, ub=self.ub,
+            compute_obj=self.compute_obj_src.encode(),
+            compute_penalty=self.compute_penalty_src.encode() if self.compute_penalty_src else None,
+            n_data=len(names), data_names=c_names, data=c_ptrs, data_lens=c_lens)
+        h = C.c_void_p()
+        log = C.create_string_buffer(8192)
+        N.check(lib.go_problem_create_user(C.byref(desc), device, C.byref(h), log, len(log)))
+        self._keepalive = (arrays, c_names, c_ptrs, c_lens)
+        self._handle = h
+        self._handle_device = device
+        return h

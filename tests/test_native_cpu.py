@@ -69,7 +69,7 @@ def test_registry_and_presets_match_oracle():
         cfg = prob.config()
         reg = G.build_registry(cfg, prob.device_sequences())
         G.apply_preset(reg, G.classify(cfg))
-        oreg = OA.build_registry(OP.Tsp(dist).spec, (0, 1, 2, 3))
+        oreg = OA.build_registry(OP.Tsp(dist).spec, None)  # the reference's full registry
         OA.apply_preset(oreg, OA.scale_of(OP.Tsp(dist).spec))
         assert reg.ids() == oreg.ids()
         assert reg.weights() == oreg.weights()
@@ -111,3 +111,21 @@ def test_config_validation_mirrors_reference():
     with pytest.raises(ValueError):
         G.builtin_problem("tsp", G.InstanceData(distance_matrix=np.array([[0, 1], [2, 0.0]])))
     assert math.isclose(sum(G.DEFAULT_K_WEIGHTS), 1.0)
+
+
+def test_custom_problem_host_side():
+    """CudaProblem (solve_custom) config / registry on the host; compile needs a device."""
+    p = G.CudaProblem("integer", 12, "return 0.0;", lb=2, ub=5, maximize=True,
+                      data={"w": np.arange(12.0)})
+    cfg = p.config()
+    assert (cfg.d1, cfg.d2, cfg.encoding.lower_bound, cfg.encoding.upper_bound) == (1, 12, 2, 5)
+    reg = G.build_registry(cfg, p.device_sequences())
+    assert reg.ids() == [7, 8, 13, 14, 15, 16]  # operators.py:597-615 for INTEGER
+    assert p.payload_nbytes() == 96
+    with pytest.raises(ValueError):
+        G.CudaProblem("tree", 4, "return 0.0;")
+    with pytest.raises(ValueError):
+        G.CudaProblem("integer", 4, "return 0.0;")  # integer needs ub
+    with pytest.raises(ValueError):
+        G.solve_custom("binary", 4, compute_obj="return 0.0;",
+                       custom_operators=[G.CustomOperator(100, "x", cuda="")])
