@@ -50,3 +50,42 @@ def test_equal_budget_gap_no_worse_than_reference(variant):
     if out.is_dir():
         (out / f"gap_parity_{variant}.json").write_text(json.dumps(summary, indent=1))
     assert p > 0.05, summary
+
+
+GOLD_ROWS = Path(__file__).with_name("golden") / "gap_rows.json"
+
+
+def _row_problem(name):
+    if name == "qap30":
+        f, d = I.qap_random(30, 100)
+        return G.builtin_problem("qap", G.InstanceData(flow_matrix=f, distance_matrix=d)), False
+    if name == "knap200":
+        w, v, cap = I.knapsack_random(200, 1000)
+        return G.builtin_problem("knapsack", G.InstanceData(weights=w, values=v,
+                                                            capacity=cap)), True
+    return G.builtin_problem("jsp_int", G.InstanceData(jobs=I.jsp_random(6, 5, 7))), False
+
+
+@pytest.mark.parametrize("name", ["qap30", "knap200", "jsp6x5"])
+def test_row_family_gap_no_worse_than_reference(name):
+    """Same bar for the row kernels (permutation / binary / integer encodings),
+    reference runs frozen by tests/golden/make_gap_golden_rows.py."""
+    from scipy.stats import mannwhitneyu
+    data = json.loads(GOLD_ROWS.read_text())
+    c = data["cases"][name]
+    prob, maximize = _row_problem(name)
+    ours = []
+    for seed in data["seeds"]:
+        res = G.run(prob, G.EngineConfig(population=c["population"], team_size=c["team_size"],
+                                         max_generations=c["max_generations"], seed=seed))
+        assert res.penalty == 0.0
+        ours.append(float(res.objectives[0]))
+    ref = [data["runs"][name][str(s)][0] for s in data["seeds"]]
+    p = mannwhitneyu(ours, ref, alternative="less" if maximize else "greater").pvalue
+    summary = {"case": name, "maximize": maximize, "ours": ours, "reference": ref,
+               "mean_ours": float(np.mean(ours)), "mean_reference": float(np.mean(ref)),
+               "p_worse": p}
+    out = Path("gpurun_out")
+    if out.is_dir():
+        (out / f"gap_parity_{name}.json").write_text(json.dumps(summary, indent=1))
+    assert p > 0.05, summary
