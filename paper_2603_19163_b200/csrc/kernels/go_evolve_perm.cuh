@@ -502,6 +502,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           }
         }
         team_bar(team, TS);
+        GO_TICK(15);
       }
     }
 

@@ -14,7 +14,8 @@ for chunk in (50, 300):
     N.check(dr.lib.go_engine_debug_counters(dr.engine, out, 16))
     v = np.array(list(out), dtype=np.float64)
     names = ["-", "s0 rank", "s0 order", "s0 exec", "s0 coop", "s1 rank", "s1 order", "s1 exec", "s1 coop",
-             "s2 rank", "s2 order", "s2 exec", "s2 coop", "argmin", "decide+apply+rec", "-"]
+             "s2 rank", "s2 order", "s2 exec", "s2 coop", "argmin", "decide+apply+rec",
+             "deferred (all steps)"]
     tot = v.sum()
     print(f"after {chunk} gens: total {tot:.3e} cycles")
     for nm, x in zip(names, v):
