@@ -275,6 +275,19 @@ def run_ours(args):
                     "final_weights_30s": {e["name"]: round(e["weight"], 4)
                                           for e in res.final_weights["sequences"]},
                     "k_weights_30s": [round(x, 4) for x in res.final_weights["k_steps"]]}
+        # time to the known optimum (44,200) through the same API: target_objective stops
+        # the run at the chunk where the global best reaches it (engine.py:712-713)
+        rt = G.run(prob, G.EngineConfig(team_size=args.team_size, seed=args.seed + 7,
+                                        custom_operators=ops, device=local,
+                                        time_limit_seconds=args.gap_seconds,
+                                        target_objective=opt, max_generations=10 ** 9,
+                                        distributed=world > 1,
+                                        islands=G.IslandsConfig(count=world, migration="hybrid",
+                                                                interval=100)),
+                   best_known=opt)
+        hit = rt.gap_pct == 0.0
+        gap_info.update({"time_to_optimum_s": rt.elapsed_seconds if hit else None,
+                         "generations_to_optimum": rt.generations_completed if hit else None})
 
     extra = other_configs(G, I, local) if (args.other_configs and world == 1) else None
     if rank != 0:
