@@ -103,10 +103,71 @@ def init_population(problem, pop_size, oversample, rng):
                 pool.extend(perm_to_sol(p, spec) for p in heuristic_perms(mat))
     for s in pool:
         evaluate(problem, s)
-    if spec.m != 1:
-        raise NotImplementedError("multi-objective init is off the hot path")
+    if spec.m != 1:  # engine.py:352-360: non-dominated fronts, crowding order
+        fronts = nondominated_sort(np.array([s.obj for s in pool]), spec.directions)
+        keep = []
+        for front in fronts:
+            for idx in front:
+                if len(keep) < pop_size:
+                    keep.append(pool[idx])
+        return keep
     pool.sort(key=cmp_to_key(lambda a, b: compare(problem, a, b)))
     return pool[:pop_size]
+
+
+def nondominated_sort(points, directions):
+    """engine.py:370-420 (fast_nondominated_sort + crowding order)."""
+    pts = np.asarray(points, dtype=np.float64).copy()
+    for j, d in enumerate(directions):
+        if d == MAX:
+            pts[:, j] = -pts[:, j]
+    n = len(pts)
+
+    def dom(a, b):
+        return bool(np.all(a <= b) and np.any(a < b))
+    dominated_by = [[] for _ in range(n)]
+    count = np.zeros(n, dtype=np.int64)
+    fronts = [[]]
+    for i in range(n):
+        for j in range(i + 1, n):
+            if dom(pts[i], pts[j]):
+                dominated_by[i].append(j)
+                count[j] += 1
+            elif dom(pts[j], pts[i]):
+                dominated_by[j].append(i)
+                count[i] += 1
+    for i in range(n):
+        if count[i] == 0:
+            fronts[0].append(i)
+    f = 0
+    while fronts[f]:
+        nxt = []
+        for p in fronts[f]:
+            for q in dominated_by[p]:
+                count[q] -= 1
+                if count[q] == 0:
+                    nxt.append(q)
+        f += 1
+        fronts.append(nxt)
+    fronts.pop()
+    out = []
+    for front in fronts:
+        if len(front) <= 2:
+            out.append(list(front))
+            continue
+        crowd = np.zeros(len(front))
+        sub = pts[front]
+        for j in range(sub.shape[1]):
+            order = np.argsort(sub[:, j], kind="stable")
+            span = sub[order[-1], j] - sub[order[0], j]
+            crowd[order[0]] = crowd[order[-1]] = math.inf
+            if span == 0:
+                continue
+            for pos in range(1, len(front) - 1):
+                crowd[order[pos]] += (sub[order[pos + 1], j] - sub[order[pos - 1], j]) / span
+        ranked = sorted(range(len(front)), key=lambda i: (-crowd[i], i))
+        out.append([front[i] for i in ranked])
+    return out
 
 
 # -- sizing (engine.py:426-461) -----------------------------------------------

@@ -71,6 +71,9 @@ class Spec:
     lb: int = 0
     ub: int = 0
     penalty_weight: float | None = None
+    # Lexicographic comparison (core.py:92-106): (priority_order, tolerances);
+    # None = Weighted with `weights` (core.py:80-90, engine.py:215-222)
+    lex: tuple | None = None
 
     @property
     def m(self):
@@ -124,13 +127,22 @@ class Tsp(Problem):
 class Routing(Problem):
     """builtins.py:80-152 (CVRP); customers are values 0..n-1 at matrix c+1."""
 
-    def __init__(self, dist, demands, capacity, vehicles):
+    def __init__(self, dist, demands, capacity, vehicles, objectives=("distance",),
+                 weights=None, lex=None):
+        """objectives: names from ("distance", "vehicles") (builtins.py:80-116);
+        weights: Weighted comparison weights (default: 1.0 per objective);
+        lex: (priority_order, tolerances) for a Lexicographic comparison."""
         self.dist = np.asarray(dist, dtype=np.float64)
         self.demands = np.asarray(demands, dtype=np.float64)
         self.capacity = float(capacity)
         self.vehicles = int(vehicles)
         self.n = len(self.demands)
-        self.spec = Spec(PERM, self.vehicles, self.n, self.n, PARTITION)
+        self.names = tuple(objectives)
+        m = len(self.names)
+        w = tuple(float(x) for x in weights) if weights is not None and lex is None \
+            else (1.0,) * m
+        self.spec = Spec(PERM, self.vehicles, self.n, self.n, PARTITION, directions=(MIN,) * m,
+                         weights=w, lex=lex)
 
     def route_len(self, route) -> float:
         if len(route) == 0:
@@ -142,6 +154,8 @@ class Routing(Problem):
         return float(total)
 
     def objective(self, i, sol):
+        if self.names[i] == "vehicles":  # builtins.py:133
+            return float(np.count_nonzero(sol.sizes))
         return sum(self.route_len(sol.row(r)) for r in range(sol.d1))
 
     def load_excess(self, sol) -> float:
@@ -164,8 +178,8 @@ class Routing(Problem):
 class Vrptw(Routing):
     """builtins.py:155-190: capacity excess + sequential lateness."""
 
-    def __init__(self, dist, demands, capacity, vehicles, ready, due, service):
-        super().__init__(dist, demands, capacity, vehicles)
+    def __init__(self, dist, demands, capacity, vehicles, ready, due, service, **mo):
+        super().__init__(dist, demands, capacity, vehicles, **mo)
         self.ready = np.asarray(ready, dtype=np.float64)
         self.due = np.asarray(due, dtype=np.float64)
         self.service = np.asarray(service, dtype=np.float64)
@@ -276,18 +290,43 @@ def scalar_fitness(problem: Problem, sol: Sol, penalty_weight: float) -> float:
 
 
 def acceptance_delta(problem, cand: Sol, cur: Sol, penalty_weight: float) -> float:
-    """engine.py:225-235 (Weighted branch — the only one on the path)."""
-    return scalar_fitness(problem, cand, penalty_weight) - \
-        scalar_fitness(problem, cur, penalty_weight)
+    """engine.py:225-246: Weighted scalarised difference, or the Lexicographic
+    difference on the first non-tied objective; penalties folded in both."""
+    spec = problem.spec
+    if spec.lex is None:
+        return scalar_fitness(problem, cand, penalty_weight) - \
+            scalar_fitness(problem, cur, penalty_weight)
+    order, tol = spec.lex
+    d = 0.0
+    for i in order:
+        diff = float(cand.obj[i]) - float(cur.obj[i])
+        if abs(diff) <= tol[i]:
+            continue
+        if spec.directions[i] == MAX:
+            diff = -diff
+        d = diff
+        break
+    return d + penalty_weight * (cand.pen - cur.pen)
 
 
 def compare(problem, a: Sol, b: Sol) -> int:
-    """core.py:315-347 (Weighted): -1 a better, 0 equal, 1 b better."""
+    """core.py:315-347: -1 a better, 0 equal, 1 b better (penalty first)."""
     fa_ok, fb_ok = a.pen == 0.0, b.pen == 0.0
     if fa_ok != fb_ok:
         return -1 if fa_ok else 1
     if not fa_ok and a.pen != b.pen:
         return -1 if a.pen < b.pen else 1
+    spec = problem.spec
+    if spec.lex is not None:  # core.py:338-346
+        order, tol = spec.lex
+        for i in order:
+            if abs(a.obj[i] - b.obj[i]) <= tol[i]:
+                continue
+            low = spec.directions[i] == MIN
+            if a.obj[i] < b.obj[i]:
+                return -1 if low else 1
+            return 1 if low else -1
+        return 0
     fa, fb = _scal(problem, a), _scal(problem, b)
     if fa == fb:
         return 0

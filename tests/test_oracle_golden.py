@@ -134,3 +134,43 @@ def test_run_trajectory_matches_reference(golden, oracle_problems, key, name):
     assert out.ids == g["ids"]
     assert [float(w) for w in out.weights] == g["weights"]
     assert list(out.k_weights) == g["k_weights"]
+
+
+def _mo_pair(g):
+    """Oracle problem for a golden_mo.json run (and the product problem)."""
+    inst, names, c = g["instance"], tuple(g["objectives_names"]), g["comparison"]
+    kw = {"objectives": names}
+    if c is not None and c[0] == "w":
+        kw["weights"] = tuple(c[1])
+    elif c is not None:
+        kw["lex"] = (tuple(c[1]), tuple(c[2]))
+    if inst["tw"]:
+        from paper_2603_19163_b200 import instances as I
+        n, veh, seed = inst["vrptw_solomon_like"]
+        vd = I.vrptw_solomon_like(n=n, vehicles=veh, seed=seed)
+        return P.Vrptw(vd.dist, vd.demands, vd.capacity, vd.vehicles, vd.ready, vd.due,
+                        vd.service, **kw), vd
+    return P.Routing(np.array(inst["dist"]), inst["demands"], inst["capacity"],
+                      inst["vehicles"], **kw), inst
+
+
+@pytest.mark.parametrize("key", ["cvrp8_w", "cvrp8_w100", "cvrp8_lex_veh", "cvrp8_lex_tol",
+                                 "vrptw30_w", "vrptw30_lex"])
+def test_multiobjective_run_matches_reference(key):
+    """Bi-objective routing, Weighted and Lexicographic, non-dominated-sort init
+    (engine.py:225-246, :352-420; core.py:315-347) — oracle in MT mode ==
+    reference run() bit-for-bit."""
+    import json
+    from pathlib import Path
+    g = json.loads((Path(__file__).with_name("golden") / "golden_mo.json").read_text())["runs"][key]
+    prob, _ = _mo_pair(g)
+    c = g["config"]
+    out = E.run(prob, E.RunCfg(population=c["population"], team_size=c["team_size"],
+                               max_generations=c["max_generations"], seed=c["seed"],
+                               islands=c["islands"], migration="hybrid", migration_interval=5,
+                               record_history=True))
+    assert sol_rows(out.best) == g["best"]["data"]
+    assert out.objectives == g["objectives"] and out.penalty == g["penalty"]
+    assert out.history["best_phi"] == g["history"]
+    assert [float(w) for w in out.weights] == g["weights"]
+    assert list(out.k_weights) == g["k_weights"]
