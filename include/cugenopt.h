@@ -87,6 +87,8 @@ typedef struct go_problem_desc {
   const int32_t* jsp_machine; /* n_jobs*ops_per_job */
   const int32_t* jsp_duration;
   int32_t lb, ub;        /* integer encoding bounds */
+  int32_t n_obj;         /* routing: 1 or 2 objectives (builtins.py:80-116); 0 = 1 */
+  int32_t obj_kind[2];   /* routing objective i: 0 "distance", 1 "vehicles" */
 } go_problem_desc;
 
 /* A user-defined single-row problem whose objective and penalty are CUDA
@@ -138,6 +140,15 @@ typedef struct go_engine_config {
   int32_t evolver_offset; /* global evolver index of local evolver 0 (multi-GPU) */
   int32_t maximize;       /* objective direction (core.py:69-77) */
   double obj_weight;      /* Weighted scalarisation weight (core.py:292-307) */
+  /* multi-objective problems (n_obj == 2) and Lexicographic comparisons:
+   * scalar_fitness weight of objective 1 (engine.py:215-222), and the mode
+   * (core.py:92-106): lex = 1 compares objective vectors in priority order
+   * (lex_first, 1 - lex_first) with tolerances lex_tol.  With n_obj == 2 the
+   * `obj` arrays of set/get_population and get_best hold 2 values per solution. */
+  double obj_weight2;
+  int32_t lex;
+  int32_t lex_first;
+  double lex_tol[2];
 } go_engine_config;
 
 typedef struct go_run_stats {

@@ -54,7 +54,8 @@ class ProblemDesc(C.Structure):
                 ("demands", _PD), ("ready", _PD), ("due", _PD), ("service", _PD),
                 ("capacity", C.c_double), ("n_jobs", C.c_int32), ("n_machines", C.c_int32),
                 ("ops_per_job", C.c_int32), ("jsp_machine", _PI), ("jsp_duration", _PI),
-                ("lb", C.c_int32), ("ub", C.c_int32)]
+                ("lb", C.c_int32), ("ub", C.c_int32), ("n_obj", C.c_int32),
+                ("obj_kind", C.c_int32 * 2)]
 
 
 class UserProblemDesc(C.Structure):  # go_user_problem_desc
@@ -79,7 +80,8 @@ class EngineConfig(C.Structure):
                 ("top_n", C.c_int32), ("elite_interval", C.c_int32),
                 ("has_target", C.c_int32), ("target_objective", C.c_double),
                 ("evolver_offset", C.c_int32), ("maximize", C.c_int32),
-                ("obj_weight", C.c_double)]
+                ("obj_weight", C.c_double), ("obj_weight2", C.c_double), ("lex", C.c_int32),
+                ("lex_first", C.c_int32), ("lex_tol", C.c_double * 2)]
 
 
 class RunStats(C.Structure):

@@ -188,6 +188,8 @@ struct go_problem {
   void* d_tri = nullptr;   // packed strict upper triangle (smem image)
   size_t full_bytes = 0, tri_bytes = 0;
   DeviceInfo dev;
+  // routing objectives (n_obj 1 or 2; kinds 0 distance, 1 vehicles)
+  int n_obj = 1, okind0 = 0, okind1 = 1;
   // user problems (RK_USER): NVRTC objective module, encoding
   gohost::JitModule user_mod;
   int enc = 0;
@@ -233,6 +235,9 @@ struct go_engine {
   short* snap = nullptr;  // [SNAP_DEPTH][P][W]
   int* prog = nullptr;     // [P] published snapshot generation per team
   short* lane_rows = nullptr;  // TSP whole-row operators: [P][T][2][n]
+  // objective vectors (multi-objective / Lexicographic runs): [P][2], [P][2], [MAX_CHUNK][P][2]
+  double *obj2 = nullptr, *best_obj2 = nullptr, *rec_obj2 = nullptr;
+  go::MoCmp mo{};
   bool xover = false, coop = false;
   static const int kDepth = 8;
   cudaEvent_t ring_ev[kDepth] = {};
@@ -422,6 +427,10 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
     p->capacity = d->capacity;
     p->tw = tw;
     p->n_cells = n;
+    p->n_obj = d->n_obj == 2 ? 2 : 1;
+    p->okind0 = d->obj_kind[0] == 1 ? 1 : 0;
+    p->okind1 = d->obj_kind[1] == 0 ? 0 : 1;
+    if (d->n_obj < 0 || d->n_obj > 2) return fail(GO_E_UNSUPPORTED, "routing supports 1 or 2 objectives");
     p->row_kind = go::RK_PART;
     p->gsize = 2;
     p->n = n + v;  // compact row length
@@ -625,6 +634,9 @@ go::RowArgs row_args(const go_problem* p) {
   x.tw = p->tw;
   x.obj_weight = 1.0;
   x.enc = p->enc;
+  x.okind0 = p->okind0;
+  x.okind1 = p->okind1;
+  x.mo.m = p->n_obj;
   return x;
 }
 
@@ -809,7 +821,7 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
     short* d_g = nullptr;
     double *d_o = nullptr, *d_p = nullptr;
     CK(cudaMalloc(&d_g, h.size() * 2));
-    CK(cudaMalloc(&d_o, (size_t)m * 8));
+    CK(cudaMalloc(&d_o, (size_t)m * p->n_obj * 8));
     CK(cudaMalloc(&d_p, (size_t)m * 8));
     CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
     CK(cudaMemset(d_p, 0, (size_t)m * 8));
@@ -840,7 +852,7 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
       void* args[] = {(void*)&inst, &off1, &nj, &pj, &nmach, &d_g, &d_o};
       CK(cudaLaunchKernel((void*)go_eval_jsp, dim3(m), dim3(32), args, (size_t)p->scratch_ints * 4, 0));
     }
-    CK(cudaMemcpy(obj_out, d_o, (size_t)m * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(obj_out, d_o, (size_t)m * p->n_obj * 8, cudaMemcpyDeviceToHost));
     if (pen_out) CK(cudaMemcpy(pen_out, d_p, (size_t)m * 8, cudaMemcpyDeviceToHost));
     cudaFree(d_g);
     cudaFree(d_o);
@@ -1078,6 +1090,15 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   e->teams_per_sm = blocks * e->E;
   if (blocks < 1) return fail(GO_E_UNSUPPORTED, "evolve kernel does not fit on an SM");
   e->coop = (long long)blocks * p->dev.sm >= e->grid;
+  e->mo.m = p->n_obj;
+  e->mo.lex = c->lex ? 1 : 0;
+  e->mo.first = c->lex_first == 1 ? 1 : 0;
+  e->mo.tol[0] = c->lex_tol[0];
+  e->mo.tol[1] = c->lex_tol[1];
+  const bool multi = p->n_obj == 2 || e->mo.lex;
+  if (multi && !(p->family == 1 && p->row_kind == go::RK_PART))
+    return fail(GO_E_UNSUPPORTED, "multi-objective / Lexicographic runs: routing problems only");
+  if (e->mo.first >= e->mo.m) return fail(GO_E_INVALID, "lex_first outside the objectives");
 
   // per-thread stack: the row kernels' guided rebuild nests numpy's recursive
   // pairwise sum (go_part.cuh) below ~1 KB of frames; the default limit is 1 KB
@@ -1107,6 +1128,11 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   CK(cudaMallocHost(&e->h_temps, (size_t)go_engine::kDepth * go::MAX_CHUNK * 8));
   CK(cudaMalloc(&e->reg, sizeof(go::RegistryDev)));
   CK(cudaMalloc(&e->gs, sizeof(go::GlobalState)));
+  if (multi) {
+    CK(cudaMalloc(&e->obj2, P * 2 * 8));
+    CK(cudaMalloc(&e->best_obj2, P * 2 * 8));
+    CK(cudaMalloc(&e->rec_obj2, (size_t)go::MAX_CHUNK * P * 2 * 8));
+  }
   CK(cudaHostAlloc(&e->h_stop, sizeof(int), cudaHostAllocMapped));
   *e->h_stop = 0;
   CK(cudaHostGetDevicePointer((void**)&e->d_stop_map, e->h_stop, 0));
@@ -1129,7 +1155,8 @@ int go_engine_destroy(go_engine* e) {
   void* bufs[] = {e->genes, e->best_genes, e->gbest_genes, e->scratch, e->scal, e->pen,
                   e->best_scal, e->best_pen, e->best_gen, e->usage, e->impr, e->k_usage,
                   e->k_impr, e->agg, e->rec_scal, e->rec_pen, e->temps, e->reg, e->gs,
-                  e->history, e->snap, e->prog, e->lane_rows};
+                  e->history, e->snap, e->prog, e->lane_rows, e->obj2, e->best_obj2,
+                  e->rec_obj2};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_temps) cudaFreeHost(e->h_temps);
@@ -1205,20 +1232,36 @@ int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* 
   const size_t P = e->P, W = e->W;
   std::vector<short> g;
   to_device_rows(e->prob, genes, sizes, (int)P, g);
-  std::vector<double> sc(P), pe(P);
+  std::vector<double> sc(P), pe(P), o2(P * 2, 0.0);
   const double w = e->cfg.obj_weight > 0 ? e->cfg.obj_weight : 1.0;
+  const int m = e->mo.m;
   int best = 0;
   for (size_t i = 0; i < P; ++i) {
-    sc[i] = 0.0 + w * (e->cfg.maximize ? -obj[i] : obj[i]);  // scalarize (core.py:303-307)
+    const double o0 = obj[i * m], o1 = m == 2 ? obj[i * m + 1] : 0.0;
+    sc[i] = 0.0 + w * (e->cfg.maximize ? -o0 : o0);  // scalarize (core.py:303-307)
+    if (m == 2) sc[i] = sc[i] + e->cfg.obj_weight2 * o1;
+    o2[2 * i] = o0;
+    o2[2 * i + 1] = o1;
     pe[i] = pen ? pen[i] : 0.0;
   }
-  for (size_t i = 1; i < P; ++i) {  // _best_index (engine.py:467-472)
-    const bool fa = pe[i] == 0.0, fb = pe[best] == 0.0;
-    bool better;
-    if (fa != fb) better = fa;
-    else if (!fa && pe[i] != pe[best]) better = pe[i] < pe[best];
-    else better = sc[i] < sc[best];
-    if (better) best = (int)i;
+  auto cmp = [&](size_t a, size_t b) -> int {  // compare (core.py:315-347)
+    const bool fa = pe[a] == 0.0, fb = pe[b] == 0.0;
+    if (fa != fb) return fa ? -1 : 1;
+    if (!fa && pe[a] != pe[b]) return pe[a] < pe[b] ? -1 : 1;
+    if (!e->mo.lex) return sc[a] < sc[b] ? -1 : (sc[b] < sc[a] ? 1 : 0);
+    for (int k = 0; k < m; ++k) {
+      const int i = k == 0 ? e->mo.first : 1 - e->mo.first;
+      const double x = o2[2 * a + i], y = o2[2 * b + i];
+      if (std::fabs(x - y) <= e->mo.tol[i]) continue;
+      return x < y ? -1 : 1;
+    }
+    return 0;
+  };
+  for (size_t i = 1; i < P; ++i)  // _best_index (engine.py:467-472)
+    if (cmp(i, (size_t)best) < 0) best = (int)i;
+  if (e->obj2) {
+    CK(cudaMemcpy(e->obj2, o2.data(), P * 2 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(e->best_obj2, o2.data(), P * 2 * 8, cudaMemcpyHostToDevice));
   }
   std::vector<long long> zeros(P, 0);
   CK(cudaMemcpy(e->genes, g.data(), P * W * 2, cudaMemcpyHostToDevice));
@@ -1232,6 +1275,8 @@ int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* 
   go::GlobalState gs{};
   gs.gscal = sc[best];
   gs.gpen = pe[best];
+  gs.gobj[0] = o2[2 * best];
+  gs.gobj[1] = o2[2 * best + 1];
   gs.gev = -1;
   gs.ggen = 0;
   CK(cudaMemcpy(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice));
@@ -1305,6 +1350,9 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.ev_offset = c.evolver_offset;
   a.team_stride = e->TS;
   a.snap = e->xover ? e->snap : nullptr;
+  a.obj2 = e->obj2;
+  a.best_obj2 = e->best_obj2;
+  a.rec_obj2 = e->rec_obj2;
   a.lane_rows = e->lane_rows;
   a.prog = e->prog;
   a.islands = c.islands;
@@ -1317,6 +1365,8 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     x.penalty_weight = c.penalty_weight;
     x.obj_weight = c.obj_weight > 0 ? c.obj_weight : 1.0;
     x.maximize = c.maximize;
+    x.w2 = c.obj_weight2;
+    x.mo = e->mo;
   } else {
     a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
     a.resync = kLayouts[e->layout].elem == E_F64;
@@ -1362,6 +1412,10 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   q.obj_sign_over_w = e->obj_sign_over_w;
   q.seed = c.seed;
   q.max_gens = max_generations;
+  q.obj2 = e->obj2;
+  q.best_obj2 = e->best_obj2;
+  q.rec_obj2 = e->rec_obj2;
+  q.mo = e->mo;
 
   double evolve_ms = 0.0;
   long long evolve_launches = 0;
@@ -1454,8 +1508,14 @@ int go_engine_get_population(go_engine* e, int32_t* genes, int32_t* sizes, doubl
   }
   std::vector<double> sc(P);
   CK(cudaMemcpy(sc.data(), e->scal, P * 8, cudaMemcpyDeviceToHost));
-  if (obj)
+  if (obj && e->obj2) {
+    std::vector<double> o2(P * 2);
+    CK(cudaMemcpy(o2.data(), e->obj2, P * 2 * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < P; ++i)
+      for (int k = 0; k < e->mo.m; ++k) obj[i * e->mo.m + k] = o2[2 * i + k];
+  } else if (obj) {
     for (size_t i = 0; i < P; ++i) obj[i] = sc[i] * e->obj_sign_over_w;
+  }
   if (pen) CK(cudaMemcpy(pen, e->pen, P * 8, cudaMemcpyDeviceToHost));
   return GO_OK;
 }
@@ -1471,7 +1531,11 @@ int go_engine_get_best(go_engine* e, int32_t* genes, int32_t* sizes, double* obj
   const short* src = gs.gev >= 0 ? e->best_genes + (size_t)gs.gev * e->W : e->gbest_genes;
   CK(cudaMemcpy(g.data(), src, (size_t)e->W * 2, cudaMemcpyDeviceToHost));
   from_device_rows(e->prob, g.data(), 1, genes, sizes);
-  if (obj) *obj = gs.gscal * e->obj_sign_over_w;
+  if (obj && e->obj2) {
+    for (int k = 0; k < e->mo.m; ++k) obj[k] = gs.gobj[k];
+  } else if (obj) {
+    *obj = gs.gscal * e->obj_sign_over_w;
+  }
   if (pen) *pen = gs.gpen;
   if (found_gen) *found_gen = gs.ggen;
   return GO_OK;
@@ -1509,7 +1573,7 @@ int go_engine_get_history(go_engine* e, double* best_phi, int64_t cap, int64_t* 
 
 int go_elite_record_bytes(go_engine* e, int64_t* bytes) {
   if (!e || !bytes) return fail(GO_E_INVALID, "bad arguments");
-  *bytes = ((int64_t)e->W * 2 + 15) / 16 * 16 + 16;
+  *bytes = ((int64_t)e->W * 2 + 15) / 16 * 16 + 32;  // {scal, pen, o0, o1} + genes
   return GO_OK;
 }
 
@@ -1522,6 +1586,8 @@ static go::IslandArgs island_args(go_engine* e, void* buf, int top_n) {
   a.pen = e->pen;
   a.gbest_genes = e->gbest_genes;
   a.gs = e->gs;
+  a.obj2 = e->obj2;
+  a.mo = e->mo;
   a.buf = (unsigned char*)buf;
   int64_t rb = 0;
   go_elite_record_bytes(e, &rb);

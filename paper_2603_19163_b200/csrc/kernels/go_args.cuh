@@ -1,5 +1,6 @@
 // go_args.cuh — POD kernel argument blocks shared by host and device code.
 #pragma once
+#include "go_common.cuh"
 
 namespace go {
 
@@ -20,6 +21,7 @@ struct RegistryDev {
 // Run-global state owned by the device (engine.py:668-750 locals).
 struct GlobalState {
   double gscal, gpen;     // global best (engine.py:668, :703-708)
+  double gobj[2];         // its objective vector (multi-objective runs)
   int gev;                // evolver holding the global best in best_genes (-1: gbest buffer)
   int pad0;
   long long ggen;         // generation the global best was found (0 = initial population)
@@ -77,6 +79,11 @@ struct EvolveArgs {
   int islands;           // island count (engine.py:790-798 contiguous partition)
   int pad_x;
   short* lane_rows;      // permutation kernel: [P][T][2][n] rows of deferred whole-row ops
+  // objective vectors [P][2] (null unless MoCmp.m == 2 or lex): current, team
+  // best-ever, and per-generation records [ngen][P][2]
+  double* obj2;
+  double* best_obj2;
+  double* rec_obj2;
 };
 
 // Problem-specific extras of the row kernel (go_evolve_row.cuh).
@@ -94,6 +101,11 @@ struct RowArgs {
   int n_cells, d1, d2, tw;
   // user problems (NVRTC objective): encoding 0 permutation, 1 binary, 2 integer
   int enc, maximize;
+  // routing objectives: kind of objective i (0 distance, 1 vehicles), second
+  // scalar_fitness weight (engine.py:215-222), comparison mode
+  int okind0, okind1;
+  double w2;
+  MoCmp mo;
 };
 
 struct EpilogueArgs {
@@ -133,6 +145,11 @@ struct EpilogueArgs {
   double obj_sign_over_w; // objective = scal * this (single objective)
   unsigned long long seed;
   long long max_gens;
+  // multi-objective (MoCmp.m == 2 or lex): objective vectors [P][2]
+  double* obj2;
+  double* best_obj2;
+  const double* rec_obj2;
+  MoCmp mo;
 };
 
 }  // namespace go

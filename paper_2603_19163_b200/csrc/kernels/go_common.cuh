@@ -419,6 +419,52 @@ __device__ __forceinline__ int compare3(double pa, double sa, double pb, double 
   return 0;
 }
 
+// Multi-objective comparison (core.py:80-106, :315-347).  lex == 0: Weighted —
+// solutions compare by (penalty, scal) where scal is the weighted scalarisation;
+// lex == 1: Lexicographic over the objective vector in priority order
+// (first, 1 - first) with per-objective tolerances.  Objectives here are
+// routing "distance" / "vehicles" (builtins.py:80-152), both minimised.
+struct MoCmp {
+  int m;       // objectives (1 or 2)
+  int lex;
+  int first;   // priority_order[0]
+  int pad;
+  double tol[2];
+};
+
+// compare (core.py:315-347) for multi-objective runs: penalty first, then
+// Weighted (scal) or Lexicographic over (o0, o1) in priority order with
+// tolerances (|a - b| <= tol counts as a tie).  -1 a better, 0 equal, 1 b better.
+__device__ __forceinline__ int compare_mo(double pa, double sa, double a0, double a1, double pb,
+                                         double sb, double b0, double b1, const MoCmp& mo) {
+  if (!mo.lex) return compare3(pa, sa, pb, sb);
+  const bool fa = pa == 0.0, fb = pb == 0.0;
+  if (fa != fb) return fa ? -1 : 1;
+  if (!fa && pa != pb) return pa < pb ? -1 : 1;
+  for (int k = 0; k < mo.m; ++k) {
+    const int i = k == 0 ? mo.first : 1 - mo.first;
+    const double x = i == 0 ? a0 : a1, y = i == 0 ? b0 : b1;
+    if (fabs(__dsub_rn(x, y)) <= mo.tol[i]) continue;
+    return x < y ? -1 : 1;
+  }
+  return 0;
+}
+
+// acceptance_delta, Lexicographic branch (engine.py:236-246): the difference on
+// the first non-tied objective, plus pw * (penalty difference)
+__device__ __forceinline__ double lex_delta(double c0, double c1, double cpen, double u0,
+                                           double u1, double upen, double pw, const MoCmp& mo) {
+  double d = 0.0;
+  for (int k = 0; k < mo.m; ++k) {
+    const int i = k == 0 ? mo.first : 1 - mo.first;
+    const double diff = __dsub_rn(i == 0 ? c0 : c1, i == 0 ? u0 : u1);
+    if (fabs(diff) <= mo.tol[i]) continue;
+    d = diff;
+    break;
+  }
+  return __dadd_rn(d, __dmul_rn(pw, __dsub_rn(cpen, upen)));
+}
+
 __device__ __forceinline__ u64 globaltimer() {
   u64 t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -24,45 +24,64 @@ namespace go {
 enum { EPI_THREADS = 512 };
 
 struct Cand {
-  double pen, scal;
+  double pen, scal, o0, o1;  // o0/o1: objective vector (multi-objective runs)
   int idx;
 };
 
+// comparison keys of a population: penalties, scalarisations and (multi-
+// objective runs) objective vectors [P][2]; obj2 == null for single-objective
+struct SolKeys {
+  const double* pen;
+  const double* scal;
+  const double* obj2;
+  __device__ __forceinline__ Cand at(int i) const {
+    Cand x;
+    x.pen = pen[i];
+    x.scal = scal[i];
+    x.o0 = obj2 ? obj2[2 * i] : 0.0;
+    x.o1 = obj2 ? obj2[2 * i + 1] : 0.0;
+    x.idx = i;
+    return x;
+  }
+};
+
+__device__ __forceinline__ int cand_cmp(const Cand& a, const Cand& b, const MoCmp& mo) {
+  return compare_mo(a.pen, a.scal, a.o0, a.o1, b.pen, b.scal, b.o0, b.o1, mo);
+}
 // a "before" b in best-first order (strictly better, ties -> lower index)
-__device__ __forceinline__ bool best_first(const Cand& a, const Cand& b) {
-  const int c = compare3(a.pen, a.scal, b.pen, b.scal);
+__device__ __forceinline__ bool best_first(const Cand& a, const Cand& b, const MoCmp& mo) {
+  const int c = cand_cmp(a, b, mo);
   return c < 0 || (c == 0 && a.idx < b.idx);
 }
 // a "before" b in worst-first order (strictly worse, ties -> lower index)
-__device__ __forceinline__ bool worst_first(const Cand& a, const Cand& b) {
-  const int c = compare3(a.pen, a.scal, b.pen, b.scal);
+__device__ __forceinline__ bool worst_first(const Cand& a, const Cand& b, const MoCmp& mo) {
+  const int c = cand_cmp(a, b, mo);
   return c > 0 || (c == 0 && a.idx < b.idx);
 }
 
 template <bool WORST>
-__device__ Cand block_select(const double* pen, const double* scal, int lo, int hi,
-                             const int* excl, int nexcl, Cand* red) {
+__device__ Cand block_select(const SolKeys& K, int lo, int hi, const int* excl, int nexcl,
+                             Cand* red, const MoCmp& mo) {
   Cand c;
   c.idx = 0x7fffffff;
-  c.pen = 0;
-  c.scal = 0;
+  c.pen = c.scal = c.o0 = c.o1 = 0;
   for (int i = lo + (int)threadIdx.x; i < hi; i += blockDim.x) {
     bool skip = false;
     for (int e = 0; e < nexcl; ++e) skip |= excl[e] == i;
     if (skip) continue;
-    Cand x;
-    x.pen = pen[i];
-    x.scal = scal[i];
-    x.idx = i;
-    if (c.idx == 0x7fffffff || (WORST ? worst_first(x, c) : best_first(x, c))) c = x;
+    const Cand x = K.at(i);
+    if (c.idx == 0x7fffffff || (WORST ? worst_first(x, c, mo) : best_first(x, c, mo))) c = x;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     Cand o;
     o.pen = __shfl_xor_sync(0xffffffffu, c.pen, off);
     o.scal = __shfl_xor_sync(0xffffffffu, c.scal, off);
+    o.o0 = __shfl_xor_sync(0xffffffffu, c.o0, off);
+    o.o1 = __shfl_xor_sync(0xffffffffu, c.o1, off);
     o.idx = __shfl_xor_sync(0xffffffffu, c.idx, off);
-    if (o.idx != 0x7fffffff && (c.idx == 0x7fffffff || (WORST ? worst_first(o, c) : best_first(o, c))))
+    if (o.idx != 0x7fffffff &&
+        (c.idx == 0x7fffffff || (WORST ? worst_first(o, c, mo) : best_first(o, c, mo))))
       c = o;
   }
   __syncthreads();
@@ -71,7 +90,8 @@ __device__ Cand block_select(const double* pen, const double* scal, int lo, int 
   Cand r = red[0];
   for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
     const Cand o = red[w];
-    if (o.idx != 0x7fffffff && (r.idx == 0x7fffffff || (WORST ? worst_first(o, r) : best_first(o, r))))
+    if (o.idx != 0x7fffffff &&
+        (r.idx == 0x7fffffff || (WORST ? worst_first(o, r, mo) : best_first(o, r, mo))))
       r = o;
   }
   __syncthreads();
@@ -109,33 +129,45 @@ __device__ __forceinline__ void island_range(int P, int islands, int i, int& lo,
   hi = lo + base + (i < extra ? 1 : 0);
 }
 
-__device__ __forceinline__ void put_solution_raw(short* genes, double* scal_a, double* pen_a, int W,
-                                                 int dst, const short* src, double pen,
-                                                 double scal) {
+__device__ __forceinline__ void put_solution_raw(short* genes, double* scal_a, double* pen_a,
+                                                 double* obj2, int W, int dst, const short* src,
+                                                 const Cand& c) {
   copy_genes(genes + (size_t)dst * W, src, W);
   if (threadIdx.x == 0) {
-    pen_a[dst] = pen;
-    scal_a[dst] = scal;
+    pen_a[dst] = c.pen;
+    scal_a[dst] = c.scal;
+    if (obj2) {
+      obj2[2 * dst] = c.o0;
+      obj2[2 * dst + 1] = c.o1;
+    }
   }
 }
 
 __device__ __forceinline__ void put_solution(const EpilogueArgs& A, int dst, const short* src,
-                                             double pen, double scal) {
-  copy_genes(A.genes + (size_t)dst * A.W, src, A.W);
-  if (threadIdx.x == 0) {
-    A.pen[dst] = pen;
-    A.scal[dst] = scal;
-  }
+                                             const Cand& c) {
+  put_solution_raw(A.genes, A.scal, A.pen, A.obj2, A.W, dst, src, c);
+}
+
+__device__ __forceinline__ Cand gbest_cand(const GlobalState* gs) {
+  Cand c;
+  c.pen = gs->gpen;
+  c.scal = gs->gscal;
+  c.o0 = gs->gobj[0];
+  c.o1 = gs->gobj[1];
+  c.idx = -1;
+  return c;
 }
 
 __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArgs A) {
   __shared__ Cand red[EPI_THREADS / 32];
   __shared__ int s_stop;
-  __shared__ double s_pen[64], s_scal[64];
+  __shared__ Cand s_don[64];
   __shared__ int s_idx[64];
   GlobalState* gs = A.gs;
   if (gs->stop) return;
   const int P = A.P;
+  const MoCmp mo = A.mo;
+  const SolKeys pop{A.pen, A.scal, A.obj2};
 
   // ---- 1. per-generation global best / stagnation / target -----------------
   if (threadIdx.x == 0) s_stop = 0;
@@ -143,12 +175,15 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
   long long last = A.gen0 - 1;
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
-    const Cand b = block_select<false>(A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
-                                       0, P, nullptr, 0, red);
+    const SolKeys rec{A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
+                      A.rec_obj2 ? A.rec_obj2 + (size_t)gi * P * 2 : nullptr};
+    const Cand b = block_select<false>(rec, 0, P, nullptr, 0, red, mo);
     if (threadIdx.x == 0) {
-      if (strictly_better(b.pen, b.scal, gs->gpen, gs->gscal)) {
+      if (cand_cmp(b, gbest_cand(gs), mo) < 0) {
         gs->gpen = b.pen;
         gs->gscal = b.scal;
+        gs->gobj[0] = b.o0;
+        gs->gobj[1] = b.o1;
         gs->gev = b.idx;
         gs->ggen = g;
         gs->stall = 0;
@@ -242,38 +277,34 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
       for (int i = 0; i < k; ++i) {
         int lo, hi;
         island_range(P, k, i, lo, hi);
-        const Cand b = block_select<false>(A.pen, A.scal, lo, hi, nullptr, 0, red);
+        const Cand b = block_select<false>(pop, lo, hi, nullptr, 0, red, mo);
         copy_genes(A.scratch + (size_t)i * A.W, A.genes + (size_t)b.idx * A.W, A.W);
-        if (threadIdx.x == 0) {
-          s_pen[i] = b.pen;
-          s_scal[i] = b.scal;
-        }
+        if (threadIdx.x == 0) s_don[i] = b;
       }
       __syncthreads();
       for (int i = 0; i < k; ++i) {
         int lo, hi;
         island_range(P, k, (i + 1) % k, lo, hi);
         if (hi - lo == 1) {
-          if (strictly_better(s_pen[i], s_scal[i], A.pen[lo], A.scal[lo]))
-            put_solution(A, lo, A.scratch + (size_t)i * A.W, s_pen[i], s_scal[i]);
+          const Cand d = s_don[i];
+          if (cand_cmp(d, pop.at(lo), mo) < 0) put_solution(A, lo, A.scratch + (size_t)i * A.W, d);
           __syncthreads();
           continue;
         }
-        const Cand w = block_select<true>(A.pen, A.scal, lo, hi, nullptr, 0, red);
-        const Cand b = block_select<false>(A.pen, A.scal, lo, hi, nullptr, 0, red);
-        if (w.idx != b.idx) put_solution(A, w.idx, A.scratch + (size_t)i * A.W, s_pen[i], s_scal[i]);
+        const Cand w = block_select<true>(pop, lo, hi, nullptr, 0, red, mo);
+        const Cand b = block_select<false>(pop, lo, hi, nullptr, 0, red, mo);
+        if (w.idx != b.idx) put_solution(A, w.idx, A.scratch + (size_t)i * A.W, s_don[i]);
         __syncthreads();
       }
     } else {  // global_top_n: stable top-n by repeated selection
       const int tn = A.top_n < 64 ? A.top_n : 64;
       int nd = 0;
       for (int d = 0; d < tn && d < P; ++d) {
-        const Cand b = block_select<false>(A.pen, A.scal, 0, P, s_idx, nd, red);
+        const Cand b = block_select<false>(pop, 0, P, s_idx, nd, red, mo);
         copy_genes(A.scratch + (size_t)d * A.W, A.genes + (size_t)b.idx * A.W, A.W);
         if (threadIdx.x == 0) {
           s_idx[d] = b.idx;
-          s_pen[d] = b.pen;
-          s_scal[d] = b.scal;
+          s_don[d] = b;
         }
         __syncthreads();
         nd = d + 1;
@@ -284,7 +315,7 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
       for (int i = 0; i < k; ++i) {
         int lo, hi;
         island_range(P, k, i, lo, hi);
-        const Cand b = block_select<false>(A.pen, A.scal, lo, hi, nullptr, 0, red);
+        const Cand b = block_select<false>(pop, lo, hi, nullptr, 0, red, mo);
         const int nslots = hi - lo - 1;
         for (int d = 0; d < nd; ++d) {
           if (nslots <= 0) break;
@@ -294,7 +325,7 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
             s_slot = s;
           }
           __syncthreads();
-          put_solution(A, s_slot, A.scratch + (size_t)d * A.W, s_pen[d], s_scal[d]);
+          put_solution(A, s_slot, A.scratch + (size_t)d * A.W, s_don[d]);
           __syncthreads();
         }
       }
@@ -305,8 +336,8 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
 
   // ---- 4. elite injection ------------------------------------------------------
   if (!s_stop && last % A.elite_interval == 0) {
-    const Cand w = block_select<true>(A.pen, A.scal, 0, P, nullptr, 0, red);
-    put_solution(A, w.idx, A.gbest_genes, gs->gpen, gs->gscal);
+    const Cand w = block_select<true>(pop, 0, P, nullptr, 0, red, mo);
+    put_solution(A, w.idx, A.gbest_genes, gbest_cand(gs));
   }
   __syncthreads();
 

@@ -833,8 +833,10 @@ struct DemV {
 // arithmetic in the same order, element access through RouteIns
 __device__ __forceinline__ void part_eval_ins(const PartView& v, const short* cells, const short* sz,
                                               int ri, int pi, int val, double& distance,
-                                              double& penalty) {
+                                              double& penalty, int& veh) {
   const int n1 = v.n + 1;
+  veh = 0;
+  for (int r = 0; r < v.d1; ++r) veh += (sz[r] + (r == ri)) > 0;
   PySum dsum;
   dsum.init();
   double cap_pen = 0.0, late = 0.0;
@@ -879,8 +881,20 @@ __device__ __forceinline__ void part_eval_ins(const PartView& v, const short* ce
 
 // partitions (operators.py:520-546): thread 0 pops / parks / re-inserts, the
 // team scores every trial slot of every open row in parallel (full evaluation)
+// scalar_fitness (engine.py:215-222) of a routing solution from its distance,
+// penalty and vehicle count, objectives in the problem's order
+__device__ __forceinline__ double part_scal(const RowArgs& X, double dist, int veh, double* o0,
+                                            double* o1) {
+  const double a = X.okind0 == 0 ? dist : (double)veh;
+  const double b = X.okind1 == 0 ? dist : (double)veh;
+  if (o0) *o0 = a;
+  if (o1) *o1 = b;
+  const double s = __dadd_rn(0.0, __dmul_rn(X.obj_weight, a));
+  return X.mo.m == 2 ? __dadd_rn(s, __dmul_rn(X.w2, b)) : s;
+}
+
 __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_cells, int d1,
-                             int d2, double wobj, double pw, const GrShared& g, double* sbuf,
+                             int d2, const RowArgs& X, double pw, const GrShared& g, double* sbuf,
                              TeamShared<double>* ts, int lane, int team, int TS) {
   const int m = g.m();
   if (m == 0) return;
@@ -927,8 +941,9 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
         k -= sz[r] + 1;
       }
       double dist, pen;
-      part_eval_ins(pv, cells, sz, r, k, v, dist, pen);
-      const double sc = __dadd_rn(__dadd_rn(0.0, __dmul_rn(wobj, dist)), __dmul_rn(pw, pen));
+      int veh;
+      part_eval_ins(pv, cells, sz, r, k, v, dist, pen, veh);
+      const double sc = __dadd_rn(part_scal(X, dist, veh, nullptr, nullptr), __dmul_rn(pw, pen));
       if (bi == 0x7fffffff || sc < bs) {
         bs = sc;
         bi = i;
@@ -1143,6 +1158,14 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     }
   }
   double bscal = A.best_scal[ev], bpen = A.best_pen[ev];
+  // objective vectors of the current row and of the team best (multi-objective)
+  double co0 = 0.0, co1 = 0.0, bo0 = 0.0, bo1 = 0.0;
+  if (A.obj2) {
+    co0 = A.obj2[2 * ev];
+    co1 = A.obj2[2 * ev + 1];
+    bo0 = A.best_obj2[2 * ev];
+    bo1 = A.best_obj2[2 * ev + 1];
+  }
   const double* kw = s_misc;
   const double total = s_misc[3];
   const unsigned lt_mask = (1u << wl) - 1u;
@@ -1357,8 +1380,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           } else if (KIND == RK_JSP) {
             team_gr_jsp(jv, lrow, gsh, scratch, X.scratch_ints, lane, team, TS);
           } else if (KIND == RK_PART) {
-            team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2,
-                         X.obj_weight, pwt, gsh, la.delta, ts, lane, team, TS);
+            team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2, X,
+                         pwt, gsh, la.delta, ts, lane, team, TS);
           } else if (KIND == RK_USER) {
             const UserScore us{inst, X.obj_weight, pwt, X.maximize};
             if (X.enc == ENC_PERM)
@@ -1385,12 +1408,17 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       double nscal = scal, npen = pen, a0 = 0.0, a1 = 0.0, dl;
       if (KIND == RK_PART) {
         double dist, pn;
-        part_eval(pv, (const short*)row, (const short*)row + X.n_cells, dist, pn);
-        nscal = __dadd_rn(0.0, __dmul_rn(X.obj_weight, dist));
+        int veh;
+        part_eval(pv, (const short*)row, (const short*)row + X.n_cells, dist, pn, &veh);
+        nscal = part_scal(X, dist, veh, &a0, &a1);  // a0 / a1: objective vector
         npen = pn;
-        const double phi_c = __dadd_rn(nscal, __dmul_rn(pwt, npen));
-        const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
-        dl = __dsub_rn(phi_c, phi0);
+        if (X.mo.lex) {
+          dl = lex_delta(a0, a1, npen, co0, co1, pen, pwt, X.mo);
+        } else {
+          const double phi_c = __dadd_rn(nscal, __dmul_rn(pwt, npen));
+          const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
+          dl = __dsub_rn(phi_c, phi0);
+        }
         rd_elem += 6u * (unsigned)X.n_cells;
       } else if (KIND == RK_USER) {  // NVRTC objective, full evaluation
         const RowSol<G> sol{row, n};
@@ -1481,7 +1509,13 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       pen = la.npen[bl];
       V = la.aux0[bl];
       W = la.aux1[bl];
+      co0 = la.aux0[bl];  // routing: objective vector of the winner
+      co1 = la.aux1[bl];
       team_bar(team, TS);
+    }
+    if (A.rec_obj2 && lane == 0) {
+      A.rec_obj2[((size_t)gi * A.P + ev) * 2] = co0;
+      A.rec_obj2[((size_t)gi * A.P + ev) * 2 + 1] = co1;
     }
     if (lane == 0) {
       A.rec_scal[(size_t)gi * A.P + ev] = scal;
@@ -1489,10 +1523,12 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     }
     if (A.snap && gi + 1 < A.ngen)
       snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, snap_min, lane, team, TS);
-    if (strictly_better(pen, scal, bpen, bscal)) {
+    if (compare_mo(pen, scal, co0, co1, bpen, bscal, bo0, bo1, X.mo) < 0) {
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = (short)cur[p];
       bscal = scal;
       bpen = pen;
+      bo0 = co0;
+      bo1 = co1;
       if (lane == 0) A.best_gen[ev] = g;
     }
   }
@@ -1512,6 +1548,12 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     A.pen[ev] = pen;
     A.best_scal[ev] = bscal;
     A.best_pen[ev] = bpen;
+    if (A.obj2) {
+      A.obj2[2 * ev] = co0;
+      A.obj2[2 * ev + 1] = co1;
+      A.best_obj2[2 * ev] = bo0;
+      A.best_obj2[2 * ev + 1] = bo1;
+    }
   }
   if (err) atomicOr(&A.gs->err, err);
 #pragma unroll

@@ -27,6 +27,8 @@ struct IslandArgs {
   short* genes;
   double* scal;
   double* pen;
+  double* obj2;      // [P][2] objective vectors (multi-objective runs) or null
+  MoCmp mo;
   short* gbest_genes;
   GlobalState* gs;
   unsigned char* buf;  // records
@@ -40,21 +42,35 @@ struct IslandArgs {
 __device__ __forceinline__ double* rec_head(unsigned char* buf, int rec_bytes, int i) {
   return (double*)(buf + (size_t)i * rec_bytes);
 }
+// record = {scal, pen, o0, o1} header (32 B) + genes
 __device__ __forceinline__ short* rec_genes(unsigned char* buf, int rec_bytes, int i) {
-  return (short*)(buf + (size_t)i * rec_bytes + 16);
+  return (short*)(buf + (size_t)i * rec_bytes + 32);
+}
+__device__ __forceinline__ Cand rec_cand(unsigned char* buf, int rec_bytes, int i) {
+  const double* h = rec_head(buf, rec_bytes, i);
+  Cand c;
+  c.scal = h[0];
+  c.pen = h[1];
+  c.o0 = h[2];
+  c.o1 = h[3];
+  c.idx = i;
+  return c;
 }
 
 __global__ void __launch_bounds__(EPI_THREADS, 1) go_export_elites_kernel(IslandArgs A) {
   __shared__ Cand red[EPI_THREADS / 32];
   __shared__ int s_idx[64];
   const int tn = A.top_n < A.P ? A.top_n : A.P;
+  const SolKeys pop{A.pen, A.scal, A.obj2};
   for (int d = 0; d < tn && d < 64; ++d) {
-    const Cand b = block_select<false>(A.pen, A.scal, 0, A.P, s_idx, d, red);
+    const Cand b = block_select<false>(pop, 0, A.P, s_idx, d, red, A.mo);
     if (threadIdx.x == 0) {
       s_idx[d] = b.idx;
       double* h = rec_head(A.buf, A.rec_bytes, d);
       h[0] = b.scal;
       h[1] = b.pen;
+      h[2] = b.o0;
+      h[3] = b.o1;
     }
     copy_genes(rec_genes(A.buf, A.rec_bytes, d), A.genes + (size_t)b.idx * A.W, A.W);
     __syncthreads();
@@ -64,6 +80,7 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_export_elites_kernel(Island
       double* h = rec_head(A.buf, A.rec_bytes, d);
       h[0] = 1.7976931348623157e308;
       h[1] = 1.7976931348623157e308;
+      h[2] = h[3] = 1.7976931348623157e308;
     }
   }
 }
@@ -77,21 +94,24 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_import_elites_kernel(Island
   const int nrec = A.n_ranks * A.top_n;
 
   // refresh the global best from every rank's best record (records d = 0)
+  const MoCmp mo = A.mo;
+  const SolKeys pop{A.pen, A.scal, A.obj2};
   if (threadIdx.x == 0) {
     int bi = -1;
-    double bp = gs->gpen, bsc = gs->gscal;
+    Cand best = gbest_cand(gs);
     for (int r = 0; r < A.n_ranks; ++r) {
-      const double* h = rec_head(A.buf, A.rec_bytes, r * A.top_n);
-      if (strictly_better(h[1], h[0], bp, bsc)) {
-        bp = h[1];
-        bsc = h[0];
+      const Cand c = rec_cand(A.buf, A.rec_bytes, r * A.top_n);
+      if (cand_cmp(c, best, mo) < 0) {
+        best = c;
         bi = r * A.top_n;
       }
     }
     s_slot = bi;
     if (bi >= 0) {
-      gs->gpen = bp;
-      gs->gscal = bsc;
+      gs->gpen = best.pen;
+      gs->gscal = best.scal;
+      gs->gobj[0] = best.o0;
+      gs->gobj[1] = best.o1;
       gs->gev = -1;
     }
   }
@@ -102,16 +122,18 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_import_elites_kernel(Island
   if (A.n_ranks < 2) return;
   if (A.strategy == 0) {  // ring: donor = previous rank's best
     const int src = ((A.rank - 1 + A.n_ranks) % A.n_ranks) * A.top_n;
-    const double* h = rec_head(A.buf, A.rec_bytes, src);
+    const Cand h = rec_cand(A.buf, A.rec_bytes, src);
     if (A.P == 1) {
-      if (strictly_better(h[1], h[0], A.pen[0], A.scal[0]))
-        put_solution_raw(A.genes, A.scal, A.pen, A.W, 0, rec_genes(A.buf, A.rec_bytes, src), h[1], h[0]);
+      if (cand_cmp(h, pop.at(0), mo) < 0)
+        put_solution_raw(A.genes, A.scal, A.pen, A.obj2, A.W, 0,
+                         rec_genes(A.buf, A.rec_bytes, src), h);
       return;
     }
-    const Cand w = block_select<true>(A.pen, A.scal, 0, A.P, nullptr, 0, red);
-    const Cand b = block_select<false>(A.pen, A.scal, 0, A.P, nullptr, 0, red);
+    const Cand w = block_select<true>(pop, 0, A.P, nullptr, 0, red, mo);
+    const Cand b = block_select<false>(pop, 0, A.P, nullptr, 0, red, mo);
     if (w.idx != b.idx)
-      put_solution_raw(A.genes, A.scal, A.pen, A.W, w.idx, rec_genes(A.buf, A.rec_bytes, src), h[1], h[0]);
+      put_solution_raw(A.genes, A.scal, A.pen, A.obj2, A.W, w.idx,
+                       rec_genes(A.buf, A.rec_bytes, src), h);
     return;
   }
   // global_top_n: stable top tn over the gathered records (rank-major order)
@@ -123,14 +145,13 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_import_elites_kernel(Island
         bool taken = false;
         for (int q = 0; q < nsel; ++q) taken |= s_sel[q] == i;
         if (taken) continue;
-        const double* h = rec_head(A.buf, A.rec_bytes, i);
-        if (h[1] == 1.7976931348623157e308) continue;  // padding
+        const Cand h = rec_cand(A.buf, A.rec_bytes, i);
+        if (h.pen == 1.7976931348623157e308) continue;  // padding
         if (bi < 0) {
           bi = i;
           continue;
         }
-        const double* hb = rec_head(A.buf, A.rec_bytes, bi);
-        if (strictly_better(h[1], h[0], hb[1], hb[0])) bi = i;
+        if (cand_cmp(h, rec_cand(A.buf, A.rec_bytes, bi), mo) < 0) bi = i;
       }
       if (bi < 0) break;
       s_sel[nsel++] = bi;
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_import_elites_kernel(Island
   }
   __syncthreads();
   const int nd = s_slot;
-  const Cand b = block_select<false>(A.pen, A.scal, 0, A.P, nullptr, 0, red);
+  const Cand b = block_select<false>(pop, 0, A.P, nullptr, 0, red, mo);
   const int nslots = A.P - 1;
   Stream mr;
   mr.init(mix64_3(A.seed, 3, (u64)A.event));
@@ -156,9 +177,9 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_import_elites_kernel(Island
       s_dst = s;
     }
     __syncthreads();
-    const double* h = rec_head(A.buf, A.rec_bytes, s_sel[d]);
-    put_solution_raw(A.genes, A.scal, A.pen, A.W, s_dst, rec_genes(A.buf, A.rec_bytes, s_sel[d]),
-                     h[1], h[0]);
+    put_solution_raw(A.genes, A.scal, A.pen, A.obj2, A.W, s_dst,
+                     rec_genes(A.buf, A.rec_bytes, s_sel[d]),
+                     rec_cand(A.buf, A.rec_bytes, s_sel[d]));
     __syncthreads();
   }
 }

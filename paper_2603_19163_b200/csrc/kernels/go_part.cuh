@@ -398,8 +398,14 @@ struct DemF {
 };
 
 // Φ parts of a compact partition row: distance objective and penalty
+// (+ the "vehicles" objective, builtins.py:133: non-empty routes)
 __device__ __forceinline__ void part_eval(const PartView& v, const short* cells, const short* sz,
-                                          double& distance, double& penalty) {
+                                          double& distance, double& penalty, int* veh = nullptr) {
+  if (veh) {
+    int c = 0;
+    for (int r = 0; r < v.d1; ++r) c += sz[r] > 0;
+    *veh = c;
+  }
   const int n1 = v.n + 1;
   PySum dsum;
   dsum.init();

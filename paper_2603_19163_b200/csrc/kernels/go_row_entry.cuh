@@ -92,9 +92,12 @@ __device__ __forceinline__ void part_eval_entry(const void* inst, go::RowArgs x,
   v.cap = x.capacity;
   v.tw = x.tw;
   const short* row = genes + (size_t)blockIdx.x * (x.n_cells + x.d1);
-  double d, p;
-  part_eval(v, row, row + x.n_cells, d, p);
-  obj[blockIdx.x] = d;
+  double d, p, o0, o1;
+  int veh;
+  part_eval(v, row, row + x.n_cells, d, p, &veh);
+  part_scal(x, d, veh, &o0, &o1);  // objectives in the problem's order
+  obj[(size_t)blockIdx.x * x.mo.m] = o0;
+  if (x.mo.m == 2) obj[(size_t)blockIdx.x * 2 + 1] = o1;
   pen[blockIdx.x] = p;
 }
 

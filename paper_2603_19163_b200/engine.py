@@ -314,10 +314,71 @@ def initialize_population(problem: ProblemDefinition, pop_size: int, oversample_
             raise ValueError(f"init_candidates produced an invalid solution: {rep.violations[0]}")
         pool.append(s.copy())
     evaluate_many(problem, pool, device)
-    if cfg.num_objectives != 1:
-        raise NotImplementedError("multi-objective runs have no device path yet (SURVEY §8f-3)")
+    if cfg.num_objectives != 1:  # engine.py:352-360: non-dominated fronts in crowding order
+        fronts = fast_nondominated_sort(np.array([s.objectives for s in pool]),
+                                        [o.direction for o in cfg.obj_defs])
+        keep = []
+        for front in fronts:
+            for idx in front:
+                if len(keep) < pop_size:
+                    keep.append(pool[idx])
+        return keep
     pool.sort(key=cmp_to_key(lambda a, b: compare(a, b, cfg)))
     return pool[:pop_size]
+
+
+def fast_nondominated_sort(points: np.ndarray, directions) -> list[list[int]]:
+    """engine.py:370-420: Deb's dominance ranking, each front ordered by crowding
+    distance descending (ties by index); Maximize objectives negated first."""
+    pts = np.asarray(points, dtype=np.float64).copy()
+    for j, d in enumerate(directions):
+        if d is Direction.MAXIMIZE:
+            pts[:, j] = -pts[:, j]
+    n = len(pts)
+
+    def dominates(a, b):
+        return bool(np.all(a <= b) and np.any(a < b))
+    dominated_by = [[] for _ in range(n)]
+    count = np.zeros(n, dtype=np.int64)
+    fronts = [[]]
+    for i in range(n):
+        for j in range(i + 1, n):
+            if dominates(pts[i], pts[j]):
+                dominated_by[i].append(j)
+                count[j] += 1
+            elif dominates(pts[j], pts[i]):
+                dominated_by[j].append(i)
+                count[i] += 1
+    fronts[0] = [i for i in range(n) if count[i] == 0]
+    f = 0
+    while fronts[f]:
+        nxt = []
+        for p in fronts[f]:
+            for q in dominated_by[p]:
+                count[q] -= 1
+                if count[q] == 0:
+                    nxt.append(q)
+        f += 1
+        fronts.append(nxt)
+    fronts.pop()
+    out = []
+    for front in fronts:
+        if len(front) <= 2:
+            out.append(list(front))
+            continue
+        crowd = np.zeros(len(front))
+        sub = pts[front]
+        for j in range(sub.shape[1]):
+            order = np.argsort(sub[:, j], kind="stable")
+            span = sub[order[-1], j] - sub[order[0], j]
+            crowd[order[0]] = crowd[order[-1]] = math.inf
+            if span == 0:
+                continue
+            for pos in range(1, len(front) - 1):
+                crowd[order[pos]] += (sub[order[pos + 1], j] - sub[order[pos - 1], j]) / span
+        ranked = sorted(range(len(front)), key=lambda i: (-crowd[i], i))
+        out.append([front[i] for i in ranked])
+    return out
 
 
 def scalar_fitness(sol: Solution, cfg: ProblemConfig, penalty_weight: float) -> float:
@@ -367,8 +428,8 @@ class DeviceRun:
         self.t_start = time.perf_counter()
         self.problem, self.config, self.seed = problem, config, seed
         cfg = problem.config()
-        if cfg.num_objectives != 1 or not isinstance(cfg.comparison_or_default(), Weighted):
-            raise NotImplementedError("the device path runs single-objective Weighted problems")
+        if cfg.num_objectives > 2:
+            raise NotImplementedError("the device path runs one or two objectives")
         self.cfg = cfg
         self.lib = N.load()
         dev = config.device
@@ -443,12 +504,20 @@ class DeviceRun:
         ec.islands, ec.migration = isl.count, N.MIG[isl.migration]
         ec.migration_interval, ec.top_n = isl.interval, isl.top_n
         ec.elite_interval = config.elite_injection_interval
-        ec.has_target = config.target_objective is not None
+        ec.has_target = config.target_objective is not None and cfg.num_objectives == 1
         ec.target_objective = config.target_objective or 0.0
         ec.evolver_offset = config.evolver_offset
         od = cfg.obj_defs[0]
         ec.maximize = od.direction is Direction.MAXIMIZE
-        ec.obj_weight = cfg.comparison_or_default().weights[0]
+        mode = cfg.comparison_or_default()
+        # scalar_fitness weights (engine.py:215-222): the Weighted mode's, else obj_defs'
+        sw = mode.weights if isinstance(mode, Weighted) else tuple(o.weight for o in cfg.obj_defs)
+        ec.obj_weight = sw[0]
+        ec.obj_weight2 = sw[1] if len(sw) > 1 else 0.0
+        if not isinstance(mode, Weighted):  # Lexicographic (core.py:92-106)
+            ec.lex, ec.lex_first = 1, mode.priority_order[0]
+            for i, t in enumerate(mode.tolerances):
+                ec.lex_tol[i] = t
         self.engine = C.c_void_p()
         N.check(self.lib.go_engine_create(self.handle, C.byref(ec), C.byref(self.engine)))
         reg = self.registry
@@ -461,7 +530,7 @@ class DeviceRun:
                                                 N.dptr(floors), N.dptr(caps), reg.total(),
                                                 N.dptr(kw)))
         genes, sizes = pack_solutions(pop, cfg)
-        obj = np.array([s.objectives[0] for s in pop], dtype=np.float64)
+        obj = np.array([s.objectives for s in pop], dtype=np.float64).reshape(-1)
         pen = np.array([s.penalty for s in pop], dtype=np.float64)
         N.check(self.lib.go_engine_set_population(self.engine, N.iptr(genes), N.iptr(sizes),
                                                   N.dptr(obj), N.dptr(pen)))
@@ -521,11 +590,13 @@ class DeviceRun:
         W = cfg.d1 * cfg.d2
         genes = np.zeros(W, dtype=np.int32)
         sizes = np.zeros(cfg.d1, dtype=np.int32)
-        obj, pen, gen = C.c_double(), C.c_double(), C.c_int64()
+        m = cfg.num_objectives
+        obj = np.zeros(m, dtype=np.float64)
+        pen, gen = C.c_double(), C.c_int64()
         N.check(self.lib.go_engine_get_best(self.engine, N.iptr(genes), N.iptr(sizes),
-                                            C.byref(obj), C.byref(pen), C.byref(gen)))
-        s = Solution(genes.reshape(cfg.d1, cfg.d2), sizes, 1)
-        s.objectives[0] = obj.value
+                                            N.dptr(obj), C.byref(pen), C.byref(gen)))
+        s = Solution(genes.reshape(cfg.d1, cfg.d2), sizes, m)
+        s.objectives[:] = obj
         s.penalty = pen.value
         return s
 
@@ -534,14 +605,15 @@ class DeviceRun:
         P, W = self.pop_size, cfg.d1 * cfg.d2
         genes = np.zeros((P, W), dtype=np.int32)
         sizes = np.zeros((P, cfg.d1), dtype=np.int32)
-        obj = np.zeros(P)
+        m = cfg.num_objectives
+        obj = np.zeros(P * m)
         pen = np.zeros(P)
         N.check(self.lib.go_engine_get_population(self.engine, N.iptr(genes), N.iptr(sizes),
                                                   N.dptr(obj), N.dptr(pen)))
         out = []
         for i in range(P):
-            s = Solution(genes[i].reshape(cfg.d1, cfg.d2), sizes[i], 1)
-            s.objectives[0] = obj[i]
+            s = Solution(genes[i].reshape(cfg.d1, cfg.d2), sizes[i], m)
+            s.objectives[:] = obj[i * m:(i + 1) * m]
             s.penalty = pen[i]
             out.append(s)
         return out
@@ -600,7 +672,8 @@ def _run_single(problem, config: EngineConfig, seed: int, best_known) -> RunResu
         dr.close()
     elapsed = time.perf_counter() - dr.t_start - dr.jit_seconds
     gap = None
-    if best_known is not None and cfg.obj_defs[0].direction is Direction.MINIMIZE and best_known:
+    if best_known is not None and cfg.num_objectives == 1 and \
+            cfg.obj_defs[0].direction is Direction.MINIMIZE and best_known:
         gap = (float(best.objectives[0]) - best_known) / best_known * 100.0
     gens = int(st.generations)
     echo = config.as_dict()

@@ -146,11 +146,12 @@ def device_evaluate(problem: ProblemDefinition, sols, device: int = 0):
     lib = N.load()
     h = problem.device_handle(device)
     genes, sizes = pack_solutions(sols, cfg)
-    obj = np.zeros(len(sols), dtype=np.float64)
+    m = cfg.num_objectives
+    obj = np.zeros(len(sols) * m, dtype=np.float64)
     pen = np.zeros(len(sols), dtype=np.float64)
     N.check(lib.go_eval_batch(h, N.iptr(genes), N.iptr(sizes), len(sols), N.dptr(obj),
                               N.dptr(pen)))
-    return obj.reshape(-1, 1), pen
+    return obj.reshape(-1, m), pen
 
 
 def evaluate(problem: ProblemDefinition, sol: Solution, *, validate: bool = True):
@@ -350,12 +351,12 @@ class RoutingProblem(ProblemDefinition):
         return z, z, z
 
     def _native_desc(self):
-        if self.objective_names != ("distance",):
-            raise TypeError("the device routing path optimises the single 'distance' objective")
         d, dem = N.f64(self.dist), N.f64(self.demands)
         ready, due, service = (N.f64(a) for a in self._arrays())
+        kinds = [1 if name == "vehicles" else 0 for name in self.objective_names] + [1]
         desc = N.ProblemDesc(kind=self._KIND, n=self.n, d1=self.vehicles, d2=self.n,
-                             capacity=self.capacity)
+                             capacity=self.capacity, n_obj=len(self.objective_names))
+        desc.obj_kind[0], desc.obj_kind[1] = kinds[0], kinds[1]
         desc.dist, desc.demands = N.dptr(d), N.dptr(dem)
         desc.ready, desc.due, desc.service = N.dptr(ready), N.dptr(due), N.dptr(service)
         return desc, (d, dem, ready, due, service)
