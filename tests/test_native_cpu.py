@@ -129,3 +129,25 @@ def test_custom_problem_host_side():
     with pytest.raises(ValueError):
         G.solve_custom("binary", 4, compute_obj="return 0.0;",
                        custom_operators=[G.CustomOperator(100, "x", cuda="")])
+
+
+def test_result_record_schema_round_trip():
+    """results.py:16-101: fixed key order, canonical text, strict parsing."""
+    from paper_2603_19163_b200 import results as R
+    rec = R.ResultRecord(problem="tsp", instance="lattice442", seed=42, objectives=[44200.0],
+                         penalty=0.0, feasible=True, gap_pct=0.0, generations=16223,
+                         elapsed_s=13.85, gens_per_sec=1171.3,
+                         final_weights={"sequences": [], "k_steps": [0.8, 0.15, 0.05]},
+                         profile={"scale": "large"}, config={"team_size": 128})
+    text = R.emit_result(rec)
+    assert list(json_keys(text)) == list(R.RESULT_SCHEMA_FIELDS)
+    assert R.emit_result(R.parse_result(text)) == text
+    assert R.parse_results(R.emit_results([rec, rec]))[1] == rec
+    with pytest.raises(ValueError):
+        R.ResultRecord.from_dict({"problem": "tsp"})
+    assert "lattice442" in R.gap_table([rec])
+
+
+def json_keys(text):
+    import json
+    return json.loads(text).keys()
