@@ -698,38 +698,65 @@ __device__ void team_gr_user_cells(G* row, int n, const GrShared& g, const UserS
 // Fast path (n_jobs, n_machines <= 32, <= 255 operations per job): lane j owns
 // job j and machine j in registers; key = (priority, job, index) orders exactly
 // like (priority, op) since op = job * per_job + index.
+// Warp-cooperative decode state (lane j owns job j and machine j).
+struct JspWarp {
+  int nx, jf, mfr, pr, span, step;
+};
+
+// Runs steps of the fast-path decode from `st` until every operation is
+// scheduled, or (stop_job >= 0) until job stop_job's next operation index
+// becomes stop_k (that operation is then a candidate and its priority matters).
+// Priority of operation ovp is ovv.
 template <class G>
-__device__ __forceinline__ int jsp_decode_warp32(const JspView& J, const G* prio, int ovp, int ovv,
-                                                 int wl) {
+__device__ __forceinline__ void jsp_warp_run(const JspView& J, const G* prio, int ovp, int ovv,
+                                             int wl, JspWarp& st, int stop_job, int stop_k) {
   const int pj = J.per_job;
   const bool mine = wl < J.n_jobs;
-  int nx = 0, jf = 0, mfr = 0, span = 0;
-  int op0 = wl * pj;
-  int pr = mine ? (op0 == ovp ? ovv : (int)prio[op0]) : 0;
   const int n_ops = J.n_jobs * pj;
-  for (int step = 0; step < n_ops; ++step) {
-    const unsigned key = mine && nx < pj
-                             ? ((unsigned)pr << 16) | ((unsigned)wl << 8) | (unsigned)nx
+  for (; st.step < n_ops; ++st.step) {
+    if (stop_job >= 0 && __shfl_sync(0xffffffffu, st.nx, stop_job) == stop_k) return;
+    const unsigned key = mine && st.nx < pj
+                             ? ((unsigned)st.pr << 16) | ((unsigned)wl << 8) | (unsigned)st.nx
                              : 0xFFFFFFFFu;
     const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
     const int j = (int)((kmin >> 8) & 0xFFu);
     const int op = j * pj + (int)(kmin & 0xFFu);
     const int m = J.mach[op], du = J.dur[op];
-    const int mfm = __shfl_sync(0xffffffffu, mfr, m);
-    const int jfo = __shfl_sync(0xffffffffu, jf, j);
+    const int mfm = __shfl_sync(0xffffffffu, st.mfr, m);
+    const int jfo = __shfl_sync(0xffffffffu, st.jf, j);
     const int done = (jfo > mfm ? jfo : mfm) + du;
-    if (wl == m) mfr = done;
+    if (wl == m) st.mfr = done;
     if (wl == j) {
-      jf = done;
-      ++nx;
-      if (nx < pj) {
+      st.jf = done;
+      ++st.nx;
+      if (st.nx < pj) {
         const int o = op + 1;
-        pr = o == ovp ? ovv : (int)prio[o];
+        st.pr = o == ovp ? ovv : (int)prio[o];
       }
     }
-    span = done > span ? done : span;
+    st.span = done > st.span ? done : st.span;
   }
-  return span;
+}
+
+template <class G>
+__device__ __forceinline__ JspWarp jsp_warp_start(const JspView& J, const G* prio, int ovp,
+                                                  int ovv, int wl) {
+  JspWarp st;
+  st.nx = st.jf = st.mfr = st.span = st.step = 0;
+  const int op0 = wl * J.per_job;
+  st.pr = wl < J.n_jobs ? (op0 == ovp ? ovv : (int)prio[op0]) : 0;
+  return st;
+}
+
+// Fast path (n_jobs, n_machines <= 32, <= 255 operations per job): lane j owns
+// job j and machine j in registers; key = (priority, job, index) orders exactly
+// like (priority, op) since op = job * per_job + index.
+template <class G>
+__device__ __forceinline__ int jsp_decode_warp32(const JspView& J, const G* prio, int ovp, int ovv,
+                                                 int wl) {
+  JspWarp st = jsp_warp_start(J, prio, ovp, ovv, wl);
+  jsp_warp_run(J, prio, ovp, ovv, wl, st, -1, 0);
+  return st.span;
 }
 
 template <class G>
@@ -790,11 +817,28 @@ __device__ void team_gr_jsp(const JspView& J, G* row, const GrShared& g, int* sc
   const int m = g.m(), nd = g.nd();
   const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
   int* mf = scratch + warp * scratch_ints;
+  const bool fast = J.n_jobs <= 32 && J.n_mach <= 32 && J.per_job < 256 &&
+                    J.n_jobs * J.per_job < 32768;
   for (int t = 0; t < m; ++t) {
     const int p = g.picks()[t];
-    for (int i = warp; i < nd; i += nwarps) {
-      const int sp = jsp_decode_warp(J, row, p, g.dom()[i], mf, wl);
-      if (wl == 0) g.score()[i] = sp;
+    if (fast) {
+      // the trials share the schedule up to the step where operation p becomes
+      // a candidate: decode that prefix once per warp, then finish each trial
+      const int jp = p / J.per_job, kp = p - jp * J.per_job;
+      JspWarp base = jsp_warp_start(J, row, -1, 0, wl);
+      jsp_warp_run(J, row, -1, 0, wl, base, jp, kp);
+      for (int i = warp; i < nd; i += nwarps) {
+        JspWarp st = base;
+        const int v = g.dom()[i];
+        if (wl == jp && st.nx == kp) st.pr = v;  // op p is job jp's head: its trial priority
+        jsp_warp_run(J, row, p, v, wl, st, -1, 0);
+        if (wl == 0) g.score()[i] = st.span;
+      }
+    } else {
+      for (int i = warp; i < nd; i += nwarps) {
+        const int sp = jsp_decode_warp(J, row, p, g.dom()[i], mf, wl);
+        if (wl == 0) g.score()[i] = sp;
+      }
     }
     team_bar(team, TS);
     if (lane == 0) {  // first minimum in domain order
