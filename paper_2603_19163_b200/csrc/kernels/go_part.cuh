@@ -333,25 +333,36 @@ __device__ __forceinline__ void run_part_op(int kind, PartCtx& c) {
 }
 
 // ---- exact evaluation --------------------------------------------------------------
-// numpy pairwise_sum (loops_utils.h) over f(lo .. lo+n-1); matches np.sum bit-for-bit
+// numpy pairwise_sum (loops_utils.h) over f(lo .. lo+n-1); matches np.sum bit-for-bit.
+// Blocks of <= 128 elements are summed inline (the functor stays in registers);
+// only longer ranges take the recursive split, out of line.
 template <class F>
-__device__ double np_pairwise(const F& f, int lo, int n) {
+__device__ __forceinline__ double np_pairwise_leaf(const F& f, int lo, int n) {
   if (n < 8) {
     double res = -0.0;
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, f(lo + i));
     return res;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(lo + i + j));
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
-    return res;
-  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(lo + i + j));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
+  return res;
+}
+template <class F>
+__device__ double np_pairwise_split(const F& f, int lo, int n);
+template <class F>
+__device__ __forceinline__ double np_pairwise(const F& f, int lo, int n) {
+  return n <= 128 ? np_pairwise_leaf(f, lo, n) : np_pairwise_split(f, lo, n);
+}
+template <class F>
+__device__ double np_pairwise_split(const F& f, int lo, int n) {
   int n2 = n / 2;
   n2 -= n2 % 8;
   return __dadd_rn(np_pairwise(f, lo, n2), np_pairwise(f, lo + n2, n - n2));
