@@ -923,6 +923,164 @@ __device__ __forceinline__ void part_eval_ins(const PartView& v, const short* ce
   penalty = v.tw ? __dadd_rn(cap_pen, late) : cap_pen;
 }
 
+// Incremental trials for partitions.  A trial inserts v into one route r*;
+// part_eval accumulates routes in order (Neumaier distance sum, capacity and
+// lateness running sums), so the state after routes 0..r*-1 and the
+// contributions of routes after r* are those of the row without v: cached
+// once per value (thread 0, one pass in part_eval's order), then each trial
+// only evaluates route r* and replays the cached terms.  Lateness terms that
+// are 0.0 are not stored (adding +0.0 leaves a non-negative sum unchanged),
+// so the result is bit-identical to part_eval_ins.
+struct PartCache {
+  double* rd;     // [d1] route distances
+  double* over;   // [d1] capacity terms max(0, load - cap)
+  double* ss;     // [d1] PySum state before route r
+  double* sc;
+  double* sf;
+  double* cap;    // [d1] capacity sum before route r
+  double* late;   // [d1] lateness sum before route r
+  double* loff;   // [d1] start of route r's positive lateness terms in lt (cells before r + r)
+  double* lcnt;   // [d1] how many
+  double* lt;     // positive lateness terms, route r's at loff[r]
+  __device__ __forceinline__ void bind(double* b, int d1) {
+    rd = b;
+    over = rd + d1;
+    ss = over + d1;
+    sc = ss + d1;
+    sf = sc + d1;
+    cap = sf + d1;
+    late = cap + d1;
+    loff = late + d1;
+    lcnt = loff + d1;
+    lt = lcnt + d1;
+  }
+  static __device__ __forceinline__ int doubles(int d1, int n) { return 9 * d1 + n + d1; }
+};
+
+// one route's (distance, capacity term, lateness terms) in part_eval's order
+template <class R, class LT>
+__device__ __forceinline__ void part_route(const PartView& v, const R& route, int len, double& rd,
+                                           double& capterm, const LT& late_term) {
+  const int n1 = v.n + 1;
+  rd = 0.0;
+  if (len > 0) {
+    rd = __dadd_rn(v.dist[route[0] + 1], v.dist[(route[len - 1] + 1) * n1]);
+    if (len > 1) {
+      double acc = 0.0;
+      if (len - 1 < 8) {  // np_pairwise small case, accessor inline
+        acc = -0.0;
+        for (int i = 0; i < len - 1; ++i)
+          acc = __dadd_rn(acc, v.dist[(route[i] + 1) * n1 + route[i + 1] + 1]);
+      } else {
+        struct Edge {
+          const double* d;
+          const R* r;
+          int n1;
+          __device__ __forceinline__ double operator()(int i) const {
+            return d[((*r)[i] + 1) * n1 + (*r)[i + 1] + 1];
+          }
+        } f{v.dist, &route, n1};
+        acc = np_pairwise(f, 0, len - 1);
+      }
+      rd = __dadd_rn(rd, acc);
+    }
+  }
+  struct Dem {
+    const double* dem;
+    const R* r;
+    __device__ __forceinline__ double operator()(int i) const { return dem[(*r)[i]]; }
+  } dm{v.demand, &route};
+  const double load = np_pairwise(dm, 0, len);
+  const double ov = __dsub_rn(load, v.cap);
+  capterm = ov > 0.0 ? ov : 0.0;
+  if (v.tw && len > 0) {
+    double t = v.ready[0];
+    int prev = 0;
+    for (int q = 0; q < len; ++q) {
+      const int node = route[q] + 1;
+      const double arr0 = __dadd_rn(t, v.dist[prev * n1 + node]);
+      const double arrival = v.ready[node] >= arr0 ? v.ready[node] : arr0;
+      const double l = __dsub_rn(arrival, v.due[node]);
+      if (l > 0.0) late_term(l);
+      t = __dadd_rn(arrival, v.service[node]);
+      prev = node;
+    }
+    const double back = __dsub_rn(__dadd_rn(t, v.dist[prev * n1]), v.due[0]);
+    if (back > 0.0) late_term(back);
+  }
+}
+
+struct PlainRoute {
+  const short* b;
+  __device__ __forceinline__ int operator[](int q) const { return b[q]; }
+};
+
+// routes in parallel (thread r: distance, capacity term, positive lateness
+// terms), then thread 0 runs the prefix sums in part_eval's order
+__device__ void part_cache_build(const PartView& v, const short* cells, const short* sz,
+                                 PartCache& pc, int lane, int team, int TS) {
+  for (int r = lane; r < v.d1; r += TS) {
+    int at = 0;
+    for (int q = 0; q < r; ++q) at += sz[q];
+    const int base = at + r;
+    int cnt = 0;
+    double rd, ct;
+    part_route(v, PlainRoute{cells + at}, sz[r], rd, ct, [&](double l) { pc.lt[base + cnt++] = l; });
+    pc.rd[r] = rd;
+    pc.over[r] = ct;
+    pc.loff[r] = base;
+    pc.lcnt[r] = cnt;
+  }
+  team_bar(team, TS);
+  if (lane == 0) {
+    PySum ds;
+    ds.init();
+    double cap = 0.0, late = 0.0;
+    for (int r = 0; r < v.d1; ++r) {
+      pc.ss[r] = ds.s;
+      pc.sc[r] = ds.c;
+      pc.sf[r] = ds.first;
+      pc.cap[r] = cap;
+      pc.late[r] = late;
+      ds.add(pc.rd[r]);
+      cap = __dadd_rn(cap, pc.over[r]);
+      const int b = (int)pc.loff[r], e = b + (int)pc.lcnt[r];
+      for (int k = b; k < e; ++k) late = __dadd_rn(late, pc.lt[k]);
+    }
+  }
+}
+
+// part_eval of the row with v inserted at (ri, pi), from the cache
+__device__ __forceinline__ void part_eval_trial(const PartView& v, const short* cells,
+                                                const short* sz, const PartCache& pc, int ri,
+                                                int pi, int val, double& distance, double& penalty,
+                                                int& veh) {
+  PySum ds;
+  ds.s = pc.ss[ri];
+  ds.c = pc.sc[ri];
+  ds.first = (int)pc.sf[ri];
+  double cap = pc.cap[ri], late = pc.late[ri];
+  int at = 0;
+  veh = 0;
+  for (int r = 0; r < v.d1; ++r) {
+    if (r < ri) at += sz[r];
+    veh += (sz[r] + (r == ri)) > 0;
+  }
+  double rd, ct;
+  part_route(v, RouteIns{cells + at, pi, val}, sz[ri] + 1, rd, ct,
+             [&](double l) { late = __dadd_rn(late, l); });
+  ds.add(rd);
+  cap = __dadd_rn(cap, ct);
+  for (int r = ri + 1; r < v.d1; ++r) {
+    ds.add(pc.rd[r]);
+    cap = __dadd_rn(cap, pc.over[r]);
+    const int b = (int)pc.loff[r], e = b + (int)pc.lcnt[r];
+    for (int k = b; k < e; ++k) late = __dadd_rn(late, pc.lt[k]);
+  }
+  distance = ds.result();
+  penalty = v.tw ? __dadd_rn(cap, late) : cap;
+}
+
 // partitions (operators.py:520-546): thread 0 pops / parks / re-inserts, the
 // team scores every trial slot of every open row in parallel (full evaluation)
 // scalar_fitness (engine.py:215-222) of a routing solution from its distance,
@@ -972,6 +1130,10 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       c.cell_at(gi, r0, p0);
       c.remove(r0, p0);
     }
+    PartCache pc;
+    const bool cached = 32 + PartCache::doubles(d1, n_cells) <= 5 * TS;
+    pc.bind(sbuf + 32, d1);
+    if (cached) part_cache_build(pv, cells, sz, pc, lane, team, TS);
     team_bar(team, TS);
     int ntr = 0;  // trial slots: open rows in order, positions 0..sz[r]
     for (int r = 0; r < d1; ++r) ntr += sz[r] < d2 ? sz[r] + 1 : 0;
@@ -986,7 +1148,8 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       }
       double dist, pen;
       int veh;
-      part_eval_ins(pv, cells, sz, r, k, v, dist, pen, veh);
+      if (cached) part_eval_trial(pv, cells, sz, pc, r, k, v, dist, pen, veh);
+      else part_eval_ins(pv, cells, sz, r, k, v, dist, pen, veh);
       const double sc = __dadd_rn(part_scal(X, dist, veh, nullptr, nullptr), __dmul_rn(pw, pen));
       if (bi == 0x7fffffff || sc < bs) {
         bs = sc;
