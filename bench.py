@@ -86,6 +86,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic():
+    """DRAM bytes per evolve launch from the committed ncu --set full capture
+    (profiles/r01_ncu_traffic.json), or None."""
+    p = ROOT / "profiles" / "r01_ncu_traffic.json"
+    try:
+        return json.loads(p.read_text())["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -330,7 +340,7 @@ def run_ours(args):
                         "go_engine_get_population(host) per step"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm, "traffic": None,
+                     "frac": achieved_gbs / hbm, "traffic": ncu_traffic(),
                      "peak_source": src, "kernel": "go_evolve_tsp_jit",
                      "evolve_ms": evolve_ms, "evolve_launches": int(evolve_launches),
                      "algorithmic_bytes": int(alg_bytes),
