@@ -28,10 +28,6 @@ __device__ __forceinline__ bool perm_deferred(int kind) {
          kind == SEQ_GUIDED_REBUILD;
 }
 
-struct DeferOut {
-  int changed;  // 0: the operator was a no-op (no materialisation kept)
-};
-
 // One warp resolves one deferred lane.  `dst` / `aux` are the lane's two
 // global rows (dst receives the candidate; aux is scratch), `C` the lane's
 // chain (its base may be `aux`).  `rng` is valid in lane 0 only.

@@ -151,3 +151,16 @@ def test_result_record_schema_round_trip():
 def json_keys(text):
     import json
     return json.loads(text).keys()
+
+
+def test_nondominated_sort_matches_oracle():
+    """engine.py:370-420 (host, multi-objective init): product == oracle restatement."""
+    from oracle import engine as OEng
+    from paper_2603_19163_b200.core import Direction
+    from paper_2603_19163_b200.engine import fast_nondominated_sort
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        pts = rng.integers(0, 6, size=(int(rng.integers(1, 40)), 2)).astype(float)
+        dirs = [Direction.MINIMIZE, Direction.MAXIMIZE if trial % 3 == 0 else Direction.MINIMIZE]
+        odirs = ["maximize" if d is Direction.MAXIMIZE else "minimize" for d in dirs]
+        assert fast_nondominated_sort(pts, dirs) == OEng.nondominated_sort(pts, odirs)
