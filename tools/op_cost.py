@@ -36,7 +36,8 @@ def time_cfg(make, ops, steps=6, gps=10):
     if ops is not None:
         prob.device_sequences = lambda: ops
     custom = G.tsp_delta_operators() if CUSTOM else ()
-    dr = G.DeviceRun(prob, G.EngineConfig(seed=42, custom_operators=custom), 42)
+    aos = G.AosConfig(update_interval=10 ** 9) if FROZEN else G.AosConfig()
+    dr = G.DeviceRun(prob, G.EngineConfig(seed=42, custom_operators=custom, aos=aos), 42)
     done = gps
     dr.run(done, None)
     ms = 0.0
@@ -53,6 +54,7 @@ def time_cfg(make, ops, steps=6, gps=10):
 
 
 CUSTOM = "--custom" in sys.argv
+FROZEN = "--frozen" in sys.argv  # no AOS updates: the preset operator mix throughout
 
 
 def main():
