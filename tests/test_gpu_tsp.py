@@ -256,3 +256,21 @@ def test_whole_row_operators_match_oracle(ops):
                      custom_ops=tuple((i, nm, f, 1.0) for i, nm, f in OM.TSP_DELTA if i in ops))
     ref = OE.run(OP.Tsp(dist), ocfg, device_stream="philox")
     _assert_same_run(res, ref)
+
+
+def test_population_beyond_one_wave_crossover_fallback():
+    """More evolvers than one resident wave: the snapshot protocol cannot spin on
+    teams that are not resident, so chunks shrink to one generation (launch
+    boundaries are the snapshot barriers) — still bit-identical to the oracle."""
+    import paper_2603_19163_b200 as G_
+    dist = I.tsp_random(12, 3, True)
+    prob = _tsp(dist)
+    cfg = G_.EngineConfig(population=3000, team_size=8, max_generations=3, seed=17,
+                          record_history=True)
+    res = G_.run(prob, cfg)
+    ref = OE.run(OP.Tsp(dist), OE.RunCfg(population=3000, team_size=8, max_generations=3,
+                                         seed=17, record_history=True,
+                                         allowed_ops=prob.device_sequences()),
+                 device_stream="philox")
+    assert res.history["best_phi"] == ref.history["best_phi"]
+    assert [s.row(0).tolist() for s in res.population] == [s.row(0).tolist() for s in ref.population]
