@@ -11,7 +11,7 @@ from paper_2603_19163_b200 import instances as I  # noqa: E402
 name, E = sys.argv[1], int(sys.argv[2])
 d = I.tsp_random(51, 51) if name == "C1" else I.tsp_lattice()[0]
 prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=d))
-dr = G.DeviceRun(prob, G.EngineConfig(seed=42, teams_per_cta=E,
+dr = G.DeviceRun(prob, G.EngineConfig(seed=42, teams_per_cta=E, population=148 * E,
                                       custom_operators=G.tsp_delta_operators()), 42)
 done = 20
 dr.run(done, None)
