@@ -1214,12 +1214,21 @@ __device__ __forceinline__ u32 warp_uniform_x(G* row, int n, const MateSel& ms, 
   hi = 0;
   if (mate < 0) return pos0;
   const short* mrow = ms.rows + (size_t)mate * n;
-  for (int p = wl; p < n; p += 32)
-    if (random_at(rng.k0, rng.k1, pos0 + 2u * (u32)p) < 0.5) {
-      row[p] = (G)__ldcg(mrow + p);
-      lo = p < lo ? p : lo;
-      hi = p + 1;
-    }
+  // lane wl draws a contiguous run of cells, so consecutive random() calls
+  // share Philox blocks (one block per two draws instead of one per draw)
+  const int c = (n + 31) >> 5, p0 = wl * c, p1 = p0 + c < n ? p0 + c : n;
+  if (p0 < p1) {
+    Stream r;
+    r.k0 = rng.k0;
+    r.k1 = rng.k1;
+    r.seek(pos0 + 2u * (u32)p0);
+    for (int p = p0; p < p1; ++p)
+      if (r.random() < 0.5) {
+        row[p] = (G)__ldcg(mrow + p);
+        lo = p < lo ? p : lo;
+        hi = p + 1;
+      }
+  }
   lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
   hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)hi);
   return pos0 + 2u * (u32)n;
