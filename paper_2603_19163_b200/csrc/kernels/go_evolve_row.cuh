@@ -700,7 +700,7 @@ __device__ void team_gr_user_cells(G* row, int n, const GrShared& g, const UserS
 // like (priority, op) since op = job * per_job + index.
 // Warp-cooperative decode state (lane j owns job j and machine j).
 struct JspWarp {
-  int nx, jf, mfr, pr, span, step;
+  int nx, jf, mfr, pr, pn, span, step;  // pn: priority of the op after the head
 };
 
 // Runs steps of the fast-path decode from `st` until every operation is
@@ -729,10 +729,9 @@ __device__ __forceinline__ void jsp_warp_run(const JspView& J, const G* prio, in
     if (wl == j) {
       st.jf = done;
       ++st.nx;
-      if (st.nx < pj) {
-        const int o = op + 1;
-        st.pr = o == ovp ? ovv : (int)prio[o];
-      }
+      st.pr = st.pn;  // prefetched priority of the new head
+      const int o2 = op + 2;  // and the one after it, off the critical path
+      if (st.nx + 1 < pj) st.pn = o2 == ovp ? ovv : (int)prio[o2];
     }
     st.span = done > st.span ? done : st.span;
   }
@@ -745,6 +744,7 @@ __device__ __forceinline__ JspWarp jsp_warp_start(const JspView& J, const G* pri
   st.nx = st.jf = st.mfr = st.span = st.step = 0;
   const int op0 = wl * J.per_job;
   st.pr = wl < J.n_jobs ? (op0 == ovp ? ovv : (int)prio[op0]) : 0;
+  st.pn = wl < J.n_jobs && J.per_job > 1 ? (op0 + 1 == ovp ? ovv : (int)prio[op0 + 1]) : 0;
   return st;
 }
 
