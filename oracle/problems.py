@@ -376,3 +376,62 @@ class Custom(Problem):
 
     def matrices(self):
         return list(self._mats)
+
+
+class Assignment(Problem):
+    """builtins.py:293-319."""
+
+    def __init__(self, cost):
+        self.cost = np.asarray(cost, dtype=np.float64)
+        self.n = self.cost.shape[0]
+        self.spec = Spec(PERM, 1, self.n, self.n, SINGLE)
+
+    def objective(self, i, sol):
+        return float(self.cost[np.arange(self.n), sol.row(0)].sum())
+
+    def matrices(self):
+        return [self.cost]
+
+
+class GraphColoring(Problem):
+    """builtins.py:322-350."""
+
+    def __init__(self, num_vertices, edges, num_colors):
+        self.n = int(num_vertices)
+        self.eu = np.array([u for u, _ in edges], dtype=np.int64)
+        self.ev = np.array([v for _, v in edges], dtype=np.int64)
+        self.spec = Spec(INTEGER, 1, self.n, self.n, SINGLE, lb=0, ub=int(num_colors) - 1)
+
+    def objective(self, i, sol):
+        c = sol.row(0)
+        return float(np.count_nonzero(c[self.eu] == c[self.ev]))
+
+
+class BinPacking(Problem):
+    """builtins.py:353-373."""
+
+    def __init__(self, sizes, capacity):
+        self.sizes = np.asarray(sizes, dtype=np.float64)
+        self.capacity = float(capacity)
+        self.n = len(self.sizes)
+        self.spec = Spec(INTEGER, 1, self.n, self.n, SINGLE, lb=0, ub=self.n - 1)
+
+    def objective(self, i, sol):
+        return float(len(np.unique(sol.row(0))))
+
+    def penalty(self, sol):
+        loads = np.bincount(sol.row(0), weights=self.sizes, minlength=self.n)
+        return float(np.maximum(loads - self.capacity, 0.0).sum())
+
+
+class LoadBalancing(Problem):
+    """builtins.py:376-394."""
+
+    def __init__(self, durations, num_machines):
+        self.d = np.asarray(durations, dtype=np.float64)
+        self.m = int(num_machines)
+        self.n = len(self.d)
+        self.spec = Spec(INTEGER, 1, self.n, self.n, SINGLE, lb=0, ub=self.m - 1)
+
+    def objective(self, i, sol):
+        return float(np.bincount(sol.row(0), weights=self.d, minlength=self.m).max())

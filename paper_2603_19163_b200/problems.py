@@ -26,7 +26,8 @@ from .operators import (SEQ_FLIP, SEQ_INSERT, SEQ_OR_OPT, SEQ_RANDOM_RESET, SEQ_
 BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph_coloring",
                  "bin_packing", "load_balancing", "jsp_int", "jsp_perm", "schedule_binary",
                  "vrp_priority", "vrp_nonlinear")
-DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int", "vrptw", "cvrp")
+DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int", "vrptw", "cvrp", "assignment",
+                   "graph_coloring", "bin_packing", "load_balancing")
 
 
 @dataclass
@@ -428,6 +429,21 @@ def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
         return VrptwProblem(instance.distance_matrix, instance.demands, instance.capacity,
                             instance.vehicles, instance.ready_times, instance.due_times,
                             instance.service_times, **_routing_kwargs(instance))
+    if name == "assignment":
+        _need(instance, "cost_matrix")
+        return AssignmentProblem(instance.cost_matrix)
+    if name == "graph_coloring":
+        _need(instance, "edges", "num_colors")
+        n = instance.meta.get("num_vertices")
+        if n is None:
+            n = 1 + max(max(u, v) for u, v in instance.edges)
+        return GraphColoringProblem(n, instance.edges, instance.num_colors)
+    if name == "bin_packing":
+        _need(instance, "item_sizes", "bin_capacity")
+        return BinPackingProblem(instance.item_sizes, instance.bin_capacity)
+    if name == "load_balancing":
+        _need(instance, "durations", "num_machines")
+        return LoadBalancingProblem(instance.durations, instance.num_machines)
     raise NotImplementedError(
         f"problem {name!r} has no B200 device path in this build "
         f"(device problems: {', '.join(DEVICE_PROBLEMS)})")
@@ -519,3 +535,107 @@ class CudaProblem(ProblemDefinition):
         self._handle = h
         self._handle_device = device
         return h
+
+
+# ---- further reference built-ins as NVRTC objectives (builtins.py:293-394) ------------
+# Each snippet restates the reference objective with its arithmetic order
+# (numpy pairwise sums where the reference sums an array, sequential per-bin
+# accumulation where it uses np.bincount), so integer-valued instances match
+# bit-for-bit and float instances within rounding of the same operation order.
+
+_PAIRWISE_COST = """
+  struct F {
+    const double* c; const Sol* s; int n;
+    __device__ double operator()(int i) const { return c[i * n + (*s)[i]]; }
+  } f{data.cost, &sol, sol.n};
+  return go::np_pairwise(f, 0, sol.n);
+"""
+
+_COLOR_CONFLICTS = """
+  int k = 0;
+  for (int e = 0; e < data.eu_len; ++e) k += sol[(int)data.eu[e]] == sol[(int)data.ev[e]];
+  return (double)k;
+"""
+
+_BINS_USED = """
+  int used = 0;  // len(np.unique(row))
+  for (int b = 0; b < sol.n; ++b) {
+    bool any = false;
+    for (int i = 0; i < sol.n && !any; ++i) any = sol[i] == b;
+    used += any;
+  }
+  return (double)used;
+"""
+_BIN_OVERFLOW = """
+  struct F {  // max(bincount(row, sizes)[b] - cap, 0), bins summed pairwise
+    const double* w; const Sol* s; double cap;
+    __device__ double operator()(int b) const {
+      double load = 0.0;
+      for (int i = 0; i < s->n; ++i) if ((*s)[i] == b) load = __dadd_rn(load, w[i]);
+      const double o = __dsub_rn(load, cap);
+      return o > 0.0 ? o : 0.0;
+    }
+  } f{data.sizes, &sol, data.cap[0]};
+  return go::np_pairwise(f, 0, sol.n);
+"""
+
+_MAKESPAN_LOADS = """
+  double mx = 0.0;  // bincount(row, durations, minlength=M).max()
+  for (int m = 0; m < (int)data.machines[0]; ++m) {
+    double load = 0.0;
+    for (int i = 0; i < sol.n; ++i) if (sol[i] == m) load = __dadd_rn(load, data.dur[i]);
+    mx = (m == 0 || load > mx) ? load : mx;
+  }
+  return mx;
+"""
+
+
+class AssignmentProblem(CudaProblem):
+    """builtins.py:293-319: Σ_i cost[i, perm[i]] (numpy pairwise)."""
+
+    def __init__(self, cost):
+        cost = np.asarray(cost, dtype=np.float64)
+        if cost.ndim != 2 or cost.shape[0] != cost.shape[1]:
+            raise ValueError("assignment cost matrix must be square")
+        super().__init__("permutation", cost.shape[0], _PAIRWISE_COST, data={"cost": cost},
+                         name="total_cost", init_matrices=[cost])
+
+
+class GraphColoringProblem(CudaProblem):
+    """builtins.py:322-350: monochromatic edges under a fixed palette."""
+
+    def __init__(self, num_vertices, edges, num_colors):
+        n = int(num_vertices)
+        edges = [(int(u), int(v)) for u, v in edges]
+        for u, v in edges:
+            if not (0 <= u < n and 0 <= v < n):
+                raise ValueError(f"edge ({u}, {v}) outside vertex range")
+        self.edges = edges
+        super().__init__("integer", n, _COLOR_CONFLICTS,
+                         data={"eu": [u for u, _ in edges] or [0.0],
+                               "ev": [v for _, v in edges] or [0.0]},
+                         lb=0, ub=int(num_colors) - 1, name="conflicts")
+        if not edges:  # no edges: zero conflicts
+            self.compute_obj_src = "return 0.0;"
+
+
+class BinPackingProblem(CudaProblem):
+    """builtins.py:353-373: bins used; penalty = Σ max(load - capacity, 0)."""
+
+    def __init__(self, item_sizes, bin_capacity):
+        sizes = np.asarray(item_sizes, dtype=np.float64)
+        n = len(sizes)
+        super().__init__("integer", n, _BINS_USED, _BIN_OVERFLOW,
+                         data={"sizes": sizes, "cap": [float(bin_capacity)]},
+                         lb=0, ub=n - 1, name="bins_used")
+
+
+class LoadBalancingProblem(CudaProblem):
+    """builtins.py:376-394: makespan of bincount(assignment, durations)."""
+
+    def __init__(self, durations, num_machines):
+        d = np.asarray(durations, dtype=np.float64)
+        m = int(num_machines)
+        super().__init__("integer", len(d), _MAKESPAN_LOADS,
+                         data={"dur": d, "machines": [float(m)]}, lb=0, ub=m - 1,
+                         name="makespan")

@@ -1,0 +1,85 @@
+"""Goldens for the further single-row built-ins (assignment, graph colouring,
+bin packing, load balancing; builtins.py:293-394) from the UNMODIFIED
+reference (build container only).
+
+    PYTHONPATH=/root/repo python tests/golden/make_golden_extra.py
+
+Writes tests/golden/golden_extra.json: instances, objective / penalty of
+seeded random solutions, and small whole-run trajectories (best, history,
+final weights) that the oracle must reproduce in MT mode.
+"""
+
+from __future__ import annotations
+
+import json
+import random
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+
+import genopt as G  # noqa: E402
+from genopt.engine import random_solution  # noqa: E402
+
+OUT = Path(__file__).with_name("golden_extra.json")
+
+
+def instances():
+    rng = np.random.default_rng(77)
+    n = 40
+    pts = rng.integers(0, 40, size=(60, 2))
+    edges = sorted({(int(min(a, b)), int(max(a, b))) for a, b in pts if a != b})
+    return {
+        "assign40": ("assignment", {"cost_matrix": rng.integers(1, 100, size=(n, n)).tolist()}),
+        "color40": ("graph_coloring", {"edges": edges, "num_colors": 4,
+                                       "meta": {"num_vertices": 40}}),
+        "binpack30": ("bin_packing", {"item_sizes": rng.integers(2, 9, size=30).tolist(),
+                                      "bin_capacity": 10.0}),
+        "loadbal40": ("load_balancing", {"durations": rng.integers(1, 30, size=40).tolist(),
+                                         "num_machines": 5}),
+    }
+
+
+def build(name, payload):
+    kw = dict(payload)
+    meta = kw.pop("meta", {})
+    for k in ("cost_matrix", "item_sizes", "durations"):
+        if k in kw:
+            kw[k] = np.asarray(kw[k], dtype=np.float64)
+    return G.builtin_problem(name, G.InstanceData(meta=meta, **kw))
+
+
+def main():
+    out = {"generator": "tests/golden/make_golden_extra.py", "instances": {}, "evaluate": {},
+           "runs": {}}
+    for key, (name, payload) in instances().items():
+        out["instances"][key] = {"problem": name, "payload": payload}
+        p = build(name, payload)
+        rows = []
+        for k in range(8):
+            s = random_solution(p.config(), random.Random(500 + k))
+            obj, pen = G.evaluate(p, s)
+            rows.append({"data": [[int(x) for x in s.row(0)]], "obj": [float(o) for o in obj],
+                         "pen": float(pen)})
+        out["evaluate"][key] = rows
+        r = G.run(p, G.EngineConfig(population=6, team_size=16, max_generations=25, seed=11,
+                                    record_history=True))
+        out["runs"][key] = {
+            "config": {"population": 6, "team_size": 16, "max_generations": 25, "seed": 11},
+            "best": {"data": [[int(x) for x in r.best.row(0)]]},
+            "objectives": [float(x) for x in r.objectives], "penalty": float(r.penalty),
+            "history": r.history["best_phi"],
+            "weights": [float(e["weight"]) for e in r.final_weights["sequences"]],
+            "ids": [e["id"] for e in r.final_weights["sequences"]],
+            "k_weights": list(r.final_weights["k_steps"]),
+        }
+        print(key, r.objectives, r.penalty, flush=True)
+    OUT.write_text(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

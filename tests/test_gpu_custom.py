@@ -160,3 +160,24 @@ def test_solve_custom_api_and_compile_errors():
     with pytest.raises(N.NativeError) as e:
         bad.device_handle(0)
     assert e.value.status == N.GO_E_COMPILE and "undefined_symbol" in str(e.value)
+
+
+@pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40"])
+def test_extra_builtins_on_device(key):
+    """Reference built-ins restated as NVRTC objectives: device evaluation equals
+    the reference goldens; whole runs equal the oracle in Philox mode."""
+    from tests.extra_problems import GOLD, oracle_problem, product_problem
+    prob, ref = product_problem(key), oracle_problem(key)
+    rows = GOLD["evaluate"][key]
+    sols = [G.Solution(np.array(r["data"]), [len(r["data"][0])], 1) for r in rows]
+    obj, pen = G.problems.device_evaluate(prob, sols)
+    for o, p, r in zip(obj[:, 0], pen, rows):
+        assert [o] == r["obj"] and p == r["pen"]
+    res = G.run(prob, G.EngineConfig(population=4, team_size=32, max_generations=15, seed=3,
+                                     record_history=True))
+    out = OE.run(ref, OE.RunCfg(population=4, team_size=32, max_generations=15, seed=3,
+                                record_history=True, allowed_ops=prob.device_sequences()),
+                 device_stream="philox")
+    assert res.history["best_phi"] == out.history["best_phi"]
+    assert [s.row(0).tolist() for s in res.population] == \
+        [s.row(0).tolist() for s in out.population]

@@ -174,3 +174,24 @@ def test_multiobjective_run_matches_reference(key):
     assert out.history["best_phi"] == g["history"]
     assert [float(w) for w in out.weights] == g["weights"]
     assert list(out.k_weights) == g["k_weights"]
+
+
+@pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40"])
+def test_extra_builtins_match_reference(key):
+    """assignment / graph colouring / bin packing / load balancing
+    (builtins.py:293-394): evaluations and a whole run == reference."""
+    from tests.extra_problems import GOLD, oracle_problem
+    prob = oracle_problem(key)
+    for row in GOLD["evaluate"][key]:
+        s = P.Sol(np.array(row["data"]), [len(row["data"][0])], 1)
+        P.evaluate(prob, s)
+        assert [float(s.obj[0])] == row["obj"] and s.pen == row["pen"]
+    g = GOLD["runs"][key]
+    c = g["config"]
+    out = E.run(prob, E.RunCfg(population=c["population"], team_size=c["team_size"],
+                               max_generations=c["max_generations"], seed=c["seed"],
+                               record_history=True))
+    assert sol_rows(out.best) == g["best"]["data"]
+    assert out.objectives == g["objectives"] and out.penalty == g["penalty"]
+    assert out.history["best_phi"] == g["history"]
+    assert [float(w) for w in out.weights] == g["weights"]
