@@ -42,7 +42,9 @@ enum go_kind {
   GO_JSP_INT = 3,   /* builtins.py:408-456 */
   GO_KNAPSACK = 4,  /* builtins.py:240-262 */
   GO_CVRP = 5,      /* builtins.py:80-152 */
-  GO_USER = 6       /* NVRTC objective (go_problem_create_user) */
+  GO_USER = 6,      /* NVRTC objective (go_problem_create_user) */
+  GO_VRP_PRIORITY = 7,   /* builtins.py:193-210 (CVRP + precedence penalty) */
+  GO_VRP_NONLINEAR = 8   /* builtins.py:213-237 (load-dependent edge cost) */
 };
 
 /* migration strategies (engine.py:483-521, :731-733) */
@@ -89,6 +91,7 @@ typedef struct go_problem_desc {
   int32_t lb, ub;        /* integer encoding bounds */
   int32_t n_obj;         /* routing: 1 or 2 objectives (builtins.py:80-116); 0 = 1 */
   int32_t obj_kind[2];   /* routing objective i: 0 "distance", 1 "vehicles" */
+  const double* priorities; /* GO_VRP_PRIORITY: n customer priorities */
 } go_problem_desc;
 
 /* A user-defined single-row problem whose objective and penalty are CUDA

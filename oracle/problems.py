@@ -209,6 +209,44 @@ class Vrptw(Routing):
             + self.service.nbytes
 
 
+class PriorityVrp(Routing):
+    """builtins.py:193-210."""
+
+    def __init__(self, dist, demands, capacity, vehicles, priorities, **mo):
+        super().__init__(dist, demands, capacity, vehicles, **mo)
+        self.prio = np.asarray(priorities, dtype=np.float64)
+
+    def penalty(self, sol):
+        v = 0
+        for r in range(sol.d1):
+            pr = self.prio[sol.row(r)]
+            for p in range(len(pr)):
+                v += int(np.count_nonzero(pr[p + 1:] > pr[p]))
+        return self.load_excess(sol) + v
+
+
+class NonlinearVrp(Routing):
+    """builtins.py:213-237."""
+
+    def objective(self, i, sol):
+        if self.names[i] == "vehicles":
+            return float(np.count_nonzero(sol.sizes))
+        total = 0.0
+        for r in range(sol.d1):
+            route = sol.row(r)
+            if len(route) == 0:
+                continue
+            load = 0.0
+            prev = 0
+            for c in route:
+                node = c + 1
+                total += self.dist[prev, node] * (1.0 + 0.3 * (load / self.capacity) ** 2)
+                load += self.demands[c]
+                prev = node
+            total += self.dist[prev, 0] * (1.0 + 0.3 * (load / self.capacity) ** 2)
+        return float(total)
+
+
 class Knapsack(Problem):
     """builtins.py:240-262 (maximise value, penalty = weight excess)."""
 

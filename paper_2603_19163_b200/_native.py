@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libcugenopt.so"
 
 GO_OK, GO_E_INVALID, GO_E_CUDA, GO_E_UNSUPPORTED, GO_E_COMPILE, GO_E_NODEVICE = 0, -1, -2, -3, -4, -5
 GO_TSP, GO_VRPTW, GO_QAP, GO_JSP_INT, GO_KNAPSACK, GO_CVRP, GO_USER = range(7)
+GO_VRP_PRIORITY, GO_VRP_NONLINEAR = 7, 8
 ENC_PERM, ENC_BINARY, ENC_INTEGER = range(3)
 MOVE_NONE, MOVE_SWAP, MOVE_REVERSE, MOVE_SEGMENT = range(4)
 MOVE_THREE_OPT = 8  # + variant 0..6
@@ -55,7 +56,7 @@ class ProblemDesc(C.Structure):
                 ("capacity", C.c_double), ("n_jobs", C.c_int32), ("n_machines", C.c_int32),
                 ("ops_per_job", C.c_int32), ("jsp_machine", _PI), ("jsp_duration", _PI),
                 ("lb", C.c_int32), ("ub", C.c_int32), ("n_obj", C.c_int32),
-                ("obj_kind", C.c_int32 * 2)]
+                ("obj_kind", C.c_int32 * 2), ("priorities", _PD)]
 
 
 class UserProblemDesc(C.Structure):  # go_user_problem_desc

@@ -190,6 +190,7 @@ struct go_problem {
   DeviceInfo dev;
   // routing objectives (n_obj 1 or 2; kinds 0 distance, 1 vehicles)
   int n_obj = 1, okind0 = 0, okind1 = 1;
+  int pvar = 0;  // partition variant (RowArgs::pvar)
   // user problems (RK_USER): NVRTC objective module, encoding
   gohost::JitModule user_mod;
   int enc = 0;
@@ -287,7 +288,8 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
 int go_problem_create(const go_problem_desc* d, int device, go_problem** out) {
   if (!d || !out) return fail(GO_E_INVALID, "null argument");
   if (d->kind == GO_QAP || d->kind == GO_KNAPSACK || d->kind == GO_JSP_INT ||
-      d->kind == GO_VRPTW || d->kind == GO_CVRP)
+      d->kind == GO_VRPTW || d->kind == GO_CVRP || d->kind == GO_VRP_PRIORITY ||
+      d->kind == GO_VRP_NONLINEAR)
     return create_row_problem(d, device, out);
   if (d->kind != GO_TSP)
     return fail(GO_E_UNSUPPORTED, "problem kind " + std::to_string(d->kind) +
@@ -405,7 +407,8 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
     p->row_kind = go::RK_KNAP;
     p->gsize = 1;
     p->ub = 1;
-  } else if (d->kind == GO_VRPTW || d->kind == GO_CVRP) {  // builtins.py:80-190
+  } else if (d->kind == GO_VRPTW || d->kind == GO_CVRP || d->kind == GO_VRP_PRIORITY ||
+             d->kind == GO_VRP_NONLINEAR) {  // builtins.py:80-237
     const int n = d->n, v = d->d1;
     if (n < 1 || n > 30000 || v < 1 || v > 2000 || !d->dist || !d->demands)
       return fail(GO_E_INVALID, "routing needs n customers, vehicles, dist (n+1)^2, demands");
@@ -423,6 +426,11 @@ static int create_row_problem(const go_problem_desc* d, int device, go_problem**
       memcpy(img.data() + p->off2, d->ready, n1 * 8);
       memcpy(img.data() + p->off3, d->due, n1 * 8);
       memcpy(img.data() + p->off4, d->service, n1 * 8);
+    }
+    p->pvar = d->kind == GO_VRP_PRIORITY ? 1 : (d->kind == GO_VRP_NONLINEAR ? 2 : 0);
+    if (p->pvar == 1) {  // priorities in the (unused) ready-time slot
+      if (!d->priorities) return fail(GO_E_INVALID, "vrp_priority needs priorities");
+      memcpy(img.data() + p->off2, d->priorities, (size_t)n * 8);
     }
     p->capacity = d->capacity;
     p->tw = tw;
@@ -637,6 +645,7 @@ go::RowArgs row_args(const go_problem* p) {
   x.okind0 = p->okind0;
   x.okind1 = p->okind1;
   x.mo.m = p->n_obj;
+  x.pvar = p->pvar;
   return x;
 }
 

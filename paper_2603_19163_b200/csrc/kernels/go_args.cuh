@@ -106,6 +106,8 @@ struct RowArgs {
   int okind0, okind1;
   double w2;
   MoCmp mo;
+  int pvar;              // partition variant: 0 plain, 1 vrp_priority (priorities at off2), 2 vrp_nonlinear
+  int pad_v;
 };
 
 struct EpilogueArgs {

@@ -851,78 +851,6 @@ __device__ void team_gr_jsp(const JspView& J, G* row, const GrShared& g, int* sc
   }
 }
 
-// a route of a compact partition row with one value virtually inserted
-struct RouteIns {
-  const short* base;
-  int ins, v;  // ins < 0: no insertion
-  __device__ __forceinline__ int operator[](int q) const {
-    return ins < 0 || q < ins ? base[q] : (q == ins ? v : base[q - 1]);
-  }
-};
-struct EdgeV {
-  const double* d;
-  RouteIns r;
-  int n1;
-  __device__ __forceinline__ double operator()(int i) const {
-    return d[(r[i] + 1) * n1 + r[i + 1] + 1];
-  }
-};
-struct DemV {
-  const double* dem;
-  RouteIns r;
-  __device__ __forceinline__ double operator()(int i) const { return dem[r[i]]; }
-};
-
-// part_eval (go_part.cuh) of the row with v inserted at (ri, pi): the same
-// arithmetic in the same order, element access through RouteIns
-__device__ __forceinline__ void part_eval_ins(const PartView& v, const short* cells, const short* sz,
-                                              int ri, int pi, int val, double& distance,
-                                              double& penalty, int& veh) {
-  const int n1 = v.n + 1;
-  veh = 0;
-  for (int r = 0; r < v.d1; ++r) veh += (sz[r] + (r == ri)) > 0;
-  PySum dsum;
-  dsum.init();
-  double cap_pen = 0.0, late = 0.0;
-  int at = 0;
-  for (int r = 0; r < v.d1; ++r) {
-    const int len0 = sz[r];
-    RouteIns route{cells + at, r == ri ? pi : -1, val};
-    const int len = len0 + (r == ri);
-    double rd = 0.0;
-    if (len > 0) {
-      rd = __dadd_rn(v.dist[route[0] + 1], v.dist[(route[len - 1] + 1) * n1]);
-      if (len > 1) {
-        EdgeV e{v.dist, route, n1};
-        rd = __dadd_rn(rd, np_pairwise(e, 0, len - 1));
-      }
-    }
-    dsum.add(rd);
-    DemV dm{v.demand, route};
-    const double load = np_pairwise(dm, 0, len);
-    const double over = __dsub_rn(load, v.cap);
-    cap_pen = __dadd_rn(cap_pen, over > 0.0 ? over : 0.0);
-    if (v.tw && len > 0) {
-      double t = v.ready[0];
-      int prev = 0;
-      for (int q = 0; q < len; ++q) {
-        const int node = route[q] + 1;
-        const double arr0 = __dadd_rn(t, v.dist[prev * n1 + node]);
-        const double arrival = v.ready[node] >= arr0 ? v.ready[node] : arr0;
-        const double lt = __dsub_rn(arrival, v.due[node]);
-        late = __dadd_rn(late, lt > 0.0 ? lt : 0.0);
-        t = __dadd_rn(arrival, v.service[node]);
-        prev = node;
-      }
-      const double back = __dsub_rn(__dadd_rn(t, v.dist[prev * n1]), v.due[0]);
-      late = __dadd_rn(late, back > 0.0 ? back : 0.0);
-    }
-    at += len0;
-  }
-  distance = dsum.result();
-  penalty = v.tw ? __dadd_rn(cap_pen, late) : cap_pen;
-}
-
 // Incremental trials for partitions.  A trial inserts v into one route r*;
 // part_eval accumulates routes in order (Neumaier distance sum, capacity and
 // lateness running sums), so the state after routes 0..r*-1 and the
@@ -1131,7 +1059,7 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       c.remove(r0, p0);
     }
     PartCache pc;
-    const bool cached = 32 + PartCache::doubles(d1, n_cells) <= 5 * TS;
+    const bool cached = pv.variant == 0 && 32 + PartCache::doubles(d1, n_cells) <= 5 * TS;
     pc.bind(sbuf + 32, d1);
     if (cached) part_cache_build(pv, cells, sz, pc, lane, team, TS);
     team_bar(team, TS);
@@ -1286,6 +1214,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     pv.d2 = X.d2;
     pv.cap = X.capacity;
     pv.tw = X.tw;
+    pv.variant = X.pvar;
+    pv.prio = (const double*)(inst + X.off2);
   } else if (KIND == RK_QAP) {
     qv.f = (const E*)inst;
     qv.d = (const E*)(inst + X.off1);

@@ -23,6 +23,8 @@ struct PartView {  // instance (float64 arrays, customer c at matrix index c + 1
   int n, d1, d2;
   double cap;
   int tw;  // 1: VRPTW (lateness), 0: CVRP
+  int variant;         // 0 plain, 1 vrp_priority (precedence penalty), 2 vrp_nonlinear
+  const double* prio;  // vrp_priority: priority per customer
 };
 
 struct PartCtx {
@@ -394,53 +396,82 @@ struct PySum {
   }
 };
 
-struct EdgeF {
+// a route of a compact partition row with one value virtually inserted
+struct RouteIns {
+  const short* base;
+  int ins, v;  // ins < 0: no insertion
+  __device__ __forceinline__ int operator[](int q) const {
+    return ins < 0 || q < ins ? base[q] : (q == ins ? v : base[q - 1]);
+  }
+};
+struct EdgeV {
   const double* d;
-  const short* cells;
+  RouteIns r;
   int n1;
   __device__ __forceinline__ double operator()(int i) const {
-    return d[(cells[i] + 1) * n1 + cells[i + 1] + 1];
+    return d[(r[i] + 1) * n1 + r[i + 1] + 1];
   }
 };
-struct DemF {
+struct DemV {
   const double* dem;
-  const short* cells;
-  __device__ __forceinline__ double operator()(int i) const { return dem[cells[i]]; }
+  RouteIns r;
+  __device__ __forceinline__ double operator()(int i) const { return dem[r[i]]; }
 };
 
-// Φ parts of a compact partition row: distance objective and penalty
-// (+ the "vehicles" objective, builtins.py:133: non-empty routes)
-__device__ __forceinline__ void part_eval(const PartView& v, const short* cells, const short* sz,
-                                          double& distance, double& penalty, int* veh = nullptr) {
-  if (veh) {
-    int c = 0;
-    for (int r = 0; r < v.d1; ++r) c += sz[r] > 0;
-    *veh = c;
-  }
+// part_eval (go_part.cuh) of the row with v inserted at (ri, pi): the same
+// arithmetic in the same order, element access through RouteIns
+__device__ __forceinline__ void part_eval_ins(const PartView& v, const short* cells, const short* sz,
+                                              int ri, int pi, int val, double& distance,
+                                              double& penalty, int& veh) {
   const int n1 = v.n + 1;
+  veh = 0;
+  for (int r = 0; r < v.d1; ++r) veh += (sz[r] + (r == ri)) > 0;
   PySum dsum;
   dsum.init();
   double cap_pen = 0.0, late = 0.0;
   int at = 0;
+  double nl_total = 0.0;  // vrp_nonlinear: one running sum over every edge
+  long long viol = 0;     // vrp_priority: precedence violations
   for (int r = 0; r < v.d1; ++r) {
-    const int len = sz[r];
-    const short* route = cells + at;
-    // route_distance (builtins.py:119-126)
-    double rd = 0.0;
-    if (len > 0) {
-      rd = __dadd_rn(v.dist[route[0] + 1], v.dist[(route[len - 1] + 1) * n1]);
-      if (len > 1) {
-        EdgeF e{v.dist, route, n1};
-        rd = __dadd_rn(rd, np_pairwise(e, 0, len - 1));
+    const int len0 = sz[r];
+    RouteIns route{cells + at, r == ri ? pi : -1, val};
+    const int len = len0 + (r == ri);
+    if (v.variant == 2) {  // NonlinearVrpProblem.compute_objective (builtins.py:219-237)
+      if (len > 0) {
+        double load = 0.0;
+        int prev = 0;
+        for (int q = 0; q < len; ++q) {
+          const int c = route[q], node = c + 1;
+          const double x = __ddiv_rn(load, v.cap);
+          const double f = __dadd_rn(1.0, __dmul_rn(0.3, __dmul_rn(x, x)));
+          nl_total = __dadd_rn(nl_total, __dmul_rn(v.dist[prev * n1 + node], f));
+          load = __dadd_rn(load, v.demand[c]);
+          prev = node;
+        }
+        const double x = __ddiv_rn(load, v.cap);
+        const double f = __dadd_rn(1.0, __dmul_rn(0.3, __dmul_rn(x, x)));
+        nl_total = __dadd_rn(nl_total, __dmul_rn(v.dist[prev * n1], f));
       }
+    } else {
+      double rd = 0.0;
+      if (len > 0) {
+        rd = __dadd_rn(v.dist[route[0] + 1], v.dist[(route[len - 1] + 1) * n1]);
+        if (len > 1) {
+          EdgeV e{v.dist, route, n1};
+          rd = __dadd_rn(rd, np_pairwise(e, 0, len - 1));
+        }
+      }
+      dsum.add(rd);
     }
-    dsum.add(rd);
-    // capacity (builtins.py:137-142)
-    DemF dm{v.demand, route};
+    if (v.variant == 1)  // PriorityVrpProblem.compute_penalty (builtins.py:203-210)
+      for (int a = 0; a < len; ++a) {
+        const double pa = v.prio[route[a]];
+        for (int b = a + 1; b < len; ++b) viol += v.prio[route[b]] > pa;
+      }
+    DemV dm{v.demand, route};
     const double load = np_pairwise(dm, 0, len);
     const double over = __dsub_rn(load, v.cap);
     cap_pen = __dadd_rn(cap_pen, over > 0.0 ? over : 0.0);
-    // lateness (builtins.py:168-184)
     if (v.tw && len > 0) {
       double t = v.ready[0];
       int prev = 0;
@@ -456,10 +487,20 @@ __device__ __forceinline__ void part_eval(const PartView& v, const short* cells,
       const double back = __dsub_rn(__dadd_rn(t, v.dist[prev * n1]), v.due[0]);
       late = __dadd_rn(late, back > 0.0 ? back : 0.0);
     }
-    at += len;
+    at += len0;
   }
-  distance = dsum.result();
+  distance = v.variant == 2 ? nl_total : dsum.result();
   penalty = v.tw ? __dadd_rn(cap_pen, late) : cap_pen;
+  if (v.variant == 1) penalty = __dadd_rn(penalty, (double)viol);
+}
+
+// Φ parts of a compact partition row: distance objective and penalty
+// (+ the "vehicles" objective, builtins.py:133: non-empty routes)
+__device__ __forceinline__ void part_eval(const PartView& v, const short* cells, const short* sz,
+                                          double& distance, double& penalty, int* veh = nullptr) {
+  int vh;
+  part_eval_ins(v, cells, sz, -1, 0, 0, distance, penalty, vh);
+  if (veh) *veh = vh;
 }
 
 }  // namespace go

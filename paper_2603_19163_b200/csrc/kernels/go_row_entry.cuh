@@ -91,6 +91,8 @@ __device__ __forceinline__ void part_eval_entry(const void* inst, go::RowArgs x,
   v.d2 = x.d2;
   v.cap = x.capacity;
   v.tw = x.tw;
+  v.variant = x.pvar;
+  v.prio = (const double*)(b + x.off2);
   const short* row = genes + (size_t)blockIdx.x * (x.n_cells + x.d1);
   double d, p, o0, o1;
   int veh;

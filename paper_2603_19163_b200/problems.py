@@ -27,7 +27,8 @@ BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph
                  "bin_packing", "load_balancing", "jsp_int", "jsp_perm", "schedule_binary",
                  "vrp_priority", "vrp_nonlinear")
 DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int", "vrptw", "cvrp", "assignment",
-                   "graph_coloring", "bin_packing", "load_balancing")
+                   "graph_coloring", "bin_packing", "load_balancing", "vrp_priority",
+                   "vrp_nonlinear")
 
 
 @dataclass
@@ -387,6 +388,34 @@ class VrptwProblem(RoutingProblem):
             self.service.nbytes
 
 
+class PriorityVrpProblem(RoutingProblem):
+    """builtins.py:193-210: CVRP whose penalty adds, per route, the number of
+    (earlier, later) customer pairs where the later one has higher priority."""
+
+    _KIND = N.GO_VRP_PRIORITY
+
+    def __init__(self, dist, demands, capacity, vehicles, priorities, objectives=("distance",),
+                 comparison=None):
+        super().__init__(dist, demands, capacity, vehicles, objectives=objectives,
+                         comparison=comparison)
+        self.priorities = np.asarray(priorities, dtype=np.float64)
+        if len(self.priorities) != self.n:
+            raise ValueError("one priority per customer required")
+
+    def _native_desc(self):
+        desc, keep = super()._native_desc()
+        pr = N.f64(self.priorities)
+        desc.priorities = N.dptr(pr)
+        return desc, keep + (pr,)
+
+
+class NonlinearVrpProblem(RoutingProblem):
+    """builtins.py:213-237: edge cost d_ij * (1 + 0.3 (load / cap)^2), the load
+    being the demand collected before the edge."""
+
+    _KIND = N.GO_VRP_NONLINEAR
+
+
 def _routing_kwargs(instance: InstanceData) -> dict:
     kwargs = {}
     meta = instance.meta or {}
@@ -429,6 +458,15 @@ def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
         return VrptwProblem(instance.distance_matrix, instance.demands, instance.capacity,
                             instance.vehicles, instance.ready_times, instance.due_times,
                             instance.service_times, **_routing_kwargs(instance))
+    if name == "vrp_priority":
+        _need(instance, "distance_matrix", "demands", "capacity", "vehicles", "priorities")
+        return PriorityVrpProblem(instance.distance_matrix, instance.demands, instance.capacity,
+                                  instance.vehicles, instance.priorities,
+                                  **_routing_kwargs(instance))
+    if name == "vrp_nonlinear":
+        _need(instance, "distance_matrix", "demands", "capacity", "vehicles")
+        return NonlinearVrpProblem(instance.distance_matrix, instance.demands, instance.capacity,
+                                   instance.vehicles, **_routing_kwargs(instance))
     if name == "assignment":
         _need(instance, "cost_matrix")
         return AssignmentProblem(instance.cost_matrix)

@@ -10,9 +10,22 @@ from oracle import problems as OP
 GOLD = json.loads((Path(__file__).with_name("golden") / "golden_extra.json").read_text())
 
 
+def sol_rows(rows, d2):
+    """(data d1 x d2 zero-padded, sizes) from a list of active rows."""
+    data = np.zeros((len(rows), d2), dtype=np.int64)
+    for r, row in enumerate(rows):
+        data[r, :len(row)] = row
+    return data, np.array([len(row) for row in rows])
+
+
 def oracle_problem(key):
     g = GOLD["instances"][key]
     name, p = g["problem"], g["payload"]
+    if name in ("vrp_priority", "vrp_nonlinear"):
+        d = np.array(p["distance_matrix"], dtype=np.float64)
+        if name == "vrp_priority":
+            return OP.PriorityVrp(d, p["demands"], p["capacity"], p["vehicles"], p["priorities"])
+        return OP.NonlinearVrp(d, p["demands"], p["capacity"], p["vehicles"])
     if name == "assignment":
         return OP.Assignment(np.array(p["cost_matrix"], dtype=np.float64))
     if name == "graph_coloring":
@@ -27,7 +40,7 @@ def product_problem(key):
     g = GOLD["instances"][key]
     kw = dict(g["payload"])
     meta = kw.pop("meta", {})
-    for k in ("cost_matrix", "item_sizes", "durations"):
+    for k in ("cost_matrix", "item_sizes", "durations", "distance_matrix", "demands", "priorities"):
         if k in kw:
             kw[k] = np.asarray(kw[k], dtype=np.float64)
     return G.builtin_problem(g["problem"], G.InstanceData(meta=meta, **kw))

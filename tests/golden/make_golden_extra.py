@@ -41,13 +41,25 @@ def instances():
                                       "bin_capacity": 10.0}),
         "loadbal40": ("load_balancing", {"durations": rng.integers(1, 30, size=40).tolist(),
                                          "num_machines": 5}),
+        "vrpprio20": ("vrp_priority", routing(rng, 20, 5, priorities=True)),
+        "vrpnl20": ("vrp_nonlinear", routing(rng, 20, 5)),
     }
+
+
+def routing(rng, n, vehicles, priorities=False):
+    pts = rng.uniform(0, 100, size=(n + 1, 2))
+    d = np.rint(np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)))
+    out = {"distance_matrix": d.tolist(), "demands": rng.integers(1, 10, size=n).tolist(),
+           "capacity": 30.0, "vehicles": vehicles}
+    if priorities:
+        out["priorities"] = rng.integers(0, 3, size=n).tolist()
+    return out
 
 
 def build(name, payload):
     kw = dict(payload)
     meta = kw.pop("meta", {})
-    for k in ("cost_matrix", "item_sizes", "durations"):
+    for k in ("cost_matrix", "item_sizes", "durations", "distance_matrix", "demands", "priorities"):
         if k in kw:
             kw[k] = np.asarray(kw[k], dtype=np.float64)
     return G.builtin_problem(name, G.InstanceData(meta=meta, **kw))
@@ -63,14 +75,14 @@ def main():
         for k in range(8):
             s = random_solution(p.config(), random.Random(500 + k))
             obj, pen = G.evaluate(p, s)
-            rows.append({"data": [[int(x) for x in s.row(0)]], "obj": [float(o) for o in obj],
-                         "pen": float(pen)})
+            rows.append({"data": [[int(x) for x in s.row(r)] for r in range(s.d1)],
+                         "obj": [float(o) for o in obj], "pen": float(pen)})
         out["evaluate"][key] = rows
         r = G.run(p, G.EngineConfig(population=6, team_size=16, max_generations=25, seed=11,
                                     record_history=True))
         out["runs"][key] = {
             "config": {"population": 6, "team_size": 16, "max_generations": 25, "seed": 11},
-            "best": {"data": [[int(x) for x in r.best.row(0)]]},
+            "best": {"data": [[int(x) for x in r.best.row(q)] for q in range(r.best.d1)]},
             "objectives": [float(x) for x in r.objectives], "penalty": float(r.penalty),
             "history": r.history["best_phi"],
             "weights": [float(e["weight"]) for e in r.final_weights["sequences"]],

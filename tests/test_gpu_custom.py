@@ -145,8 +145,8 @@ def test_user_problem_guided_rebuild_dominant(name, ops):
     out = OE.run(ref, OE.RunCfg(population=3, team_size=16, max_generations=5, seed=9,
                                 record_history=True, allowed_ops=ops), device_stream="philox")
     assert res.history["best_phi"] == out.history["best_phi"]
-    assert [s.row(0).tolist() for s in res.population] == \
-        [s.row(0).tolist() for s in out.population]
+    assert [[s.row(r).tolist() for r in range(s.d1)] for s in res.population] == \
+        [[s.row(r).tolist() for r in range(s.d1)] for s in out.population]
 
 
 def test_solve_custom_api_and_compile_errors():
@@ -162,14 +162,16 @@ def test_solve_custom_api_and_compile_errors():
     assert e.value.status == N.GO_E_COMPILE and "undefined_symbol" in str(e.value)
 
 
-@pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40"])
+@pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40", "vrpprio20",
+                                 "vrpnl20"])
 def test_extra_builtins_on_device(key):
-    """Reference built-ins restated as NVRTC objectives: device evaluation equals
-    the reference goldens; whole runs equal the oracle in Philox mode."""
-    from tests.extra_problems import GOLD, oracle_problem, product_problem
+    """Further reference built-ins on the device (NVRTC objectives, partition
+    variants): device evaluation equals the reference goldens; whole runs equal
+    the oracle in Philox mode."""
+    from tests.extra_problems import GOLD, oracle_problem, product_problem, sol_rows
     prob, ref = product_problem(key), oracle_problem(key)
     rows = GOLD["evaluate"][key]
-    sols = [G.Solution(np.array(r["data"]), [len(r["data"][0])], 1) for r in rows]
+    sols = [G.Solution(*sol_rows(r["data"], ref.spec.d2), 1) for r in rows]
     obj, pen = G.problems.device_evaluate(prob, sols)
     for o, p, r in zip(obj[:, 0], pen, rows):
         assert [o] == r["obj"] and p == r["pen"]
@@ -179,5 +181,5 @@ def test_extra_builtins_on_device(key):
                                 record_history=True, allowed_ops=prob.device_sequences()),
                  device_stream="philox")
     assert res.history["best_phi"] == out.history["best_phi"]
-    assert [s.row(0).tolist() for s in res.population] == \
-        [s.row(0).tolist() for s in out.population]
+    assert [[s.row(r).tolist() for r in range(s.d1)] for s in res.population] == \
+        [[s.row(r).tolist() for r in range(s.d1)] for s in out.population]

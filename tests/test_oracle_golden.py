@@ -176,14 +176,15 @@ def test_multiobjective_run_matches_reference(key):
     assert list(out.k_weights) == g["k_weights"]
 
 
-@pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40"])
+@pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40", "vrpprio20",
+                                 "vrpnl20"])
 def test_extra_builtins_match_reference(key):
-    """assignment / graph colouring / bin packing / load balancing
-    (builtins.py:293-394): evaluations and a whole run == reference."""
-    from tests.extra_problems import GOLD, oracle_problem
+    """assignment / graph colouring / bin packing / load balancing / priority and
+    nonlinear VRP (builtins.py:193-394): evaluations and a whole run == reference."""
+    from tests.extra_problems import GOLD, oracle_problem, sol_rows as rows_of
     prob = oracle_problem(key)
     for row in GOLD["evaluate"][key]:
-        s = P.Sol(np.array(row["data"]), [len(row["data"][0])], 1)
+        s = P.Sol(*rows_of(row["data"], prob.spec.d2), 1)
         P.evaluate(prob, s)
         assert [float(s.obj[0])] == row["obj"] and s.pen == row["pen"]
     g = GOLD["runs"][key]
