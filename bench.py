@@ -272,6 +272,7 @@ def run_ours(args):
                                          custom_operators=ops, device=local,
                                          time_limit_seconds=args.gap_seconds,
                                          max_generations=10 ** 9, distributed=world > 1,
+                                         device_init=True,
                                          islands=G.IslandsConfig(count=world, migration="hybrid",
                                                                  interval=100)),
                     best_known=opt)
@@ -291,7 +292,7 @@ def run_ours(args):
                                         custom_operators=ops, device=local,
                                         time_limit_seconds=args.gap_seconds,
                                         target_objective=opt, max_generations=10 ** 9,
-                                        distributed=world > 1,
+                                        distributed=world > 1, device_init=True,
                                         islands=G.IslandsConfig(count=world, migration="hybrid",
                                                                 interval=100)),
                    best_known=opt)

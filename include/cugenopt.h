@@ -195,6 +195,22 @@ int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_
 /* evaluate(problem, sol) for m solutions (problems.py:77-94) */
 int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int m,
                   double* obj_out, double* pen_out);
+/* Device-side population initialisation (engine.py:327-360).
+ * Draws `count` random solutions on the device, solution i from the Philox
+ * stream mix64(seed, 2 = init stream, salt, i) with the reference's draw order
+ * (random.shuffle / randrange, engine.py:252-287); appends the `n_extra` host
+ * candidates (row/column-sum argsorts, init_candidates; genes[n_extra][d1*d2],
+ * sizes[n_extra][d1]); evaluates the pool on the device.  keep > 0 (single
+ * objective only): outputs the `keep` best in compare order (core.py:315-347,
+ * stable: equal solutions keep pool order), scalarised as
+ * obj_weight * (maximize ? -obj : obj); keep == 0: outputs the whole pool.
+ * Outputs: genes_out[k][d1*d2], sizes_out[k][d1], obj_out[k][n_obj], pen_out[k],
+ * index_out[k] = pool index (random draws first, then the extras). */
+int go_init_population(go_problem* p, int count, uint64_t seed, uint64_t salt,
+                       const int32_t* extra_genes, const int32_t* extra_sizes, int n_extra,
+                       int keep, int maximize, double obj_weight, int32_t* genes_out,
+                       int32_t* sizes_out, double* obj_out, double* pen_out,
+                       int32_t* index_out);
 /* acceptance_delta(cand, cur) (engine.py:225-246) for m solutions, each with
  * up to 3 chained primitive moves (`moves[m][3]`, unused = GO_MOVE_NONE);
  * writes the delta and the candidate genes (`cand_out[m][d1*d2]`). */

@@ -29,7 +29,7 @@ from .problems import (MAX, MIN, MULTI_FIXED, PARTITION, PERM, SINGLE, BINARY,
                        Sol, acceptance_delta, compare, evaluate, scalar_fitness,
                        validate)
 from .rng import (STREAM_ACCEPT, STREAM_INIT, STREAM_LANE, STREAM_MIGRATION,
-                  STREAM_PROBE, STREAMS, mt_stream)
+                  STREAM_PROBE, STREAMS, mt_stream, philox_stream)
 
 
 # -- construction -------------------------------------------------------------
@@ -96,7 +96,24 @@ def perm_to_sol(perm, spec) -> Sol:
 def init_population(problem, pop_size, oversample, rng):
     """engine.py:327-360 (single-objective branch)."""
     spec = problem.spec
-    pool = [random_solution(spec, rng) for _ in range(oversample * pop_size)]
+    return _init_from_pool(problem, pop_size,
+                           [random_solution(spec, rng) for _ in range(oversample * pop_size)])
+
+
+def init_population_philox(problem, pop_size, oversample, seed, salt=0):
+    """The GPU engine's device-side initialisation (EngineConfig.device_init,
+    csrc/kernels/go_init.cuh): random solution i is drawn, in the reference's
+    draw order (engine.py:252-287), from its own stream
+    philox_stream(seed, STREAM_INIT, salt, i); the heuristic candidates and the
+    selection are engine.py:327-360's."""
+    spec = problem.spec
+    pool = [random_solution(spec, philox_stream(seed, STREAM_INIT, salt, i))
+            for i in range(oversample * pop_size)]
+    return _init_from_pool(problem, pop_size, pool)
+
+
+def _init_from_pool(problem, pop_size, pool):
+    spec = problem.spec
     if spec.kind == PERM:
         for mat in problem.matrices():
             if mat.shape == (spec.n, spec.n):
@@ -343,6 +360,7 @@ class RunCfg:
     target_objective: float | None = None
     record_history: bool = False
     allowed_ops: tuple | None = None  # restrict build_registry
+    device_init: bool = False       # the GPU engine's Philox initialisation (init_population_philox)
 
 
 @dataclass
@@ -418,7 +436,9 @@ def run_single(problem, cfg: RunCfg, seed, best_known=None, device_stream="mt",
                                    cfg.working_set_bytes or working_set(problem),
                                    cfg.fast_budget_bytes)
     pop_size = max(pop_size, cfg.islands)
-    if initial_population is None:
+    if initial_population is None and cfg.device_init:
+        pop = init_population_philox(problem, pop_size, cfg.oversample_factor, seed)
+    elif initial_population is None:
         pop = init_population(problem, pop_size, cfg.oversample_factor,
                               mt_stream(seed, STREAM_INIT))
     else:

@@ -17,7 +17,8 @@ from .core import (ComparisonMode, Direction, Encoding, EncodingKind, Lexicograp
 from .demo_ops import demo_operator_set, tsp_delta_operators
 from .engine import (DeviceRun, EngineConfig, EvolverState, IslandsConfig, RunResult,
                      adaptive_population_size, b200_population_size, heuristic_candidates,
-                     initialize_population, random_solution, run, scalar_fitness)
+                     initialize_population, initialize_population_device, random_solution, run,
+                     scalar_fitness)
 from .operators import (CustomOperator, SequenceEntry, SequenceRegistry, build_registry,
                         lns_scope)
 from .problems import (BUILTIN_NAMES, CudaProblem, InstanceData, ProblemDefinition,
@@ -27,6 +28,7 @@ from .profiles import PRESETS, ProblemProfile, Scale, WeightPreset, apply_preset
 
 def solve_tsp(dist_matrix, time_limit=30.0, **kw) -> RunResult:
     """PAPER.md:850-856 `cugenopt.solve_tsp(dist_matrix, time_limit=30)`."""
+    kw.setdefault("device_init", True)  # the paper's API initialises on the GPU
     cfg = EngineConfig(time_limit_seconds=time_limit,
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
     return run(builtin_problem("tsp", InstanceData(distance_matrix=dist_matrix)), cfg)
@@ -34,6 +36,7 @@ def solve_tsp(dist_matrix, time_limit=30.0, **kw) -> RunResult:
 
 def solve_knapsack(weights, values, capacity, time_limit=30.0, **kw) -> RunResult:
     """PAPER.md:850-856 `cugenopt.solve_knapsack(weights, values, cap)`."""
+    kw.setdefault("device_init", True)  # the paper's API initialises on the GPU
     cfg = EngineConfig(time_limit_seconds=time_limit,
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
     return run(builtin_problem("knapsack", InstanceData(weights=weights, values=values,
@@ -54,6 +57,7 @@ def solve_custom(encoding, dim2, n=None, compute_obj=None, compute_penalty=None,
         raise ValueError("single-row custom problems need n == dim2")
     prob = CudaProblem(encoding, int(dim2), compute_obj, compute_penalty, data, lb=lb, ub=ub,
                        maximize=maximize)
+    kw.setdefault("device_init", True)  # the paper's API initialises on the GPU
     cfg = EngineConfig(time_limit_seconds=time_limit,
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
     return run(prob, cfg, best_known=best_known)

@@ -112,6 +112,8 @@ def _bind(lib):
         "go_problem_occupancy": ([V, C.c_int, C.c_int, _PI, _PI, _PI, P(C.c_int64)], C.c_int),
         "go_eval_batch": ([V, _PI, _PI, C.c_int, _PD, _PD], C.c_int),
         "go_delta_batch": ([V, _PI, _PI, C.c_int, P(Move), C.c_double, _PD, _PI], C.c_int),
+        "go_init_population": ([V, C.c_int, C.c_uint64, C.c_uint64, _PI, _PI, C.c_int, C.c_int,
+                                C.c_int, C.c_double, _PI, _PI, _PD, _PD, _PI], C.c_int),
         "go_problem_set_custom_ops": ([V, P(CustomOp), C.c_int, _PI, _PI, C.c_uint64, _PI,
                                        C.c_char_p, C.c_int], C.c_int),
         "go_jit_compile": ([C.c_int, P(CustomOp), C.c_int, C.c_char_p, C.c_int, C.c_char_p],

@@ -26,6 +26,7 @@
 #include "go_drv.h"
 #include "go_jit.h"
 #include "kernels/go_epilogue.cuh"
+#include "kernels/go_init.cuh"
 #include "kernels/go_islands.cuh"
 #include "kernels/go_row_entry.cuh"
 #include "kernels/go_tsp_entry.cuh"
@@ -649,6 +650,60 @@ go::RowArgs row_args(const go_problem* p) {
   return x;
 }
 
+// Scoped device allocations (freed on every return path).
+struct DevBufs {
+  std::vector<void*> v;
+  ~DevBufs() { for (void* q : v) cudaFree(q); }
+  template <class T> cudaError_t get(T** q, size_t bytes) {
+    cudaError_t e = cudaMalloc((void**)q, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) v.push_back(*q);
+    return e;
+  }
+};
+
+// Objectives [m][n_obj] and penalties [m] of m device rows (p->n shorts each,
+// the layout to_device_rows produces), on the legacy stream.
+int eval_device_rows(go_problem* p, const short* d_g, int m, double* d_o, double* d_p) {
+  const int n = p->n;
+  CK(cudaMemset(d_p, 0, (size_t)m * 8));
+  int nn = n;
+  if (p->family == 0) {
+    void* fn = p->elem == E_I16 ? (void*)go_eval_tsp_i16
+                                : (p->elem == E_I32 ? (void*)go_eval_tsp_i32 : (void*)go_eval_tsp_f64);
+    const void* inst = p->d_full;
+    void* args[] = {(void*)&inst, &nn, (void*)&d_g, &d_o};
+    CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
+    return GO_OK;
+  }
+  const void* inst = p->d_img;
+  unsigned off1 = p->off1;
+  if (p->row_kind == go::RK_QAP) {
+    void* fn = p->elem == E_I16 ? (void*)go_eval_qap_i16
+                                : (p->elem == E_I32 ? (void*)go_eval_qap_i32 : (void*)go_eval_qap_f64);
+    void* args[] = {(void*)&inst, &off1, &nn, (void*)&d_g, &d_o};
+    CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
+  } else if (p->row_kind == go::RK_PART) {
+    go::RowArgs x = row_args(p);
+    void* args[] = {(void*)&inst, &x, (void*)&d_g, &d_o, &d_p};
+    CK(cudaLaunchKernel((void*)go_eval_part, dim3(m), dim3(32), args, 0, 0));
+  } else if (p->row_kind == go::RK_KNAP) {
+    double cap = p->capacity;
+    void* args[] = {(void*)&inst, &off1, &nn, &cap, (void*)&d_g, &d_o, &d_p};
+    CK(cudaLaunchKernel((void*)go_eval_knap, dim3(m), dim3(128), args, 0, 0));
+  } else if (p->row_kind == go::RK_USER) {
+    int mm = m;
+    void* args[] = {(void*)&inst, &nn, &mm, (void*)&d_g, &d_o, &d_p};
+    CU(gohost::drv()->LaunchKernel(p->user_mod.probe, (unsigned)((m + 127) / 128), 1, 1, 128, 1,
+                                   1, 0, nullptr, args, nullptr));
+  } else {
+    int nj = p->n_jobs, pj = p->per_job, nmach = p->n_mach;
+    void* args[] = {(void*)&inst, &off1, &nj, &pj, &nmach, (void*)&d_g, &d_o};
+    CK(cudaLaunchKernel((void*)go_eval_jsp, dim3(m), dim3(32), args, (size_t)p->scratch_ints * 4, 0));
+  }
+  CK(cudaDeviceSynchronize());
+  return GO_OK;
+}
+
 // ---- row family helpers ----------------------------------------------------------
 void* row_kernel(const go_problem* p) {
   if (p->row_kind == go::RK_USER) return nullptr;  // JIT (p->user_mod.evolve)
@@ -823,71 +878,112 @@ int go_eval_batch(go_problem* p, const int32_t* genes, const int32_t* sizes, int
   if (!p || !genes || !obj_out || m < 0) return fail(GO_E_INVALID, "bad arguments");
   if (m == 0) return GO_OK;
   CK(cudaSetDevice(p->device));
-  const int n = p->n;
-  if (p->family == 1) {
-    std::vector<short> h;
-    to_device_rows(p, genes, sizes, m, h);
-    short* d_g = nullptr;
-    double *d_o = nullptr, *d_p = nullptr;
-    CK(cudaMalloc(&d_g, h.size() * 2));
-    CK(cudaMalloc(&d_o, (size_t)m * p->n_obj * 8));
-    CK(cudaMalloc(&d_p, (size_t)m * 8));
-    CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
-    CK(cudaMemset(d_p, 0, (size_t)m * 8));
-    const void* inst = p->d_img;
-    unsigned off1 = p->off1;
-    int nn = n;
-    if (p->row_kind == go::RK_QAP) {
-      void* fn = p->elem == E_I16 ? (void*)go_eval_qap_i16
-                                  : (p->elem == E_I32 ? (void*)go_eval_qap_i32 : (void*)go_eval_qap_f64);
-      void* args[] = {(void*)&inst, &off1, &nn, &d_g, &d_o};
-      CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
-    } else if (p->row_kind == go::RK_PART) {
-      go::RowArgs x = row_args(p);
-      void* args[] = {(void*)&inst, &x, &d_g, &d_o, &d_p};
-      CK(cudaLaunchKernel((void*)go_eval_part, dim3(m), dim3(32), args, 0, 0));
-    } else if (p->row_kind == go::RK_KNAP) {
-      double cap = p->capacity;
-      void* args[] = {(void*)&inst, &off1, &nn, &cap, &d_g, &d_o, &d_p};
-      CK(cudaLaunchKernel((void*)go_eval_knap, dim3(m), dim3(128), args, 0, 0));
-    } else if (p->row_kind == go::RK_USER) {
-      int mm = m;
-      void* args[] = {(void*)&inst, &nn, &mm, &d_g, &d_o, &d_p};
-      CU(gohost::drv()->LaunchKernel(p->user_mod.probe, (unsigned)((m + 127) / 128), 1, 1, 128, 1,
-                                     1, 0, nullptr, args, nullptr));
-      CK(cudaDeviceSynchronize());
-    } else {
-      int nj = p->n_jobs, pj = p->per_job, nmach = p->n_mach;
-      void* args[] = {(void*)&inst, &off1, &nj, &pj, &nmach, &d_g, &d_o};
-      CK(cudaLaunchKernel((void*)go_eval_jsp, dim3(m), dim3(32), args, (size_t)p->scratch_ints * 4, 0));
-    }
+  std::vector<short> h;
+  to_device_rows(p, genes, sizes, m, h);
+  short* d_g = nullptr;
+  double *d_o = nullptr, *d_p = nullptr;
+  CK(cudaMalloc(&d_g, h.size() * 2));
+  CK(cudaMalloc(&d_o, (size_t)m * p->n_obj * 8));
+  CK(cudaMalloc(&d_p, (size_t)m * 8));
+  CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  const int rc = eval_device_rows(p, d_g, m, d_o, d_p);
+  if (rc == GO_OK) {
     CK(cudaMemcpy(obj_out, d_o, (size_t)m * p->n_obj * 8, cudaMemcpyDeviceToHost));
     if (pen_out) CK(cudaMemcpy(pen_out, d_p, (size_t)m * 8, cudaMemcpyDeviceToHost));
-    cudaFree(d_g);
-    cudaFree(d_o);
-    cudaFree(d_p);
-    (void)sizes;
-    return GO_OK;
   }
-  std::vector<short> h((size_t)m * n);
-  for (size_t i = 0; i < h.size(); ++i) h[i] = (short)genes[i];
-  short* d_g = nullptr;
-  double* d_o = nullptr;
-  CK(cudaMalloc(&d_g, h.size() * 2));
-  CK(cudaMalloc(&d_o, (size_t)m * 8));
-  CK(cudaMemcpy(d_g, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
-  void* fn = p->elem == E_I16 ? (void*)go_eval_tsp_i16
-                              : (p->elem == E_I32 ? (void*)go_eval_tsp_i32 : (void*)go_eval_tsp_f64);
-  const void* inst = p->d_full;
-  int nn = n;
-  void* args[] = {(void*)&inst, &nn, &d_g, &d_o};
-  CK(cudaLaunchKernel(fn, dim3(m), dim3(128), args, 0, 0));
-  CK(cudaMemcpy(obj_out, d_o, (size_t)m * 8, cudaMemcpyDeviceToHost));
   cudaFree(d_g);
   cudaFree(d_o);
-  if (pen_out)
-    for (int i = 0; i < m; ++i) pen_out[i] = 0.0;
-  (void)sizes;
+  cudaFree(d_p);
+  return rc;
+}
+
+int go_init_population(go_problem* p, int count, uint64_t seed, uint64_t salt,
+                       const int32_t* extra_genes, const int32_t* extra_sizes, int n_extra,
+                       int keep, int maximize, double obj_weight, int32_t* genes_out,
+                       int32_t* sizes_out, double* obj_out, double* pen_out,
+                       int32_t* index_out) {
+  if (!p || count < 0 || n_extra < 0 || (n_extra > 0 && !extra_genes)) return fail(GO_E_INVALID, "bad arguments");
+  const int M = count + n_extra;
+  if (M == 0 || keep < 0 || keep > M) return fail(GO_E_INVALID, "need 0 <= keep <= count + n_extra, pool > 0");
+  if (keep > 0 && p->n_obj != 1)
+    return fail(GO_E_INVALID, "device selection is single-objective (select fronts on the host)");
+  if (!genes_out || !obj_out || !pen_out) return fail(GO_E_INVALID, "null output");
+  CK(cudaSetDevice(p->device));
+  go::InitArgs a{};
+  a.count = count;
+  a.W = p->n;
+  a.seed = seed;
+  a.salt = salt;
+  if (p->family == 0 || p->row_kind == go::RK_QAP || (p->row_kind == go::RK_USER && p->enc == 0)) {
+    a.kind = 0;
+    a.n = p->n;
+  } else if (p->row_kind == go::RK_PART) {
+    a.kind = 1;
+    a.n = p->n_cells;
+    a.d1 = p->d1;
+    a.d2 = p->d2;
+  } else {
+    a.kind = 2;
+    a.n = p->n;
+    a.lo = p->lb;
+    a.hi = p->ub;
+  }
+  const int W = p->n, out_n = keep > 0 ? keep : M;
+  DevBufs B;
+  short *rows = nullptr, *out_rows = nullptr;
+  double *d_o = nullptr, *d_p = nullptr;
+  int* d_idx = nullptr;
+  CK(B.get(&rows, (size_t)M * W * 2));
+  CK(B.get(&d_o, (size_t)M * p->n_obj * 8));
+  CK(B.get(&d_p, (size_t)M * 8));
+  if (a.kind == 1) CK(B.get(&a.scratch, (size_t)count * (2 * a.n + a.d1) * 2));
+  a.rows = rows;
+  if (count > 0) {
+    go::init_random_kernel<<<(count + 127) / 128, 128>>>(a);
+    CK(cudaGetLastError());
+  }
+  if (n_extra > 0) {
+    std::vector<short> h;
+    to_device_rows(p, extra_genes, extra_sizes, n_extra, h);
+    CK(cudaMemcpy(rows + (size_t)count * W, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+  }
+  const int rc = eval_device_rows(p, rows, M, d_o, d_p);
+  if (rc != GO_OK) return rc;
+  std::vector<double> ho((size_t)M * p->n_obj), hp(M);
+  CK(cudaMemcpy(ho.data(), d_o, ho.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hp.data(), d_p, hp.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<int> idx(out_n);
+  const short* src = rows;
+  if (keep > 0) {
+    CK(B.get(&out_rows, (size_t)keep * W * 2));
+    CK(B.get(&d_idx, (size_t)keep * 4));
+    go::SelectArgs s{};
+    s.obj = d_o;
+    s.pen = d_p;
+    s.rows = rows;
+    s.M = M;
+    s.m_obj = p->n_obj;
+    s.W = W;
+    s.keep = keep;
+    s.w = obj_weight;
+    s.maximize = maximize;
+    s.out_rows = out_rows;
+    s.out_idx = d_idx;
+    go::init_select_kernel<<<(M + 255) / 256, 256>>>(s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(idx.data(), d_idx, (size_t)keep * 4, cudaMemcpyDeviceToHost));
+    src = out_rows;
+  } else {
+    for (int i = 0; i < M; ++i) idx[i] = i;
+  }
+  std::vector<short> hr((size_t)out_n * W);
+  CK(cudaMemcpy(hr.data(), src, hr.size() * 2, cudaMemcpyDeviceToHost));
+  from_device_rows(p, hr.data(), out_n, genes_out, sizes_out);
+  for (int k = 0; k < out_n; ++k) {
+    for (int j = 0; j < p->n_obj; ++j) obj_out[(size_t)k * p->n_obj + j] = ho[(size_t)idx[k] * p->n_obj + j];
+    pen_out[k] = hp[idx[k]];
+    if (index_out) index_out[k] = idx[k];
+  }
   return GO_OK;
 }
 

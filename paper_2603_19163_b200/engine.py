@@ -102,6 +102,8 @@ class EngineConfig:
     teams_per_cta: int = 0          # evolver teams sharing one CTA's staged instance (0 = auto)
     evolver_offset: int = 0         # global index of local evolver 0 (multi-GPU islands)
     distributed: bool = False       # ranks of the torch.distributed group are islands (islands.py)
+    device_init: bool = False       # draw, evaluate and select the initial pool on the device
+                                    # (Philox streams; False = the reference's MT19937 init stream)
 
     def __post_init__(self):
         if self.team_size < 1:
@@ -303,18 +305,15 @@ def initialize_population(problem: ProblemDefinition, pop_size: int, oversample_
     pool, evaluate on the device in one batch, keep the comparison-best."""
     cfg = problem.config()
     pool = [random_solution(cfg, rng) for _ in range(oversample_factor * pop_size)]
-    if cfg.encoding.kind is EncodingKind.PERMUTATION:
-        for mat in problem.init_matrices():
-            if mat.shape == (cfg.n, cfg.n):
-                pool.extend(permutation_as_solution(p, cfg) for p in heuristic_candidates(mat))
-    seeded = problem.init_candidates(rng)
-    for s in seeded or ():
-        rep = validate_solution(s, cfg)
-        if not rep.ok:
-            raise ValueError(f"init_candidates produced an invalid solution: {rep.violations[0]}")
-        pool.append(s.copy())
+    pool += _extra_candidates(problem, cfg, rng)
     evaluate_many(problem, pool, device)
-    if cfg.num_objectives != 1:  # engine.py:352-360: non-dominated fronts in crowding order
+    return _select_initial(pool, pop_size, cfg)
+
+
+def _select_initial(pool, pop_size, cfg):
+    """engine.py:345-360: compare order (stable), or non-dominated fronts in
+    crowding order for more than one objective."""
+    if cfg.num_objectives != 1:
         fronts = fast_nondominated_sort(np.array([s.objectives for s in pool]),
                                         [o.direction for o in cfg.obj_defs])
         keep = []
@@ -325,6 +324,64 @@ def initialize_population(problem: ProblemDefinition, pop_size: int, oversample_
         return keep
     pool.sort(key=cmp_to_key(lambda a, b: compare(a, b, cfg)))
     return pool[:pop_size]
+
+
+def _extra_candidates(problem, cfg, rng):
+    out = []
+    if cfg.encoding.kind is EncodingKind.PERMUTATION:
+        for mat in problem.init_matrices():
+            if mat.shape == (cfg.n, cfg.n):
+                out.extend(permutation_as_solution(p, cfg) for p in heuristic_candidates(mat))
+    for s in problem.init_candidates(rng) or ():
+        rep = validate_solution(s, cfg)
+        if not rep.ok:
+            raise ValueError(f"init_candidates produced an invalid solution: {rep.violations[0]}")
+        out.append(s.copy())
+    return out
+
+
+def initialize_population_device(problem: ProblemDefinition, pop_size: int,
+                                 oversample_factor: int, seed: int, salt: int,
+                                 rng: random.Random, device: int = 0) -> list[Solution]:
+    """engine.py:327-360 on the device (go_init_population): the
+    oversample·P random draws run one solution per thread, random solution i from
+    the Philox stream mix64(seed, init stream, salt, i) in the reference's draw
+    order; heuristic and init_candidates solutions (drawn from `rng`) are
+    appended; the pool is evaluated on the device and, for one Weighted
+    objective, selected there in compare order.  Multi-objective pools come back
+    whole and take the host's non-dominated selection."""
+    cfg = problem.config()
+    lib = N.load()
+    h = problem.device_handle(device)
+    extra = _extra_candidates(problem, cfg, rng)
+    count = oversample_factor * pop_size
+    m = cfg.num_objectives
+    mode = cfg.comparison_or_default()
+    device_select = m == 1 and isinstance(mode, Weighted)
+    keep = pop_size if device_select else 0
+    k = keep or count + len(extra)
+    if extra:
+        eg, es = pack_solutions(extra, cfg)
+        eg_p, es_p = N.iptr(eg), N.iptr(es)
+    else:
+        eg_p = es_p = None
+    genes = np.zeros((k, cfg.d1 * cfg.d2), dtype=np.int32)
+    sizes = np.zeros((k, cfg.d1), dtype=np.int32)
+    obj = np.zeros(k * m)
+    pen = np.zeros(k)
+    idx = np.zeros(k, dtype=np.int32)
+    w = mode.weights[0] if device_select else 1.0
+    maximize = cfg.obj_defs[0].direction is Direction.MAXIMIZE
+    N.check(lib.go_init_population(h, count, seed & _MASK64, salt & _MASK64, eg_p, es_p,
+                                   len(extra), keep, int(maximize), w, N.iptr(genes),
+                                   N.iptr(sizes), N.dptr(obj), N.dptr(pen), N.iptr(idx)))
+    pool = []
+    for i in range(k):
+        s = Solution(genes[i].reshape(cfg.d1, cfg.d2), sizes[i], m)
+        s.objectives[:] = obj[i * m:(i + 1) * m]
+        s.penalty = float(pen[i])
+        pool.append(s)
+    return pool if device_select else _select_initial(pool, pop_size, cfg)
 
 
 def fast_nondominated_sort(points: np.ndarray, directions) -> list[list[int]]:
@@ -424,7 +481,7 @@ class DeviceRun:
 
     def __init__(self, problem: ProblemDefinition, config: EngineConfig, seed: int,
                  initial_population: list[Solution] | None = None,
-                 init_rng: random.Random | None = None):
+                 init_rng: random.Random | None = None, init_salt: int = 0):
         self.t_start = time.perf_counter()
         self.problem, self.config, self.seed = problem, config, seed
         cfg = problem.config()
@@ -470,7 +527,11 @@ class DeviceRun:
         pop_size = max(pop_size, config.islands.count)
         self.pop_size = pop_size
 
-        if initial_population is None:
+        if initial_population is None and config.device_init:
+            pop = initialize_population_device(problem, pop_size, config.oversample_factor,
+                                               seed, init_salt,
+                                               init_rng or derived_rng(seed, _STREAM_INIT), dev)
+        elif initial_population is None:
             pop = initialize_population(problem, pop_size, config.oversample_factor,
                                         init_rng or derived_rng(seed, _STREAM_INIT), dev)
         else:

@@ -43,7 +43,8 @@ class DeviceIsland:
         self.N = N
         local = replace(config, islands=replace(config.islands, count=1),
                         evolver_offset=rank * RANK_STRIDE)
-        self.dr = DeviceRun(problem, local, seed, init_rng=derived_rng(seed, _STREAM_INIT, rank))
+        self.dr = DeviceRun(problem, local, seed, init_rng=derived_rng(seed, _STREAM_INIT, rank),
+                            init_salt=rank)
         rb = C.c_int64()
         N.check(self.dr.lib.go_elite_record_bytes(self.dr.engine, C.byref(rb)))
         self.record_bytes = rb.value
