@@ -17,7 +17,9 @@ distances are unrounded and symmetrised with the mean (parsers.py:217-224).
 
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 
@@ -126,3 +128,96 @@ def knapsack_random(n: int = 1000, seed: int = 1000):
     w = rng.integers(1, 1001, n).astype(np.float64)
     v = rng.integers(1, 1001, n).astype(np.float64)
     return w, v, float(np.floor(w.sum() / 2))
+
+
+# ---- desk-scale demo instances (instances.py:20-208 of the reference) ----------
+# The instance data with its independently verified optima is the reference's;
+# tests/golden/make_golden_formats.py dumps it to data/demo_instances.json.
+
+_DEMO_FILE = Path(__file__).with_name("data") / "demo_instances.json"
+_ARRAY_FIELDS = ("distance_matrix", "weights", "values", "flow_matrix", "cost_matrix",
+                 "item_sizes", "durations", "demands", "ready_times", "due_times",
+                 "service_times", "priorities", "requirements")
+
+
+@dataclass(frozen=True)
+class DemoInstance:
+    name: str
+    problem_name: str
+    instance: "InstanceData"
+    best_known: float | None
+    note: str = ""
+
+    def problem(self):
+        from .problems import builtin_problem
+        return builtin_problem(self.problem_name, self.instance)
+
+
+def _instance_from_json(doc: dict):
+    from .problems import InstanceData
+    kw = {}
+    for key, val in doc.items():
+        if key == "meta":
+            continue
+        if key in _ARRAY_FIELDS:
+            kw[key] = np.asarray(val, dtype=np.float64)
+        elif key == "edges":
+            kw[key] = [tuple(int(x) for x in e) for e in val]
+        elif key == "jobs":
+            kw[key] = [[(int(m), int(t)) for m, t in ops] for ops in val]
+        else:
+            kw[key] = val
+    return InstanceData(meta=dict(doc.get("meta", {})), **kw)
+
+
+def _demo_table() -> dict:
+    return json.loads(_DEMO_FILE.read_text())
+
+
+def demo_instances() -> dict[str, DemoInstance]:
+    """instances.py:197-198: name -> DemoInstance (fresh objects per call)."""
+    return {name: DemoInstance(name, d["problem"], _instance_from_json(d["instance"]),
+                               d["best_known"], d.get("note", ""))
+            for name, d in _demo_table()["demos"].items()}
+
+
+def demo_instance(name: str) -> DemoInstance:
+    """instances.py:201-208."""
+    table = demo_instances()
+    if name not in table:
+        raise ValueError(f"unknown demo instance {name!r}; available: {', '.join(sorted(table))}")
+    return table[name]
+
+
+GENERALITY_SUITE = tuple(_demo_table()["generality_suite"]) if _DEMO_FILE.exists() else ()
+
+
+def chain_cluster_matrix(num_nodes: int, chains, end_leg: float, interior_leg: float,
+                         step: float, inter: float) -> np.ndarray:
+    """Depot 0 plus clusters laid out as chains: `step`·|a-b| along a chain,
+    `interior_leg` from the depot to a chain's inner nodes and `end_leg` to its
+    two ends, `inter` between clusters (instances.py:32-47)."""
+    d = np.full((num_nodes, num_nodes), float(inter))
+    np.fill_diagonal(d, 0.0)
+    for chain in chains:
+        idx = np.asarray(chain)
+        k = np.arange(len(idx))
+        block = step * np.abs(k[:, None] - k[None, :]).astype(np.float64)
+        d[np.ix_(idx, idx)] = block
+        d[0, idx] = d[idx, 0] = interior_leg
+        for end in (idx[0], idx[-1]):
+            d[0, end] = d[end, 0] = end_leg
+    return d
+
+
+def cvrp8_instance(objectives=("distance", "vehicles"), comparison=None):
+    """instances.py:170-184: bi-objective routing fixture, two chains of four;
+    distance optimum 170 with 2 vehicles, one route covers all at 190."""
+    from .problems import InstanceData
+    meta = {"objectives": tuple(objectives)}
+    if comparison is not None:
+        meta["comparison"] = comparison
+    d = chain_cluster_matrix(9, ((1, 2, 3, 4), (5, 6, 7, 8)), end_leg=20.0, interior_leg=45.0,
+                             step=15.0, inter=60.0)
+    return InstanceData(distance_matrix=d, demands=np.ones(8), capacity=8.0, vehicles=3,
+                        meta=meta)
