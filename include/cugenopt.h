@@ -104,7 +104,7 @@ typedef struct go_problem_desc {
  * (const double*, length data.<name>_len).  Data arrays are copied at creation. */
 typedef struct go_user_problem_desc {
   int32_t encoding;               /* 0 permutation, 1 binary, 2 integer (core.py:18-66) */
-  int32_t n;                      /* genes of the single row (dim2) */
+  int32_t n;                      /* genes per row (dim2) */
   int32_t lb, ub;                 /* integer encoding bounds (ignored otherwise) */
   const char* compute_obj;        /* snippet body (required) */
   const char* compute_penalty;    /* snippet body or NULL: penalty 0 */
@@ -112,6 +112,8 @@ typedef struct go_user_problem_desc {
   const char* const* data_names;  /* C identifiers */
   const double* const* data;
   const int64_t* data_lens;
+  int32_t rows;                   /* 0 or 1: one row; > 1: MULTI_FIXED rows of n genes each
+                                   * (core.py:28-35), sol[r * n + i] in the snippets */
 } go_user_problem_desc;
 
 typedef struct go_problem go_problem;

@@ -473,3 +473,63 @@ class LoadBalancing(Problem):
 
     def objective(self, i, sol):
         return float(np.bincount(sol.row(0), weights=self.d, minlength=self.m).max())
+
+
+class JspPerm(Problem):
+    """builtins.py:459-516: row m orders the jobs on machine m; the decoder
+    sweeps the machines until no head operation can start, penalising
+    operations left unscheduled by a cyclic wait."""
+
+    def __init__(self, jobs):
+        self.jobs = [[(int(m), int(d)) for m, d in ops] for ops in jobs]
+        self.n_jobs, self.per_job = len(self.jobs), len(self.jobs[0])
+        self.n_mach = 1 + max(m for ops in self.jobs for m, _ in ops)
+        self.spec = Spec(PERM, self.n_mach, self.n_jobs, self.n_jobs, MULTI_FIXED)
+
+    def decode(self, sol):
+        ptr = [0] * self.n_mach
+        nxt = [0] * self.n_jobs
+        javail = [0.0] * self.n_jobs
+        mavail = [0.0] * self.n_mach
+        done_ops, total, span = 0, self.n_jobs * self.per_job, 0.0
+        moved = True
+        while moved and done_ops < total:
+            moved = False
+            for m in range(self.n_mach):
+                if ptr[m] >= self.n_jobs:
+                    continue
+                j = int(sol.data[m, ptr[m]])
+                k = nxt[j]
+                if k >= self.per_job or self.jobs[j][k][0] != m:
+                    continue
+                end = max(javail[j], mavail[m]) + self.jobs[j][k][1]
+                javail[j] = mavail[m] = end
+                nxt[j] += 1
+                ptr[m] += 1
+                done_ops += 1
+                span = max(span, end)
+                moved = True
+        return span, total - done_ops
+
+    def objective(self, i, sol):
+        return float(self.decode(sol)[0])
+
+    def penalty(self, sol):
+        return float(self.decode(sol)[1])
+
+
+class BinarySchedule(Problem):
+    """builtins.py:519-545: worker x shift 0/1 matrix; cost sum (numpy over the
+    whole matrix), penalty = uncovered requirement per shift."""
+
+    def __init__(self, cost, requirements):
+        self.cost = np.asarray(cost, dtype=np.float64)
+        self.req = np.asarray(requirements, dtype=np.float64)
+        w, sh = self.cost.shape
+        self.spec = Spec(BINARY, w, sh, w * sh, MULTI_FIXED)
+
+    def objective(self, i, sol):
+        return float((self.cost * sol.data).sum())
+
+    def penalty(self, sol):
+        return float(np.maximum(self.req - sol.data.sum(axis=0), 0.0).sum())

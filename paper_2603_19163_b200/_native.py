@@ -63,7 +63,8 @@ class UserProblemDesc(C.Structure):  # go_user_problem_desc
     _fields_ = [("encoding", C.c_int32), ("n", C.c_int32), ("lb", C.c_int32), ("ub", C.c_int32),
                 ("compute_obj", C.c_char_p), ("compute_penalty", C.c_char_p),
                 ("n_data", C.c_int32), ("data_names", C.POINTER(C.c_char_p)),
-                ("data", C.POINTER(_PD)), ("data_lens", C.POINTER(C.c_int64))]
+                ("data", C.POINTER(_PD)), ("data_lens", C.POINTER(C.c_int64)),
+                ("rows", C.c_int32)]
 
 
 class CustomOp(C.Structure):

@@ -195,6 +195,7 @@ struct go_problem {
   // user problems (RK_USER): NVRTC objective module, encoding
   gohost::JitModule user_mod;
   int enc = 0;
+  int mf = 0;  // MULTI_FIXED user rows: 1 permutation rows, 2 binary / integer cells
   // user operators
   std::vector<gohost::UserOpSrc> ops;  // registered (compiled and probed)
   std::map<int, gohost::JitModule> jit;  // per layout
@@ -524,9 +525,12 @@ int go_problem_create_user(const go_user_problem_desc* d, int device, go_problem
     up.lens.push_back(d->data_lens[i]);
   }
   if (img.empty()) img.assign(16, 0);
-  p->n = d->n;
-  p->d1 = 1;
+  const int rows = d->rows > 1 ? d->rows : 1;
+  if ((long long)rows * d->n > 32767) return fail(GO_E_INVALID, "rows * n must be <= 32767");
+  p->n = rows * d->n;  // device row: the d1 x d2 genes, row-major
+  p->d1 = rows;
   p->d2 = d->n;
+  p->mf = rows > 1 ? (d->encoding == 0 ? 1 : 2) : 0;
   p->enc = d->encoding;
   p->lb = d->encoding == 0 ? 0 : (d->encoding == 1 ? 0 : d->lb);
   p->ub = d->encoding == 0 ? d->n - 1 : (d->encoding == 1 ? 1 : d->ub);
@@ -616,10 +620,12 @@ void from_device_rows(const go_problem* p, const short* rows, int m, int32_t* ge
     }
     return;
   }
+  const int d1 = p->mf ? p->d1 : 1;  // MULTI_FIXED: every row full
   for (int s = 0; s < m; ++s) {
     if (genes)
       for (int q = 0; q < p->n; ++q) genes[(size_t)s * p->n + q] = rows[(size_t)s * p->n + q];
-    if (sizes) sizes[s] = p->n;
+    if (sizes)
+      for (int r = 0; r < d1; ++r) sizes[(size_t)s * d1 + r] = p->n / d1;
   }
 }
 
@@ -633,7 +639,8 @@ go::RowArgs row_args(const go_problem* p) {
   x.n_jobs = p->n_jobs;
   x.per_job = p->per_job;
   x.n_mach = p->n_mach;
-  x.n_cfg = p->row_kind == go::RK_PART ? p->n_cells : p->n;
+  // ProblemConfig.n (lns_scope): permutation rows hold n values each (core.py:28-35)
+  x.n_cfg = p->row_kind == go::RK_PART ? p->n_cells : (p->mf == 1 ? p->d2 : p->n);
   x.lb = p->lb;
   x.ub = p->ub;
   x.scratch_ints = p->scratch_ints;
@@ -647,6 +654,7 @@ go::RowArgs row_args(const go_problem* p) {
   x.okind1 = p->okind1;
   x.mo.m = p->n_obj;
   x.pvar = p->pvar;
+  x.mf = p->mf;
   return x;
 }
 
@@ -915,8 +923,9 @@ int go_init_population(go_problem* p, int count, uint64_t seed, uint64_t salt,
   a.seed = seed;
   a.salt = salt;
   if (p->family == 0 || p->row_kind == go::RK_QAP || (p->row_kind == go::RK_USER && p->enc == 0)) {
-    a.kind = 0;
-    a.n = p->n;
+    a.kind = 0;  // d1 rows, each a shuffle of range(d2) (engine.py:262-266)
+    a.nrows = p->mf ? p->d1 : 1;
+    a.n = p->n / a.nrows;
   } else if (p->row_kind == go::RK_PART) {
     a.kind = 1;
     a.n = p->n_cells;

@@ -107,7 +107,7 @@ struct RowArgs {
   double w2;
   MoCmp mo;
   int pvar;              // partition variant: 0 plain, 1 vrp_priority (priorities at off2), 2 vrp_nonlinear
-  int pad_v;
+  int mf;                // MULTI_FIXED user rows (d1 x d2 flat): 0 no, 1 permutation rows, 2 cells
 };
 
 struct EpilogueArgs {

@@ -43,13 +43,15 @@ struct OvSol {  // gene p replaced by v (binary / integer trials)
   __device__ __forceinline__ int size() const { return n; }
 };
 template <class G>
-struct InsSol {  // v moved from slot q0 to slot pos (permutation insertion trials)
-  const G* r;
-  int n, q0, pos, v;
+struct InsSol {  // v moved from slot q0 to slot pos of the row block [off, off + nb)
+  const G* r;    // (permutation insertion trials; the block is the whole row, or one
+  int n, off, nb, q0, pos, v;  // MULTI_FIXED row of the d1 x d2 solution)
   __device__ __forceinline__ int operator[](int i) const {
-    if (i == pos) return v;
-    const int j = i < pos ? i : i - 1;  // index in the row without v
-    return r[j < q0 ? j : j + 1];
+    const int b = i - off;
+    if (b < 0 || b >= nb) return r[i];
+    if (b == pos) return v;
+    const int j = b < pos ? b : b - 1;  // index in the block without v
+    return r[off + (j < q0 ? j : j + 1)];
   }
   __device__ __forceinline__ int size() const { return n; }
 };
@@ -404,6 +406,7 @@ struct GrShared {  // views into the team scratch (TeamShared::cnt, 128 ints)
   __device__ __forceinline__ int& nd() const { return gx[1]; }
   __device__ __forceinline__ int& res() const { return gx[2]; }
   __device__ __forceinline__ int& aux() const { return gx[3]; }
+  __device__ __forceinline__ int& row() const { return gx[4]; }  // MULTI_FIXED home row
   __device__ __forceinline__ int* picks() const { return gx + 8; }   // [30]
   __device__ __forceinline__ int* taken() const { return gx + 40; }  // [30]
   __device__ __forceinline__ int* dom() const { return gx + 72; }    // [16]
@@ -617,11 +620,12 @@ struct UserScore {
 };
 
 template <class U, class G>
-__device__ void team_gr_user_perm(G* row, int n, const GrShared& g, const UserScore& us,
-                                  double* sbuf, TeamShared<double>* ts, int lane, int team,
-                                  int TS) {
+__device__ void team_gr_user_perm(G* full, int ntot, int off, int n, const GrShared& g,
+                                  const UserScore& us, double* sbuf, TeamShared<double>* ts,
+                                  int lane, int team, int TS) {
   const int m = g.m();
   if (m == 0) return;
+  G* row = full + off;  // the rebuilt row; trials are scored on the whole solution
   const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
   team_pop_park(row, n, g, lane, team, TS);
   for (int t = 0; t < m; ++t) {
@@ -633,7 +637,7 @@ __device__ void team_gr_user_perm(G* row, int n, const GrShared& g, const UserSc
     double bs = 0.0;
     int bi = 0x7fffffff;
     for (int pos = lane; pos < n; pos += TS) {  // ascending per thread: first minimum
-      const InsSol<G> sol{row, n, q0, pos, v};
+      const InsSol<G> sol{full, ntot, off, n, q0, pos, v};
       const double sc = user_phi(U::obj(sol, us.inst), U::pen(sol, us.inst), us.w, us.maximize,
                                  us.pw);
       if (bi == 0x7fffffff || sc < bs) {
@@ -1420,7 +1424,11 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           RowCtx<G> c;
           c.rng = rng;
           c.row = (G*)(rows + (size_t)L * rs);
-          c.n = n;
+          c.full = c.row;
+          c.mf = X.mf;
+          c.d1 = X.mf ? X.d1 : 1;
+          c.d2 = X.d2;
+          c.n = X.mf == 1 ? X.d2 : n;  // permutation rows: ops see one row
           c.n_cfg = X.n_cfg;
           c.lb = X.lb;
           c.ub = X.ub;
@@ -1506,7 +1514,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
             Stream rng;
             rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
             rng.seek(la.pos[L]);
-            gr_draw<KIND>(rng, gsh, KIND == RK_PART ? X.n_cells : n, X.n_cfg, X.lb, X.ub,
+            // MULTI_FIXED permutation rows: home_row = randrange(d1) (operators.py:519-521)
+            gsh.row() = (KIND == RK_USER && X.mf == 1) ? rng.randbelow(X.d1) : 0;
+            gr_draw<KIND>(rng, gsh, KIND == RK_PART ? X.n_cells : (X.mf == 1 ? X.d2 : n), X.n_cfg,
+                          X.lb, X.ub,
                           (const short*)lrow + X.n_cells, X.d1,
                           KIND == RK_JSP || (KIND == RK_USER && X.enc != ENC_PERM));
             const u32 meta = la.meta[L];
@@ -1531,7 +1542,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           } else if (KIND == RK_USER) {
             const UserScore us{inst, X.obj_weight, pwt, X.maximize};
             if (X.enc == ENC_PERM)
-              team_gr_user_perm<U>(lrow, n, gsh, us, la.delta, ts, lane, team, TS);
+              team_gr_user_perm<U>(lrow, n, gsh.row() * X.d2, X.mf == 1 ? X.d2 : n, gsh, us,
+                                   la.delta, ts, lane, team, TS);
             else
               team_gr_user_cells<U>(lrow, n, gsh, us, la.delta, lane, team, TS);
           }

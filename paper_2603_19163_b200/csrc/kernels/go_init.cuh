@@ -23,7 +23,7 @@ struct InitArgs {
   int kind;        // 0 permutation of n values, 1 partition, 2 cells in [lo, hi]
   int n, d1, d2;   // partition: n values dealt to d1 rows of capacity d2 (W = n + d1)
   int lo, hi;
-  int pad;
+  int nrows;       // permutation: rows of n values each (MULTI_FIXED)
   u64 seed, salt;
 };
 
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(128) init_random_kernel(InitArgs a) {
   s.init(mix64_4(a.seed, STREAM_INIT_ID, a.salt, (u64)idx));
   short* row = a.rows + (size_t)idx * a.W;
   if (a.kind == 0) {
-    shuffle_iota(s, row, a.n);
+    for (int r = 0; r < a.nrows; ++r) shuffle_iota(s, row + r * a.n, a.n);
   } else if (a.kind == 2) {
     const int width = a.hi + 1 - a.lo;
     for (int q = 0; q < a.n; ++q) row[q] = (short)(a.lo + s.randbelow(width));

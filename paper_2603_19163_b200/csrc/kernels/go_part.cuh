@@ -303,6 +303,10 @@ __device__ __forceinline__ void pop_scatter_shuffle(PartCtx& c) {
   rc.rstride = 1;
   rc.nr = 0;
   rc.err = 0;
+  rc.full = c.cells;
+  rc.d1 = 1;
+  rc.d2 = c.total;
+  rc.mf = 0;
   rop_scatter_shuffle(rc);
   c.rng = rc.rng;
 }

@@ -26,6 +26,24 @@ struct RowCtx {
   int rstride;
   int err;
   const MateSel* mates;  // crossover mates (engine.py:553-559)
+  // MULTI_FIXED rows (user problems): `full` holds d1 rows of d2 genes; mf = 1
+  // permutation rows (ops act on one row, n = d2), mf = 2 binary / integer cells
+  // (cell ops act on all d1*d2 cells, segment ops on one row)
+  G* full;
+  int d1, d2, mf;
+
+  // _pick_row (operators.py:140-144): every row holds d2 genes, so the draw is
+  // randrange(d1) (randrange(1) for single-row problems); the op continues on
+  // that row
+  __device__ __forceinline__ int pick_row() {
+    const int r = rng.randbelow(d1);
+    if (mf) {
+      row = full + r * d2;
+      n = d2;
+    }
+    return r;
+  }
+  __device__ __forceinline__ int row_len() const { return mf ? d2 : n; }
 
   __device__ __forceinline__ void mark(int lo, int hi) {
     if (nr < MAX_RANGES) {
@@ -67,7 +85,7 @@ template <class G>
 __device__ __forceinline__ void rop_swap(RowCtx<G>& c) {
   const int n = c.n;
   if (n < 2) return;
-  c.randbelow(1);
+  c.pick_row();
   const int i = c.randbelow(n);
   int j = c.randbelow(n - 1);
   j += j >= i;
@@ -82,7 +100,7 @@ template <class G>
 __device__ __forceinline__ void rop_insert(RowCtx<G>& c) {
   const int n = c.n;
   if (n < 2) return;
-  c.randbelow(1);
+  c.pick_row();
   const int i = c.randbelow(n);
   const int j = c.randbelow(n);
   row_move_one(c.row, i, j);
@@ -93,7 +111,7 @@ template <class G>
 __device__ __forceinline__ void rop_reverse(RowCtx<G>& c) {
   const int n = c.n;
   if (n < 2) return;
-  c.randbelow(1);
+  c.pick_row();
   const int i = c.randbelow(n - 1);
   const int j = c.randrange(i + 1, n);
   row_reverse_range(c.row, i, j);
@@ -105,7 +123,7 @@ __device__ __forceinline__ void rop_or_opt(RowCtx<G>& c) {
   const int L = c.randrange(2, 4);
   const int n = c.n;
   if (n < L + 1) return;
-  c.randbelow(1);
+  c.pick_row();
   const int s = c.randbelow(n - L + 1);
   G seg[3];
   for (int t = 0; t < L; ++t) seg[t] = c.row[s + t];
@@ -123,7 +141,7 @@ __device__ __forceinline__ void rop_three_opt(RowCtx<G>& c) {
     rop_reverse(c);
     return;
   }
-  c.randbelow(1);
+  c.pick_row();
   int i, j, k;
   sample3_sorted(c, n, i, j, k);
   const int variant = c.randbelow(7);
@@ -160,9 +178,9 @@ __device__ __forceinline__ void rop_flip(RowCtx<G>& c) {
 
 template <class G>
 __device__ __forceinline__ void rop_seg_flip(RowCtx<G>& c) {
+  if (c.row_len() < 1) return;
+  c.pick_row();
   const int n = c.n;
-  if (n < 1) return;
-  c.randbelow(1);
   const int i = c.randbelow(n);
   const int j = c.randrange(i, n);
   for (int p = i; p <= j; ++p) c.row[p] = (G)(1 - c.row[p]);
@@ -179,9 +197,9 @@ __device__ __forceinline__ void rop_random_reset(RowCtx<G>& c) {
 
 template <class G>
 __device__ __forceinline__ void rop_seg_reset(RowCtx<G>& c) {
+  if (c.row_len() < 1) return;
+  c.pick_row();
   const int n = c.n;
-  if (n < 1) return;
-  c.randbelow(1);
   const int i = c.randbelow(n);
   const int j = c.randrange(i, n);
   for (int p = i; p <= j; ++p) c.row[p] = (G)c.randrange(c.lb, c.ub + 1);
@@ -228,8 +246,10 @@ template <class G>
 __device__ __forceinline__ void rop_ox(RowCtx<G>& c) {
   const short* mate = c.mates->pick(c);
   if (mate == nullptr) return;
-  if (c.n < 2) return;  // SINGLE_SEQ: row 0, equal sizes
-  ox_in_place(c.row, mate, c.n, c);
+  // SINGLE_SEQ: row 0 without a draw; MULTI_FIXED: randrange(d1) (operators.py:450)
+  const int off = c.mf == 1 ? c.pick_row() * c.d2 : 0;
+  if (c.n < 2) return;
+  ox_in_place(c.row, mate + off, c.n, c);
   c.mark_all();
 }
 
@@ -259,9 +279,9 @@ __device__ __forceinline__ void rop_uniform_x(RowCtx<G>& c) {
 // ---- LNS shuffles (operators.py:468-499) -----------------------------------------
 template <class G>
 __device__ __forceinline__ void rop_seg_shuffle(RowCtx<G>& c) {
+  if (c.row_len() < 2) return;
+  c.pick_row();
   const int n = c.n;
-  if (n < 2) return;
-  c.randbelow(1);
   const int len = lns_scope(c.n_cfg) < n ? lns_scope(c.n_cfg) : n;
   const int s = c.randbelow(n - len + 1);
   G* seg = c.row + s;
@@ -276,6 +296,7 @@ __device__ __forceinline__ void rop_seg_shuffle(RowCtx<G>& c) {
 
 template <class G>
 __device__ __forceinline__ void rop_scatter_shuffle(RowCtx<G>& c) {
+  if (c.mf == 1) c.pick_row();  // permutation rows: one row (operators.py:481-494)
   const int total = c.n;
   if (total < 2) return;
   int m = lns_scope(c.n_cfg);

@@ -28,7 +28,7 @@ BUILTIN_NAMES = ("tsp", "cvrp", "vrptw", "knapsack", "qap", "assignment", "graph
                  "vrp_priority", "vrp_nonlinear")
 DEVICE_PROBLEMS = ("tsp", "qap", "knapsack", "jsp_int", "vrptw", "cvrp", "assignment",
                    "graph_coloring", "bin_packing", "load_balancing", "vrp_priority",
-                   "vrp_nonlinear")
+                   "vrp_nonlinear", "jsp_perm", "schedule_binary")
 
 
 @dataclass
@@ -482,6 +482,12 @@ def builtin_problem(name: str, instance: InstanceData) -> ProblemDefinition:
     if name == "load_balancing":
         _need(instance, "durations", "num_machines")
         return LoadBalancingProblem(instance.durations, instance.num_machines)
+    if name == "jsp_perm":
+        _need(instance, "jobs")
+        return JspPermProblem(instance.jobs)
+    if name == "schedule_binary":
+        _need(instance, "cost_matrix", "requirements")
+        return BinaryScheduleProblem(instance.cost_matrix, instance.requirements)
     raise NotImplementedError(
         f"problem {name!r} has no B200 device path in this build "
         f"(device problems: {', '.join(DEVICE_PROBLEMS)})")
@@ -517,12 +523,14 @@ class CudaProblem(ProblemDefinition):
     def __init__(self, encoding: str, n: int, compute_obj: str, compute_penalty: str | None = None,
                  data: dict | None = None, lb: int = 0, ub: int | None = None,
                  maximize: bool = False, name: str = "objective",
-                 init_matrices: list | None = None):
+                 init_matrices: list | None = None, rows: int = 1):
         if encoding not in self._ENC:
             raise ValueError(f"encoding must be one of {sorted(self._ENC)}, got {encoding!r}")
         if not isinstance(compute_obj, str) or not compute_obj.strip():
             raise ValueError("compute_obj must be a CUDA snippet (function body)")
-        self.encoding, self.n = encoding, int(n)
+        self.encoding, self.n, self.rows = encoding, int(n), int(rows)
+        if self.rows < 1:
+            raise ValueError("rows must be >= 1")
         self.compute_obj_src, self.compute_penalty_src = compute_obj, compute_penalty
         self.data = {k: np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
                      for k, v in (data or {}).items()}
@@ -536,8 +544,13 @@ class CudaProblem(ProblemDefinition):
             enc = Encoding.integer(int(lb), int(ub))
         self.lb, self.ub = (int(lb), int(ub)) if encoding == "integer" else (0, 0)
         self._matrices = [np.asarray(m, dtype=np.float64) for m in (init_matrices or [])]
+        # rows > 1: MULTI_FIXED (core.py:28-35) — every row holds n genes (a full
+        # permutation of range(n) for the permutation encoding); snippets read
+        # row r, column i as sol[r * n + i]
         self._cfg = ProblemConfig(
-            encoding=enc, d1=1, d2=self.n, n=self.n, row_mode=RowModeKind.SINGLE_SEQ,
+            encoding=enc, d1=self.rows, d2=self.n,
+            n=self.n if encoding == "permutation" else self.rows * self.n,
+            row_mode=RowModeKind.SINGLE_SEQ if self.rows == 1 else RowModeKind.MULTI_FIXED,
             obj_defs=(ObjDef(name, Direction.MAXIMIZE if maximize else Direction.MINIMIZE),))
 
     def config(self):
@@ -565,7 +578,8 @@ class CudaProblem(ProblemDefinition):
             encoding=self._ENC[self.encoding], n=self.n, lb=self.lb, ub=self.ub,
             compute_obj=self.compute_obj_src.encode(),
             compute_penalty=self.compute_penalty_src.encode() if self.compute_penalty_src else None,
-            n_data=len(names), data_names=c_names, data=c_ptrs, data_lens=c_lens)
+            n_data=len(names), data_names=c_names, data=c_ptrs, data_lens=c_lens,
+            rows=self.rows)
         h = C.c_void_p()
         log = C.create_string_buffer(8192)
         N.check(lib.go_problem_create_user(C.byref(desc), device, C.byref(h), log, len(log)))
@@ -626,6 +640,95 @@ _MAKESPAN_LOADS = """
   }
   return mx;
 """
+
+
+_JSPP_DECODE = """
+  constexpr int MAXJ = 64;  // JspPermProblem._decode (builtins.py:480-508)
+  const int nj = (int)data.dims[0], pj = (int)data.dims[1], nm = (int)data.dims[2];
+  int ptr[MAXJ], nxt[MAXJ];
+  double ja[MAXJ], ma[MAXJ];
+  for (int i = 0; i < nm; ++i) { ptr[i] = 0; ma[i] = 0.0; }
+  for (int j = 0; j < nj; ++j) { nxt[j] = 0; ja[j] = 0.0; }
+  const int total = nj * pj;
+  int done = 0;
+  double span = 0.0;
+  bool moved = true;
+  while (moved && done < total) {
+    moved = false;
+    for (int m = 0; m < nm; ++m) {  // one sweep over the machines' head jobs
+      if (ptr[m] >= nj) continue;
+      const int j = sol[m * nj + ptr[m]];
+      const int k = nxt[j];
+      if (k >= pj || (int)data.mach[j * pj + k] != m) continue;
+      const double end = __dadd_rn(ja[j] > ma[m] ? ja[j] : ma[m], data.dur[j * pj + k]);
+      ja[j] = end;
+      ma[m] = end;
+      ++nxt[j];
+      ++ptr[m];
+      ++done;
+      span = end > span ? end : span;
+      moved = true;
+    }
+  }
+"""
+
+_SCHED_COST = """
+  struct F {  // (cost * data).sum(): numpy pairwise over the d1 x d2 cells
+    const double* c; const Sol* s;
+    __device__ double operator()(int i) const { return __dmul_rn(c[i], (double)(*s)[i]); }
+  } f{data.cost, &sol};
+  return go::np_pairwise(f, 0, sol.n);
+"""
+_SCHED_UNCOVERED = """
+  struct F {  // max(requirements - data.sum(axis=0), 0).sum()
+    const double* req; const Sol* s; int d1, d2;
+    __device__ double operator()(int sh) const {
+      long long cov = 0;
+      for (int r = 0; r < d1; ++r) cov += (*s)[r * d2 + sh];
+      const double u = __dsub_rn(req[sh], (double)cov);
+      return u > 0.0 ? u : 0.0;
+    }
+  } f{data.req, &sol, (int)data.dims[0], (int)data.dims[1]};
+  return go::np_pairwise(f, 0, (int)data.dims[1]);
+"""
+
+
+class JspPermProblem(CudaProblem):
+    """builtins.py:459-516: MULTI_FIXED permutation rows, row m = the job order
+    on machine m; makespan of the sweep decoder, penalty = operations left
+    unscheduled by a cyclic wait."""
+
+    def __init__(self, jobs):
+        jobs = [[(int(m), int(d)) for m, d in ops] for ops in jobs]
+        if not jobs or any(len(ops) != len(jobs[0]) for ops in jobs) or not jobs[0]:
+            raise ValueError("every job needs the same, nonzero number of operations")
+        nj, pj = len(jobs), len(jobs[0])
+        nm = 1 + max(m for ops in jobs for m, _ in ops)
+        if nj > 64 or nm > 64:
+            raise ValueError("jsp_perm on the device supports up to 64 jobs and 64 machines")
+        self.jobs = jobs
+        data = {"mach": [m for ops in jobs for m, _ in ops],
+                "dur": [d for ops in jobs for _, d in ops], "dims": [nj, pj, nm]}
+        super().__init__("permutation", nj, _JSPP_DECODE + "  return span;\n",
+                         _JSPP_DECODE + "  return (double)(total - done);\n", data=data,
+                         name="makespan", rows=nm)
+
+
+class BinaryScheduleProblem(CudaProblem):
+    """builtins.py:519-545: worker x shift 0/1 MULTI_FIXED rows; cost sum,
+    penalty = uncovered requirement summed over shifts."""
+
+    def __init__(self, cost, requirements):
+        cost = np.asarray(cost, dtype=np.float64)
+        if cost.ndim != 2:
+            raise ValueError("cost must be a worker x shift matrix")
+        req = np.asarray(requirements, dtype=np.float64)
+        if len(req) != cost.shape[1]:
+            raise ValueError("one coverage requirement per shift required")
+        w, sh = cost.shape
+        super().__init__("binary", sh, _SCHED_COST, _SCHED_UNCOVERED,
+                         data={"cost": cost, "req": req, "dims": [w, sh]}, name="total_cost",
+                         rows=w)
 
 
 class AssignmentProblem(CudaProblem):

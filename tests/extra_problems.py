@@ -1,4 +1,4 @@
-"""Shared builders for the further single-row built-ins (golden_extra.json)."""
+"""Shared builders for the further built-ins (golden_extra.json)."""
 
 import json
 from pathlib import Path
@@ -26,6 +26,10 @@ def oracle_problem(key):
         if name == "vrp_priority":
             return OP.PriorityVrp(d, p["demands"], p["capacity"], p["vehicles"], p["priorities"])
         return OP.NonlinearVrp(d, p["demands"], p["capacity"], p["vehicles"])
+    if name == "jsp_perm":
+        return OP.JspPerm(p["jobs"])
+    if name == "schedule_binary":
+        return OP.BinarySchedule(p["cost_matrix"], p["requirements"])
     if name == "assignment":
         return OP.Assignment(np.array(p["cost_matrix"], dtype=np.float64))
     if name == "graph_coloring":
@@ -40,7 +44,10 @@ def product_problem(key):
     g = GOLD["instances"][key]
     kw = dict(g["payload"])
     meta = kw.pop("meta", {})
-    for k in ("cost_matrix", "item_sizes", "durations", "distance_matrix", "demands", "priorities"):
+    for k in ("cost_matrix", "item_sizes", "durations", "distance_matrix", "demands", "priorities",
+              "requirements"):
         if k in kw:
             kw[k] = np.asarray(kw[k], dtype=np.float64)
+    if "jobs" in kw:
+        kw["jobs"] = [[tuple(op) for op in ops] for ops in kw["jobs"]]
     return G.builtin_problem(g["problem"], G.InstanceData(meta=meta, **kw))

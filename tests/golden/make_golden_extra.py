@@ -1,6 +1,7 @@
-"""Goldens for the further single-row built-ins (assignment, graph colouring,
-bin packing, load balancing; builtins.py:293-394) from the UNMODIFIED
-reference (build container only).
+"""Goldens for the further built-ins (assignment, graph colouring, bin packing,
+load balancing, priority / nonlinear VRP, job-shop permutation rows, binary
+schedule; builtins.py:193-545) from the UNMODIFIED reference (build container
+only).
 
     PYTHONPATH=/root/repo python tests/golden/make_golden_extra.py
 
@@ -43,6 +44,10 @@ def instances():
                                          "num_machines": 5}),
         "vrpprio20": ("vrp_priority", routing(rng, 20, 5, priorities=True)),
         "vrpnl20": ("vrp_nonlinear", routing(rng, 20, 5)),
+        "jspperm6x4": ("jsp_perm", {"jobs": [[[int(m), int(rng.integers(1, 20))]
+                                              for m in rng.permutation(4)] for _ in range(6)]}),
+        "sched8x6": ("schedule_binary", {"cost_matrix": rng.integers(1, 20, size=(8, 6)).tolist(),
+                                         "requirements": rng.integers(1, 4, size=6).tolist()}),
     }
 
 
@@ -59,9 +64,12 @@ def routing(rng, n, vehicles, priorities=False):
 def build(name, payload):
     kw = dict(payload)
     meta = kw.pop("meta", {})
-    for k in ("cost_matrix", "item_sizes", "durations", "distance_matrix", "demands", "priorities"):
+    for k in ("cost_matrix", "item_sizes", "durations", "distance_matrix", "demands", "priorities",
+              "requirements"):
         if k in kw:
             kw[k] = np.asarray(kw[k], dtype=np.float64)
+    if "jobs" in kw:
+        kw["jobs"] = [[tuple(op) for op in ops] for ops in kw["jobs"]]
     return G.builtin_problem(name, G.InstanceData(meta=meta, **kw))
 
 

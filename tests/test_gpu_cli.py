@@ -43,9 +43,13 @@ def test_cli_solve_and_bench_documents(tmp_path, capsys):
                    "--generations", "100", "--pop", "8", "--team-size", "32"])
     cap = capsys.readouterr()
     assert rc == 0 and json.loads(cap.out)["instance"] == "euc17.tsp"
-    # no device path -> exit 3 with the reason
-    rc = cli.main(["solve", "--instance", "demo:schedule3x4"])
-    assert rc == 3 and "no B200 device path" in capsys.readouterr().err
+    # MULTI_FIXED rows (binary worker x shift schedule) through the same CLI
+    rc = cli.main(["solve", "--instance", "demo:schedule3x4", "--pop", "8", "--team-size", "8",
+                   "--generations", "500", "--target", "21"])
+    cap = capsys.readouterr()
+    assert rc == 0 and json.loads(cap.out)["objectives"] == [21.0]
+    rc = cli.main(["solve", "--instance", "demo:nope"])
+    assert rc == 3 and "unknown demo instance" in capsys.readouterr().err
 
 
 @pytest.mark.parametrize("name", [n for n in I.GENERALITY_SUITE])

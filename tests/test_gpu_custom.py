@@ -163,7 +163,7 @@ def test_solve_custom_api_and_compile_errors():
 
 
 @pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40", "vrpprio20",
-                                 "vrpnl20"])
+                                 "vrpnl20", "jspperm6x4", "sched8x6"])
 def test_extra_builtins_on_device(key):
     """Further reference built-ins on the device (NVRTC objectives, partition
     variants): device evaluation equals the reference goldens; whole runs equal
@@ -180,6 +180,26 @@ def test_extra_builtins_on_device(key):
     out = OE.run(ref, OE.RunCfg(population=4, team_size=32, max_generations=15, seed=3,
                                 record_history=True, allowed_ops=prob.device_sequences()),
                  device_stream="philox")
+    assert res.history["best_phi"] == out.history["best_phi"]
+    assert [[s.row(r).tolist() for r in range(s.d1)] for s in res.population] == \
+        [[s.row(r).tolist() for r in range(s.d1)] for s in out.population]
+
+
+@pytest.mark.parametrize("key,ops", [("jspperm6x4", (16, 12)), ("jspperm6x4", (14, 15, 4)),
+                                     ("jspperm6x4", (0, 1, 2, 3)), ("sched8x6", (16, 13)),
+                                     ("sched8x6", (6, 14, 15)), ("sched8x6", (5, 6, 13))])
+def test_multi_fixed_rows_operator_mixes(key, ops):
+    """MULTI_FIXED rows (jsp_perm permutation rows, schedule_binary cells):
+    row draws (_pick_row / randrange(d1), operators.py:140-144, :450, :481,
+    :519), per-row OX / shuffles / rebuilds with whole-solution trial scoring —
+    bit-identical to the oracle with operator-dominated registries."""
+    from tests.extra_problems import oracle_problem, product_problem
+    prob, ref = product_problem(key), oracle_problem(key)
+    prob.device_sequences = lambda: ops
+    res = G.run(prob, G.EngineConfig(population=4, team_size=32, max_generations=12, seed=21,
+                                     record_history=True))
+    out = OE.run(ref, OE.RunCfg(population=4, team_size=32, max_generations=12, seed=21,
+                                record_history=True, allowed_ops=ops), device_stream="philox")
     assert res.history["best_phi"] == out.history["best_phi"]
     assert [[s.row(r).tolist() for r in range(s.d1)] for s in res.population] == \
         [[s.row(r).tolist() for r in range(s.d1)] for s in out.population]

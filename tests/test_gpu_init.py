@@ -56,7 +56,8 @@ def _rows(s, d1):
 
 
 @pytest.mark.parametrize("name", ["tsp", "tsp_float", "qap", "knap", "jsp", "vrptw", "cvrp",
-                                  "assign40", "binpack30", "loadbal40", "vrpprio20"])
+                                  "assign40", "binpack30", "loadbal40", "vrpprio20",
+                                  "jspperm6x4", "sched8x6"])
 @pytest.mark.parametrize("pop,over,seed", [(16, 4, 42), (5, 3, 2024)])
 def test_device_init_equals_oracle(name, pop, over, seed):
     prob, ref = _pair(name)

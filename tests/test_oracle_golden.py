@@ -177,7 +177,7 @@ def test_multiobjective_run_matches_reference(key):
 
 
 @pytest.mark.parametrize("key", ["assign40", "color40", "binpack30", "loadbal40", "vrpprio20",
-                                 "vrpnl20"])
+                                 "vrpnl20", "jspperm6x4", "sched8x6"])
 def test_extra_builtins_match_reference(key):
     """assignment / graph colouring / bin packing / load balancing / priority and
     nonlinear VRP (builtins.py:193-394): evaluations and a whole run == reference."""
