@@ -45,18 +45,21 @@ def solve_knapsack(weights, values, capacity, time_limit=30.0, **kw) -> RunResul
 
 def solve_custom(encoding, dim2, n=None, compute_obj=None, compute_penalty=None, data=None,
                  custom_operators=(), time_limit=30.0, lb=0, ub=None, maximize=False,
-                 best_known=None, **kw) -> RunResult:
+                 best_known=None, dim1=1, **kw) -> RunResult:
     """PAPER.md:858-868 `cugenopt.solve_custom(encoding=, dim2=, n=, compute_obj=,
-    compute_penalty=, data=, custom_operators=, time_limit=)`: a single-row
-    problem whose objective / penalty are CUDA snippets (see CudaProblem),
+    compute_penalty=, data=, custom_operators=, time_limit=)`: a single-row (or,
+    with dim1 > 1, MULTI_FIXED) problem whose objective / penalty are CUDA
+    snippets (see CudaProblem),
     compiled by NVRTC into the device evolve kernel."""
     if custom_operators:
         raise ValueError("user operators are supported on the TSP path only; custom problems "
                          "run every built-in operator applicable to their encoding")
-    if n is not None and int(n) != int(dim2):
-        raise ValueError("single-row custom problems need n == dim2")
+    # ProblemConfig.n: dim2 values per permutation row, dim1 * dim2 cells otherwise
+    want_n = int(dim2) if encoding == "permutation" else int(dim1) * int(dim2)
+    if n is not None and int(n) != want_n:
+        raise ValueError(f"{encoding} problems with dim1={dim1}, dim2={dim2} need n == {want_n}")
     prob = CudaProblem(encoding, int(dim2), compute_obj, compute_penalty, data, lb=lb, ub=ub,
-                       maximize=maximize)
+                       maximize=maximize, rows=int(dim1))
     kw.setdefault("device_init", True)  # the paper's API initialises on the GPU
     cfg = EngineConfig(time_limit_seconds=time_limit,
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
