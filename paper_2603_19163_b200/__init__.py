@@ -51,9 +51,6 @@ def solve_custom(encoding, dim2, n=None, compute_obj=None, compute_penalty=None,
     with dim1 > 1, MULTI_FIXED) problem whose objective / penalty are CUDA
     snippets (see CudaProblem),
     compiled by NVRTC into the device evolve kernel."""
-    if custom_operators:
-        raise ValueError("user operators are supported on the TSP path only; custom problems "
-                         "run every built-in operator applicable to their encoding")
     # ProblemConfig.n: dim2 values per permutation row, dim1 * dim2 cells otherwise
     want_n = int(dim2) if encoding == "permutation" else int(dim1) * int(dim2)
     if n is not None and int(n) != want_n:
@@ -61,7 +58,7 @@ def solve_custom(encoding, dim2, n=None, compute_obj=None, compute_penalty=None,
     prob = CudaProblem(encoding, int(dim2), compute_obj, compute_penalty, data, lb=lb, ub=ub,
                        maximize=maximize, rows=int(dim1))
     kw.setdefault("device_init", True)  # the paper's API initialises on the GPU
-    cfg = EngineConfig(time_limit_seconds=time_limit,
+    cfg = EngineConfig(time_limit_seconds=time_limit, custom_operators=tuple(custom_operators),
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
     return run(prob, cfg, best_known=best_known)
 

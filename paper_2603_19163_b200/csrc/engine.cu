@@ -194,6 +194,7 @@ struct go_problem {
   int pvar = 0;  // partition variant (RowArgs::pvar)
   // user problems (RK_USER): NVRTC objective module, encoding
   gohost::JitModule user_mod;
+  gohost::UserProblemSrc user_src;  // kept to rebuild the module with user operators
   int enc = 0;
   int mf = 0;  // MULTI_FIXED user rows: 1 permutation rows, 2 binary / integer cells
   // user operators
@@ -538,6 +539,7 @@ int go_problem_create_user(const go_user_problem_desc* d, int device, go_problem
   p->gsize = 2;
   p->img_bytes = img.size();
   std::string jlog;
+  p->user_src = up;
   rc = gohost::jit_build_user(up, &p->user_mod, &jlog);
   if (log && log_len > 0) {
     std::strncpy(log, jlog.c_str(), (size_t)log_len - 1);
@@ -1061,6 +1063,99 @@ int go_jit_compile(int layout, const go_custom_op* ops, int n_ops, char* log, in
   return GO_OK;
 }
 
+}  // extern "C"
+
+// register_custom (operators.py:634-669) for a user problem: each operator is
+// compiled into the problem's NVRTC module on its own (a compile error excludes
+// only it), probed once on the probe solution (a device error or an invalid
+// result excludes it), and the kept ones are built into the problem's module.
+template <class Note>
+static int set_user_problem_ops(go_problem* p, const go_custom_op* ops, int n_ops,
+                                const int32_t* probe_genes, uint64_t probe_seed,
+                                int32_t* status_out, Note note) {
+  std::vector<gohost::UserOpSrc> keep;
+  const int n = p->n;
+  for (int i = 0; i < n_ops; ++i) {
+    status_out[i] = 0;
+    if (ops[i].id < 100) return fail(GO_E_INVALID, "custom operator id must be >= 100");
+    if (!ops[i].cuda_body) {
+      note(i, "no CUDA snippet");
+      continue;
+    }
+    gohost::UserOpSrc s{ops[i].id, ops[i].name ? ops[i].name : "op", ops[i].cuda_body};
+    gohost::UserProblemSrc up = p->user_src;
+    up.ops = {s};
+    gohost::JitModule m;
+    std::string log;
+    if (gohost::jit_build_user(up, &m, &log)) {
+      note(i, "compile failed: " + log.substr(0, 400));
+      continue;
+    }
+    std::vector<short> h(n);
+    for (int j = 0; j < n; ++j) h[j] = (short)probe_genes[j];
+    DevBufs B;
+    short* d_g = nullptr;
+    int* d_e = nullptr;
+    CK(B.get(&d_g, (size_t)n * 2));
+    CK(B.get(&d_e, sizeof(int)));
+    CK(cudaMemcpy(d_g, h.data(), (size_t)n * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d_e, 0, sizeof(int)));
+    auto mix = [](uint64_t hh, uint64_t part) {
+      hh ^= part;
+      hh *= 0xBF58476D1CE4E5B9ull;
+      hh ^= hh >> 27;
+      hh *= 0x94D049BB133111EBull;
+      hh ^= hh >> 31;
+      return hh;
+    };
+    unsigned long long key =
+        mix(mix(mix(0x9E3779B97F4A7C15ull, probe_seed), 4), (uint64_t)ops[i].id);
+    go::RowArgs x = row_args(p);
+    const void* inst = p->d_img;
+    int nn = n, slot = 0;
+    void* args[] = {(void*)&inst, &x, &nn, &slot, &key, &d_g, &d_e};
+    CU(gohost::drv()->LaunchKernel(m.probe_op, 1, 1, 1, 32, 1, 1, 0, 0, args, nullptr));
+    const cudaError_t ce = cudaDeviceSynchronize();
+    gohost::drv()->ModuleUnload(m.mod);
+    if (ce != cudaSuccess) return fail(GO_E_CUDA, std::string("probe kernel: ") + cudaGetErrorString(ce));
+    int err = 0;
+    CK(cudaMemcpy(&err, d_e, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.data(), d_g, (size_t)n * 2, cudaMemcpyDeviceToHost));
+    bool valid = err == 0;
+    if (p->enc == go::ENC_PERM) {  // every row a permutation of 0 .. d2-1
+      for (int r = 0; r < p->d1 && valid; ++r) {
+        std::vector<char> seen(p->d2, 0);
+        for (int j = 0; j < p->d2 && valid; ++j) {
+          const int v = h[(size_t)r * p->d2 + j];
+          if (v < 0 || v >= p->d2 || seen[v]) valid = false;
+          else seen[v] = 1;
+        }
+      }
+    } else {
+      for (int j = 0; j < n && valid; ++j) valid = h[j] >= p->lb && h[j] <= p->ub;
+    }
+    if (!valid) {
+      note(i, err ? "probe raised a device error" : "probe output invalid");
+      continue;
+    }
+    keep.push_back(s);
+    status_out[i] = 1;
+    note(i, "registered");
+  }
+  gohost::UserProblemSrc up = p->user_src;
+  up.ops = keep;
+  gohost::JitModule m;
+  std::string log;
+  const int rc = gohost::jit_build_user(up, &m, &log);
+  if (rc) return fail(rc, "NVRTC build of the user problem with its operators failed: " + log.substr(0, 2000));
+  if (p->user_mod.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod.mod);
+  p->user_mod = m;
+  p->ops = keep;
+  return GO_OK;
+}
+
+extern "C" {
+
 int go_problem_set_custom_ops(go_problem* p, const go_custom_op* ops, int n_ops,
                               const int32_t* probe_genes, const int32_t* probe_sizes,
                               uint64_t probe_seed, int32_t* status_out, char* msg_out,
@@ -1075,6 +1170,11 @@ int go_problem_set_custom_ops(go_problem* p, const go_custom_op* ops, int n_ops,
   auto note = [&](int i, const std::string& m) {
     if (msg_out && msg_len > 0) snprintf(msg_out + (size_t)i * msg_len, msg_len, "%s", m.c_str());
   };
+  if (p->row_kind == go::RK_USER) return set_user_problem_ops(p, ops, n_ops, probe_genes,
+                                                               probe_seed, status_out, note);
+  if (p->family == 1)
+    return fail(GO_E_UNSUPPORTED, "user operators run on the TSP path and on user problems "
+                                  "(CudaProblem), not on the built-in row kernels");
   int layout = 0, E = 0;
   choose_layout(p, 128, 0, &layout, &E);
   // compile each operator on its own first so a broken snippet only excludes
@@ -1169,7 +1269,8 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   e->n = p->n;
   e->W = p->n;
   if (p->family == 1) {
-    if (!p->ops.empty()) return fail(GO_E_UNSUPPORTED, "user operators run on the TSP path only");
+    if (!p->ops.empty() && p->row_kind != go::RK_USER)
+      return fail(GO_E_UNSUPPORTED, "user operators run on the TSP path and on user problems");
     if (!choose_row(p, e->TS, c->teams_per_cta, &e->layout, &e->E, &e->smem))
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
     e->inst = p->d_img;

@@ -293,8 +293,20 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
       << "template <class Sol> __device__ __forceinline__ double compute_penalty(const Sol& sol, "
          "const Data& data) {\n#line 1 \"@OPDIR@/compute_penalty.cuh\"\n"
       << (up.pen.empty() ? std::string("return 0.0;") : up.pen) << "\n}\n"
-      << "}  // namespace user\n"
+      ;
+  for (size_t i = 0; i < up.ops.size(); ++i)
+    src << "// user operator " << up.ops[i].id << " (" << up.ops[i].name << ")\n"
+        << "template <class Ctx> __device__ __forceinline__ void op_slot" << i
+        << "(Ctx& ctx, const Data& data) {\n#line 1 \"@OPDIR@/" << up.ops[i].name << ".cuh\"\n"
+        << up.ops[i].body << "\n}\n";
+  src << "}  // namespace user\n"
       << "struct UserProblem {\n"
+      << "  template <class C> __device__ __forceinline__ static void op(int slot, C& ctx, "
+         "const unsigned char* b) {\n"
+      << "    const user::Data data = user::make_data(b);\n    (void)data;\n    switch (slot) {\n";
+  for (size_t i = 0; i < up.ops.size(); ++i)
+    src << "      case " << i << ": user::op_slot" << i << "(ctx, data); break;\n";
+  src << "      default: ctx.err() |= ERR_UNKNOWN_SEQ;\n    }\n  }\n"
       << "  template <class S> __device__ __forceinline__ static double obj(const S& s, "
          "const unsigned char* b) { return user::compute_obj(s, user::make_data(b)); }\n"
       << "  template <class S> __device__ __forceinline__ static double pen(const S& s, "
@@ -302,6 +314,7 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
       << "};\n}  // namespace go\nGO_USER_KERNELS(go::UserProblem)\n";
   std::vector<UserOpSrc> files = {{0, "compute_obj", up.obj},
                                   {1, "compute_penalty", up.pen.empty() ? "return 0.0;" : up.pen}};
+  for (const auto& op : up.ops) files.push_back(op);
   std::string cubin;
   bool hit = false;
   int rc = jit_compile_source(src.str(), files, &cubin, &out->key, &hit, log);
@@ -319,8 +332,9 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
     return GO_E_CUDA;
   }
   if (d->ModuleGetFunction(&out->evolve, out->mod, "go_evolve_user") != CUDA_SUCCESS ||
-      d->ModuleGetFunction(&out->probe, out->mod, "go_eval_user") != CUDA_SUCCESS) {
-    *log = "JIT module lacks go_evolve_user / go_eval_user";
+      d->ModuleGetFunction(&out->probe, out->mod, "go_eval_user") != CUDA_SUCCESS ||
+      d->ModuleGetFunction(&out->probe_op, out->mod, "go_probe_user_op") != CUDA_SUCCESS) {
+    *log = "JIT module lacks go_evolve_user / go_eval_user / go_probe_user_op";
     return GO_E_COMPILE;
   }
   out->cache_hit = hit;

@@ -17,6 +17,7 @@ struct JitModule {
   CUmodule mod = nullptr;
   CUfunction evolve = nullptr;
   CUfunction probe = nullptr;
+  CUfunction probe_op = nullptr;  // user problems: go_probe_user_op
   std::string key;
   double compile_seconds = 0.0;
   bool cache_hit = false;
@@ -43,6 +44,7 @@ struct UserProblemSrc {
   std::vector<std::string> names;
   std::vector<unsigned long long> offsets;
   std::vector<long long> lens;
+  std::vector<UserOpSrc> ops;  // user operators, compiled in as slots 0..n-1
 };
 // Builds go_evolve_user (JitModule::evolve) and go_eval_user (JitModule::probe).
 int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log);

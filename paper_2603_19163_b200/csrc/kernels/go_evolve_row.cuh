@@ -61,6 +61,10 @@ struct NoUser {  // built-in kinds: never called
   __device__ __forceinline__ static double obj(const S&, const unsigned char*) { return 0.0; }
   template <class S>
   __device__ __forceinline__ static double pen(const S&, const unsigned char*) { return 0.0; }
+  template <class C>
+  __device__ __forceinline__ static void op(int, C& ctx, const unsigned char*) {
+    ctx.err() |= ERR_UNKNOWN_SEQ;
+  }
 };
 
 // scalar_fitness (engine.py:215-222) of one objective + penalty, rounding each product
@@ -68,6 +72,35 @@ __device__ __forceinline__ double user_phi(double obj, double pen, double w, int
                                            double pw) {
   return __dadd_rn(__dadd_rn(0.0, __dmul_rn(w, maximize ? -obj : obj)), __dmul_rn(pw, pen));
 }
+
+// What a user operator snippet on a row problem sees as `ctx` (the reference's
+// CustomOperator.apply(sol, rng, ctx), operators.py:79-88): the lane's candidate
+// (d1 x d2 genes, row-major, flat index i < ctx.n), the lane stream with
+// CPython's draw algorithms, and Φ of the candidate (the `ctx.phi` the reference
+// hands operators, engine.py:215-222) through the problem's own objective.
+template <class G, class U>
+struct RowOpCtx {
+  RowCtx<G>* c;
+  const unsigned char* inst;
+  double w, pw;
+  int maximize;
+  int n, rows, width;  // flat genes, d1, d2
+  __device__ __forceinline__ int get(int i) const { return c->full[i]; }
+  __device__ __forceinline__ void set(int i, int v) { c->full[i] = (G)v; }
+  __device__ __forceinline__ void swap(int i, int j) {
+    const G t = c->full[i];
+    c->full[i] = c->full[j];
+    c->full[j] = t;
+  }
+  __device__ __forceinline__ int randbelow(int k) { return c->rng.randbelow(k); }
+  __device__ __forceinline__ int randrange(int a, int b) { return c->rng.randrange(a, b); }
+  __device__ __forceinline__ double random() { return c->rng.random(); }
+  __device__ __forceinline__ double phi() const {
+    const RowSol<G> s{c->full, n};
+    return user_phi(U::obj(s, inst), U::pen(s, inst), w, maximize, pw);
+  }
+  __device__ __forceinline__ int& err() { return c->err; }
+};
 
 // Instance views (all in shared memory once staged; `use_s` reads via ld.shared).
 template <class E>
@@ -1449,6 +1482,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           } else if (kind == SEQ_UNIFORM_X) {  // warp-resolved below
             la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
             pending = true;
+          } else if (KIND == RK_USER && kind >= SEQ_CUSTOM_BASE) {  // user operator
+            RowOpCtx<G, U> oc{&c, inst, X.obj_weight, pwt, X.maximize, n, c.d1, X.d2};
+            U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
+            c.mark_all();
           } else {
             run_row_op(kind, c);
           }

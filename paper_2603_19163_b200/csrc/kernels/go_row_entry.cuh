@@ -115,6 +115,37 @@ __device__ __forceinline__ void user_eval_entry(const void* inst, int n, int m,
   pen[i] = U::pen(sol, (const unsigned char*)inst);
 }
 
+// One application of user operator `slot` to a probe row (register_custom's
+// probe, operators.py:646-665): single thread, stream key `key`; the host
+// checks the row's validity and the error flag.
+template <class U>
+__device__ __forceinline__ void user_probe_entry(const void* inst, RowArgs x, int n, int slot,
+                                                 unsigned long long key, short* genes, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  RowCtx<short> c;
+  c.rng.init(key);
+  c.row = genes;
+  c.full = genes;
+  c.mf = x.mf;
+  c.d1 = x.mf ? x.d1 : 1;
+  c.d2 = x.d2;
+  c.n = n;
+  c.n_cfg = x.n_cfg;
+  c.lb = x.lb;
+  c.ub = x.ub;
+  short dummy[MAX_RANGES * 2];
+  c.rlo = dummy;
+  c.rhi = dummy + MAX_RANGES;
+  c.rstride = 1;
+  c.nr = 0;
+  c.err = 0;
+  c.mates = nullptr;
+  RowOpCtx<short, U> oc{&c, (const unsigned char*)inst, x.obj_weight, x.penalty_weight,
+                        x.maximize, n, c.d1, x.d2};
+  U::op(slot, oc, (const unsigned char*)inst);
+  *err = c.err;
+}
+
 }  // namespace go
 
 // Kernels of one NVRTC user problem (go_jit.cpp generates `U`).
@@ -126,6 +157,10 @@ __device__ __forceinline__ void user_eval_entry(const void* inst, int n, int m,
   extern "C" __global__ void go_eval_user(const void* inst, int n, int m, const short* g,     \
                                           double* obj, double* pen) {                          \
     go::user_eval_entry<U>(inst, n, m, g, obj, pen);                                          \
+  }                                                                                           \
+  extern "C" __global__ void go_probe_user_op(const void* inst, go::RowArgs x, int n, int slot, \
+                                              unsigned long long key, short* g, int* err) {   \
+    go::user_probe_entry<U>(inst, x, n, slot, key, g, err);                                   \
   }
 
 #define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \

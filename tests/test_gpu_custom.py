@@ -203,3 +203,94 @@ def test_multi_fixed_rows_operator_mixes(key, ops):
     assert res.history["best_phi"] == out.history["best_phi"]
     assert [[s.row(r).tolist() for r in range(s.d1)] for s in res.population] == \
         [[s.row(r).tolist() for r in range(s.d1)] for s in out.population]
+
+
+# ---- user operators on user problems (CustomOperator, operators.py:79-88, :634-669) --------
+SWAP_KICK = """
+  const int i = ctx.randbelow(ctx.n), j = ctx.randbelow(ctx.n);
+  if (i != j) ctx.swap(i, j);
+  if (ctx.random() < 0.3) {
+    const int k = ctx.randrange(0, ctx.n);
+    ctx.swap(k, k + 1 == ctx.n ? 0 : k + 1);
+  }
+"""
+GREEDY_FLIP = """
+  double best = 0.0;
+  int bi = -1;
+  for (int t = 0; t < 3; ++t) {  // best of three single flips, scored by ctx.phi()
+    const int p = ctx.randbelow(ctx.n);
+    ctx.set(p, 1 - ctx.get(p));
+    const double f = ctx.phi();
+    ctx.set(p, 1 - ctx.get(p));
+    if (bi < 0 || f < best) { best = f; bi = p; }
+  }
+  ctx.set(bi, 1 - ctx.get(bi));
+"""
+BROKEN = "ctx.set(0, ctx.get(0) + ;"
+OUT_OF_RANGE = "ctx.set(0, 7);"  # leaves the encoding: excluded by the probe
+
+
+def _swap_kick_py(sol, rng, ctx):
+    row = sol.data[0]
+    n = len(row)
+    i, j = rng.randrange(n), rng.randrange(n)
+    if i != j:
+        row[i], row[j] = row[j], row[i]
+    if rng.random() < 0.3:
+        k = rng.randrange(0, n)
+        k2 = 0 if k + 1 == n else k + 1
+        row[k], row[k2] = row[k2], row[k]
+
+
+def _greedy_flip_py(sol, rng, ctx):
+    row = sol.data[0]
+    best, bi = 0.0, -1
+    for _ in range(3):
+        p = rng.randrange(len(row))
+        row[p] = 1 - row[p]
+        f = ctx.phi(sol)
+        row[p] = 1 - row[p]
+        if bi < 0 or f < best:
+            best, bi = f, p
+    row[bi] = 1 - row[bi]
+
+
+@pytest.mark.parametrize("name,ops,P,T,Gn,seed", [
+    ("tour", [(100, "swap_kick", SWAP_KICK, _swap_kick_py, 2.0)], 4, 32, 15, 5),
+    ("knap", [(100, "greedy_flip", GREEDY_FLIP, _greedy_flip_py, 1.0),
+              (101, "broken", BROKEN, None, 1.0), (102, "oob", OUT_OF_RANGE, None, 1.0)],
+     4, 32, 15, 6)])
+def test_user_operators_on_user_problems(name, ops, P, T, Gn, seed):
+    """CUDA-snippet operators compete in AOS on a user problem; compile errors and
+    invalid probe outputs exclude only that operator (operators.py:649-665); the
+    run is bit-identical to the oracle with the Python restatements."""
+    prob, ref = _cases()[name]
+    cops = tuple(G.CustomOperator(i, nm, initial_weight=w, cuda=src) for i, nm, src, _, w in ops)
+    with pytest.warns(RuntimeWarning) if len(ops) > 1 else _nullcontext():
+        res = G.run(prob, G.EngineConfig(population=P, team_size=T, max_generations=Gn,
+                                         seed=seed, record_history=True, custom_operators=cops))
+    kept = [(i, nm, fn, w) for i, nm, _, fn, w in ops if fn is not None]
+    assert [e["id"] for e in res.final_weights["sequences"]][-len(kept):] == [k[0] for k in kept]
+    out = OE.run(ref, OE.RunCfg(population=P, team_size=T, max_generations=Gn, seed=seed,
+                                record_history=True, allowed_ops=prob.device_sequences(),
+                                custom_ops=tuple(kept)), device_stream="philox")
+    assert res.history["best_phi"] == out.history["best_phi"]
+    assert [e["weight"] for e in res.final_weights["sequences"]] == [float(w) for w in out.weights]
+    assert [s.row(0).tolist() for s in res.population] == [s.row(0).tolist() for s in out.population]
+
+
+class _nullcontext:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def test_solve_custom_with_user_operators():
+    d = I.tsp_random(20, 3, True)
+    r = G.solve_custom(encoding="permutation", dim2=20, compute_obj=TOUR, data={"dist": d},
+                       custom_operators=[G.CustomOperator(100, "swap_kick", cuda=SWAP_KICK)],
+                       time_limit=2.0, max_generations=200)
+    assert any(e["id"] == 100 for e in r.final_weights["sequences"])
+    assert r.feasible and sorted(r.best.row(0).tolist()) == list(range(20))

@@ -127,8 +127,7 @@ def test_custom_problem_host_side():
     with pytest.raises(ValueError):
         G.CudaProblem("integer", 4, "return 0.0;")  # integer needs ub
     with pytest.raises(ValueError):
-        G.solve_custom("binary", 4, compute_obj="return 0.0;",
-                       custom_operators=[G.CustomOperator(100, "x", cuda="")])
+        G.solve_custom("binary", 4, n=5, compute_obj="return 0.0;")  # n must be 4
 
 
 def test_result_record_schema_round_trip():
