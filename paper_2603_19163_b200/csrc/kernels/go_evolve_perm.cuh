@@ -432,6 +432,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
               bp = op;
             }
           }
+          __syncwarp();  // every lane has read the request before lane 0 rewrites it
           if (wl == 0) {
             rd_pos += (unsigned)m + 3u;
             rd_elem += (len == 1 ? 2u : 3u) * (unsigned)m + 1u;
@@ -489,6 +490,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
             bits = META_MAT | (nsel ? META_SEL : 0u);
             nm2 = 0;
           }
+          __syncwarp();  // every lane has read la.pos / la.meta before lane 0 updates them
           if (wl == 0) {
             if (s + 1 < k) {
               const int nq = sample_seq(s_cum, nseq, total, rng);

@@ -1095,6 +1095,7 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       c.cell_at(gi, r0, p0);
       c.remove(r0, p0);
     }
+    team_bar(team, TS);  // the trials below read the row without v
     PartCache pc;
     const bool cached = pv.variant == 0 && 32 + PartCache::doubles(d1, n_cells) <= 5 * TS;
     pc.bind(sbuf + 32, d1);
