@@ -1516,6 +1516,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           rng.seek(la.pos[L]);
           int lo, hi;
           const u32 pend = warp_uniform_x((G*)(rows + (size_t)L * rs), n, ms, rng, wl, lo, hi);
+          __syncwarp();  // every lane has read la.pos before lane 0 updates it
           if (wl == 0) {
             rng.seek(pend);
             const u32 meta = la.meta[L];

@@ -31,6 +31,29 @@ runs["vrptw"] = G.builtin_problem("vrptw", G.InstanceData(
     distance_matrix=vd.dist, demands=vd.demands, capacity=vd.capacity, vehicles=vd.vehicles,
     ready_times=vd.ready, due_times=vd.due, service_times=vd.service))
 runs["jsp_perm"] = G.builtin_problem("jsp_perm", G.InstanceData(jobs=I.jsp_random(5, 4, 11)))
+runs["vrp_priority"] = G.builtin_problem("vrp_priority", G.InstanceData(
+    distance_matrix=vd.dist, demands=vd.demands, capacity=vd.capacity, vehicles=vd.vehicles,
+    priorities=np.arange(20) % 3))
+runs["cvrp_lex"] = G.builtin_problem("cvrp", G.InstanceData(
+    distance_matrix=vd.dist, demands=vd.demands, capacity=vd.capacity, vehicles=vd.vehicles,
+    meta={"objectives": ("distance", "vehicles"),
+          "comparison": G.Lexicographic((1, 0), (0.0, 0.0))}))
+runs["schedule"] = G.builtin_problem("schedule_binary", G.InstanceData(
+    cost_matrix=np.arange(24.0).reshape(6, 4) % 7 + 1, requirements=np.array([2.0, 1, 3, 1])))
+# guided-rebuild / crossover dominated registries (the rare whole-row paths)
+GR_HEAVY = {"tsp": (16, 12, 0), "qap": (16, 12), "knap": (16, 13), "jsp": (16, 13),
+            "vrptw": (16, 12, 9), "vrp_priority": (16, 15, 10), "jsp_perm": (16, 12, 15),
+            "schedule": (16, 13, 6)}
+for name, ops in GR_HEAVY.items():
+    prob = runs[name]
+    prob.device_sequences = (lambda o: lambda: o)(ops)
+    r = G.run(prob, G.EngineConfig(population=4, team_size=32, max_generations=4, seed=5,
+                                   islands=G.IslandsConfig(count=2, migration="hybrid",
+                                                           interval=2)))
+    print(f"{name} GR-heavy {ops}: {r.objectives} err {r.device.get('error_flags')}", flush=True)
+for name, prob in runs.items():
+    if name in GR_HEAVY:
+        del prob.device_sequences  # back to the class's full registry
 for name, prob in runs.items():
     ops = G.tsp_delta_operators() if name == "tsp" else ()
     r = G.run(prob, G.EngineConfig(custom_operators=ops, **cfg))
