@@ -338,7 +338,10 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "move evals/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(h2d),
                 "path": "go_engine_set_population(host) + go_engine_run + "
-                        "go_engine_get_population(host) per step"},
+                        "go_engine_get_population(host) per step",
+                "l2": "not flushed between e2e steps (host copies take the flush's place); the "
+                      "device-timed value flushes L2, so its steps start with cold L2 and "
+                      "instruction fetch"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                      "frac": achieved_gbs / hbm, "traffic": ncu_traffic(),
