@@ -114,6 +114,7 @@ typedef struct go_user_problem_desc {
   const int64_t* data_lens;
   int32_t rows;                   /* 0 or 1: one row; > 1: MULTI_FIXED rows of n genes each
                                    * (core.py:28-35), sol[r * n + i] in the snippets */
+  const char* compute_obj2;       /* second objective's snippet body, or NULL (one objective) */
 } go_user_problem_desc;
 
 typedef struct go_problem go_problem;
@@ -154,6 +155,7 @@ typedef struct go_engine_config {
   int32_t lex;
   int32_t lex_first;
   double lex_tol[2];
+  int32_t maximize2;      /* direction of the second objective (two-objective user problems) */
 } go_engine_config;
 
 typedef struct go_run_stats {

@@ -400,14 +400,22 @@ class Custom(Problem):
     problems.py:49-74).  `obj(row)` / `pen(row)` restate the test's CUDA snippet
     in Python with the same arithmetic order (test infrastructure only)."""
 
-    def __init__(self, kind, n, obj, pen=None, lb=0, ub=0, maximize=False, mats=()):
+    def __init__(self, kind, n, obj, pen=None, lb=0, ub=0, maximize=False, mats=(),
+                 weights=None, lex=None):
+        # obj: one function or a list of two (core.py:69-106: per-objective
+        # direction and weight; lex = (priority_order, tolerances))
         self.n = n
-        self.spec = Spec(kind, 1, n, n, SINGLE, directions=(MAX if maximize else MIN,),
-                         lb=lb, ub=ub)
-        self._obj, self._pen, self._mats = obj, pen, [np.asarray(m, np.float64) for m in mats]
+        objs = list(obj) if isinstance(obj, (list, tuple)) else [obj]
+        maxes = [maximize] * len(objs) if isinstance(maximize, bool) else list(maximize)
+        self.spec = Spec(kind, 1, n, n, SINGLE,
+                         directions=tuple(MAX if mx else MIN for mx in maxes),
+                         weights=tuple(weights) if weights else (1.0,) * len(objs),
+                         lb=lb, ub=ub, lex=lex)
+        self._objs, self._pen = objs, pen
+        self._mats = [np.asarray(m, np.float64) for m in mats]
 
     def objective(self, i, sol):
-        return float(self._obj(sol.row(0)))
+        return float(self._objs[i](sol.row(0)))
 
     def penalty(self, sol):
         return float(self._pen(sol.row(0))) if self._pen is not None else 0.0

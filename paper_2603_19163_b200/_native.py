@@ -64,7 +64,7 @@ class UserProblemDesc(C.Structure):  # go_user_problem_desc
                 ("compute_obj", C.c_char_p), ("compute_penalty", C.c_char_p),
                 ("n_data", C.c_int32), ("data_names", C.POINTER(C.c_char_p)),
                 ("data", C.POINTER(_PD)), ("data_lens", C.POINTER(C.c_int64)),
-                ("rows", C.c_int32)]
+                ("rows", C.c_int32), ("compute_obj2", C.c_char_p)]
 
 
 class CustomOp(C.Structure):
@@ -83,7 +83,7 @@ class EngineConfig(C.Structure):
                 ("has_target", C.c_int32), ("target_objective", C.c_double),
                 ("evolver_offset", C.c_int32), ("maximize", C.c_int32),
                 ("obj_weight", C.c_double), ("obj_weight2", C.c_double), ("lex", C.c_int32),
-                ("lex_first", C.c_int32), ("lex_tol", C.c_double * 2)]
+                ("lex_first", C.c_int32), ("lex_tol", C.c_double * 2), ("maximize2", C.c_int32)]
 
 
 class RunStats(C.Structure):

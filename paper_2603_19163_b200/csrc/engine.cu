@@ -510,6 +510,7 @@ int go_problem_create_user(const go_user_problem_desc* d, int device, go_problem
   gohost::UserProblemSrc up;
   up.obj = d->compute_obj;
   up.pen = d->compute_penalty ? d->compute_penalty : "";
+  up.obj2 = d->compute_obj2 ? d->compute_obj2 : "";
   std::vector<unsigned char> img;
   for (int i = 0; i < d->n_data; ++i) {
     if (!c_identifier(d->data_names[i]) || d->data_lens[i] < 0 ||
@@ -532,6 +533,7 @@ int go_problem_create_user(const go_user_problem_desc* d, int device, go_problem
   p->d1 = rows;
   p->d2 = d->n;
   p->mf = rows > 1 ? (d->encoding == 0 ? 1 : 2) : 0;
+  p->n_obj = d->compute_obj2 ? 2 : 1;
   p->enc = d->encoding;
   p->lb = d->encoding == 0 ? 0 : (d->encoding == 1 ? 0 : d->lb);
   p->ub = d->encoding == 0 ? d->n - 1 : (d->encoding == 1 ? 1 : d->ub);
@@ -1308,11 +1310,13 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   e->mo.m = p->n_obj;
   e->mo.lex = c->lex ? 1 : 0;
   e->mo.first = c->lex_first == 1 ? 1 : 0;
+  e->mo.maxmask = (c->maximize ? 1 : 0) | (c->maximize2 ? 2 : 0);
   e->mo.tol[0] = c->lex_tol[0];
   e->mo.tol[1] = c->lex_tol[1];
   const bool multi = p->n_obj == 2 || e->mo.lex;
-  if (multi && !(p->family == 1 && p->row_kind == go::RK_PART))
-    return fail(GO_E_UNSUPPORTED, "multi-objective / Lexicographic runs: routing problems only");
+  if (multi && !(p->family == 1 && (p->row_kind == go::RK_PART || p->row_kind == go::RK_USER)))
+    return fail(GO_E_UNSUPPORTED,
+                "multi-objective / Lexicographic runs: routing and user problems only");
   if (e->mo.first >= e->mo.m) return fail(GO_E_INVALID, "lex_first outside the objectives");
 
   // per-thread stack: the row kernels' guided rebuild nests numpy's recursive
@@ -1454,7 +1458,7 @@ int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* 
   for (size_t i = 0; i < P; ++i) {
     const double o0 = obj[i * m], o1 = m == 2 ? obj[i * m + 1] : 0.0;
     sc[i] = 0.0 + w * (e->cfg.maximize ? -o0 : o0);  // scalarize (core.py:303-307)
-    if (m == 2) sc[i] = sc[i] + e->cfg.obj_weight2 * o1;
+    if (m == 2) sc[i] = sc[i] + e->cfg.obj_weight2 * (e->cfg.maximize2 ? -o1 : o1);
     o2[2 * i] = o0;
     o2[2 * i + 1] = o1;
     pe[i] = pen ? pen[i] : 0.0;
@@ -1468,7 +1472,7 @@ int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* 
       const int i = k == 0 ? e->mo.first : 1 - e->mo.first;
       const double x = o2[2 * a + i], y = o2[2 * b + i];
       if (std::fabs(x - y) <= e->mo.tol[i]) continue;
-      return x < y ? -1 : 1;
+      return (x < y) != ((e->mo.maxmask >> i & 1) != 0) ? -1 : 1;  // low wins unless Maximize
     }
     return 0;
   };
@@ -1647,6 +1651,9 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     end = std::min(end, next_mult(done, EI));
     if (c.islands >= 2) end = std::min(end, next_mult(done, MI));
     if (e->xover && !e->coop) end = done + 1;  // launch boundary = snapshot barrier
+    // Lexicographic runs: the global best's genes are taken from the current
+    // rows at the end of a one-generation chunk (go_epilogue.cuh)
+    if (e->mo.lex) end = done + 1;
     const int slot = (int)(chunk % go_engine::kDepth);
     if (chunk >= go_engine::kDepth) {
       CK(cudaEventSynchronize(e->ring_ev[slot]));

@@ -293,7 +293,9 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
       << "template <class Sol> __device__ __forceinline__ double compute_penalty(const Sol& sol, "
          "const Data& data) {\n#line 1 \"@OPDIR@/compute_penalty.cuh\"\n"
       << (up.pen.empty() ? std::string("return 0.0;") : up.pen) << "\n}\n"
-      ;
+      << "template <class Sol> __device__ __forceinline__ double compute_obj2(const Sol& sol, "
+         "const Data& data) {\n#line 1 \"@OPDIR@/compute_obj2.cuh\"\n"
+      << (up.obj2.empty() ? std::string("return 0.0;") : up.obj2) << "\n}\n";
   for (size_t i = 0; i < up.ops.size(); ++i)
     src << "// user operator " << up.ops[i].id << " (" << up.ops[i].name << ")\n"
         << "template <class Ctx> __device__ __forceinline__ void op_slot" << i
@@ -307,6 +309,9 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
   for (size_t i = 0; i < up.ops.size(); ++i)
     src << "      case " << i << ": user::op_slot" << i << "(ctx, data); break;\n";
   src << "      default: ctx.err() |= ERR_UNKNOWN_SEQ;\n    }\n  }\n"
+      << "  static constexpr int kObjectives = " << (up.obj2.empty() ? 1 : 2) << ";\n"
+      << "  template <class S> __device__ __forceinline__ static double obj2(const S& s, "
+         "const unsigned char* b) { return user::compute_obj2(s, user::make_data(b)); }\n"
       << "  template <class S> __device__ __forceinline__ static double obj(const S& s, "
          "const unsigned char* b) { return user::compute_obj(s, user::make_data(b)); }\n"
       << "  template <class S> __device__ __forceinline__ static double pen(const S& s, "
@@ -314,6 +319,7 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
       << "};\n}  // namespace go\nGO_USER_KERNELS(go::UserProblem)\n";
   std::vector<UserOpSrc> files = {{0, "compute_obj", up.obj},
                                   {1, "compute_penalty", up.pen.empty() ? "return 0.0;" : up.pen}};
+  if (!up.obj2.empty()) files.push_back({2, "compute_obj2", up.obj2});
   for (const auto& op : up.ops) files.push_back(op);
   std::string cubin;
   bool hit = false;

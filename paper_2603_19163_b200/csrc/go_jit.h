@@ -40,7 +40,7 @@ int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& op
 // A user problem: objective / penalty snippet bodies and the named float64
 // data arrays they read (byte offsets into the instance image).
 struct UserProblemSrc {
-  std::string obj, pen;
+  std::string obj, pen, obj2;  // obj2 empty: one objective
   std::vector<std::string> names;
   std::vector<unsigned long long> offsets;
   std::vector<long long> lens;

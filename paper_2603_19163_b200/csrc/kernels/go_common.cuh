@@ -428,7 +428,7 @@ struct MoCmp {
   int m;       // objectives (1 or 2)
   int lex;
   int first;   // priority_order[0]
-  int pad;
+  int maxmask; // bit i: objective i is Maximize (core.py:69-77)
   double tol[2];
 };
 
@@ -445,7 +445,7 @@ __device__ __forceinline__ int compare_mo(double pa, double sa, double a0, doubl
     const int i = k == 0 ? mo.first : 1 - mo.first;
     const double x = i == 0 ? a0 : a1, y = i == 0 ? b0 : b1;
     if (fabs(__dsub_rn(x, y)) <= mo.tol[i]) continue;
-    return x < y ? -1 : 1;
+    return (x < y) != ((mo.maxmask >> i & 1) != 0) ? -1 : 1;  // low wins unless Maximize
   }
   return 0;
 }
@@ -459,7 +459,7 @@ __device__ __forceinline__ double lex_delta(double c0, double c1, double cpen, d
     const int i = k == 0 ? mo.first : 1 - mo.first;
     const double diff = __dsub_rn(i == 0 ? c0 : c1, i == 0 ? u0 : u1);
     if (fabs(diff) <= mo.tol[i]) continue;
-    d = diff;
+    d = (mo.maxmask >> i & 1) ? -diff : diff;
     break;
   }
   return __dadd_rn(d, __dmul_rn(pw, __dsub_rn(cpen, upen)));

@@ -65,6 +65,26 @@ __device__ Cand block_select(const SolKeys& K, int lo, int hi, const int* excl, 
   Cand c;
   c.idx = 0x7fffffff;
   c.pen = c.scal = c.o0 = c.o1 = 0;
+  if (mo.lex) {
+    // Lexicographic comparison with tolerances is not transitive, so the
+    // result depends on the scan order: thread 0 scans in index order like
+    // best_index / worst_index (engine.py:467-480), strict improvements only
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = lo; i < hi; ++i) {
+        bool skip = false;
+        for (int e = 0; e < nexcl; ++e) skip |= excl[e] == i;
+        if (skip) continue;
+        const Cand x = K.at(i);
+        if (c.idx == 0x7fffffff || (WORST ? cand_cmp(x, c, mo) > 0 : cand_cmp(x, c, mo) < 0)) c = x;
+      }
+      red[0] = c;
+    }
+    __syncthreads();
+    const Cand r = red[0];
+    __syncthreads();
+    return r;
+  }
   for (int i = lo + (int)threadIdx.x; i < hi; i += blockDim.x) {
     bool skip = false;
     for (int e = 0; e < nexcl; ++e) skip |= excl[e] == i;
@@ -177,19 +197,31 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
     const long long g = A.gen0 + gi;
     const SolKeys rec{A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
                       A.rec_obj2 ? A.rec_obj2 + (size_t)gi * P * 2 : nullptr};
-    const Cand b = block_select<false>(rec, 0, P, nullptr, 0, red, mo);
+    // engine.py:703-708: each evolver in order against the running global best
+    // (a population argmin is the same thing unless the comparison is the
+    // non-transitive Lexicographic one)
+    const Cand b = mo.lex ? Cand{} : block_select<false>(rec, 0, P, nullptr, 0, red, mo);
     if (threadIdx.x == 0) {
-      if (cand_cmp(b, gbest_cand(gs), mo) < 0) {
-        gs->gpen = b.pen;
-        gs->gscal = b.scal;
-        gs->gobj[0] = b.o0;
-        gs->gobj[1] = b.o1;
-        gs->gev = b.idx;
+      bool improved = false;
+      auto take = [&](const Cand& x) {
+        gs->gpen = x.pen;
+        gs->gscal = x.scal;
+        gs->gobj[0] = x.o0;
+        gs->gobj[1] = x.o1;
+        gs->gev = x.idx;
         gs->ggen = g;
-        gs->stall = 0;
-      } else {
-        gs->stall += 1;
+        improved = true;
+      };
+      if (mo.lex) {
+        for (int ev = 0; ev < P; ++ev) {
+          const Cand x = rec.at(ev);
+          if (cand_cmp(x, gbest_cand(gs), mo) < 0) take(x);
+        }
+      } else if (cand_cmp(b, gbest_cand(gs), mo) < 0) {
+        take(b);
       }
+      if (improved) gs->stall = 0;
+      else gs->stall += 1;
       gs->gens_done = g;
       if (A.history && g - 1 < A.hist_cap) {
         A.history[g - 1] = __dadd_rn(gs->gscal, __dmul_rn(A.pw, gs->gpen));
@@ -205,9 +237,12 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
     last = g;
     if (s_stop) break;
   }
-  // the global best's genes: the team best-ever of its evolver
+  // the global best's genes: the team best-ever of its evolver.
+  // Under the non-transitive Lexicographic comparison a new global best need
+  // not be its team's best-ever; those runs use one-generation chunks and take
+  // the evolver's current row instead.
   if (gs->gev >= 0) {
-    copy_genes(A.gbest_genes, A.best_genes + (size_t)gs->gev * A.W, A.W);
+    copy_genes(A.gbest_genes, (mo.lex ? A.genes : A.best_genes) + (size_t)gs->gev * A.W, A.W);
     __syncthreads();
     if (threadIdx.x == 0) gs->gev = -1;
   }

@@ -61,17 +61,34 @@ struct NoUser {  // built-in kinds: never called
   __device__ __forceinline__ static double obj(const S&, const unsigned char*) { return 0.0; }
   template <class S>
   __device__ __forceinline__ static double pen(const S&, const unsigned char*) { return 0.0; }
+  template <class S>
+  __device__ __forceinline__ static double obj2(const S&, const unsigned char*) { return 0.0; }
   template <class C>
   __device__ __forceinline__ static void op(int, C& ctx, const unsigned char*) {
     ctx.err() |= ERR_UNKNOWN_SEQ;
   }
 };
 
-// scalar_fitness (engine.py:215-222) of one objective + penalty, rounding each product
-__device__ __forceinline__ double user_phi(double obj, double pen, double w, int maximize,
-                                           double pw) {
-  return __dadd_rn(__dadd_rn(0.0, __dmul_rn(w, maximize ? -obj : obj)), __dmul_rn(pw, pen));
-}
+
+// scalar_fitness of a user solution view with one or two objectives
+// (engine.py:215-222): Σ w_i·(±obj_i) from 0.0, then + pw·penalty
+struct UserScore {
+  const unsigned char* inst;
+  double w, pw;
+  int maximize;  // bit 0 / bit 1: objective 0 / 1 is Maximize
+  double w2;
+  int m;
+  template <class U, class S>
+  __device__ __forceinline__ double phi(const S& s) const {
+    const double o0 = U::obj(s, inst);
+    double sc = __dadd_rn(0.0, __dmul_rn(w, (maximize & 1) ? -o0 : o0));
+    if (m == 2) {
+      const double o1 = U::obj2(s, inst);
+      sc = __dadd_rn(sc, __dmul_rn(w2, (maximize & 2) ? -o1 : o1));
+    }
+    return __dadd_rn(sc, __dmul_rn(pw, U::pen(s, inst)));
+  }
+};
 
 // What a user operator snippet on a row problem sees as `ctx` (the reference's
 // CustomOperator.apply(sol, rng, ctx), operators.py:79-88): the lane's candidate
@@ -81,9 +98,7 @@ __device__ __forceinline__ double user_phi(double obj, double pen, double w, int
 template <class G, class U>
 struct RowOpCtx {
   RowCtx<G>* c;
-  const unsigned char* inst;
-  double w, pw;
-  int maximize;
+  UserScore us;
   int n, rows, width;  // flat genes, d1, d2
   __device__ __forceinline__ int get(int i) const { return c->full[i]; }
   __device__ __forceinline__ void set(int i, int v) { c->full[i] = (G)v; }
@@ -97,7 +112,7 @@ struct RowOpCtx {
   __device__ __forceinline__ double random() { return c->rng.random(); }
   __device__ __forceinline__ double phi() const {
     const RowSol<G> s{c->full, n};
-    return user_phi(U::obj(s, inst), U::pen(s, inst), w, maximize, pw);
+    return us.template phi<U>(s);
   }
   __device__ __forceinline__ int& err() { return c->err; }
 };
@@ -646,11 +661,6 @@ __device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& 
 
 // user objectives: guided rebuild trials scored by the NVRTC-compiled objective
 // on virtual rows (no copies), in parallel over the team
-struct UserScore {
-  const unsigned char* inst;
-  double w, pw;
-  int maximize;
-};
 
 template <class U, class G>
 __device__ void team_gr_user_perm(G* full, int ntot, int off, int n, const GrShared& g,
@@ -671,8 +681,7 @@ __device__ void team_gr_user_perm(G* full, int ntot, int off, int n, const GrSha
     int bi = 0x7fffffff;
     for (int pos = lane; pos < n; pos += TS) {  // ascending per thread: first minimum
       const InsSol<G> sol{full, ntot, off, n, q0, pos, v};
-      const double sc = user_phi(U::obj(sol, us.inst), U::pen(sol, us.inst), us.w, us.maximize,
-                                 us.pw);
+      const double sc = us.template phi<U>(sol);
       if (bi == 0x7fffffff || sc < bs) {
         bs = sc;
         bi = pos;
@@ -717,7 +726,7 @@ __device__ void team_gr_user_cells(G* row, int n, const GrShared& g, const UserS
     const int p = g.picks()[t];
     for (int i = lane; i < nd; i += TS) {
       const OvSol<G> sol{row, n, p, g.dom()[i]};
-      sbuf[i] = user_phi(U::obj(sol, us.inst), U::pen(sol, us.inst), us.w, us.maximize, us.pw);
+      sbuf[i] = us.template phi<U>(sol);
     }
     team_bar(team, TS);
     if (lane == 0) {  // first minimum in domain order
@@ -1484,7 +1493,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
             la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
             pending = true;
           } else if (KIND == RK_USER && kind >= SEQ_CUSTOM_BASE) {  // user operator
-            RowOpCtx<G, U> oc{&c, inst, X.obj_weight, pwt, X.maximize, n, c.d1, X.d2};
+            RowOpCtx<G, U> oc{&c, UserScore{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m},
+                              n, c.d1, X.d2};
             U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
             c.mark_all();
           } else {
@@ -1579,7 +1589,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
             team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2, X,
                          pwt, gsh, la.delta, ts, lane, team, TS);
           } else if (KIND == RK_USER) {
-            const UserScore us{inst, X.obj_weight, pwt, X.maximize};
+            const UserScore us{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m};
             if (X.enc == ENC_PERM)
               team_gr_user_perm<U>(lrow, n, gsh.row() * X.d2, X.mf == 1 ? X.d2 : n, gsh, us,
                                    la.delta, ts, lane, team, TS);
@@ -1617,15 +1627,22 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           dl = __dsub_rn(phi_c, phi0);
         }
         rd_elem += 6u * (unsigned)X.n_cells;
-      } else if (KIND == RK_USER) {  // NVRTC objective, full evaluation
+      } else if (KIND == RK_USER) {  // NVRTC objective(s), full evaluation
         const RowSol<G> sol{row, n};
-        nscal = __dadd_rn(0.0, __dmul_rn(X.obj_weight, X.maximize ? -U::obj(sol, inst)
-                                                                   : U::obj(sol, inst)));
+        a0 = U::obj(sol, inst);
+        nscal = __dadd_rn(0.0, __dmul_rn(X.obj_weight, (X.mo.maxmask & 1) ? -a0 : a0));
+        if (X.mo.m == 2) {
+          a1 = U::obj2(sol, inst);
+          nscal = __dadd_rn(nscal, __dmul_rn(X.w2, (X.mo.maxmask & 2) ? -a1 : a1));
+        }
         npen = U::pen(sol, inst);
-        const double phi_c = __dadd_rn(nscal, __dmul_rn(pwt, npen));
-        const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
-        dl = __dsub_rn(phi_c, phi0);
-        rd_pos += 0u;
+        if (X.mo.lex) {
+          dl = lex_delta(a0, a1, npen, co0, co1, pen, pwt, X.mo);
+        } else {
+          const double phi_c = __dadd_rn(nscal, __dmul_rn(pwt, npen));
+          const double phi0 = __dadd_rn(scal, __dmul_rn(pwt, pen));
+          dl = __dsub_rn(phi_c, phi0);
+        }
       } else if (KIND == RK_QAP) {
         unsigned rd = 0;
         const double dq = qap_delta(qv, cur, row, nm, lo, hi, rd);

@@ -111,8 +111,14 @@ __device__ __forceinline__ void user_eval_entry(const void* inst, int n, int m,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const RowSol<short> sol{genes + (size_t)i * n, n};
-  obj[i] = U::obj(sol, (const unsigned char*)inst);
-  pen[i] = U::pen(sol, (const unsigned char*)inst);
+  const unsigned char* b = (const unsigned char*)inst;
+  if (U::kObjectives == 2) {
+    obj[2 * i] = U::obj(sol, b);
+    obj[2 * i + 1] = U::obj2(sol, b);
+  } else {
+    obj[i] = U::obj(sol, b);
+  }
+  pen[i] = U::pen(sol, b);
 }
 
 // One application of user operator `slot` to a probe row (register_custom's
@@ -140,8 +146,10 @@ __device__ __forceinline__ void user_probe_entry(const void* inst, RowArgs x, in
   c.nr = 0;
   c.err = 0;
   c.mates = nullptr;
-  RowOpCtx<short, U> oc{&c, (const unsigned char*)inst, x.obj_weight, x.penalty_weight,
-                        x.maximize, n, c.d1, x.d2};
+  RowOpCtx<short, U> oc{&c,
+                        UserScore{(const unsigned char*)inst, x.obj_weight, x.penalty_weight,
+                                  x.mo.maxmask, x.w2, x.mo.m},
+                        n, c.d1, x.d2};
   U::op(slot, oc, (const unsigned char*)inst);
   *err = c.err;
 }

@@ -570,6 +570,7 @@ class DeviceRun:
         ec.evolver_offset = config.evolver_offset
         od = cfg.obj_defs[0]
         ec.maximize = od.direction is Direction.MAXIMIZE
+        ec.maximize2 = len(cfg.obj_defs) > 1 and cfg.obj_defs[1].direction is Direction.MAXIMIZE
         mode = cfg.comparison_or_default()
         # scalar_fitness weights (engine.py:215-222): the Weighted mode's, else obj_defs'
         sw = mode.weights if isinstance(mode, Weighted) else tuple(o.weight for o in cfg.obj_defs)

@@ -520,14 +520,27 @@ class CudaProblem(ProblemDefinition):
                     SEQ_SCATTER_SHUFFLE, SEQ_GUIDED_REBUILD),
     }
 
-    def __init__(self, encoding: str, n: int, compute_obj: str, compute_penalty: str | None = None,
+    def __init__(self, encoding: str, n: int, compute_obj, compute_penalty: str | None = None,
                  data: dict | None = None, lb: int = 0, ub: int | None = None,
-                 maximize: bool = False, name: str = "objective",
-                 init_matrices: list | None = None, rows: int = 1):
+                 maximize=False, name="objective", init_matrices: list | None = None,
+                 rows: int = 1, comparison=None, weights=None):
         if encoding not in self._ENC:
             raise ValueError(f"encoding must be one of {sorted(self._ENC)}, got {encoding!r}")
-        if not isinstance(compute_obj, str) or not compute_obj.strip():
-            raise ValueError("compute_obj must be a CUDA snippet (function body)")
+        # one objective, or two (compute_obj = [obj0, obj1]; maximize / name / weights
+        # per objective; comparison Weighted or Lexicographic, core.py:80-106)
+        objs = [compute_obj] if isinstance(compute_obj, str) else list(compute_obj)
+        if not 1 <= len(objs) <= 2 or any(not isinstance(o, str) or not o.strip() for o in objs):
+            raise ValueError("compute_obj must be one CUDA snippet (function body) or two")
+        m = len(objs)
+        maxes = [maximize] * m if isinstance(maximize, bool) else list(maximize)
+        names = [name] * m if isinstance(name, str) else list(name)
+        if m == 2 and isinstance(name, str):
+            names = [f"{name}0", f"{name}1"]
+        ws = list(weights) if weights is not None else [1.0] * m
+        if not (len(maxes) == len(names) == len(ws) == m):
+            raise ValueError("maximize / name / weights need one entry per objective")
+        compute_obj = objs[0]
+        self.compute_obj2_src = objs[1] if m == 2 else None
         self.encoding, self.n, self.rows = encoding, int(n), int(rows)
         if self.rows < 1:
             raise ValueError("rows must be >= 1")
@@ -551,7 +564,9 @@ class CudaProblem(ProblemDefinition):
             encoding=enc, d1=self.rows, d2=self.n,
             n=self.n if encoding == "permutation" else self.rows * self.n,
             row_mode=RowModeKind.SINGLE_SEQ if self.rows == 1 else RowModeKind.MULTI_FIXED,
-            obj_defs=(ObjDef(name, Direction.MAXIMIZE if maximize else Direction.MINIMIZE),))
+            obj_defs=tuple(ObjDef(nm, Direction.MAXIMIZE if mx else Direction.MINIMIZE, w)
+                           for nm, mx, w in zip(names, maxes, ws)),
+            comparison=comparison)
 
     def config(self):
         return self._cfg
@@ -579,7 +594,8 @@ class CudaProblem(ProblemDefinition):
             compute_obj=self.compute_obj_src.encode(),
             compute_penalty=self.compute_penalty_src.encode() if self.compute_penalty_src else None,
             n_data=len(names), data_names=c_names, data=c_ptrs, data_lens=c_lens,
-            rows=self.rows)
+            rows=self.rows,
+            compute_obj2=self.compute_obj2_src.encode() if self.compute_obj2_src else None)
         h = C.c_void_p()
         log = C.create_string_buffer(8192)
         N.check(lib.go_problem_create_user(C.byref(desc), device, C.byref(h), log, len(log)))

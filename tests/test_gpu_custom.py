@@ -294,3 +294,45 @@ def test_solve_custom_with_user_operators():
                        time_limit=2.0, max_generations=200)
     assert any(e["id"] == 100 for e in r.final_weights["sequences"])
     assert r.feasible and sorted(r.best.row(0).tolist()) == list(range(20))
+
+
+# ---- two-objective user problems (core.py:69-106, engine.py:225-246, :352-420) ------------
+ASCENTS = """
+  int k = 0;  // adjacent ascending pairs (to be maximised)
+  for (int i = 0; i + 1 < sol.n; ++i) k += sol[i] < sol[i + 1];
+  return (double)k;
+"""
+
+
+def _ascents_py(t):
+    return float(sum(1 for i in range(len(t) - 1) if t[i] < t[i + 1]))
+
+
+@pytest.mark.parametrize("mode", ["weighted", "lex"])
+def test_two_objective_user_problem(mode):
+    """(tour length Minimize, ascents Maximize) under Weighted((0.7, 0.3)) or
+    Lexicographic((1, 0), (0, 2)): NSGA-II initial fronts, the Lexicographic
+    delta with a Maximize objective, vector compare in the epilogue — equal to
+    the oracle."""
+    from paper_2603_19163_b200.core import Lexicographic, Weighted
+    d = I.tsp_random(24, 17, True)
+    if mode == "weighted":
+        comp, kw = Weighted((0.7, 0.3)), dict(weights=(0.7, 0.3))
+    else:
+        comp, kw = Lexicographic((1, 0), (0.0, 2.0)), dict(lex=((1, 0), (0.0, 2.0)))
+    prob = G.CudaProblem("permutation", 24, [TOUR, ASCENTS], data={"dist": d},
+                         maximize=(False, True), name=("length", "ascents"), comparison=comp)
+    ref = OP.Custom(OP.PERM, 24, [_tour_py(d), _ascents_py], maximize=(False, True), **kw)
+    sols = [OE.random_solution(ref.spec, random.Random(s)) for s in range(6)]
+    obj, _ = G.problems.device_evaluate(prob, [G.Solution(s.data, s.sizes, 2) for s in sols])
+    for s, o in zip(sols, obj):
+        OP.evaluate(ref, s)
+        assert list(o) == list(s.obj)
+    res = G.run(prob, G.EngineConfig(population=6, team_size=32, max_generations=20, seed=9,
+                                     record_history=True))
+    out = OE.run(ref, OE.RunCfg(population=6, team_size=32, max_generations=20, seed=9,
+                                record_history=True, allowed_ops=prob.device_sequences()),
+                 device_stream="philox")
+    assert res.objectives == list(out.best.obj) and res.penalty == out.best.pen
+    assert [s.row(0).tolist() for s in res.population] == [s.row(0).tolist() for s in out.population]
+    assert [list(s.objectives) for s in res.population] == [list(s.obj) for s in out.population]
