@@ -40,7 +40,8 @@ struct TeamShared {
   int wl[32];
   Move chain[MAX_CHAIN];
   double bd;
-  int nm, k, accept, pad;
+  int nm, k, accept;
+  int dnext;                       // next deferred request to hand out (dynamic, per warp)
   int sq[MAX_CHAIN];
   int usage[MAX_SEQ];
   int impr[MAX_SEQ];
@@ -48,6 +49,7 @@ struct TeamShared {
   int k_impr[3];
   int nreq;                        // pending cooperative relocations this step
   int ndreq;                       // pending deferred whole-row operators this step
+  int ngr;                         // ... of which guided rebuilds (queued from the back)
   unsigned char cnt[16][MAX_SEQ];  // per-warp lane counts per sequence (lane sort)
 };
 
@@ -294,6 +296,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       if (lane == 0) {
         ts->nreq = 0;
         ts->ndreq = 0;
+        ts->ngr = 0;
+        ts->dnext = 0;
       }
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
@@ -342,7 +346,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
         bool pending = false;
         if (perm_deferred(kind)) {  // whole-row operator: resolved by a warp below
-          la.dreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
+          // guided rebuilds (the longest) queue from the back and are handed out first
+          if (kind == SEQ_GUIDED_REBUILD) la.dreq[TS - 1 - atomicAdd(&ts->ngr, 1)] = (unsigned short)L;
+          else la.dreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
           pending = true;
         } else {
           run_perm_op<Policy, Custom>(kind, c);
@@ -463,11 +469,15 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       }
 
       // ---- deferred whole-row operators (go_perm_lns.cuh): one warp per lane
-      const int ndreq = ts->ndreq;
+      const int ngr = ts->ngr, ndreq = ts->ndreq + ngr;
       if (ndreq > 0) {
 #pragma unroll 1
-        for (int r = warp; r < ndreq; r += nwarps) {
-          const int L = la.dreq[r];
+        for (;;) {  // warps take requests as they free up (longest first)
+          int r = 0;
+          if (wl == 0) r = atomicAdd(&ts->dnext, 1);
+          r = __shfl_sync(0xffffffffu, r, 0);
+          if (r >= ndreq) break;
+          const int L = r < ngr ? la.dreq[TS - 1 - r] : la.dreq[r - ngr];
           const u32 meta = la.meta[L];
           const int nm = meta_nm(meta), k = meta_k(meta);
           int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
