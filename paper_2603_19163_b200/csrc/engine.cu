@@ -727,22 +727,26 @@ void* row_kernel(const go_problem* p) {
   return (void*)go_evolve_jsp;
 }
 
-unsigned row_team_bytes(const go_problem* p, int TS) {
-  return go::RowSmem::team_bytes(p->n, p->gsize, TS, p->scratch_ints * 4);
+// layout codes for the row family: 10 = instance and lane rows in shared memory,
+// 11 = instance global, 12 = lane rows global, 13 = both global (long rows)
+bool row_rows_smem(int layout) { return layout == 10 || layout == 11; }
+bool row_inst_smem(int layout) { return layout == 10 || layout == 12; }
+
+unsigned row_team_bytes(const go_problem* p, int TS, int layout = 10) {
+  return go::RowSmem::team_bytes(p->n, p->gsize, TS, p->scratch_ints * 4, row_rows_smem(layout));
 }
 
-// layout codes for the row family: 10 = instance staged in shared memory, 11 = global
 bool choose_row(const go_problem* p, int TS, int E_req, int* layout, int* E_out, size_t* smem) {
   const size_t optin = (size_t)p->dev.smem_optin;
   const int Emax = std::max(1, std::min(8, 512 / TS));
   const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
-  const unsigned tb = row_team_bytes(p, TS);
-  for (int pass = 0; pass < 2; ++pass) {
-    const unsigned inst = pass == 0 ? pad16(p->img_bytes) : 0u;
+  for (int L = 10; L <= 13; ++L) {
+    const unsigned inst = row_inst_smem(L) ? pad16(p->img_bytes) : 0u;
+    const unsigned tb = row_team_bytes(p, TS, L);
     for (int E = E0; E >= 1; --E) {
       const size_t need = go::PermSmem::team_off(inst) + (size_t)E * tb;
       if (need <= optin) {
-        *layout = pass == 0 ? 10 : 11;
+        *layout = L;
         *E_out = E;
         *smem = need;
         return true;
@@ -1276,7 +1280,7 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
     if (!choose_row(p, e->TS, c->teams_per_cta, &e->layout, &e->E, &e->smem))
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
     e->inst = p->d_img;
-    e->inst_bytes = e->layout == 10 ? pad16(p->img_bytes) : 0u;
+    e->inst_bytes = row_inst_smem(e->layout) ? pad16(p->img_bytes) : 0u;
     e->k_evolve = row_kernel(p);
     if (p->row_kind == go::RK_USER) e->k_evolve_jit = p->user_mod.evolve;
   } else {
@@ -1439,6 +1443,9 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
                  ids[i] == go::SEQ_SCATTER_SHUFFLE || ids[i] == go::SEQ_GUIDED_REBUILD;
   if (e->prob->family == 0 && whole_row && !e->lane_rows)
     CK(cudaMalloc(&e->lane_rows, (size_t)e->P * e->T * 2 * e->n * 2));
+  if (e->prob->family == 1 && !row_rows_smem(e->layout) && !e->lane_rows)  // long rows
+    CK(cudaMalloc(&e->lane_rows, (size_t)e->P * e->TS *
+                                     go::RowSmem::row_stride(e->n, e->prob->gsize)));
   CK(cudaMemcpyAsync(e->reg, &r, sizeof(r), cudaMemcpyHostToDevice, e->stream));
   CK(cudaStreamSynchronize(e->stream));
   return GO_OK;
@@ -1578,7 +1585,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   go::RowArgs x{};
   if (e->prob->family == 1) {
     const go_problem* p = e->prob;
-    a.team_smem = (int)row_team_bytes(p, e->TS);
+    a.team_smem = (int)row_team_bytes(p, e->TS, e->layout);
     a.resync = 0;
     x = row_args(p);
     x.penalty_weight = c.penalty_weight;

@@ -189,7 +189,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   }
   if (threadIdx.x < 3) s_misc[threadIdx.x] = R->kw[threadIdx.x];
   if (threadIdx.x == 3) s_misc[3] = R->total;
-  if (threadIdx.x == 32) {  // lane-sort order: user operators first (long loops), then built-ins
+  if (threadIdx.x == blockDim.x - 1) {  // lane-sort order: user operators first (long loops), then built-ins (any CTA size)
     int j = 0;
     for (int pass = 0; pass < 2; ++pass)
       for (int i = 0; i < nseq; ++i)

@@ -186,8 +186,11 @@ struct RowLaneState {
 struct RowSmem {
   static __host__ __device__ unsigned align(unsigned x, unsigned a) { return (x + a - 1) / a * a; }
   static __host__ __device__ unsigned row_stride(int n, int gsize) { return align((unsigned)(n * gsize), 16); }
-  static __host__ __device__ unsigned team_bytes(int n, int gsize, int TS, int scratch_per_lane) {
-    return align(row_stride(n, gsize) * (TS + 1) + RowLaneState::bytes(TS) +
+  // rows_smem: the T lane rows live in shared memory after the current row;
+  // otherwise (long rows) they live in global memory (EvolveArgs::lane_rows)
+  static __host__ __device__ unsigned team_bytes(int n, int gsize, int TS, int scratch_per_lane,
+                                                 bool rows_smem = true) {
+    return align(row_stride(n, gsize) * (rows_smem ? TS + 1 : 1) + RowLaneState::bytes(TS) +
                      (unsigned)sizeof(TeamShared<double>) + (unsigned)(scratch_per_lane * TS),
                  16);
   }
@@ -1236,7 +1239,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   }
   if (threadIdx.x < 3) s_misc[threadIdx.x] = R->kw[threadIdx.x];
   if (threadIdx.x == 3) s_misc[3] = R->total;
-  if (threadIdx.x == 32) {
+  if (threadIdx.x == blockDim.x - 1) {  // (a CTA may be a single 32-thread team)
     for (int i = 0; i < nseq; ++i) {
       s_gord[i] = i;
       s_grank[i] = i;
@@ -1292,11 +1295,15 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   const unsigned rs = RowSmem::row_stride(n, (int)sizeof(G));
   unsigned char* tb = sm + PermSmem::team_off(A.inst_bytes) + team * A.team_smem;
   G* cur = (G*)tb;
-  unsigned char* rows = tb + rs;  // TS lane rows
+  // TS lane rows: shared memory after the current row, or (rows too long for
+  // the opt-in shared memory) this team's slice of the global lane_rows buffer
+  const bool rows_g = A.lane_rows != nullptr;
+  unsigned char* rows = rows_g ? (unsigned char*)A.lane_rows + (size_t)ev * TS * rs : tb + rs;
+  unsigned char* lst = tb + rs * (rows_g ? 1 : TS + 1);
   RowLaneState la;
-  la.bind(tb + rs * (TS + 1), TS);
+  la.bind(lst, TS);
   TeamShared<double>* ts =
-      (TeamShared<double>*)(tb + rs * (TS + 1) + RowSmem::align(RowLaneState::bytes(TS), 16));
+      (TeamShared<double>*)(lst + RowSmem::align(RowLaneState::bytes(TS), 16));
   int* scratch = (int*)((unsigned char*)ts + sizeof(TeamShared<double>));  // JSP decode
 
   for (int p = lane; p < n; p += TS) cur[p] = (G)A.genes[(size_t)ev * n + p];
