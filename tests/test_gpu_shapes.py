@@ -48,3 +48,26 @@ def test_launch_shapes_bit_identical(kind, T, P):
     d1 = ref.spec.d1
     assert [[s.row(r).tolist() for r in range(d1)] for s in res.population] == \
         [[s.row(r).tolist() for r in range(d1)] for s in out.population]
+
+
+@pytest.mark.parametrize("kind", ["tsp", "knap", "cvrp"])
+@pytest.mark.parametrize("islands,migration,top_n", [(2, "ring", 1), (5, "ring", 1),
+                                                     (3, "global_top_n", 2),
+                                                     (5, "global_top_n", 3), (4, "hybrid", 2)])
+def test_island_migration_sweep(kind, islands, migration, top_n):
+    """engine.py:483-532: ring / global_top_n / hybrid migration every 2
+    generations and elite injection every 3, uneven island sizes (P = 7)."""
+    prob, ref, _ = _pair(kind)
+    kw = dict(population=7, team_size=16, max_generations=9, seed=islands * 10 + top_n,
+              record_history=True)
+    res = G.run(prob, G.EngineConfig(islands=G.IslandsConfig(count=islands, migration=migration,
+                                                             interval=2, top_n=top_n),
+                                     elite_injection_interval=3, **kw))
+    out = OE.run(ref, OE.RunCfg(islands=islands, migration=migration, migration_interval=2,
+                                top_n=top_n, elite_interval=3,
+                                allowed_ops=prob.device_sequences(), **kw),
+                 device_stream="philox")
+    assert res.history["best_phi"] == out.history["best_phi"]
+    d1 = ref.spec.d1
+    assert [[s.row(r).tolist() for r in range(d1)] for s in res.population] == \
+        [[s.row(r).tolist() for r in range(d1)] for s in out.population]
