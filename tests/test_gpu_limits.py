@@ -85,3 +85,28 @@ def test_tsp_global_distance_matrix():
                  device_stream="philox")
     assert res.history["best_phi"] == out.history["best_phi"]
     assert res.best.row(0).tolist() == out.best.row(0).tolist()
+
+
+@pytest.mark.parametrize("kind", ["qap", "knap"])
+def test_float_row_instances_within_tolerance(kind):
+    """Float-valued QAP / knapsack (the incremental device deltas are not the
+    reference's summation order): every reported objective and penalty equals
+    the oracle's evaluation of the returned solution within 1e-9 relative (the
+    north star allows 1e-6)."""
+    rng = np.random.default_rng(31)
+    if kind == "qap":
+        f, d = rng.uniform(0, 10, (40, 40)), rng.uniform(0, 10, (40, 40))
+        prob = G.builtin_problem("qap", G.InstanceData(flow_matrix=f, distance_matrix=d))
+        ref = OP.Qap(f, d)
+    else:
+        w, v = rng.uniform(1, 50, 300), rng.uniform(1, 50, 300)
+        cap = float(w.sum() / 3)
+        prob = G.builtin_problem("knapsack", G.InstanceData(weights=w, values=v, capacity=cap))
+        ref = OP.Knapsack(w, v, cap)
+    res = G.run(prob, G.EngineConfig(population=8, team_size=64, max_generations=40, seed=2))
+    assert res.device["error_flags"] == 0
+    for s in [res.best] + res.population:
+        o = OP.Sol(s.data.copy(), s.dim2_sizes.copy(), 1)
+        OP.evaluate(ref, o)
+        assert s.objectives[0] == pytest.approx(o.obj[0], rel=1e-9)
+        assert s.penalty == pytest.approx(o.pen, rel=1e-9, abs=1e-9)
