@@ -1,7 +1,7 @@
 """Diagnostic: per-phase clock64 breakdown of the evolve kernel (GO_PHASE_TIMING)."""
 import ctypes as C, os, sys
 os.environ["GO_JIT_DEFINE"] = "GO_PHASE_TIMING=1"
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2603_19163_b200 as G
 from paper_2603_19163_b200 import _native as N, instances as I
