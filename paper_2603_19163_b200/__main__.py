@@ -1,7 +1,6 @@
-"""`python -m paper_2603_19163_b200 ...` (the reference's __main__.py:1-5)."""
+"""Entry point of `python -m paper_2603_19163_b200 <command>` (see cli.py)."""
 
-import sys
+if __name__ == "__main__":
+    from .cli import main as _cli_main
 
-from .cli import main
-
-sys.exit(main())
+    raise SystemExit(_cli_main())
