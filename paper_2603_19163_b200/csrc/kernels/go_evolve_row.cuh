@@ -1414,11 +1414,11 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       ts->cnt[warp][wl] = 0;
       __syncwarp();
       if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
-      if (lane == 0) {
+      team_bar(team, TS);
+      if (lane == 0) {  // after the barrier: every thread has read the previous step's counts
         ts->nreq = 0;
         ts->ndreq = 0;
       }
-      team_bar(team, TS);
       int tj = 0;
       if (wl < nseq) {
         const int q = s_gord[wl];

@@ -72,4 +72,19 @@ r = G.solve_custom(encoding="permutation", dim2=40, compute_obj=TOUR, data={"dis
                    custom_operators=[G.CustomOperator(100, "kick", cuda=KICK)], time_limit=None,
                    **cfg)
 print(f"user: {r.objectives} gens {r.generations_completed}", flush=True)
+# long rows in global memory (row layouts 12 / 13), single-team CTAs
+w, v, cap = I.knapsack_random(6000, 77)
+r = G.run(G.builtin_problem("knapsack", G.InstanceData(weights=w, values=v, capacity=cap)),
+          G.EngineConfig(population=3, team_size=64, max_generations=4, seed=3))
+print(f"knap6000: layout {r.device['layout']} {r.objectives}", flush=True)
+r = G.run(G.CudaProblem("permutation", 40, TOUR, data={"dist": d}),
+          G.EngineConfig(population=2, team_size=32, teams_per_cta=1, max_generations=6, seed=1))
+print(f"single-team CTA: {r.objectives}", flush=True)
+# two objectives, Lexicographic with a Maximize objective
+ASC = "int k = 0; for (int i = 0; i + 1 < sol.n; ++i) k += sol[i] < sol[i + 1]; return (double)k;"
+prob2 = G.CudaProblem("permutation", 40, [TOUR, ASC], data={"dist": d}, maximize=(False, True),
+                      comparison=G.Lexicographic((1, 0), (0.0, 2.0)))
+r = G.run(prob2, G.EngineConfig(population=4, team_size=32, max_generations=6, seed=2,
+                                islands=G.IslandsConfig(count=2, migration="hybrid", interval=2)))
+print(f"two-objective lex: {r.objectives}", flush=True)
 print("sanitize_run done")
