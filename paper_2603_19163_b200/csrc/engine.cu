@@ -194,6 +194,7 @@ struct go_problem {
   int pvar = 0;  // partition variant (RowArgs::pvar)
   // user problems (RK_USER): NVRTC objective module, encoding
   gohost::JitModule user_mod;
+  gohost::JitModule user_mod_g;  // lane rows in global memory, built when first needed
   gohost::UserProblemSrc user_src;  // kept to rebuild the module with user operators
   int enc = 0;
   int mf = 0;  // MULTI_FIXED user rows: 1 permutation rows, 2 binary / integer cells
@@ -561,6 +562,7 @@ int go_problem_destroy(go_problem* p) {
   for (auto& kv : p->jit)
     if (kv.second.mod && gohost::drv()) gohost::drv()->ModuleUnload(kv.second.mod);
   if (p->user_mod.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod.mod);
+  if (p->user_mod_g.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod_g.mod);
   cudaFree(p->d_full);
   cudaFree(p->d_tri);
   delete p;
@@ -717,20 +719,44 @@ int eval_device_rows(go_problem* p, const short* d_g, int m, double* d_o, double
 }
 
 // ---- row family helpers ----------------------------------------------------------
-void* row_kernel(const go_problem* p) {
-  if (p->row_kind == go::RK_USER) return nullptr;  // JIT (p->user_mod.evolve)
-  if (p->row_kind == go::RK_QAP)
-    return p->elem == E_I16 ? (void*)go_evolve_qap_i16
-                            : (p->elem == E_I32 ? (void*)go_evolve_qap_i32 : (void*)go_evolve_qap_f64);
-  if (p->row_kind == go::RK_KNAP) return (void*)go_evolve_knap;
-  if (p->row_kind == go::RK_PART) return (void*)go_evolve_part;
-  return (void*)go_evolve_jsp;
-}
-
 // layout codes for the row family: 10 = instance and lane rows in shared memory,
 // 11 = instance global, 12 = lane rows global, 13 = both global (long rows)
 bool row_rows_smem(int layout) { return layout == 10 || layout == 11; }
 bool row_inst_smem(int layout) { return layout == 10 || layout == 12; }
+
+void* row_kernel(const go_problem* p, int layout) {
+  if (p->row_kind == go::RK_USER) return nullptr;  // JIT (row_kernel_jit)
+  const bool s = row_rows_smem(layout);
+  if (p->row_kind == go::RK_QAP) {
+    if (p->elem == E_I16) return s ? (void*)go_evolve_qap_i16 : (void*)go_evolve_qap_i16_g;
+    if (p->elem == E_I32) return s ? (void*)go_evolve_qap_i32 : (void*)go_evolve_qap_i32_g;
+    return s ? (void*)go_evolve_qap_f64 : (void*)go_evolve_qap_f64_g;
+  }
+  if (p->row_kind == go::RK_KNAP) return s ? (void*)go_evolve_knap : (void*)go_evolve_knap_g;
+  if (p->row_kind == go::RK_PART) return s ? (void*)go_evolve_part : (void*)go_evolve_part_g;
+  return s ? (void*)go_evolve_jsp : (void*)go_evolve_jsp_g;
+}
+
+// the user problem's evolve kernel for a layout (the global-rows module is
+// compiled on first use)
+int row_kernel_jit(go_problem* p, int layout, CUfunction* out) {
+  *out = nullptr;
+  if (p->row_kind != go::RK_USER) return GO_OK;
+  if (row_rows_smem(layout)) {
+    *out = p->user_mod.evolve;
+    return GO_OK;
+  }
+  if (!p->user_mod_g.mod) {
+    gohost::UserProblemSrc up = p->user_src;
+    up.ops = p->ops;
+    up.rows_global = true;
+    std::string log;
+    const int rc = gohost::jit_build_user(up, &p->user_mod_g, &log);
+    if (rc) return fail(rc, "NVRTC build (global lane rows) failed: " + log.substr(0, 2000));
+  }
+  *out = p->user_mod_g.evolve;
+  return GO_OK;
+}
 
 unsigned row_team_bytes(const go_problem* p, int TS, int layout = 10) {
   return go::RowSmem::team_bytes(p->n, p->gsize, TS, p->scratch_ints * 4, row_rows_smem(layout));
@@ -859,8 +885,10 @@ int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_
     size_t smem = 0;
     if (!choose_row(p, TS, teams_per_cta, &L, &E, &smem))
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
-    void* fn = row_kernel(p);
-    CUfunction jf = p->row_kind == go::RK_USER ? p->user_mod.evolve : nullptr;
+    void* fn = row_kernel(p, L);
+    CUfunction jf = nullptr;
+    int jrc = row_kernel_jit(p, L, &jf);
+    if (jrc) return jrc;
     int rc = set_smem_attr(fn, jf, smem);
     if (rc) return rc;
     int blocks = 0;
@@ -1155,6 +1183,8 @@ static int set_user_problem_ops(go_problem* p, const go_custom_op* ops, int n_op
   const int rc = gohost::jit_build_user(up, &m, &log);
   if (rc) return fail(rc, "NVRTC build of the user problem with its operators failed: " + log.substr(0, 2000));
   if (p->user_mod.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod.mod);
+  if (p->user_mod_g.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod_g.mod);
+  p->user_mod_g = gohost::JitModule{};
   p->user_mod = m;
   p->ops = keep;
   return GO_OK;
@@ -1281,8 +1311,8 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
     e->inst = p->d_img;
     e->inst_bytes = row_inst_smem(e->layout) ? pad16(p->img_bytes) : 0u;
-    e->k_evolve = row_kernel(p);
-    if (p->row_kind == go::RK_USER) e->k_evolve_jit = p->user_mod.evolve;
+    e->k_evolve = row_kernel(p, e->layout);
+    if (int jrc = row_kernel_jit(p, e->layout, &e->k_evolve_jit)) return jrc;
   } else {
   choose_layout(p, e->TS, c->teams_per_cta, &e->layout, &e->E);
   const LayoutInfo& L = kLayouts[e->layout];

@@ -316,7 +316,8 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
          "const unsigned char* b) { return user::compute_obj(s, user::make_data(b)); }\n"
       << "  template <class S> __device__ __forceinline__ static double pen(const S& s, "
          "const unsigned char* b) { return user::compute_penalty(s, user::make_data(b)); }\n"
-      << "};\n}  // namespace go\nGO_USER_KERNELS(go::UserProblem)\n";
+      << "};\n}  // namespace go\nGO_USER_KERNELS_RG(go::UserProblem, "
+      << (up.rows_global ? "true" : "false") << ")\n";
   std::vector<UserOpSrc> files = {{0, "compute_obj", up.obj},
                                   {1, "compute_penalty", up.pen.empty() ? "return 0.0;" : up.pen}};
   if (!up.obj2.empty()) files.push_back({2, "compute_obj2", up.obj2});

@@ -45,6 +45,7 @@ struct UserProblemSrc {
   std::vector<unsigned long long> offsets;
   std::vector<long long> lens;
   std::vector<UserOpSrc> ops;  // user operators, compiled in as slots 0..n-1
+  bool rows_global = false;    // lane rows in global memory (long rows)
 };
 // Builds go_evolve_user (JitModule::evolve) and go_eval_user (JitModule::probe).
 int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log);

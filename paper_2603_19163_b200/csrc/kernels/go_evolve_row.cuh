@@ -1212,7 +1212,9 @@ __device__ __forceinline__ u32 warp_uniform_x(G* row, int n, const MateSel& ms, 
   return pos0 + 2u * (u32)n;
 }
 
-template <int KIND, class E, class G, class U = NoUser>
+// RG: lane rows in global memory (long rows); a template constant so the
+// shared-memory variant keeps ld.shared / st.shared on its lane rows
+template <int KIND, class E, class G, class U = NoUser, bool RG = false>
 __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X) {
   extern __shared__ __align__(128) unsigned char sm[];
   if (A.gs->stop) return;
@@ -1297,7 +1299,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   G* cur = (G*)tb;
   // TS lane rows: shared memory after the current row, or (rows too long for
   // the opt-in shared memory) this team's slice of the global lane_rows buffer
-  const bool rows_g = A.lane_rows != nullptr;
+  constexpr bool rows_g = RG;
   unsigned char* rows = rows_g ? (unsigned char*)A.lane_rows + (size_t)ev * TS * rs : tb + rs;
   unsigned char* lst = tb + rs * (rows_g ? 1 : TS + 1);
   RowLaneState la;

@@ -156,11 +156,13 @@ __device__ __forceinline__ void user_probe_entry(const void* inst, RowArgs x, in
 
 }  // namespace go
 
-// Kernels of one NVRTC user problem (go_jit.cpp generates `U`).
-#define GO_USER_KERNELS(U)                                                                    \
+// Kernels of one NVRTC user problem (go_jit.cpp generates `U`); RG: lane rows
+// in global memory (a second module, built only for problems that need it).
+#define GO_USER_KERNELS(U) GO_USER_KERNELS_RG(U, false)
+#define GO_USER_KERNELS_RG(U, RG)                                                             \
   extern "C" __global__ void __launch_bounds__(512, 1) go_evolve_user(go::EvolveArgs a,        \
                                                                       go::RowArgs x) {        \
-    go::evolve_row<go::RK_USER, double, short, U>(a, x);                                      \
+    go::evolve_row<go::RK_USER, double, short, U, RG>(a, x);                                  \
   }                                                                                           \
   extern "C" __global__ void go_eval_user(const void* inst, int n, int m, const short* g,     \
                                           double* obj, double* pen) {                          \
@@ -174,4 +176,8 @@ __device__ __forceinline__ void user_probe_entry(const void* inst, RowArgs x, in
 #define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \
   extern "C" __global__ void __launch_bounds__(512, 1) NAME(go::EvolveArgs a, go::RowArgs x) { \
     go::evolve_row<KIND, E, G>(a, x);                                                         \
+  }                                                                                           \
+  extern "C" __global__ void __launch_bounds__(512, 1) NAME##_g(go::EvolveArgs a,              \
+                                                              go::RowArgs x) {                \
+    go::evolve_row<KIND, E, G, go::NoUser, true>(a, x);                                       \
   }
