@@ -68,7 +68,7 @@ def test_import_matches_reference_migration(strategy, event, top_n):
         dr.close()
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, device_init=False):
     import os
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -76,7 +76,7 @@ def _rank_main(rank, world, port, q):
     d = I.tsp_random(40, 5)
     prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=d))
     res = G.run(prob, G.EngineConfig(population=8, team_size=32, max_generations=250, seed=3,
-                                     distributed=True, device=0,
+                                     distributed=True, device=0, device_init=device_init,
                                      islands=G.IslandsConfig(count=world, migration="hybrid",
                                                              interval=50, top_n=2)))
     o = OP.Tsp(d)
@@ -86,7 +86,8 @@ def _rank_main(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_run_distributed_two_ranks_one_gpu():
+@pytest.mark.parametrize("device_init", [False, True])
+def test_run_distributed_two_ranks_one_gpu(device_init):
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -95,7 +96,7 @@ def test_run_distributed_two_ranks_one_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, device_init)) for r in range(2)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=300) for _ in procs)
