@@ -487,7 +487,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
           const int nsel = (meta & META_MAT) && !(meta & META_SEL) ? 1 : 0;
           i16* dst = lrow + ((size_t)L * 2 + nsel) * n;
-          i16* aux = lrow + ((size_t)L * 2 + (1 - nsel)) * n;
+          // the first guided rebuild of the step (handed out first) works in the
+          // team's idle shared-memory row: its scans and rotations stay on-chip
+          i16* aux = r == 0 && ngr > 0 ? nxt : lrow + ((size_t)L * 2 + (1 - nsel)) * n;
           Stream rng;
           rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
