@@ -119,3 +119,28 @@ def test_cli_engine_config_mapping():
     assert [op.name for op in cfg.custom_operators] == \
         ["delta_two_opt", "delta_or_opt", "delta_node_insert"]
     assert cfg.fast_budget_bytes == 4096 and cfg.device_init and cfg.target_objective == 18
+
+
+@pytest.mark.parametrize("name", ["euc17.tsp", "upper9.tsp", "full9.tsp", "qap7.dat", "sol12.txt",
+                                  "js5x4.jsp"])
+def test_truncation_fuzz_raises_positioned_errors(name, tmp_path):
+    """Reference acceptance criterion 10 (test_acceptance.py:313-343): every
+    prefix of a valid file either parses or raises ParseError — never another
+    exception."""
+    raw = (ROOT / "tests" / "fixtures" / name).read_bytes()
+    parse = PARSE[Path(name).suffix]
+    step = max(1, len(raw) // 40)
+    for cut in range(0, len(raw), step):
+        stub = tmp_path / name
+        stub.write_bytes(raw[:cut])
+        try:
+            parse(str(stub))
+        except PZ.ParseError as exc:
+            assert str(stub) in str(exc)
+
+
+def test_parsed_matrices_are_symmetric_nonnegative():
+    for name, parse in (("euc17.tsp", PZ.parse_tsplib), ("upper9.tsp", PZ.parse_tsplib),
+                        ("sol12.txt", PZ.parse_solomon)):
+        d = parse(f"tests/fixtures/{name}").distance_matrix
+        assert np.array_equal(d, d.T) and not np.any(np.diag(d)) and np.all(d >= 0)
