@@ -353,6 +353,10 @@ def run_ours(args):
                           "frac": achieved_gbs / smem_peak,
                           "peak_formula": f"{info.sm_count} SM x 128 B/clk x {sm_mhz} MHz"},
         "clocks": clocks,
+        "communicator": ({"backend": torch.distributed.get_backend(), "world": world,
+                          "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                          "exchange": "elite all_gather every 100 generations"}
+                         if world > 1 else None),
         "cpu_baseline": cpu,
         **gap_info,
         "other_configs": extra,
@@ -405,6 +409,55 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(n: int, argv: list[str]) -> int:
+    """`bench.py --gpus N` outside torchrun: re-execute this script as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1, the same
+    launch the driver uses, and return the launcher's exit status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
+
+
+def selftest_dist(args):
+    """Launcher / timing-protocol check without GPUs (gloo): every rank does a
+    fixed amount of host work between barriers, the time is the MAX over ranks
+    and rank 0 prints one line with the whole-job value (tests/test_bench_cpu.py)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    t0 = time.perf_counter()
+    units = 0
+    for _ in range(args.steps):
+        x = 0
+        for i in range(20000):
+            x += i * i
+        units += 20000
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64)
+    u = torch.tensor([float(units)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(u)
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": "selftest units/s", "value": float(u.item() / t.item()),
+                          "n_gpus": world, "steps": args.steps, "ranks_seen": world,
+                          "backend": "gloo" if world > 1 else None}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -421,7 +474,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--other-configs", type=int, default=1,
                     help="also measure C1/C3/C4/C5 device throughput (N=1 only)")
+    ap.add_argument("--selftest-dist", action="store_true",
+                    help="check the N-rank launcher and max-over-ranks timing on CPU (gloo)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus, sys.argv[1:]))
+    _, world, _ = dist_env()
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE",
+              file=sys.stderr)
+    if args.selftest_dist:
+        selftest_dist(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
