@@ -1591,6 +1591,9 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.best_scal = e->best_scal;
   a.best_pen = e->best_pen;
   a.best_gen = e->best_gen;
+  a.has_target = c.has_target;
+  a.target = c.target_objective;
+  a.obj_sign_over_w = e->obj_sign_over_w;
   a.usage = e->usage;
   a.impr = e->impr;
   a.k_usage = e->k_usage;

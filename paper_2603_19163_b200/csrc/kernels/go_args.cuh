@@ -84,7 +84,21 @@ struct EvolveArgs {
   double* obj2;
   double* best_obj2;
   double* rec_obj2;
+  // target_objective (engine.py:712-716, single objective): once a team's
+  // best-ever reaches the target its best_genes row is frozen, so a run the
+  // epilogue stops at generation g mid-chunk returns the genes of generation g
+  int has_target;
+  int pad_t;
+  double target;
+  double obj_sign_over_w; // objective = scal * this
 };
+
+// the epilogue's target predicate (go_epilogue.cuh) on one (penalty, scal)
+__device__ __forceinline__ bool target_reached(const EvolveArgs& A, double pen, double scal) {
+  if (!A.has_target || pen > 0.0) return false;
+  const double v = scal * A.obj_sign_over_w;
+  return A.obj_sign_over_w > 0 ? v <= A.target + 1e-9 : v >= A.target - 1e-9;
+}
 
 // Problem-specific extras of the row kernel (go_evolve_row.cuh).
 struct RowArgs {

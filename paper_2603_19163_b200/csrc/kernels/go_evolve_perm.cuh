@@ -581,7 +581,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     }
     if (A.snap && gi + 1 < A.ngen)
       snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, snap_min, lane, team, TS);
-    if (strictly_better(0.0, phi, bpen, bscal)) {  // team best-ever, first occurrence
+    if (strictly_better(0.0, phi, bpen, bscal) && !target_reached(A, bpen, bscal)) {  // team best-ever, first occurrence
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = cur[p];
       bscal = phi;
       bpen = 0.0;

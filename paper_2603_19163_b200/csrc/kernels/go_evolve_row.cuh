@@ -1746,7 +1746,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     }
     if (A.snap && gi + 1 < A.ngen)
       snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, snap_min, lane, team, TS);
-    if (compare_mo(pen, scal, co0, co1, bpen, bscal, bo0, bo1, X.mo) < 0) {
+    if (compare_mo(pen, scal, co0, co1, bpen, bscal, bo0, bo1, X.mo) < 0 && !target_reached(A, bpen, bscal)) {
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = (short)cur[p];
       bscal = scal;
       bpen = pen;

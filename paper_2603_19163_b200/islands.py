@@ -138,13 +138,15 @@ def run_island_loop(island, config, dist, rank, world, t_start, device="cpu"):
 
 
 def best_over_ranks(problem, best, dist, world, device="cpu"):
-    """Comparison-best over ranks (engine.py:609-614): all_gather of
-    (penalty, objective, rank) then of the winner's genes."""
+    """Comparison-best over ranks (engine.py:609-614): all_gather of each
+    rank's (penalty, objective vector), then a broadcast of the winner's
+    genes.  The whole vector is compared, so two-objective runs (routing
+    distance + vehicles, Weighted or Lexicographic) pick the right rank."""
     import torch
     cfg = problem.config()
     device = _coll_device(dist, device)
-    row = torch.tensor([best.penalty, float(best.objectives[0])], dtype=torch.float64,
-                       device=device)
+    row = torch.tensor([best.penalty, *[float(x) for x in best.objectives]],
+                       dtype=torch.float64, device=device)
     rows = [torch.zeros_like(row) for _ in range(world)]
     dist.all_gather(rows, row)
     vals = [r.cpu().numpy() for r in rows]
@@ -157,49 +159,65 @@ def best_over_ranks(problem, best, dist, world, device="cpu"):
     sizes = torch.tensor(best.dim2_sizes, dtype=torch.int64, device=device)
     dist.broadcast(genes, src=win)
     dist.broadcast(sizes, src=win)
-    out = best.copy()
+    out = _as_sol(best, vals[win])
     out.data = genes.cpu().numpy().reshape(best.data.shape)
     out.dim2_sizes = sizes.cpu().numpy()
-    out.penalty = float(vals[win][0])
-    out.objectives[0] = vals[win][1]
     return out, win
 
 
 def _as_sol(template, v):
     s = template.copy()
     s.penalty = float(v[0])
-    s.objectives[0] = float(v[1])
+    s.objectives[:] = [float(x) for x in v[1:]]
     return s
+
+
+def gap_pct(cfg, objectives, best_known):
+    """RunResult.gap_pct as _run_single computes it: single objective,
+    minimised, best_known given and non-zero."""
+    if best_known is None or not best_known or cfg.num_objectives != 1 or \
+            cfg.obj_defs[0].direction is not Direction.MINIMIZE:
+        return None
+    return (float(objectives[0]) - best_known) / best_known * 100.0
 
 
 def run_distributed(problem, config, best_known=None):
     """`run()` across the ranks of an initialised torch.distributed NCCL group
-    (one GPU per rank, e.g. launched with torchrun)."""
+    (one GPU per rank, e.g. launched with torchrun).  The ranks ARE the
+    replicas of the paper's multi-GPU mode, so
+    `replicas > 1` together with `distributed=True` is rejected.  As in
+    _run_single, NVRTC compile time is reported apart from the budget
+    (PAPER.md:811-812)."""
     import torch.distributed as dist
 
     from .engine import RunResult
+    if config.replicas != 1:
+        raise ValueError("distributed runs use one island per rank; replicas must be 1 "
+                         "(use EngineConfig(replicas=N) without distributed=True instead)")
     rank, world = dist.get_rank(), dist.get_world_size()
     t_start = time.perf_counter()
     island = DeviceIsland(problem, config, config.seed, rank)
+    jit = island.dr.jit_seconds
     try:
-        gens, events = run_island_loop(island, config, dist, rank, world, t_start,
+        gens, events = run_island_loop(island, config, dist, rank, world, t_start + jit,
                                        device=island.device)
         best, winner = best_over_ranks(problem, island.best(), dist, world, island.device)
         w, kw = island.dr.weights()
     finally:
         island.close()
-    elapsed = time.perf_counter() - t_start
+    elapsed = time.perf_counter() - t_start - jit
     cfg = problem.config()
-    gap = None
-    if best_known and cfg.obj_defs[0].direction is Direction.MINIMIZE:
-        gap = (float(best.objectives[0]) - best_known) / best_known * 100.0
+    echo = config.as_dict()
+    echo["population_effective"] = island.dr.pop_size
     return RunResult(
-        best=best, objectives=[float(best.objectives[0])], penalty=float(best.penalty),
-        feasible=best.penalty == 0.0, gap_pct=gap, generations_completed=gens,
+        best=best, objectives=[float(v) for v in best.objectives], penalty=float(best.penalty),
+        feasible=best.penalty == 0.0, gap_pct=gap_pct(cfg, best.objectives, best_known),
+        generations_completed=gens,
         elapsed_seconds=elapsed, gens_per_sec=gens / elapsed if elapsed > 0 else 0.0,
         final_weights={"sequences": [{"id": e.id, "name": e.name, "weight": float(x)}
                                      for e, x in zip(island.dr.registry.entries, w)],
                        "k_steps": [float(x) for x in kw]},
-        profile=island.dr.profile.as_dict(), config=config.as_dict(), seed=config.seed,
+        profile=island.dr.profile.as_dict(), config=echo, seed=config.seed,
         device={"rank": rank, "world": world, "migration_events": events,
-                "winner_rank": winner, "population_per_rank": island.dr.pop_size})
+                "winner_rank": winner, "population_per_rank": island.dr.pop_size,
+                "jit_seconds": jit})

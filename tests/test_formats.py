@@ -142,5 +142,5 @@ def test_truncation_fuzz_raises_positioned_errors(name, tmp_path):
 def test_parsed_matrices_are_symmetric_nonnegative():
     for name, parse in (("euc17.tsp", PZ.parse_tsplib), ("upper9.tsp", PZ.parse_tsplib),
                         ("sol12.txt", PZ.parse_solomon)):
-        d = parse(f"tests/fixtures/{name}").distance_matrix
+        d = parse(str(ROOT / "tests" / "fixtures" / name)).distance_matrix
         assert np.array_equal(d, d.T) and not np.any(np.diag(d)) and np.all(d >= 0)

@@ -120,3 +120,35 @@ def test_criterion_11_monotone_best_and_temperature():
     assert all(b <= a for a, b in zip(phis, phis[1:]))
     for g, temp in enumerate(r.history["temperature"]):
         assert abs(temp - t0 * alpha ** g) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["tsp", "knapsack"])
+def test_target_stop_mid_chunk_returns_genes_of_that_generation(kind):
+    """engine.py:712-716: a run stopped by target_objective returns the global
+    best as it was at the stopping generation.  The target is set to a value
+    first reached in the middle of a 10-generation chunk, and the returned
+    genes must evaluate to the reported objective (the team's
+    best-ever row used to keep improving until the chunk's end)."""
+    if kind == "tsp":
+        prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=I.tsp_random(51, 51)))
+    else:
+        w, v, cap = I.knapsack_random(200, 7)
+        prob = G.builtin_problem("knapsack", G.InstanceData(weights=w, values=v, capacity=cap))
+    base = dict(population=8, team_size=32, max_generations=300, seed=5, record_history=True)
+    free = G.run(prob, G.EngineConfig(**base))
+    hist = free.history["best_phi"]
+    # a generation g (not a chunk end) where the global best improves and keeps improving
+    # within the same chunk afterwards
+    cand = [g for g in range(2, len(hist)) if g % 10 not in (0, 9) and hist[g - 1] < hist[g - 2]
+            and min(hist[g:g - g % 10 + 10]) < hist[g - 1]]
+    assert cand, "no mid-chunk improvement to target"
+    g = cand[len(cand) // 2]
+    sign = -1.0 if kind == "knapsack" else 1.0
+    target = sign * hist[g - 1]  # objective value of the best after generation g
+    r = G.run(prob, G.EngineConfig(**base, target_objective=target))
+    assert r.objectives[0] == pytest.approx(target)
+    check = r.best.copy()
+    G.evaluate(prob, check)
+    assert check.objectives[0] == r.objectives[0] and check.penalty == r.penalty
+    assert r.history["best_phi"][-1] == hist[g - 1]

@@ -139,3 +139,45 @@ def test_two_rank_island_exchange_over_gloo(strategy):
     assert n0 > 0 and n1 > 0                           # both islands received migrants
     assert best0 == best1 == min(b0)                   # comparison-best over ranks, agreed
     assert w0 == w1 and genes0 == genes1 == list(range(12))
+
+
+def _mo_worker(rank, world, port, out):
+    """Two-objective CVRP (distance, vehicles) under Lexicographic vehicles-first:
+    rank 0 has the shorter distance, rank 1 fewer vehicles — rank 1 must win and
+    the returned objective vector must be rank 1's whole vector."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(0)
+    xy = rng.uniform(0, 100, (7, 2))
+    d = np.sqrt(((xy[:, None] - xy[None]) ** 2).sum(-1))
+    prob = G.builtin_problem("cvrp", G.InstanceData(
+        distance_matrix=d, demands=np.ones(6), capacity=6.0, vehicles=3,
+        meta={"objectives": ("distance", "vehicles"),
+              "comparison": G.Lexicographic((1, 0), (0.0, 0.0))}))
+    cfg = prob.config()
+    s = G.Solution(np.zeros((cfg.d1, cfg.d2), dtype=np.int64), np.zeros(cfg.d1, np.int64), 2)
+    s.data[0, :6] = np.arange(6) if rank == 1 else [0, 1, 2, 0, 0, 0]
+    s.dim2_sizes[0] = 6 if rank == 1 else 3
+    if rank == 0:
+        s.data[1, :3] = [3, 4, 5]
+        s.dim2_sizes[1] = 3
+    s.objectives[:] = [100.0, 2.0] if rank == 0 else [150.0, 1.0]
+    s.penalty = 0.0
+    best, win = ISL.best_over_ranks(prob, s, dist, world)
+    out.put((rank, win, [float(x) for x in best.objectives], best.dim2_sizes.tolist()))
+    dist.destroy_process_group()
+
+
+def test_best_over_ranks_compares_whole_objective_vector():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, win, objs, sizes in res:
+        assert win == 1 and objs == [150.0, 1.0] and sizes[0] == 6
