@@ -252,6 +252,12 @@ int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* 
  * (`time_limit_s` measured from now; <= 0 = none) or the target */
 int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
                   go_run_stats* stats);
+/* one generation of every evolver at an explicit generation index and
+ * temperature, no epilogue: evolve_generation (engine.py:538-595) per evolver.
+ * Per-evolver AOS credit of that generation: usage/impr [P][nseq],
+ * k_usage/k_impr [P][3] (each may be NULL). */
+int go_engine_step(go_engine* e, int64_t generation, double temperature, int32_t* usage,
+                   int32_t* impr, int32_t* k_usage, int32_t* k_impr);
 int go_engine_get_population(go_engine* e, int32_t* genes, int32_t* sizes, double* obj,
                              double* pen);
 int go_engine_get_best(go_engine* e, int32_t* genes, int32_t* sizes, double* obj, double* pen,

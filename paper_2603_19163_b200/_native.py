@@ -124,6 +124,7 @@ def _bind(lib):
         "go_engine_set_registry": ([V, C.c_int, _PI, _PD, _PD, _PD, C.c_double, _PD], C.c_int),
         "go_engine_set_population": ([V, _PI, _PI, _PD, _PD], C.c_int),
         "go_engine_run": ([V, C.c_int64, C.c_double, P(RunStats)], C.c_int),
+        "go_engine_step": ([V, C.c_int64, C.c_double, _PI, _PI, _PI, _PI], C.c_int),
         "go_engine_get_population": ([V, _PI, _PI, _PD, _PD], C.c_int),
         "go_engine_get_best": ([V, _PI, _PI, _PD, _PD, P(C.c_int64)], C.c_int),
         "go_engine_get_registry": ([V, _PD, _PD, _PI], C.c_int),

@@ -1548,39 +1548,12 @@ int go_engine_set_history(go_engine* e, int enabled) {
   return GO_OK;
 }
 
-int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
-                  go_run_stats* stats) {
-  if (!e) return fail(GO_E_INVALID, "null engine");
-  if (e->nseq == 0) return fail(GO_E_INVALID, "registry not set");
-  CK(cudaSetDevice(e->prob->device));
+// Evolve-kernel arguments of an engine (everything but the chunk: gen0,
+// ngen, temps are set per launch).
+static void build_evolve_args(go_engine* e, go::EvolveArgs& a, go::RowArgs& x) {
   const go_engine_config& c = e->cfg;
-  go::GlobalState gs{};
-  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
-  long long done = gs.gens_done;
-  const unsigned long long rp0 = gs.rd_pos, re0 = gs.rd_elem;
-  if (gs.stop) {  // a previous run stopped; resume from the same state
-    gs.stop = 0;
-    *e->h_stop = 0;
-  }
-  // history buffer sized for the generations this call may run
-  if (e->history_on && max_generations > e->hist_cap) {
-    if (e->history) cudaFree(e->history);
-    e->hist_cap = std::max<long long>(max_generations, 1);
-    CK(cudaMalloc(&e->history, (size_t)e->hist_cap * 8));
-  }
-  gs.deadline_ns = 0;
-  CK(cudaMemcpyAsync(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice, e->stream));
-  if (time_limit_s > 0) {
-    const long long budget = (long long)(time_limit_s * 1e9);
-    go::go_arm_deadline_kernel<<<1, 1, 0, e->stream>>>(e->gs, budget);
-    CK(cudaGetLastError());
-  }
-  CK(cudaEventRecord(e->t_start, e->stream));
-  long long launches = 0;
-  long long chunk = 0;
-  const int I = c.aos_interval, EI = c.elite_interval, MI = c.migration_interval;
-  auto next_mult = [](long long g, long long m) { return (g / m + 1) * m; };
-  go::EvolveArgs a{};
+  a = go::EvolveArgs{};
+  x = go::RowArgs{};
   a.inst = e->inst;
   a.inst_bytes = e->inst_bytes;
   a.n = e->n;
@@ -1615,7 +1588,6 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   a.lane_rows = e->lane_rows;
   a.prog = e->prog;
   a.islands = c.islands;
-  go::RowArgs x{};
   if (e->prob->family == 1) {
     const go_problem* p = e->prob;
     a.team_smem = (int)row_team_bytes(p, e->TS, e->layout);
@@ -1630,6 +1602,43 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     a.team_smem = (int)team_bytes_for(kLayouts[e->layout].elem, e->n, e->TS);
     a.resync = kLayouts[e->layout].elem == E_F64;
   }
+}
+
+int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
+                  go_run_stats* stats) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  if (e->nseq == 0) return fail(GO_E_INVALID, "registry not set");
+  CK(cudaSetDevice(e->prob->device));
+  const go_engine_config& c = e->cfg;
+  go::GlobalState gs{};
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  long long done = gs.gens_done;
+  const unsigned long long rp0 = gs.rd_pos, re0 = gs.rd_elem;
+  if (gs.stop) {  // a previous run stopped; resume from the same state
+    gs.stop = 0;
+    *e->h_stop = 0;
+  }
+  // history buffer sized for the generations this call may run
+  if (e->history_on && max_generations > e->hist_cap) {
+    if (e->history) cudaFree(e->history);
+    e->hist_cap = std::max<long long>(max_generations, 1);
+    CK(cudaMalloc(&e->history, (size_t)e->hist_cap * 8));
+  }
+  gs.deadline_ns = 0;
+  CK(cudaMemcpyAsync(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice, e->stream));
+  if (time_limit_s > 0) {
+    const long long budget = (long long)(time_limit_s * 1e9);
+    go::go_arm_deadline_kernel<<<1, 1, 0, e->stream>>>(e->gs, budget);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(e->t_start, e->stream));
+  long long launches = 0;
+  long long chunk = 0;
+  const int I = c.aos_interval, EI = c.elite_interval, MI = c.migration_interval;
+  auto next_mult = [](long long g, long long m) { return (g / m + 1) * m; };
+  go::EvolveArgs a;
+  go::RowArgs x;
+  build_evolve_args(e, a, x);
   go::EpilogueArgs q{};
   q.P = e->P;
   q.W = e->W;
@@ -1754,6 +1763,62 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     stats->evolve_ms = evolve_ms;
     stats->evolve_launches = evolve_launches;
   }
+  return GO_OK;
+}
+
+// One generation of the evolve kernel for every evolver at an explicit
+// generation index and temperature, without the epilogue (no global best,
+// AOS update, migration or elite injection): the reference's
+// evolve_generation (engine.py:538-595) for each evolver.  Each evolver's AOS
+// credit of that generation comes back in usage/impr ([P][nseq]) and
+// k_usage/k_impr ([P][3]); any pointer may be null.
+int go_engine_step(go_engine* e, int64_t generation, double temperature, int32_t* usage,
+                   int32_t* impr, int32_t* k_usage, int32_t* k_impr) {
+  if (!e) return fail(GO_E_INVALID, "null engine");
+  if (e->nseq == 0) return fail(GO_E_INVALID, "registry not set");
+  if (generation < 1) return fail(GO_E_INVALID, "generation must be >= 1");
+  CK(cudaSetDevice(e->prob->device));
+  CK(cudaStreamSynchronize(e->stream));
+  go::GlobalState gs{};
+  CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
+  gs.stop = 0;
+  gs.deadline_ns = 0;
+  *e->h_stop = 0;
+  CK(cudaMemcpy(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice));
+  go::EvolveArgs a;
+  go::RowArgs x;
+  build_evolve_args(e, a, x);
+  e->h_temps[0] = temperature;
+  CK(cudaMemcpyAsync(e->temps, e->h_temps, 8, cudaMemcpyHostToDevice, e->stream));
+  a.temps = e->temps;
+  a.gen0 = generation;
+  a.ngen = 1;
+  if (e->xover) {  // the island snapshot of this generation = the population now
+    CK(cudaMemcpyAsync(e->snap + (size_t)(a.gen0 % go::SNAP_DEPTH) * e->P * e->W, e->genes,
+                       (size_t)e->P * e->W * 2, cudaMemcpyDeviceToDevice, e->stream));
+    go::go_fill_i32_kernel<<<(e->P + 255) / 256, 256, 0, e->stream>>>(e->prog, e->P,
+                                                                      (int)a.gen0);
+    CK(cudaGetLastError());
+  }
+  void* args[] = {&a, &x};
+  int rc = launch_static_or_jit(e->k_evolve, e->k_evolve_jit, dim3(e->grid), dim3(e->E * e->TS),
+                                e->smem, e->stream, args, false);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(e->stream));
+  e->launches += 1;
+  const size_t P = e->P;
+  if (usage || impr) {
+    std::vector<int> u(P * go::MAX_SEQ), v(P * go::MAX_SEQ);
+    CK(cudaMemcpy(u.data(), e->usage, u.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(v.data(), e->impr, v.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t ev = 0; ev < P; ++ev)
+      for (int i = 0; i < e->nseq; ++i) {
+        if (usage) usage[ev * e->nseq + i] = u[ev * go::MAX_SEQ + i];
+        if (impr) impr[ev * e->nseq + i] = v[ev * go::MAX_SEQ + i];
+      }
+  }
+  if (k_usage) CK(cudaMemcpy(k_usage, e->k_usage, P * 3 * 4, cudaMemcpyDeviceToHost));
+  if (k_impr) CK(cudaMemcpy(k_impr, e->k_impr, P * 3 * 4, cudaMemcpyDeviceToHost));
   return GO_OK;
 }
 

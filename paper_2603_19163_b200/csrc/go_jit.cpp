@@ -121,10 +121,14 @@ static std::string cache_dir() {
   return d;
 }
 
+// 384 threads = 3 teams of 128 lanes per CTA, 168 registers per thread: the
+// C2 shared-memory budget (int16 triangle + per-warp scratch rows) holds 3
+// teams, and the register headroom removes most of the 128-register spills
+// (C2: 84.8 M vs 76.8 M move evals/s at 512, profiles/r02_*).
 int jit_max_threads() {
   const char* e = getenv("GO_EVOLVE_MAX_THREADS");
-  const int v = e ? atoi(e) : 512;
-  return (v >= 128 && v <= 1024 && v % 32 == 0) ? v : 512;
+  const int v = e ? atoi(e) : 384;
+  return (v >= 128 && v <= 1024 && v % 32 == 0) ? v : 384;
 }
 
 static const char* kHeaders[] = {"go_common.cuh",      "go_dist.cuh",      "go_perm.cuh",

@@ -182,11 +182,13 @@ __device__ __forceinline__ int lns_scope(int n) {
 }
 
 // random.sample(range(total), m) for m <= 30: CPython's pool method (a
-// virtual pool of overrides) when total <= setsize(m), else the set method
+// virtual pool of overrides in ovi/ovv, >= m entries each) when
+// total <= setsize(m), else the set method
 template <class C>
-__device__ __forceinline__ void sample_range(C& c, int total, int m, int* picks) {
+__device__ __forceinline__ void sample_range_buf(C& c, int total, int m, int* picks, int* ovi,
+                                                 int* ovv) {
   if (total <= sample_setsize(m)) {
-    int ovi[30], ovv[30], no = 0;
+    int no = 0;
     for (int t = 0; t < m; ++t) {
       const int jj = c.randbelow(total - t);
       int val = jj;
@@ -221,6 +223,12 @@ __device__ __forceinline__ void sample_range(C& c, int total, int m, int* picks)
       picks[t] = jj;
     }
   }
+}
+
+template <class C>
+__device__ __forceinline__ void sample_range(C& c, int total, int m, int* picks) {
+  int ovi[30], ovv[30];
+  sample_range_buf(c, total, m, picks, ovi, ovv);
 }
 
 // sample(range(1, n), 3) sorted (operators.py:300)

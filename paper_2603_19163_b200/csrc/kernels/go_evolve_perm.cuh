@@ -35,22 +35,51 @@ struct NoCustomOps {
 };
 
 template <class Acc>
-struct TeamShared {
+struct TeamShared {  // (row kernels: go_evolve_row.cuh)
   Acc wd[32];
   int wl[32];
   Move chain[MAX_CHAIN];
   double bd;
   int nm, k, accept;
-  int dnext;                       // next deferred request to hand out (dynamic, per warp)
+  int dnext;
   int sq[MAX_CHAIN];
   int usage[MAX_SEQ];
   int impr[MAX_SEQ];
   int k_usage[3];
   int k_impr[3];
+  int nreq;
+  int ndreq;
+  int ngr;
+  unsigned char cnt[16][MAX_SEQ];
+};
+
+// Team state of the permutation kernel; the per-warp arrays (argmin
+// partials, lane-sort counts) follow it, sized by the team's warp count.
+struct PermTeam {
+  int accept;
+  int dnext;                       // next deferred request to hand out (dynamic, per warp)
   int nreq;                        // pending cooperative relocations this step
   int ndreq;                       // pending deferred whole-row operators this step
   int ngr;                         // ... of which guided rebuilds (queued from the back)
-  unsigned char cnt[16][MAX_SEQ];  // per-warp lane counts per sequence (lane sort)
+  int pad;
+  int usage[MAX_SEQ];
+  int impr[MAX_SEQ];
+  int k_usage[3];
+  int k_impr[3];
+};
+template <class Acc>
+struct PermWarpArrays {
+  Acc* wd;               // [nw] warp argmin partials
+  int* wl;               // [nw]
+  unsigned char* cnt;    // [nw][MAX_SEQ] per-warp lane counts per sequence (lane sort)
+  static __host__ __device__ unsigned bytes(int nw) {
+    return (unsigned)(nw * (sizeof(Acc) + 4 + MAX_SEQ));
+  }
+  __device__ __forceinline__ void bind(unsigned char* p, int nw) {
+    wd = (Acc*)p;
+    wl = (int*)(p + nw * sizeof(Acc));
+    cnt = p + nw * (sizeof(Acc) + 4);
+  }
 };
 
 // Per logical lane state handed between threads across chain steps
@@ -141,7 +170,11 @@ __device__ __forceinline__ void run_perm_op(int kind, PermCtx<Policy>& c) {
 }
 
 // Shared-memory carve-up common to the kernel and the host (engine.cu).
+// Per team: [current row][PermTeam][per-warp arrays][LaneArrays]
+// [per-warp scratch: row of n int16 + 32 ints].  Warp 0's scratch row doubles
+// as the ping-pong row of the winner's apply (cur <-> nxt).
 struct PermSmem {
+  enum { WINTS = 32 };
   static __host__ __device__ unsigned align(unsigned x, unsigned a) { return (x + a - 1) / a * a; }
   static __host__ __device__ unsigned inst_off() { return 0; }
   static __host__ __device__ unsigned reg_off(unsigned inst_bytes) { return align(inst_bytes, 128); }
@@ -149,15 +182,23 @@ struct PermSmem {
     return reg_off(inst_bytes) + 768;
   }
   static __host__ __device__ unsigned row_bytes(int n) { return align(2u * n, 16); }
+  static __host__ __device__ unsigned shared_off(int n) { return row_bytes(n); }
   template <class Acc>
-  static __host__ __device__ unsigned shared_off(int n) { return 2 * row_bytes(n); }
+  static __host__ __device__ unsigned warps_off(int n) {
+    return align(shared_off(n) + (unsigned)sizeof(PermTeam), 16);
+  }
   template <class Acc>
-  static __host__ __device__ unsigned lanes_off(int n) {
-    return align(shared_off<Acc>(n) + (unsigned)sizeof(TeamShared<Acc>), 16);
+  static __host__ __device__ unsigned lanes_off(int n, int TS) {
+    return align(warps_off<Acc>(n) + PermWarpArrays<Acc>::bytes(TS / 32), 16);
+  }
+  static __host__ __device__ unsigned scratch_bytes(int n) { return row_bytes(n) + 4 * WINTS; }
+  template <class Acc>
+  static __host__ __device__ unsigned scratch_off(int n, int TS) {
+    return align(lanes_off<Acc>(n, TS) + LaneArrays<Acc>::bytes(TS), 16);
   }
   template <class Acc>
   static __host__ __device__ unsigned team_bytes(int n, int TS) {
-    return align(lanes_off<Acc>(n) + LaneArrays<Acc>::bytes(TS), 16);
+    return align(scratch_off<Acc>(n, TS) + (unsigned)(TS / 32) * scratch_bytes(n), 16);
   }
 };
 
@@ -208,11 +249,18 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   const long long evg = (long long)A.ev_offset + ev;
 
   unsigned char* tb = sm + PermSmem::team_off(A.inst_bytes) + team * A.team_smem;
+  unsigned char* scr = tb + PermSmem::scratch_off<Acc>(n, TS);
+  const unsigned scr_bytes = PermSmem::scratch_bytes(n);
   i16* cur = (i16*)tb;
-  i16* nxt = (i16*)(tb + PermSmem::row_bytes(n));
-  TeamShared<Acc>* ts = (TeamShared<Acc>*)(tb + PermSmem::shared_off<Acc>(n));
+  i16* nxt = (i16*)scr;  // warp 0's scratch row
+  // this warp's shared-memory scratch (deferred whole-row operators)
+  i16* const my_row = (i16*)(scr + warp * scr_bytes);  // warp 0: see nxt
+  int* const my_int = (int*)(scr + warp * scr_bytes + PermSmem::row_bytes(n));
+  PermTeam* ts = (PermTeam*)(tb + PermSmem::shared_off(n));
+  PermWarpArrays<Acc> wa;
+  wa.bind(tb + PermSmem::warps_off<Acc>(n), nwarps);
   LaneArrays<Acc> la;
-  la.bind(tb + PermSmem::lanes_off<Acc>(n), TS);
+  la.bind(tb + PermSmem::lanes_off<Acc>(n, TS), TS);
 
   for (int p = lane; p < n; p += TS) cur[p] = A.genes[(size_t)ev * n + p];
   // lane-private global rows of deferred whole-row operators (2 per lane)
@@ -235,10 +283,10 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     Acc part = pol.partial(cur, n, lane, TS);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-    if (wl == 0) ts->wd[warp] = part;
+    if (wl == 0) wa.wd[warp] = part;
     team_bar(team, TS);
     Acc tot = 0;
-    for (int w = 0; w < nwarps; ++w) tot += ts->wd[w];
+    for (int w = 0; w < nwarps; ++w) tot += wa.wd[w];
     phi = (double)tot;
     team_bar(team, TS);
   }
@@ -288,9 +336,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       }
       const unsigned grp = __match_any_sync(0xffffffffu, hold_seq);
       const int rank = __popc(grp & lt_mask);
-      ts->cnt[warp][wl] = 0;
+      wa.cnt[warp * MAX_SEQ + wl] = 0;
       __syncwarp();
-      if (hold_seq != 31 && rank == 0) ts->cnt[warp][hold_seq] = (unsigned char)__popc(grp);
+      if (hold_seq != 31 && rank == 0) wa.cnt[warp * MAX_SEQ + hold_seq] = (unsigned char)__popc(grp);
       team_bar(team, TS);
       GO_TICK(1 + 4 * s);
       if (lane == 0) {
@@ -303,7 +351,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       int tj = 0;
       if (wl < nseq) {
         const int q = s_gord[wl];
-        for (int w = 0; w < nwarps; ++w) tj += ts->cnt[w][q];
+        for (int w = 0; w < nwarps; ++w) tj += wa.cnt[w * MAX_SEQ + q];
       }
       int incl = tj;
 #pragma unroll
@@ -315,7 +363,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       const int my_pos = hold_seq != 31 ? s_grank[hold_seq] : 0;
       int base = __shfl_sync(0xffffffffu, incl - tj, my_pos);
       if (hold_seq != 31) {
-        for (int w = 0; w < warp; ++w) base += ts->cnt[w][hold_seq];
+        for (int w = 0; w < warp; ++w) base += wa.cnt[w * MAX_SEQ + hold_seq];
         la.order[base + rank] = (unsigned short)lane;
       }
       team_bar(team, TS);
@@ -487,13 +535,11 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
           const int nsel = (meta & META_MAT) && !(meta & META_SEL) ? 1 : 0;
           i16* dst = lrow + ((size_t)L * 2 + nsel) * n;
-          // the first guided rebuild of the step (handed out first) works in the
-          // team's idle shared-memory row: its scans and rotations stay on-chip
-          i16* aux = r == 0 && ngr > 0 ? nxt : lrow + ((size_t)L * 2 + (1 - nsel)) * n;
           Stream rng;
           rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
-          const DeferRes<Acc> dr = perm_defer(pol, C, kind, dst, aux, &rng, &ms, n, wl);
+          const DeferRes<Acc> dr = perm_defer(pol, C, kind, dst, warp == 0 ? nxt : my_row, my_int,
+                                              &rng, &ms, n, wl);
           Acc nd = la.delta[L];
           u32 bits = meta & META_BASE;
           int nm2 = nm;
@@ -525,18 +571,18 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     int bl = lane < T ? lane : 0x7fffffff;
     argmin_warp(bd, bl);
     if (wl == 0) {
-      ts->wd[warp] = bd;
-      ts->wl[warp] = bl;
+      wa.wd[warp] = bd;
+      wa.wl[warp] = bl;
     }
     team_bar(team, TS);
     GO_TICK(13);
-    bd = ts->wd[0];
-    bl = ts->wl[0];
+    bd = wa.wd[0];
+    bl = wa.wl[0];
     for (int w = 1; w < nwarps; ++w) {
-      const Acc od = ts->wd[w];
+      const Acc od = wa.wd[w];
       if (od < bd) {  // warps are in lane order: ties keep the lower lane
         bd = od;
-        bl = ts->wl[w];
+        bl = wa.wl[w];
       }
     }
     const double bdd = (double)bd;

@@ -4,15 +4,15 @@
 // rewrite the tour globally, so they cannot be position maps on the shared
 // current tour.  A lane that draws one is DEFERRED: after the chain step, one
 // warp per deferred lane
-//   1. materialises the lane's candidate (current tour composed with its
-//      chain) into one of the lane's two global rows (the other row may be
-//      the chain's own base);
-//   2. runs the operator on that row — lane 0 of the warp replays the lane's
-//      stream from the operator's first draw (the reference's draw order), the
-//      warp does the bulk work (OX fill by ballot/prefix, row shifts, first-
-//      minimum insertion scans);
-//   3. re-evaluates the row exactly (warp-reduced tour length) and restarts the
-//      lane's chain on it: nm = 0, delta = Φ(row) − Φ(cur).
+//   1. runs the operator — lane 0 of the warp replays the lane's stream from
+//      the operator's first draw (the reference's draw order), the warp does
+//      the bulk work in its own shared-memory scratch row (OX slice bit set
+//      and fill by ballot/prefix, row rotations, first-minimum insertion
+//      scans);
+//   2. writes the new row once into one of the lane's two global rows (the
+//      other may be the chain's own base) and measures it exactly
+//      (warp-reduced tour length);
+//   3. the lane's chain restarts on it: nm = 0, delta = Φ(row) − Φ(cur).
 // Guided rebuild scores trials with the insertion delta d(prev,v) + d(v,next)
 // − d(prev,next) instead of a full evaluation: on integer matrices Φ(trial) =
 // Φ(row without v) + that delta exactly, so first-minimum choices equal the
@@ -28,14 +28,47 @@ __device__ __forceinline__ bool perm_deferred(int kind) {
          kind == SEQ_GUIDED_REBUILD;
 }
 
-// One warp resolves one deferred lane.  `dst` / `aux` are the lane's two
-// global rows (dst receives the candidate; aux is scratch), `C` the lane's
-// chain (its base may be `aux`).  `rng` is valid in lane 0 only.
+// exact tour length of a materialised row (whole warp)
 template <class Policy>
-__device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int kind, i16* dst,
-                                           i16* aux, Stream* rng, const MateSel* ms, int n_cfg,
-                                           int wl) {
+__device__ __forceinline__ typename Policy::Acc perm_row_length(const Policy& pol, const i16* row,
+                                                                int n, int wl) {
+  typedef typename Policy::Acc Acc;
+  Acc s = 0;
+  for (int p = wl; p < n; p += 32) s += pol.cost_acc(row[p], row[p + 1 == n ? 0 : p + 1]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
+template <class Acc>
+struct DeferRes {
+  int changed;
+  Acc len;  // exact tour length of the new row (valid when changed)
+};
+
+// One warp resolves one deferred lane.  `dst` is the lane's global row that
+// receives the candidate, `wrow` / `wint` the warp's shared-memory scratch
+// (a row of n int16 and 32 ints), `C` the lane's chain.  All bulk work runs
+// in shared memory and dst is written exactly once:
+//   OX        no materialised parent: the kept slice's values are marked in a
+//             bit set (wrow), the child is written in one pass over the mate
+//             and, on integer matrices, its tour length summed on the way
+//   shuffles  parent materialised in wrow, lane 0 permutes it in place
+//   rebuild   parked row gathered into wrow straight from the chain, then
+//             every re-insertion is a scan + a span rotation in wrow
+// `rng` is valid in lane 0 only.  (A register-resident variant of OX / guided
+// rebuild was measured 2x slower end to end on C2 in round 1: its unrolled
+// shuffle code evicted the evolve loop from the instruction cache.)
+template <class Policy>
+__device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
+    const Policy pol, const Chain C, int kind, i16* dst, i16* wrow, int* wint, Stream* rng,
+    const MateSel* ms, int n_cfg, int wl) {
+  typedef typename Policy::Acc Acc;
   const int n = C.n;
+  const unsigned FULL = 0xffffffffu;
+  DeferRes<Acc> out;
+  out.changed = 0;
+  out.len = 0;
   // ---- draws that precede any row access (lane 0), broadcast to the warp ----
   int a0 = 0, a1 = 0, a2 = 0, live = 0;
   if (wl == 0) {
@@ -59,23 +92,45 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
       live = n >= 2;
     }
   }
-  live = __shfl_sync(0xffffffffu, live, 0);
-  if (!live) return 0;
-  a0 = __shfl_sync(0xffffffffu, a0, 0);
-  a1 = __shfl_sync(0xffffffffu, a1, 0);
-  a2 = __shfl_sync(0xffffffffu, a2, 0);
-
-  // ---- 1. materialise the candidate --------------------------------------------
-  for (int p = wl; p < n; p += 32) dst[p] = (i16)C.at(p);
-  __syncwarp();
+  live = __shfl_sync(FULL, live, 0);
+  if (!live) return out;
+  out.changed = 1;
 
   if (kind == SEQ_OX) {  // _ox_sequence (operators.py:412-425)
+    a0 = __shfl_sync(FULL, a0, 0);
+    const int c1 = __shfl_sync(FULL, a1, 0), c2 = __shfl_sync(FULL, a2, 0);
     const short* mate = ms->rows + (size_t)a0 * n;
-    const int c1 = a1, c2 = a2;
-    for (int p = wl; p < n; p += 32) aux[dst[p]] = (i16)p;  // inverse permutation
+    unsigned* mask = (unsigned*)wrow;  // n bits (the row holds 16 n)
+    const int nwords = (n + 31) >> 5;
+    for (int i = wl; i < nwords; i += 32) mask[i] = 0u;
     __syncwarp();
+    // kept slice child[c1..c2] = parent[c1..c2]: copied, marked, inner edges summed
+    Acc len = 0;
+    int carry = 0, s_first = 0;
+    for (int b = c1; b <= c2; b += 32) {
+      const int p = b + wl;
+      int v = 0;
+      if (p <= c2) {
+        v = C.at(p);
+        dst[p] = (i16)v;
+        atomicOr(mask + (v >> 5), 1u << (v & 31));
+      }
+      if (b == c1) s_first = __shfl_sync(FULL, v, 0);
+      int pv = __shfl_up_sync(FULL, v, 1);
+      if (wl == 0) pv = carry;
+      if (Policy::kIntegral && p <= c2 && p > c1) len += pol.cost_acc(pv, v);
+      const int last_lane = c2 - b < 31 ? c2 - b : 31;
+      carry = __shfl_sync(FULL, v, last_lane);
+    }
+    const int s_last = carry;
+    __syncwarp();
+    // fill: mate values from c2+1 (cyclic) not in the slice, into the free
+    // positions from c2+1 (cyclic); with F the fill sequence and S the slice
+    // the child read cyclically from c2+1 is F ++ S
     const int s0 = c2 + 1 == n ? 0 : c2 + 1;
-    int filled = 0;
+    int filled = 0, f_first = -1, f_last = -1;
+    const unsigned lt = (1u << wl) - 1u;
+#pragma unroll 2
     for (int b = 0; b < n; b += 32) {
       const int t = b + wl;
       int v = 0;
@@ -84,97 +139,113 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
         int src = s0 + t;
         src = src >= n ? src - n : src;
         v = __ldcg(mate + src);
-        const int at = aux[v];
-        keep = at < c1 || at > c2;
+        keep = !((mask[v >> 5] >> (v & 31)) & 1u);
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      const unsigned bal = __ballot_sync(FULL, keep);
+      if (Policy::kIntegral) {
+        // previous fill value: the nearest kept lane below, else the last so far
+        const unsigned below = bal & lt;
+        const int src_lane = below ? 31 - __clz(below) : 0;
+        const int pv_in = __shfl_sync(FULL, v, src_lane);
+        if (keep && (below || f_last >= 0)) len += pol.cost_acc(below ? pv_in : f_last, v);
+        if (bal) {
+          const int fv = __shfl_sync(FULL, v, __ffs(bal) - 1);
+          const int lv = __shfl_sync(FULL, v, 31 - __clz(bal));
+          if (f_first < 0) f_first = fv;
+          f_last = lv;
+        }
+      }
       if (keep) {
-        int w = s0 + filled + __popc(bal & ((1u << wl) - 1u));
+        int w = s0 + filled + __popc(bal & lt);
         w = w >= n ? w - n : w;
         dst[w] = (i16)v;
       }
       filled += __popc(bal);
     }
     __syncwarp();
-    return 1;
-  }
-  if (kind == SEQ_SEG_SHUFFLE) {  // operators.py:468-477, lane 0 serial
-    if (wl == 0) {
-      rng->randbelow(1);  // _pick_row(sol, rng, 2) over the single row
-      const int ls = lns_scope(n_cfg);
-      const int len = ls < n ? ls : n;
-      const int s = rng->randbelow(n - len + 1);
-      for (int i = len - 1; i >= 1; --i) {
-        const int j = rng->randbelow(i + 1);
-        const i16 t = dst[s + i];
-        dst[s + i] = dst[s + j];
-        dst[s + j] = t;
-      }
+    if (Policy::kIntegral) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) len += __shfl_xor_sync(FULL, len, off);
+      if (f_first >= 0) len += pol.cost_acc(f_last, s_first) + pol.cost_acc(s_last, f_first);
+      else len += pol.cost_acc(s_last, s_first);
+      out.len = len;
+    } else {  // float matrices: the materialised row in the usual summation order
+      __threadfence_block();
+      out.len = perm_row_length(pol, dst, n, wl);
     }
-    __syncwarp();
-    return 1;
+    return out;
   }
-  if (kind == SEQ_SCATTER_SHUFFLE) {  // operators.py:480-499, lane 0 serial
-    if (wl == 0) {
-      const int ls = lns_scope(n_cfg);
-      const int m = ls < n ? ls : n;
-      int picks[30];
-      i16 vals[30];
-      sample_range(*rng, n, m, picks);
-      for (int t = 0; t < m; ++t) vals[t] = dst[picks[t]];
-      for (int i = m - 1; i >= 1; --i) {
-        const int j = rng->randbelow(i + 1);
-        const i16 t = vals[i];
-        vals[i] = vals[j];
-        vals[j] = t;
-      }
-      for (int t = 0; t < m; ++t) dst[picks[t]] = vals[t];
-    }
-    __syncwarp();
-    return 1;
-  }
-  // ---- guided rebuild (operators.py:501-546), single row, home = None -----------
-  // One gather builds the parked row (survivors in order, then the taken
-  // values in pick order) in `aux`; every re-insertion is then one insertion
-  // scan of the row without the value (read through an index skip, two chunks
-  // in flight) plus one rotation of the span between its old and new slot.
-  // Lane t tracks the position of taken value t, so no search pass is needed.
+
   const int ls = lns_scope(n_cfg);
-  const int m = ls < n - 1 ? ls : n - 1;
-  int picks[30];
-  if (wl == 0) {
-    sample_range(*rng, n, m, picks);
-    for (int i = 1; i < m; ++i) {  // sorted by (r, -p): descending positions
-      const int v = picks[i];
-      int j = i;
-      while (j > 0 && picks[j - 1] < v) {
-        picks[j] = picks[j - 1];
-        --j;
+  if (kind == SEQ_SEG_SHUFFLE || kind == SEQ_SCATTER_SHUFFLE) {
+    // operators.py:468-499; scatter draws its cells before the row is read,
+    // then both shuffles permute the parent in place in wrow
+    const int m = ls < n ? ls : n;
+    if (kind == SEQ_SCATTER_SHUFFLE && wl == 0)
+      sample_range_buf(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
+    __syncwarp();
+    for (int p = wl; p < n; p += 32) wrow[p] = (i16)C.at(p);
+    __syncwarp();
+    if (wl == 0) {
+      if (kind == SEQ_SEG_SHUFFLE) {
+        rng->randbelow(1);  // _pick_row(sol, rng, 2) over the single row
+        const int s = rng->randbelow(n - m + 1);
+        for (int i = m - 1; i >= 1; --i) {
+          const int j = rng->randbelow(i + 1);
+          const i16 t = wrow[s + i];
+          wrow[s + i] = wrow[s + j];
+          wrow[s + j] = t;
+        }
+      } else {  // shuffling values[t] = row[picks[t]] == swapping the picked cells
+        for (int i = m - 1; i >= 1; --i) {
+          const int j = rng->randbelow(i + 1);
+          const int pi = wint[i], pj = wint[j];
+          const i16 t = wrow[pi];
+          wrow[pi] = wrow[pj];
+          wrow[pj] = t;
+        }
       }
-      picks[j] = v;
     }
+    __syncwarp();
+    for (int p = wl; p < n; p += 32) dst[p] = wrow[p];
+    out.len = perm_row_length(pol, wrow, n, wl);
+    return out;
   }
-  int mypick = 0;
-  for (int t = 0; t < m; ++t) {
-    const int x = __shfl_sync(0xffffffffu, wl == 0 ? picks[t] : 0, 0);
-    if (wl == t) mypick = x;
-  }
-  const int mytaken = wl < m ? dst[mypick] : 0;
+
+  // ---- guided rebuild (operators.py:501-546), single row, home = None -----------
+  // The parked row (survivors in order, then the taken values in pick order)
+  // is gathered into wrow straight from the chain; every re-insertion is then
+  // one insertion scan of the row without the value (an index skip, two
+  // chunks in flight) plus one rotation of the span between its old and new
+  // slot.  Lane t tracks the position of taken value t.
+  const int m = ls < n - 1 ? ls : n - 1;
+  if (wl == 0) sample_range_buf(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
+  __syncwarp();
+  // sorted by (r, -p): descending positions; picks are distinct, so a pick's
+  // rank is the number of larger picks
+  const int raw = wl < m ? wint[wl] : -1;
+  int rank = 0;
+  for (int j = 0; j < m; ++j) rank += __shfl_sync(FULL, raw, j) > raw;
+  __syncwarp();
+  if (wl < m) wint[rank] = raw;
+  __syncwarp();
+  const int mypick = wl < m ? wint[wl] : 0;
+  const int mytaken = wl < m ? C.at(mypick) : 0;
   const int keep = n - m;
-  for (int b = 0; b < n; b += 32) {  // gather the parked row into aux
+  for (int b = 0; b < n; b += 32) {  // gather the parked row into wrow
     const int d = b + wl;
     int src = d;  // d-th survivor: skip picked positions in ascending order
-    for (int j = m - 1; j >= 0; --j) src += __shfl_sync(0xffffffffu, mypick, j) <= src;
-    const int pk = __shfl_sync(0xffffffffu, mypick, d >= keep && d < n ? d - keep : 0);
-    if (d < n) aux[d] = d < keep ? dst[src] : dst[pk];
+    for (int j = m - 1; j >= 0; --j) src += __shfl_sync(FULL, mypick, j) <= src;
+    const int tk = __shfl_sync(FULL, mytaken, d >= keep && d < n ? d - keep : 0);
+    if (d < n) wrow[d] = (i16)(d < keep ? C.at(src) : tk);
   }
   __syncwarp();
-  typedef typename Policy::Acc Acc;
+  i16* aux = wrow;
   int mypos = keep + wl;  // current slot of taken value wl
   const int sz = n - 1;  // trials pos = 0 .. n-1 of the (n-1)-row without v (cyclic tour)
   for (int t = 0; t < m; ++t) {
-    const int v = __shfl_sync(0xffffffffu, mytaken, t);
-    const int q0 = __shfl_sync(0xffffffffu, mypos, t);
+    const int v = __shfl_sync(FULL, mytaken, t);
+    const int q0 = __shfl_sync(FULL, mypos, t);
     auto rv = [&](int i) -> int { return aux[i < q0 ? i : i + 1]; };  // row without v
     const int first = rv(0), last = rv(sz - 1);
     Acc best = 0;
@@ -184,14 +255,14 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
       const int p0 = b + wl, p1 = b + 32 + wl;
       const int e0 = p0 < sz ? rv(p0) : first;
       const int e1 = p1 < sz ? rv(p1) : first;
-      int pv0 = __shfl_up_sync(0xffffffffu, e0, 1);
-      int pv1 = __shfl_up_sync(0xffffffffu, e1, 1);
-      const int e0_31 = __shfl_sync(0xffffffffu, e0, 31);
+      int pv0 = __shfl_up_sync(FULL, e0, 1);
+      int pv1 = __shfl_up_sync(FULL, e1, 1);
+      const int e0_31 = __shfl_sync(FULL, e0, 31);
       if (wl == 0) {
         pv0 = carry;
         pv1 = e0_31;
       }
-      carry = __shfl_sync(0xffffffffu, e1, 31);
+      carry = __shfl_sync(FULL, e1, 31);
       if (p0 < n) {
         const Acc sc = pol.insertion(pv0, v, v, e0);
         if (bp == 0x7fffffff || sc < best) {
@@ -209,8 +280,8 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      const Acc ob = __shfl_xor_sync(0xffffffffu, best, off);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+      const Acc ob = __shfl_xor_sync(FULL, best, off);
+      const int op = __shfl_xor_sync(FULL, bp, off);
       if (op != 0x7fffffff && (bp == 0x7fffffff || ob < best || (ob == best && op < bp))) {
         best = ob;
         bp = op;
@@ -245,40 +316,7 @@ __device__ __noinline__ int perm_defer_run(const Policy pol, const Chain C, int 
     __syncwarp();
   }
   for (int p = wl; p < n; p += 32) dst[p] = aux[p];
-  __syncwarp();
-  return 1;
-}
-
-// exact tour length of a materialised row (whole warp)
-template <class Policy>
-__device__ __forceinline__ typename Policy::Acc perm_row_length(const Policy& pol, const i16* row,
-                                                                int n, int wl) {
-  typedef typename Policy::Acc Acc;
-  Acc s = 0;
-  for (int p = wl; p < n; p += 32) s += pol.cost_acc(row[p], row[p + 1 == n ? 0 : p + 1]);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  return s;
-}
-
-
-template <class Acc>
-struct DeferRes {
-  int changed;
-  Acc len;  // exact tour length of the new row (valid when changed)
-};
-
-// Runs the deferred operator and measures the new row.  (A register-resident
-// variant of OX / guided rebuild was measured 2x slower end to end on C2: its
-// unrolled shuffle code evicted the evolve loop from the instruction cache.)
-template <class Policy>
-__device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(const Policy pol, const Chain C,
-                                                                  int kind, i16* dst, i16* aux,
-                                                                  Stream* rng, const MateSel* ms,
-                                                                  int n_cfg, int wl) {
-  DeferRes<typename Policy::Acc> out;
-  out.changed = perm_defer_run(pol, C, kind, dst, aux, rng, ms, n_cfg, wl);
-  out.len = out.changed ? perm_row_length(pol, dst, C.n, wl) : 0;
+  out.len = perm_row_length(pol, aux, n, wl);
   return out;
 }
 

@@ -156,8 +156,11 @@ class EngineConfig:
 
 @dataclass
 class EvolverState:
+    """engine.py:187-192.  `stats` is the evolver's AosStats (the reference
+    requires it; None is accepted and skips host-side credit)."""
     current: Solution
     island_id: int
+    stats: object = None
     temperature: float = 0.0
 
 
@@ -452,6 +455,123 @@ def _best_index(pop, cfg) -> int:
     return b
 
 
+def _worst_index(pop, cfg) -> int:
+    w = 0
+    for i in range(1, len(pop)):
+        if compare(pop[i], pop[w], cfg) == B_BETTER:
+            w = i
+    return w
+
+
+# ---------------------------------------------------------------------------
+# host list forms of the island operations (engine.py:483-532).  The engine's
+# own migration and elite injection run in the device epilogue
+# (kernels/go_epilogue.cuh) and across GPUs in islands.py; these keep the
+# reference's list-of-Solutions helpers for callers that drive islands
+# themselves.
+
+def island_migrate(populations: list[list[Solution]], strategy: str, cfg: ProblemConfig,
+                   rng: random.Random, top_n: int = 1):
+    """ring: each island's best replaces the next island's worst (a
+    one-member island only takes a strictly better donor); global_top_n: the
+    global top-n, each into a random non-best slot of every island.  An
+    island's best is never displaced (engine.py:483-521)."""
+    k = len(populations)
+    if k < 2:
+        return
+    if strategy == "ring":
+        donors = [pop[_best_index(pop, cfg)].copy() for pop in populations]
+        for i, donor in enumerate(donors):
+            recv = populations[(i + 1) % k]
+            if len(recv) == 1:
+                if compare(donor, recv[0], cfg) == A_BETTER:
+                    recv[0] = donor
+                continue
+            w, b = _worst_index(recv, cfg), _best_index(recv, cfg)
+            if w != b:
+                recv[w] = donor
+        return
+    if strategy != "global_top_n":
+        raise ValueError(f"unknown migration strategy {strategy!r}")
+    flat = [s for pop in populations for s in pop]
+    order = sorted(range(len(flat)), key=cmp_to_key(lambda a, b: compare(flat[a], flat[b], cfg)))
+    donors = [flat[i].copy() for i in order[:top_n]]
+    for pop in populations:
+        b = _best_index(pop, cfg)
+        free = [i for i in range(len(pop)) if i != b]
+        for donor in donors:
+            if not free:
+                break
+            pop[free[rng.randrange(len(free))]] = donor.copy()
+
+
+def elite_inject(population: list[Solution], global_best: Solution, interval: int,
+                 generation: int, cfg: ProblemConfig) -> bool:
+    """Every interval-th generation the comparison-worst member becomes a copy
+    of the tracked best (engine.py:524-532)."""
+    if generation % interval != 0:
+        return False
+    population[_worst_index(population, cfg)] = global_best.copy()
+    return True
+
+
+# ---------------------------------------------------------------------------
+# one generation of one evolver (engine.py:538-595), on the device
+
+def evolve_generation(ev: EvolverState, ev_idx: int, generation: int, temperature: float,
+                      problem: ProblemDefinition, cfg: ProblemConfig, registry: SequenceRegistry,
+                      k_weights, seed: int, team_size: int, penalty_weight: float,
+                      island_snapshot: list[Solution], member_pos: int,
+                      device: int = 0) -> bool:
+    """The reference's evolve_generation run by the evolve kernel: the island
+    snapshot becomes a device population (ev.current at member_pos), evolver
+    member_pos draws its lane streams as global evolver `ev_idx`, and one
+    generation runs at `temperature` with the given registry weights and K
+    weights (go_engine_step: no epilogue, so no global best, AOS update or
+    migration).  On acceptance ev.current becomes the winner and the winner's
+    sequences and k are credited to ev.stats.  Returns the acceptance.
+
+    Lane streams are Philox words keyed by mix64(seed, ev_idx, generation,
+    lane, 0), so trajectories follow the device's streams, not
+    MT19937."""
+    snap = list(island_snapshot) if island_snapshot else [ev.current]
+    if not 0 <= member_pos < len(snap):
+        raise ValueError("member_pos outside the island snapshot")
+    pop = [s.copy() for s in snap]
+    pop[member_pos] = ev.current.copy()
+    ecfg = EngineConfig(population=len(pop), team_size=team_size, seed=seed,
+                        evolver_offset=ev_idx - member_pos, device=device,
+                        aos=AosConfig(update_interval=1 << 30),
+                        elite_injection_interval=1 << 30, max_generations=1)
+    reg = registry.copy()
+    dr = DeviceRun(problem, ecfg, seed, initial_population=pop, registry=reg,
+                   k_weights=k_weights, penalty_weight=penalty_weight)
+    try:
+        nseq, P = len(reg.entries), len(pop)
+        usage = np.zeros((P, nseq), dtype=np.int32)
+        impr = np.zeros((P, nseq), dtype=np.int32)
+        k_usage = np.zeros((P, 3), dtype=np.int32)
+        k_impr = np.zeros((P, 3), dtype=np.int32)
+        N.check(dr.lib.go_engine_step(dr.engine, int(generation), float(temperature),
+                                      N.iptr(usage), N.iptr(impr), N.iptr(k_usage),
+                                      N.iptr(k_impr)))
+        after = dr.population()[member_pos]
+    finally:
+        dr.close()
+    ev.temperature = temperature
+    accepted = int(k_usage[member_pos].sum()) == 1
+    if not accepted:
+        return False
+    ev.current = after
+    if ev.stats is not None:
+        improved = bool(k_impr[member_pos].any())
+        for i, e in enumerate(reg.entries):
+            for _ in range(int(usage[member_pos, i])):
+                ev.stats.record(e.id, improved)
+        ev.stats.record_k(int(np.argmax(k_usage[member_pos])) + 1, improved)
+    return True
+
+
 # ---------------------------------------------------------------------------
 # runs
 
@@ -481,7 +601,9 @@ class DeviceRun:
 
     def __init__(self, problem: ProblemDefinition, config: EngineConfig, seed: int,
                  initial_population: list[Solution] | None = None,
-                 init_rng: random.Random | None = None, init_salt: int = 0):
+                 init_rng: random.Random | None = None, init_salt: int = 0,
+                 registry: SequenceRegistry | None = None, k_weights=None,
+                 penalty_weight: float | None = None):
         self.t_start = time.perf_counter()
         self.problem, self.config, self.seed = problem, config, seed
         cfg = problem.config()
@@ -497,8 +619,11 @@ class DeviceRun:
         self.jit_seconds = time.perf_counter() - t_jit if getattr(problem, "JIT", False) else 0.0
         self.profile = classify(cfg)
         dev_seqs = problem.device_sequences()
-        self.registry = build_registry(cfg, dev_seqs)
-        apply_preset(self.registry, self.profile)
+        if registry is not None:  # a caller-owned registry state (evolve_generation)
+            self.registry = registry
+        else:
+            self.registry = build_registry(cfg, dev_seqs)
+            apply_preset(self.registry, self.profile)
         self.missing_ops = missing_device_sequences(cfg, dev_seqs)
         if config.custom_operators:
             self._register_custom(config.custom_operators)
@@ -538,7 +663,9 @@ class DeviceRun:
             pop = [s.copy() for s in initial_population]
             evaluate_many(problem, pop, dev)
         self.initial_population = pop
-        if cfg.penalty_weight is not None:
+        if penalty_weight is not None:
+            pw = penalty_weight
+        elif cfg.penalty_weight is not None:
             pw = cfg.penalty_weight
         else:
             scale = float(np.mean([abs(s.objectives[0]) for s in pop]))
@@ -587,7 +714,8 @@ class DeviceRun:
         w = np.array(reg.weights(), dtype=np.float64)
         floors = np.array([e.floor for e in reg.entries], dtype=np.float64)
         caps = np.array([e.cap for e in reg.entries], dtype=np.float64)
-        kw = np.array(DEFAULT_K_WEIGHTS, dtype=np.float64)
+        kw = np.array(DEFAULT_K_WEIGHTS if k_weights is None else tuple(k_weights),
+                      dtype=np.float64)
         N.check(self.lib.go_engine_set_registry(self.engine, len(ids), N.iptr(ids), N.dptr(w),
                                                 N.dptr(floors), N.dptr(caps), reg.total(),
                                                 N.dptr(kw)))
