@@ -10,17 +10,20 @@ GPU.
 __version__ = "0.1.0"
 
 from ._native import NativeError, NativeUnavailable
-from .aos import DEFAULT_K_WEIGHTS, AosConfig
+from .aos import (DEFAULT_K_WEIGHTS, AosConfig, AosStats, record, sample_k, sample_sequence,
+                  stagnation_check_and_reset, update_weights)
 from .core import (ComparisonMode, Direction, Encoding, EncodingKind, Lexicographic, ObjDef,
                    ProblemConfig, RowModeKind, Solution, StructuralError, ValidityReport,
                    Weighted, compare, scalarize, validate_solution)
 from .demo_ops import demo_operator_set, tsp_delta_operators
 from .engine import (DeviceRun, EngineConfig, EvolverState, IslandsConfig, RunResult,
-                     adaptive_population_size, b200_population_size, heuristic_candidates,
-                     initialize_population, initialize_population_device, random_solution, run,
-                     scalar_fitness)
-from .operators import (CustomOperator, SequenceEntry, SequenceRegistry, build_registry,
-                        lns_scope)
+                     adaptive_population_size, b200_population_size, elite_inject,
+                     evolve_generation, fast_nondominated_sort, heuristic_candidates,
+                     initialize_population, initialize_population_device, island_migrate,
+                     random_solution, run, scalar_fitness)
+from .instances import DemoInstance, demo_instance, demo_instances
+from .operators import (CustomOperator, OperatorContext, SequenceEntry, SequenceRegistry,
+                        apply_sequence, build_registry, lns_scope, register_custom)
 from .problems import (BUILTIN_NAMES, CudaProblem, InstanceData, ProblemDefinition,
                        builtin_problem, evaluate)
 from .profiles import PRESETS, ProblemProfile, Scale, WeightPreset, apply_preset, classify
@@ -61,6 +64,23 @@ def solve_custom(encoding, dim2, n=None, compute_obj=None, compute_penalty=None,
     cfg = EngineConfig(time_limit_seconds=time_limit, custom_operators=tuple(custom_operators),
                        max_generations=kw.pop("max_generations", 10 ** 9), **kw)
     return run(prob, cfg, best_known=best_known)
+
+
+from . import problems as builtins  # noqa: E402  (the reference's genopt.builtins)
+
+
+def install_genopt_alias() -> None:
+    """Make `import genopt` (and `genopt.engine`, `genopt.operators`, ...)
+    resolve to this package, so code written against the reference runs
+    unchanged: the drop-in switch.  The reference's
+    `genopt.builtins` is this package's `problems` module."""
+    import importlib
+    import sys
+    sys.modules["genopt"] = sys.modules[__name__]
+    for sub in ("aos", "core", "demo_ops", "engine", "instances", "operators", "parsers",
+                "problems", "profiles", "results", "cli"):
+        sys.modules[f"genopt.{sub}"] = importlib.import_module(f"{__name__}.{sub}")
+    sys.modules["genopt.builtins"] = sys.modules[f"{__name__}.problems"]
 
 
 __all__ = [name for name in dir() if not name.startswith("_")]

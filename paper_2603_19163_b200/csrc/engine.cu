@@ -573,12 +573,16 @@ int go_problem_destroy(go_problem* p) {
 
 namespace {
 
+// thread cap of the JIT TSP module for a team stride: the default launch
+// bound (jit_max_threads) unless one team alone needs more
+int tsp_jit_cap(int TS) { return std::max(gohost::jit_max_threads(), TS); }
+
 // Layout + teams-per-CTA choice (paper §4.3 three-layer split: the problem
 // states its bytes, the solver asks CUDA for them, overflow -> global/L2).
 void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_out) {
   const int n = p->n;
   const size_t optin = (size_t)p->dev.smem_optin;
-  const int cap = p->ops.empty() ? 512 : gohost::jit_max_threads();
+  const int cap = p->ops.empty() ? 512 : tsp_jit_cap(TS);
   const int Emax = std::max(1, std::min(8, cap / TS));
   const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
   const int full = p->elem * 2, tri = p->elem * 2 + 1;
@@ -839,18 +843,21 @@ int set_smem_attr(void* fn, CUfunction jf, size_t smem) {
   return GO_OK;
 }
 
-int ensure_jit(go_problem* p, int layout, gohost::JitModule** out) {
-  auto it = p->jit.find(layout);
+// JIT TSP module for a layout and a CTA thread cap (launch bound)
+int ensure_jit(go_problem* p, int layout, gohost::JitModule** out, int cap = 0) {
+  if (cap <= 0) cap = gohost::jit_max_threads();
+  const int key = layout * 4096 + cap;
+  auto it = p->jit.find(key);
   if (it != p->jit.end()) {
     *out = &it->second;
     return GO_OK;
   }
   gohost::JitModule m;
   std::string log;
-  const int rc = gohost::jit_build_tsp(kLayouts[layout].dist_type, p->ops, &m, &log);
+  const int rc = gohost::jit_build_tsp(kLayouts[layout].dist_type, p->ops, &m, &log, cap);
   if (rc) return fail(rc, "NVRTC build failed: " + log);
-  p->jit[layout] = m;
-  *out = &p->jit[layout];
+  p->jit[key] = m;
+  *out = &p->jit[key];
   return GO_OK;
 }
 
@@ -1323,7 +1330,7 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   e->grid = (e->P + e->E - 1) / e->E;
   if (p->family == 0 && !p->ops.empty()) {
     gohost::JitModule* m = nullptr;
-    int rc = ensure_jit(p, e->layout, &m);
+    int rc = ensure_jit(p, e->layout, &m, tsp_jit_cap(e->TS));
     if (rc) return rc;
     e->k_evolve_jit = m->evolve;
   } else if (p->family == 0) {

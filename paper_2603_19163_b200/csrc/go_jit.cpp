@@ -140,7 +140,7 @@ static const char* kHeaders[] = {"go_common.cuh",      "go_dist.cuh",      "go_p
 // #line-references) with the SHA-256 cubin cache.
 static int jit_compile_source(const std::string& source, const std::vector<UserOpSrc>& ops,
                               std::string* cubin_out, std::string* key_out, bool* hit_out,
-                              std::string* log) {
+                              std::string* log, int max_threads = 0) {
 
   const std::string kdir = kernel_dir();
   std::string headers_blob;
@@ -155,7 +155,8 @@ static int jit_compile_source(const std::string& source, const std::vector<UserO
   const std::string inc = "-I" + kdir;
   const char* extra = getenv("GO_JIT_DEFINE");  // e.g. GO_PHASE_TIMING (profiling builds)
   const std::string extra_opt = std::string("-D") + (extra && *extra ? extra : "GO_JIT_DEFAULT=1");
-  const std::string thr_opt = "-DGO_EVOLVE_MAX_THREADS=" + std::to_string(jit_max_threads());
+  const std::string thr_opt = "-DGO_EVOLVE_MAX_THREADS=" +
+                              std::to_string(max_threads > 0 ? max_threads : jit_max_threads());
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
                         "-default-device", "-DGO_JIT=1", extra_opt.c_str(), thr_opt.c_str(),
                         inc.c_str()};
@@ -224,7 +225,7 @@ static int jit_compile_source(const std::string& source, const std::vector<UserO
 
 int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
                     std::string* cubin_out, std::string* key_out, bool* hit_out,
-                    std::string* log) {
+                    std::string* log, int max_threads) {
   std::ostringstream src;
   src << "// generated by go_jit.cpp — user operators for the TSP evolve kernel\n"
       << "#include \"go_tsp_entry.cuh\"\n"
@@ -242,15 +243,15 @@ int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& 
     src << "      case " << i << ": user::op_slot" << i << "(ctx); break;\n";
   src << "      default: ctx.err |= ERR_UNKNOWN_SEQ;\n    }\n  }\n};\n}  // namespace go\n"
       << "GO_TSP_KERNELS(jit, " << dist_type << ", go::UserOps)\n";
-  return jit_compile_source(src.str(), ops, cubin_out, key_out, hit_out, log);
+  return jit_compile_source(src.str(), ops, cubin_out, key_out, hit_out, log, max_threads);
 }
 
 int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
-                  JitModule* out, std::string* log) {
+                  JitModule* out, std::string* log, int max_threads) {
   const auto t0 = std::chrono::steady_clock::now();
   std::string cubin;
   bool hit = false;
-  const int rc = jit_compile_tsp(dist_type, ops, &cubin, &out->key, &hit, log);
+  const int rc = jit_compile_tsp(dist_type, ops, &cubin, &out->key, &hit, log, max_threads);
   if (rc) return rc;
   const Drv* d = drv();
   if (!d) {

@@ -31,11 +31,13 @@ std::string kernel_dir();
 // TSP path specialised for distance type `dist_type` with the given user
 // operators compiled in as slots 0..n-1.  Returns 0 or a GO_E_* status and a
 // compiler log.
+// `max_threads` is the kernel's launch bound (GO_EVOLVE_MAX_THREADS; 0 = the
+// default jit_max_threads()): teams x lanes per CTA may not exceed it.
 int jit_compile_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
                     std::string* cubin_out, std::string* key_out, bool* hit_out,
-                    std::string* log);
+                    std::string* log, int max_threads = 0);
 int jit_build_tsp(const std::string& dist_type, const std::vector<UserOpSrc>& ops,
-                  JitModule* out, std::string* log);
+                  JitModule* out, std::string* log, int max_threads = 0);
 
 // A user problem: objective / penalty snippet bodies and the named float64
 // data arrays they read (byte offsets into the instance image).

@@ -25,12 +25,16 @@ from functools import cmp_to_key
 import numpy as np
 
 from . import _native as N
-from .aos import DEFAULT_K_WEIGHTS, AosConfig
-from .core import (A_BETTER, B_BETTER, Direction, EncodingKind, ProblemConfig, RowModeKind,
-                   Solution, Weighted, compare, scalarize, validate_solution)
+from .aos import (DEFAULT_K_WEIGHTS, AosConfig, AosStats, sample_k,  # noqa: F401 (API)
+                  sample_sequence, stagnation_check_and_reset, update_k_weights,
+                  update_weights)
+from .core import (A_BETTER, B_BETTER, Direction, EncodingKind, Lexicographic,  # noqa: F401
+                   ProblemConfig, RowModeKind, Solution, Weighted, compare, scalarize,
+                   validate_solution)
 from .operators import (CustomOperator, SequenceRegistry, append_custom, build_registry,
                         missing_device_sequences, validate_custom_id)
-from .problems import ProblemDefinition, evaluate_many, pack_solutions
+from .operators import OperatorContext, apply_sequence, register_custom  # noqa: F401 (API)
+from .problems import ProblemDefinition, evaluate, evaluate_many, pack_solutions  # noqa: F401
 from .profiles import apply_preset, classify
 
 _MASK64 = (1 << 64) - 1
@@ -447,6 +451,25 @@ def scalar_fitness(sol: Solution, cfg: ProblemConfig, penalty_weight: float) -> 
     return scalarize(sol.objectives, cfg.obj_defs, weights) + penalty_weight * sol.penalty
 
 
+def acceptance_delta(cand: Solution, current: Solution, cfg: ProblemConfig,
+                     penalty_weight: float) -> float:
+    """engine.py:225-246 on host Solutions (the device computes the same δ per
+    lane): Weighted — Φ(cand) − Φ(cur); Lexicographic — the difference on the
+    first objective not tied within its tolerance (sign-flipped for Maximize),
+    plus penalty_weight · (penalty difference)."""
+    mode = cfg.comparison_or_default()
+    if isinstance(mode, Weighted):
+        return scalar_fitness(cand, cfg, penalty_weight) - scalar_fitness(current, cfg,
+                                                                          penalty_weight)
+    d = 0.0
+    for i in mode.priority_order:
+        diff = float(cand.objectives[i]) - float(current.objectives[i])
+        if abs(diff) > mode.tolerances[i]:
+            d = -diff if cfg.obj_defs[i].direction is Direction.MAXIMIZE else diff
+            break
+    return d + penalty_weight * (cand.penalty - current.penalty)
+
+
 def _best_index(pop, cfg) -> int:
     b = 0
     for i in range(1, len(pop)):
@@ -570,6 +593,82 @@ def evolve_generation(ev: EvolverState, ev_idx: int, generation: int, temperatur
                 ev.stats.record(e.id, improved)
         ev.stats.record_k(int(np.argmax(k_usage[member_pos])) + 1, improved)
     return True
+
+
+def apply_operator_device(registry: SequenceRegistry, seq_id: int, sol: Solution, rng,
+                          ctx) -> None:
+    """operators.apply_sequence on the device: a one-evolver, one-lane evolve
+    step whose registry holds only `seq_id`, with K weights (1, 0, 0) and an
+    infinite temperature, so the lane applies exactly that operator once and
+    its candidate is always accepted (exp(-d/inf) = 1 > random()).  A
+    crossover's mate comes from ctx.pick_mate(rng) on the host and sits in the
+    population as the only other member; guided rebuild without ctx.phi falls
+    back to scatter shuffle as in the reference (operators.py:510-512).  The
+    lane stream is keyed by 64 bits drawn from `rng`."""
+    from .operators import (CROSSOVER_IDS, SEQ_GUIDED_REBUILD, SEQ_SCATTER_SHUFFLE,
+                            SequenceEntry)
+    problem = ctx.problem
+    eff = seq_id
+    if seq_id == SEQ_GUIDED_REBUILD and ctx.phi is None:
+        eff = SEQ_SCATTER_SHUFFLE
+    entry = registry.get(seq_id)
+    one = SequenceRegistry([SequenceEntry(eff, entry.name if eff == seq_id else
+                                          "scatter_shuffle", None, 1.0)])
+    pop = [sol.copy()]
+    if eff in CROSSOVER_IDS:
+        mate = ctx.pick_mate(rng) if ctx.pick_mate is not None else None
+        if mate is None:
+            return
+        pop.append(mate.copy())
+    seed = rng.getrandbits(64)
+    ecfg = EngineConfig(population=len(pop), team_size=1, seed=seed,
+                        aos=AosConfig(update_interval=1 << 30),
+                        elite_injection_interval=1 << 30, max_generations=1)
+    dr = DeviceRun(problem, ecfg, seed, initial_population=pop, registry=one,
+                   k_weights=(1.0, 0.0, 0.0))
+    try:
+        N.check(dr.lib.go_engine_step(dr.engine, 1, math.inf, None, None, None, None))
+        after = dr.population()[0]
+    finally:
+        dr.close()
+    sol.data[...] = after.data
+    sol.dim2_sizes[...] = after.dim2_sizes
+
+
+def probe_custom_device(problem: ProblemDefinition, op: CustomOperator, probe: Solution,
+                        probe_rng) -> tuple[bool, str]:
+    """NVRTC compile + one device probe of `op` together with the CUDA
+    operators already registered on `problem` (go_problem_set_custom_ops).
+    On failure the previous operator set is restored."""
+    cfg = problem.config()
+    lib = N.load()
+    h = problem.device_handle(0)
+    prev = list(getattr(problem, "_registered_cuda_ops", ()))
+    seed = probe_rng.getrandbits(64)
+
+    def install(ops):
+        arr = (N.CustomOp * max(1, len(ops)))()
+        keep = []
+        for i, o in enumerate(ops):
+            name, body = o.name.encode(), o.cuda.encode()
+            keep.append((name, body))
+            arr[i] = N.CustomOp(o.id, name, body)
+        status = np.zeros(max(1, len(ops)), dtype=np.int32)
+        msg_len = 512
+        msgs = C.create_string_buffer(msg_len * max(1, len(ops)))
+        genes, sizes = pack_solutions([probe], cfg)
+        N.check(lib.go_problem_set_custom_ops(h, arr, len(ops), N.iptr(genes), N.iptr(sizes),
+                                              seed, N.iptr(status), msgs, msg_len))
+        return status, msgs, msg_len
+
+    status, msgs, msg_len = install(prev + [op])
+    i = len(prev)
+    if status[i]:
+        problem._registered_cuda_ops = prev + [op]
+        return True, ""
+    text = msgs.raw[i * msg_len:(i + 1) * msg_len].split(b"\0")[0].decode()
+    install(prev)
+    return False, text
 
 
 # ---------------------------------------------------------------------------

@@ -38,6 +38,21 @@ BUILTIN_NAMES = {
 
 
 @dataclass
+class OperatorContext:
+    """operators.py:54-66: what an operator may consult besides the solution.
+    On the device `pick_mate` draws from the population snapshot and `phi` is
+    the kernel's scalarised fitness; here `pick_mate` is called on the host to
+    supply apply_sequence's crossover mate, and `phi=None` keeps the
+    reference's guided-rebuild fallback to scatter shuffle
+    (operators.py:510-512)."""
+
+    problem: object
+    cfg: ProblemConfig
+    pick_mate: Callable | None = None
+    phi: Callable | None = None
+
+
+@dataclass
 class SequenceEntry:
     id: int
     name: str
@@ -162,3 +177,38 @@ def append_custom(registry: SequenceRegistry, op: CustomOperator):
     """operators.py:666-668: append, then renormalise after each registration."""
     registry.entries.append(SequenceEntry(op.id, op.name, None, weight=op.initial_weight))
     registry.normalize()
+
+
+def apply_sequence(registry: SequenceRegistry, seq_id: int, sol, rng, ctx: OperatorContext):
+    """operators.py:627-631: apply exactly one registered operator to `sol` in
+    place — on the device (engine.apply_operator_device): a one-lane evolve
+    step whose registry holds only this sequence, always accepted.  Draws come
+    from a Philox stream keyed by 64 bits of `rng`, not from `rng` itself."""
+    registry.get(seq_id)  # KeyError for an unregistered id (operators.py:107-111)
+    from .engine import apply_operator_device
+    apply_operator_device(registry, seq_id, sol, rng, ctx)
+
+
+def register_custom(registry: SequenceRegistry, op: CustomOperator, probe, ctx: OperatorContext,
+                    probe_rng) -> bool:
+    """operators.py:634-669 for CUDA operators: a bad id is a hard error; the
+    snippet is compiled by NVRTC together with the operators already
+    registered on ctx.problem and probed once on `probe` on the device.  A
+    compile error, a device fault or an invalid result excludes it with a
+    RuntimeWarning (registry unchanged, returns False); otherwise it is
+    appended with its initial weight and the registry renormalised."""
+    import warnings
+    validate_custom_id(registry, op)
+    if not op.cuda:
+        warnings.warn(f"custom operator {op.name!r} (id {op.id}) excluded: no CUDA snippet "
+                      "(the device engine cannot run Python operators)", RuntimeWarning,
+                      stacklevel=2)
+        return False
+    from .engine import probe_custom_device
+    ok, msg = probe_custom_device(ctx.problem, op, probe, probe_rng)
+    if not ok:
+        warnings.warn(f"custom operator {op.name!r} (id {op.id}) excluded: {msg}", RuntimeWarning,
+                      stacklevel=2)
+        return False
+    append_custom(registry, op)
+    return True
