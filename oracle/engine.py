@@ -383,10 +383,14 @@ class RunOut:
 
 
 def run(problem, cfg: RunCfg, best_known=None, device_stream="mt", trace=None,
-        initial_population=None):
+        initial_population=None, workers=1):
+    """`workers` > 1 evolves the evolvers of each generation in that many forked
+    processes (evolvers are independent within a generation given the island
+    snapshot, engine.py:687-701), so the oracle can check the device at the
+    benchmark's own population sizes; results are identical to workers=1."""
     if cfg.replicas == 1:
         return run_single(problem, cfg, cfg.seed, best_known, device_stream, trace,
-                          initial_population)
+                          initial_population, workers)
     outs = [run_single(problem, cfg, cfg.seed + i, best_known, device_stream)
             for i in range(cfg.replicas)]
     best = outs[0]
@@ -401,8 +405,25 @@ def working_set(problem):
     return problem.payload_nbytes() + problem.spec.d1 * problem.spec.d2 * 4
 
 
+_PAR = {}
+
+
+def _evolve_chunk(idxs):
+    """Worker body of run_single(workers > 1): the generation's context is
+    inherited through fork (_PAR)."""
+    c = _PAR
+    out = []
+    for e_idx in idxs:
+        ev = c["evs"][e_idx]
+        evolve_generation(c["problem"], ev, e_idx, c["gen"], c["temp"], c["reg"], c["kw"],
+                          c["seed"], c["team"], c["pw"], c["snaps"][ev.island],
+                          c["member_pos"][e_idx], c["stream"])
+        out.append((e_idx, ev))
+    return out
+
+
 def run_single(problem, cfg: RunCfg, seed, best_known=None, device_stream="mt",
-               trace=None, initial_population=None):
+               trace=None, initial_population=None, workers=1):
     t_start = time.perf_counter()
     stream = STREAMS[device_stream]
     spec = problem.spec
@@ -474,9 +495,22 @@ def run_single(problem, cfg: RunCfg, seed, best_known=None, device_stream="mt",
             break
         temp = t0 * cfg.cooling_alpha ** (gen - 1)
         snaps = [[evs[i].cur for i in members] for members in isl]
-        for e_idx, ev in enumerate(evs):
-            evolve_generation(problem, ev, e_idx, gen, temp, reg, kw, seed, cfg.team_size,
-                              pw, snaps[ev.island], member_pos[e_idx], stream, trace)
+        if workers > 1 and trace is None:
+            import multiprocessing as mp
+            _PAR.update(problem=problem, evs=evs, gen=gen, temp=temp, reg=reg, kw=kw, seed=seed,
+                        team=cfg.team_size, pw=pw, snaps=snaps, member_pos=member_pos,
+                        stream=stream)
+            with mp.get_context("fork").Pool(workers) as pool:
+                parts = pool.map(_evolve_chunk, [list(range(w, len(evs), workers))
+                                                 for w in range(workers)])
+            _PAR.clear()
+            for part in parts:
+                for e_idx, ev in part:
+                    evs[e_idx] = ev
+        else:
+            for e_idx, ev in enumerate(evs):
+                evolve_generation(problem, ev, e_idx, gen, temp, reg, kw, seed, cfg.team_size,
+                                  pw, snaps[ev.island], member_pos[e_idx], stream, trace)
         lane_evals += len(evs) * cfg.team_size
         improved = False
         for ev in evs:

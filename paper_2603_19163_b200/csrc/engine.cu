@@ -1962,7 +1962,7 @@ int go_engine_debug_counters(go_engine* e, int64_t* out, int n) {
   CK(cudaStreamSynchronize(e->stream));
   go::GlobalState gs{};
   CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
-  for (int i = 0; i < n && i < 16; ++i) out[i] = (int64_t)gs.prof[i];
+  for (int i = 0; i < n && i < 32; ++i) out[i] = (int64_t)gs.prof[i];
   return GO_OK;
 }
 

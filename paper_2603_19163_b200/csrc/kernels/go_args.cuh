@@ -34,7 +34,7 @@ struct GlobalState {
   long long hist_count;
   unsigned long long rd_pos;   // positions read by move evaluations (all lanes)
   unsigned long long rd_elem;  // matrix elements read by move evaluations
-  unsigned long long prof[16]; // per-phase clock64 totals (GO_PHASE_TIMING builds)
+  unsigned long long prof[32]; // per-phase clock64 totals / deferred-op timings (GO_PHASE_TIMING)
 };
 
 struct EvolveArgs {

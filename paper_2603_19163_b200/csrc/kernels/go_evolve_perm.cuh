@@ -538,8 +538,18 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           Stream rng;
           rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
+#ifdef GO_PHASE_TIMING
+          const unsigned long long t_op = clock64();
+#endif
           const DeferRes<Acc> dr = perm_defer(pol, C, kind, dst, warp == 0 ? nxt : my_row, my_int,
                                               &rng, &ms, n, wl);
+#ifdef GO_PHASE_TIMING
+          if (wl == 0) {  // slots 16.. : (cycles, count) per deferred kind OX / shuffles / rebuild
+            const int b = kind == SEQ_OX ? 16 : (kind == SEQ_GUIDED_REBUILD ? 20 : 18);
+            atomicAdd(&A.gs->prof[b], clock64() - t_op);
+            atomicAdd(&A.gs->prof[b + 1], 1ull);
+          }
+#endif
           Acc nd = la.delta[L];
           u32 bits = meta & META_BASE;
           int nm2 = nm;

@@ -585,6 +585,7 @@ def evolve_generation(ev: EvolverState, ev_idx: int, generation: int, temperatur
     accepted = int(k_usage[member_pos].sum()) == 1
     if not accepted:
         return False
+    evaluate(problem, after, validate=False)  # full evaluation, as the reference's candidate
     ev.current = after
     if ev.stats is not None:
         improved = bool(k_impr[member_pos].any())

@@ -221,3 +221,37 @@ def cvrp8_instance(objectives=("distance", "vehicles"), comparison=None):
                              step=15.0, inter=60.0)
     return InstanceData(distance_matrix=d, demands=np.ones(8), capacity=8.0, vehicles=3,
                         meta=meta)
+
+
+# ---- the BASELINE.json workloads -----------------------------------
+DATA_DIR = Path(__file__).with_name("data")
+FIXTURES = {  # the reference's benchmark-format fixtures (pkg/tests/fixtures, README there)
+    "R101": DATA_DIR / "R101.txt",    # synthetic Solomon R101-format, 100 customers, 25 vehicles
+    "eil51": DATA_DIR / "eil51.tsp",  # TSPLIB eil51, best known 426
+    "ft06": DATA_DIR / "ft06.jsp",    # Fisher-Thompson 6x6, optimum 55
+    "nug12": DATA_DIR / "nug12.dat",  # QAPLIB layout at nug12 size
+}
+KNOWN_OPTIMA = {"eil51": 426.0, "ft06": 55.0, "lattice442": 44200.0}
+
+
+def baseline_instances() -> dict:
+    """name -> (problem name, InstanceData, best known or None) for the named
+    BASELINE shapes: C1 random Euclidean TSP n=51, C2 the pcb442-shaped 26x17
+    lattice (known optimum 44,200) and its +-30 jittered twin, C3 VRPTW on the
+    reference's R101 fixture, C4 QAP n=100, C5a JSP 20x15 (integer encoding),
+    C5b knapsack n=1000."""
+    from .parsers import parse_solomon
+    from .problems import InstanceData
+    d2, opt2 = tsp_lattice()
+    dj, _ = tsp_lattice(jitter=30)
+    f, dq = qap_random(100, 100)
+    w, v, cap = knapsack_random(1000, 1000)
+    return {
+        "C1": ("tsp", InstanceData(distance_matrix=tsp_random(51, 51)), None),
+        "C2": ("tsp", InstanceData(distance_matrix=d2), opt2),
+        "C2j": ("tsp", InstanceData(distance_matrix=dj), None),
+        "C3": ("vrptw", parse_solomon(FIXTURES["R101"]), None),
+        "C4": ("qap", InstanceData(flow_matrix=f, distance_matrix=dq), None),
+        "C5a": ("jsp_int", InstanceData(jobs=jsp_random(20, 15, 2015)), None),
+        "C5b": ("knapsack", InstanceData(weights=w, values=v, capacity=cap), None),
+    }

@@ -27,8 +27,8 @@ CFG = {"population": 16, "team_size": 32, "max_generations": 300, "instance": "t
 
 def one(args):
     variant, seed = args
-    sys.path.insert(0, REF)
     sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, REF)  # the reference genopt wins over the repo's drop-in shim
     import genopt as G
     from genopt import demo_ops
 

@@ -28,8 +28,8 @@ CASES = {
 
 
 def instance(name):
-    sys.path.insert(0, REF)
     sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, REF)  # the reference genopt wins over the repo's drop-in shim
     import genopt as G
 
     from paper_2603_19163_b200 import instances as I

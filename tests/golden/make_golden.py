@@ -19,8 +19,8 @@ from pathlib import Path
 import numpy as np
 
 REF = "/root/reference/pkg/src"
-sys.path.insert(0, REF)
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+sys.path.insert(0, REF)  # the reference genopt wins over the repo's drop-in shim
 
 import genopt as G  # noqa: E402
 from genopt import aos as GA  # noqa: E402

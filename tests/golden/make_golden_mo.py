@@ -16,8 +16,8 @@ import sys
 from pathlib import Path
 
 REF = "/root/reference/pkg/src"
-sys.path.insert(0, REF)
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+sys.path.insert(0, REF)  # the reference genopt wins over the repo's drop-in shim
 
 import genopt as G  # noqa: E402
 from genopt import instances as GI  # noqa: E402

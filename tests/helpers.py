@@ -46,3 +46,31 @@ def sol_from_json(problem, js):
 
 def sol_rows(sol):
     return [[int(x) for x in sol.row(r)] for r in range(sol.d1)]
+
+
+def bench_pairs(names=("C1", "C2", "C3", "C4", "C5a", "C5b")):
+    """The BASELINE workloads as (device problem, oracle problem, custom ops):
+    instances.baseline_instances(), C2 with the tsp-delta user operators."""
+    import paper_2603_19163_b200 as G
+    from oracle import moves as M
+    out = {}
+    table = I.baseline_instances()
+    for name in names:
+        kind, inst, _ = table[name]
+        prob = G.builtin_problem(kind, inst)
+        if kind == "tsp":
+            ref = P.Tsp(inst.distance_matrix)
+        elif kind == "vrptw":
+            ref = P.Vrptw(inst.distance_matrix, inst.demands, inst.capacity, inst.vehicles,
+                          inst.ready_times, inst.due_times, inst.service_times)
+        elif kind == "qap":
+            ref = P.Qap(inst.flow_matrix, inst.distance_matrix)
+        elif kind == "jsp_int":
+            ref = P.JspInt(inst.jobs)
+        else:
+            ref = P.Knapsack(inst.weights, inst.values, inst.capacity)
+        custom = name in ("C2", "C2j")
+        ops = G.tsp_delta_operators() if custom else ()
+        oops = tuple((i, nm, f, 1.0) for i, nm, f in M.TSP_DELTA) if custom else ()
+        out[name] = (prob, ref, ops, oops)
+    return out
