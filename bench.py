@@ -110,42 +110,113 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def other_configs(G, I, local, steps=5, gps=10):
-    """Device throughput on the other BASELINE shapes (C1, C3, C4, C5a, C5b):
-    a few 10-generation steps each with the B200 population rule."""
-    vd = I.vrptw_solomon_like()
-    f, dq = I.qap_random(100, 100)
-    w, v, cap = I.knapsack_random(1000, 1000)
-    probs = {
-        "C1 TSP n=51 (nint)": G.builtin_problem("tsp", G.InstanceData(
-            distance_matrix=I.tsp_random(51, 51))),
-        "C3 VRPTW n=100, 25 vehicles": G.builtin_problem("vrptw", G.InstanceData(
-            distance_matrix=vd.dist, demands=vd.demands, capacity=vd.capacity,
-            vehicles=vd.vehicles, ready_times=vd.ready, due_times=vd.due,
-            service_times=vd.service)),
-        "C4 QAP n=100": G.builtin_problem("qap", G.InstanceData(flow_matrix=f,
-                                                                distance_matrix=dq)),
-        "C5a JSP-int 20x15": G.builtin_problem("jsp_int", G.InstanceData(
-            jobs=I.jsp_random(20, 15, 2015))),
-        "C5b knapsack n=1000": G.builtin_problem("knapsack", G.InstanceData(
-            weights=w, values=v, capacity=cap)),
-    }
+def best_known():
+    """profiles/best_known.json: the reference values the gap figures use
+    (exact optima and bounds from tools/bounds.py, best-known tours from long
+    device runs, tools/best_known_runs.py)."""
+    p = ROOT / "profiles" / "best_known.json"
+    try:
+        return json.loads(p.read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+def gap_of(value, ref, sense):
+    if ref is None or value is None or not ref:
+        return None
+    return (value - ref) / abs(ref) * 100.0 if sense == "min" else (ref - value) / abs(ref) * 100.0
+
+
+OTHER = {  # name -> label (BASELINE.json configs)
+    "C1": "C1 random Euclidean TSP n=51 (nint)",
+    "C2j": "C2j pcb442-shaped lattice with +-30 jitter + tsp-delta",
+    "C3": "C3 VRPTW R101 fixture (100 customers, 25 vehicles)",
+    "C4": "C4 QAP n=100",
+    "C5a": "C5a JSP-int 20x15",
+    "C5b": "C5b knapsack n=1000",
+}
+
+
+def other_configs(G, I, local, args, hbm, smem_peak, steps=5, gps=10):
+    """The other BASELINE shapes at N=1: device throughput with its roofline,
+    gap at the wall-clock budget through the public run(), and the reference
+    beside it on the host cores — its gap@budget runs in a background process
+    pool during the device's own budget, its steady-state throughput on a
+    bounded sample afterwards."""
+    from baseline import refbench as R
+    table = I.baseline_instances()
+    bk = best_known()
+    procs = cpu_cores() if args.cpu_procs == 0 else args.cpu_procs
     out = {}
-    for name, prob in probs.items():
-        dr = G.DeviceRun(prob, G.EngineConfig(device=local), 42)
+    for name, label in OTHER.items():
+        if args.only and name not in args.only.split(","):
+            continue
+        kind, inst, opt = table[name]
+        prob = G.builtin_problem(kind, inst)
+        ops = G.tsp_delta_operators() if name == "C2j" else ()
+        ref = bk.get(name, {})
+        sense = ref.get("sense", "min")
+        known = ref.get("optimum", ref.get("best_known"))
+        dr = G.DeviceRun(prob, G.EngineConfig(device=local, custom_operators=ops), args.seed)
         done = 0
         for _ in range(2):
             done += gps
             dr.run(done, None)
-        ms = 0.0
+        ms = emsum = 0.0
+        rp = re_ = 0
+        st = None
         for _ in range(steps):
             done += gps
-            ms += dr.run(done, None).device_ms
-        evals = dr.pop_size * 128 * gps * steps
-        out[name] = {"move_evals_per_s": evals / (ms / 1e3), "population": dr.pop_size,
-                     "ms_per_step": ms / steps, "smem_bytes": dr.smem_bytes,
-                     "layout": dr.layout, "best_after": float(dr.best().objectives[0])}
+            st = dr.run(done, None)
+            ms += st.device_ms
+            emsum += st.evolve_ms
+            rp += st.reads_pos
+            re_ += st.reads_elem
+        evals = dr.pop_size * dr.config.team_size * gps * steps
+        alg = rp * 2 + re_ * st.elem_bytes
+        ach = alg / (emsum / 1e3) / 1e9 if emsum > 0 else 0.0
+        row = {"workload": label, "move_evals_per_s": evals / (ms / 1e3),
+               "population": dr.pop_size, "team_size": dr.config.team_size,
+               "ms_per_step": ms / steps, "generations_per_step": gps,
+               "smem_bytes": dr.smem_bytes, "layout": dr.layout, "teams_per_sm": dr.teams_per_sm,
+               "roofline": {"bound": "smem (on-chip instance)", "achieved": ach, "unit": "GB/s",
+                            "peak_hbm": hbm, "frac_hbm": ach / hbm, "peak_smem": smem_peak,
+                            "frac_smem": ach / smem_peak, "algorithmic_bytes": int(alg),
+                            "evolve_ms": emsum}}
         dr.close()
+        if args.other_gap_seconds > 0:
+            import threading
+            cpu_gap = {}
+            th = None
+            if not args.no_cpu_baseline:
+                th = threading.Thread(target=lambda: cpu_gap.update(R.gap_at(
+                    name, args.other_gap_seconds, procs, known, sense)), daemon=True)
+                th.start()
+            res = G.run(prob, G.EngineConfig(device=local, seed=args.seed + 7,
+                                             custom_operators=ops, device_init=True,
+                                             time_limit_seconds=args.other_gap_seconds,
+                                             max_generations=10 ** 9))
+            if th is not None:
+                th.join()
+            val = float(res.objectives[0]) if res.penalty == 0.0 else None
+            row.update({"gap_seconds": args.other_gap_seconds, "best": val,
+                        "gap_pct": gap_of(val, known, sense),
+                        "gap_reference": {k: v for k, v in ref.items()},
+                        "generations": res.generations_completed,
+                        "move_evals_per_s_run": res.device["lane_evals"] / res.elapsed_seconds})
+            if "lower_bound" in ref:
+                row["gap_pct_vs_lower_bound"] = gap_of(val, ref["lower_bound"], "min")
+            if cpu_gap:
+                cpu_gap["gap_pct_vs_reference"] = gap_of(cpu_gap.get("best"), known, sense)
+                row["cpu_gap"] = cpu_gap
+        if not args.no_cpu_baseline:
+            tb = R.steady_throughput(name, procs, pop=8, team=128, warm=2, gens=2)
+            row["cpu_baseline"] = {"value": tb["value"], "unit": "move evals/s", "cores": procs,
+                                   "kind": tb["kind"], "cpu_model": R.cpu_model(),
+                                   "sample": f"{procs} processes x genopt.run(P=8, T=128), "
+                                             f"generations 3-4 timed ({tb['evals']} evals)"}
+        out[name] = row
+        print(f"[bench] {name}: {json.dumps(row)}", file=sys.stderr, flush=True)
     return out
 
 
@@ -300,11 +371,6 @@ def run_ours(args):
         gap_info.update({"time_to_optimum_s": rt.elapsed_seconds if hit else None,
                          "generations_to_optimum": rt.generations_completed if hit else None})
 
-    extra = other_configs(G, I, local) if (args.other_configs and world == 1) else None
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
     hbm, src, pk = peaks()
     alg_bytes = reads_pos * 2 + reads_elem * (st.elem_bytes if st else 2)
     achieved_gbs = alg_bytes / (evolve_ms / 1e3) / 1e9 if evolve_ms > 0 else 0.0
@@ -312,15 +378,24 @@ def run_ours(args):
     info = N.device_info(local)
     sm_mhz = clocks.get("sm_mhz") or pk.get("clocks_under_load", {}).get("sm_mhz_median", 1965.0)
     smem_peak = info.sm_count * 128 * sm_mhz * 1e6 / 1e9
+    extra = other_configs(G, I, local, args, hbm, smem_peak) \
+        if (args.other_configs and world == 1) else None
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
     cpu = None
     if not args.no_cpu_baseline:
-        from oracle import cpu_bench
+        from baseline import refbench as R
         procs = cpu_cores() if args.cpu_procs == 0 else args.cpu_procs
-        cb = cpu_bench.throughput(d, procs, pop=8, team=128, gens=args.cpu_gens)
-        cpu = {"value": cb["value"], "unit": "move evals/s", "cores": procs, "kind": "port",
-               "sample": f"oracle engine (== reference run(), MT19937) on C2 with tsp-delta, full "
-                         f"reference registry: {procs} processes x P=8 x T=128 x "
-                         f"{args.cpu_gens} generations ({cb['evals']} evals in "
+        cb = R.steady_throughput("C2", procs, pop=8, team=128, warm=args.cpu_warm_gens,
+                                 gens=args.cpu_gens)
+        cpu = {"value": cb["value"], "unit": "move evals/s", "cores": procs, "kind": cb["kind"],
+               "cpu_model": R.cpu_model(),
+               "sample": f"{'genopt.run() (the unmodified reference)' if cb['kind'] == 'reference' else 'oracle port of genopt.run()'}"
+                         f" on C2 with tsp-delta and its full registry: {procs} processes x "
+                         f"P=8 x T=128, generations {args.cpu_warm_gens + 1}-"
+                         f"{args.cpu_warm_gens + args.cpu_gens} timed ({cb['evals']} evals in "
                          f"{cb['wall_s']:.1f} s)"}
     out = {
         "metric": METRIC, "value": value, "unit": "move evals/s", "n_gpus": world,
@@ -368,39 +443,38 @@ def run_ours(args):
 
 # ---------------------------------------------------------------------------
 def run_reference(args):
-    """The reference's own algorithm on the host cores: the oracle in MT mode
-    reproduces genopt.run() bit-for-bit (pinned by tests/golden)."""
+    """The reference's own implementation on the host cores: genopt.run() of
+    the unmodified reference package (baseline/_ref, tools/stage_reference.sh)
+    in one process per core (its evolver threads are GIL-bound), same C2
+    workload and registry; the oracle port stands in when it is absent.
+    A step = one generation of every process, after `warmup` generations."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle import cpu_bench
-    from paper_2603_19163_b200 import instances as I
-    d, opt = I.tsp_lattice()
+    from baseline import refbench as R
     procs = cpu_cores() if args.cpu_procs == 0 else args.cpu_procs
-    vals = []
     t_all = time.perf_counter()
-    for _ in range(args.warmup):
-        cpu_bench.throughput(d, procs, pop=4, team=128, gens=1)
-    for _ in range(args.steps):
-        vals.append(cpu_bench.throughput(d, procs, pop=8, team=128, gens=args.cpu_gens))
-    value = sum(v["evals"] for v in vals) / sum(v["wall_s"] for v in vals)
+    tb = R.steady_throughput("C2", procs, pop=8, team=128, warm=args.warmup, gens=args.steps)
+    value = tb["value"]
     gap = {}
     if args.gap_seconds > 0:
-        g = cpu_bench.gap_at(d, args.gap_seconds, procs, opt)
-        gap = {"gap_pct_30s": g["best_gap_pct"], "median_gap_pct_30s": g["median_gap_pct"],
-               "move_evals_per_s_30s": g["evals_per_s"]}
+        g = R.gap_at("C2", args.gap_seconds, procs, 44200.0, "min")
+        gap = {"gap_pct_30s": g.get("gap_pct"), "median_gap_pct_30s": g.get("median_gap_pct"),
+               "best_30s": g.get("best"), "generations_30s": g.get("generations")}
+    sample = (f"{procs} processes x {'genopt.run()' if tb['kind'] == 'reference' else 'oracle port'}"
+              f" (P=8, T=128, C2 + tsp-delta), generations {args.warmup + 1}-"
+              f"{args.warmup + args.steps} timed")
     out = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "move evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(v["wall_s"] for v in vals) / max(1, len(vals)),
+        "ms_per_step": 1e3 * tb["wall_s"] / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded 26x17 lattice, permuted labels, TSPLIB nint)",
         "config": {"workload": "C2 pcb442-shaped lattice TSP n=442 + user tsp-delta ops",
                    "population_per_process": 8, "team_size": 128,
-                   "generations_per_step": args.cpu_gens},
-        "cpu_baseline": {"value": value, "unit": "move evals/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} processes x P=8 x T=128 x {args.cpu_gens} "
-                                   "generations per step, oracle MT mode == reference run()"},
+                   "generations_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "move evals/s", "cores": procs,
+                         "kind": tb["kind"], "cpu_model": R.cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "move evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t_all,
@@ -469,7 +543,11 @@ def main():
     ap.add_argument("--population", type=int, default=0)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--gap-seconds", type=float, default=30.0)
-    ap.add_argument("--cpu-gens", type=int, default=4)
+    ap.add_argument("--cpu-gens", type=int, default=2)
+    ap.add_argument("--cpu-warm-gens", type=int, default=2)
+    ap.add_argument("--other-gap-seconds", type=float, default=30.0,
+                    help="wall-clock budget of the other shapes' gap runs (0 = skip)")
+    ap.add_argument("--only", default="", help="comma list of other shapes to measure")
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--other-configs", type=int, default=1,

@@ -63,3 +63,71 @@ def gap_at(dist, seconds: float, procs: int, best_known: float, seed: int = 42):
     wall = max(r[3] for r in res)
     return {"best_gap_pct": gaps[0], "median_gap_pct": gaps[len(gaps) // 2],
             "evals_per_s": evals / wall, "generations": [r[4] for r in res], "procs": procs}
+
+
+def workload_problem(name):
+    """An oracle problem for a BASELINE workload (instances.baseline_instances)."""
+    from paper_2603_19163_b200 import instances as I
+    kind, inst, _ = I.baseline_instances()[name]
+    if kind == "tsp":
+        return P.Tsp(inst.distance_matrix)
+    if kind == "vrptw":
+        return P.Vrptw(inst.distance_matrix, inst.demands, inst.capacity, inst.vehicles,
+                       inst.ready_times, inst.due_times, inst.service_times)
+    if kind == "qap":
+        return P.Qap(inst.flow_matrix, inst.distance_matrix)
+    if kind == "jsp_int":
+        return P.JspInt(inst.jobs)
+    return P.Knapsack(inst.weights, inst.values, inst.capacity)
+
+
+def _ops(name):
+    return tuple((i, n, f, 1.0) for i, n, f in M.TSP_DELTA) if name in ("C2", "C2j") else ()
+
+
+def _steady_worker(args):
+    name, seed, pop, team, warm, gens = args
+    prob = workload_problem(name)
+    t = time.perf_counter()
+    E.run(prob, E.RunCfg(population=pop, team_size=team, max_generations=warm, seed=seed,
+                         custom_ops=_ops(name)))
+    t_warm = time.perf_counter() - t
+    t = time.perf_counter()
+    out = E.run(prob, E.RunCfg(population=pop, team_size=team, max_generations=warm + gens,
+                               seed=seed, custom_ops=_ops(name)))
+    return gens * pop * team, max(1e-9, time.perf_counter() - t - t_warm), out.generations
+
+
+def throughput_workload(name, procs, pop=8, team=128, warm=2, gens=2, seed=42):
+    """Port stand-in for baseline.refbench.steady_throughput: the warm-up is
+    timed separately and subtracted (runs are deterministic)."""
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_steady_worker, [(name, seed + i, pop, team, warm, gens)
+                                        for i in range(procs)])
+    evals = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": evals / wall, "evals": evals, "wall_s": wall, "procs": procs}
+
+
+def _gap_worker2(args):
+    name, seed, seconds = args
+    out = E.run(workload_problem(name), E.RunCfg(population=None, team_size=128,
+                                                 max_generations=10 ** 9,
+                                                 time_limit_seconds=seconds, seed=seed,
+                                                 concurrency_hint=os.cpu_count() or 1,
+                                                 custom_ops=_ops(name)))
+    return out.objectives[0], out.penalty, out.generations
+
+
+def gap_workload(name, seconds, procs, best_known, sense="min", seed=1000):
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_gap_worker2, [(name, seed + i, seconds) for i in range(procs)])
+    objs = sorted((r[0] for r in res if r[1] == 0.0), reverse=(sense == "max"))
+    out = {"best": objs[0] if objs else None, "median": objs[len(objs) // 2] if objs else None,
+           "feasible_runs": len(objs), "procs": procs, "seconds": seconds,
+           "generations": sorted(r[2] for r in res)}
+    if best_known and objs:
+        sgn = 1.0 if sense == "min" else -1.0
+        out["gap_pct"] = sgn * (objs[0] - best_known) / abs(best_known) * 100.0
+        out["median_gap_pct"] = sgn * (out["median"] - best_known) / abs(best_known) * 100.0
+    return out

@@ -1,0 +1,52 @@
+"""Best-known values for the gap references (profiles/best_known.json): long
+device runs of every BASELINE shape through the public run() (device_init,
+several seeds), merged with the exact optima / lower bounds of
+tools/bounds.py.  A later run that beats a stored value replaces it.
+
+    python tools/best_known_runs.py [seconds] [seeds] [names]
+"""
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2603_19163_b200 as G  # noqa: E402
+from paper_2603_19163_b200 import instances as I  # noqa: E402
+
+OUT = ROOT / "profiles" / "best_known.json"
+SENSE = {"C5b": "max"}
+
+
+def main():
+    seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 90.0
+    seeds = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    names = sys.argv[3].split(",") if len(sys.argv) > 3 else ["C1", "C2j", "C3", "C4", "C5a",
+                                                                "C5b"]
+    table = I.baseline_instances()
+    cur = json.loads(OUT.read_text()) if OUT.exists() else {}
+    for name in names:
+        kind, inst, _ = table[name]
+        prob = G.builtin_problem(kind, inst)
+        ops = G.tsp_delta_operators() if name in ("C2", "C2j") else ()
+        sense = SENSE.get(name, "min")
+        entry = cur.setdefault(name, {"sense": sense})
+        for s in range(seeds):
+            r = G.run(prob, G.EngineConfig(seed=9000 + s, custom_operators=ops, device_init=True,
+                                           time_limit_seconds=seconds, max_generations=10 ** 9))
+            if r.penalty != 0.0:
+                continue
+            v = float(r.objectives[0])
+            old = entry.get("best_known")
+            if old is None or (v < old if sense == "min" else v > old):
+                entry["best_known"] = v
+                entry["best_known_how"] = (f"device run, {seconds:.0f} s, seed {9000 + s}, "
+                                           f"{r.generations_completed} generations x P="
+                                           f"{r.config['population_effective']}")
+            print(name, s, v, flush=True)
+        OUT.write_text(json.dumps(cur, indent=1, sort_keys=True) + "\n")
+
+
+if __name__ == "__main__":
+    main()
