@@ -741,21 +741,47 @@ void* row_kernel(const go_problem* p, int layout) {
   return s ? (void*)go_evolve_jsp : (void*)go_evolve_jsp_g;
 }
 
-// the user problem's evolve kernel for a layout (the global-rows module is
-// compiled on first use)
+// template arguments of a built-in row problem's evolve kernel (GO_ROW_KERNEL list)
+gohost::RowOpsSrc rowops_src(const go_problem* p, bool rows_global) {
+  gohost::RowOpsSrc r;
+  r.rows_global = rows_global;
+  r.gene_type = "short";
+  r.elem_type = "double";
+  if (p->row_kind == go::RK_QAP) {
+    r.kind = "go::RK_QAP";
+    r.elem_type = p->elem == E_I16 ? "short" : (p->elem == E_I32 ? "int" : "double");
+  } else if (p->row_kind == go::RK_KNAP) {
+    r.kind = "go::RK_KNAP";
+    r.gene_type = "unsigned char";
+  } else if (p->row_kind == go::RK_JSP) {
+    r.kind = "go::RK_JSP";
+    r.elem_type = "int";
+  } else {
+    r.kind = "go::RK_PART";
+  }
+  return r;
+}
+
+// the user problem's (or a built-in row problem's with user operators) evolve
+// kernel for a layout (the global-rows module is compiled on first use)
 int row_kernel_jit(go_problem* p, int layout, CUfunction* out) {
   *out = nullptr;
-  if (p->row_kind != go::RK_USER) return GO_OK;
+  if (p->row_kind != go::RK_USER && p->ops.empty()) return GO_OK;  // static kernels
   if (row_rows_smem(layout)) {
     *out = p->user_mod.evolve;
     return GO_OK;
   }
   if (!p->user_mod_g.mod) {
-    gohost::UserProblemSrc up = p->user_src;
-    up.ops = p->ops;
-    up.rows_global = true;
     std::string log;
-    const int rc = gohost::jit_build_user(up, &p->user_mod_g, &log);
+    int rc;
+    if (p->row_kind == go::RK_USER) {
+      gohost::UserProblemSrc up = p->user_src;
+      up.ops = p->ops;
+      up.rows_global = true;
+      rc = gohost::jit_build_user(up, &p->user_mod_g, &log);
+    } else {
+      rc = gohost::jit_build_rowops(rowops_src(p, true), p->ops, &p->user_mod_g, &log);
+    }
     if (rc) return fail(rc, "NVRTC build (global lane rows) failed: " + log.substr(0, 2000));
   }
   *out = p->user_mod_g.evolve;
@@ -1197,13 +1223,121 @@ static int set_user_problem_ops(go_problem* p, const go_custom_op* ops, int n_op
   return GO_OK;
 }
 
+// register_custom (operators.py:634-669) for a BUILT-IN row problem (QAP,
+// knapsack, JSP-int, VRPTW / CVRP and the routing variants): each operator is
+// compiled alone into the problem's hand-written evolve kernel (a compile
+// error excludes only it), probed once on the probe solution (device error
+// or an invalid result excludes it), then the kept ones are built together.
+template <class Note>
+static int set_rowops_problem_ops(go_problem* p, const go_custom_op* ops, int n_ops,
+                                  const int32_t* probe_genes, const int32_t* probe_sizes,
+                                  uint64_t probe_seed, int32_t* status_out, Note note) {
+  std::vector<gohost::UserOpSrc> keep;
+  const int n = p->n;  // device row length (partitions: cells + route sizes)
+  std::vector<short> h0;
+  to_device_rows(p, probe_genes, probe_sizes, 1, h0);
+  auto valid_row = [&](const std::vector<short>& h) {
+    if (p->row_kind == go::RK_PART) {
+      int tot = 0;
+      for (int r = 0; r < p->d1; ++r) {
+        const int sz = h[p->n_cells + r];
+        if (sz < 0 || sz > p->d2) return false;
+        tot += sz;
+      }
+      if (tot != p->n_cells) return false;
+      std::vector<char> seen(p->n_cells, 0);
+      for (int q = 0; q < p->n_cells; ++q) {
+        const int v = h[q];
+        if (v < 0 || v >= p->n_cells || seen[v]) return false;
+        seen[v] = 1;
+      }
+      return true;
+    }
+    if (p->row_kind == go::RK_QAP) {
+      std::vector<char> seen(n, 0);
+      for (int j = 0; j < n; ++j) {
+        if (h[j] < 0 || h[j] >= n || seen[h[j]]) return false;
+        seen[h[j]] = 1;
+      }
+      return true;
+    }
+    const int lo = p->row_kind == go::RK_KNAP ? 0 : p->lb;
+    const int hi = p->row_kind == go::RK_KNAP ? 1 : p->ub;
+    for (int j = 0; j < n; ++j)
+      if (h[j] < lo || h[j] > hi) return false;
+    return true;
+  };
+  auto mix = [](uint64_t hh, uint64_t part) {
+    hh ^= part;
+    hh *= 0xBF58476D1CE4E5B9ull;
+    hh ^= hh >> 27;
+    hh *= 0x94D049BB133111EBull;
+    hh ^= hh >> 31;
+    return hh;
+  };
+  for (int i = 0; i < n_ops; ++i) {
+    status_out[i] = 0;
+    if (ops[i].id < 100) return fail(GO_E_INVALID, "custom operator id must be >= 100");
+    if (!ops[i].cuda_body) {
+      note(i, "no CUDA snippet");
+      continue;
+    }
+    gohost::UserOpSrc src{ops[i].id, ops[i].name ? ops[i].name : "op", ops[i].cuda_body};
+    gohost::JitModule m;
+    std::string log;
+    if (gohost::jit_build_rowops(rowops_src(p, false), {src}, &m, &log)) {
+      note(i, "compile failed: " + log.substr(0, 400));
+      continue;
+    }
+    std::vector<short> h = h0;
+    DevBufs B;
+    short* d_g = nullptr;
+    int* d_e = nullptr;
+    CK(B.get(&d_g, (size_t)n * 2));
+    CK(B.get(&d_e, sizeof(int)));
+    CK(cudaMemcpy(d_g, h.data(), (size_t)n * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d_e, 0, sizeof(int)));
+    unsigned long long key =
+        mix(mix(mix(0x9E3779B97F4A7C15ull, probe_seed), 4), (uint64_t)ops[i].id);
+    go::RowArgs x = row_args(p);
+    const void* inst = p->d_img;
+    int nn = p->row_kind == go::RK_PART ? p->n_cells : n, slot = 0;
+    void* args[] = {(void*)&inst, &x, &nn, &slot, &key, &d_g, &d_e};
+    CU(gohost::drv()->LaunchKernel(m.probe_op, 1, 1, 1, 32, 1, 1, 0, 0, args, nullptr));
+    const cudaError_t ce = cudaDeviceSynchronize();
+    gohost::drv()->ModuleUnload(m.mod);
+    if (ce != cudaSuccess) return fail(GO_E_CUDA, std::string("probe kernel: ") + cudaGetErrorString(ce));
+    int err = 0;
+    CK(cudaMemcpy(&err, d_e, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.data(), d_g, (size_t)n * 2, cudaMemcpyDeviceToHost));
+    if (err || !valid_row(h)) {
+      note(i, err ? "probe raised a device error" : "probe output invalid");
+      continue;
+    }
+    keep.push_back(src);
+    status_out[i] = 1;
+    note(i, "registered");
+  }
+  if (p->user_mod.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod.mod);
+  if (p->user_mod_g.mod && gohost::drv()) gohost::drv()->ModuleUnload(p->user_mod_g.mod);
+  p->user_mod = gohost::JitModule{};
+  p->user_mod_g = gohost::JitModule{};
+  p->ops = keep;
+  if (keep.empty()) return GO_OK;  // the static kernels again
+  gohost::JitModule m;
+  std::string log;
+  const int rc = gohost::jit_build_rowops(rowops_src(p, false), keep, &m, &log);
+  if (rc) return fail(rc, "NVRTC build of the row kernel with its operators failed: " + log.substr(0, 2000));
+  p->user_mod = m;
+  return GO_OK;
+}
+
 extern "C" {
 
 int go_problem_set_custom_ops(go_problem* p, const go_custom_op* ops, int n_ops,
                               const int32_t* probe_genes, const int32_t* probe_sizes,
                               uint64_t probe_seed, int32_t* status_out, char* msg_out,
                               int msg_len) {
-  (void)probe_sizes;
   if (!p || (n_ops > 0 && !ops) || !status_out) return fail(GO_E_INVALID, "bad arguments");
   CK(cudaSetDevice(p->device));
   for (auto& kv : p->jit)
@@ -1215,9 +1349,8 @@ int go_problem_set_custom_ops(go_problem* p, const go_custom_op* ops, int n_ops,
   };
   if (p->row_kind == go::RK_USER) return set_user_problem_ops(p, ops, n_ops, probe_genes,
                                                                probe_seed, status_out, note);
-  if (p->family == 1)
-    return fail(GO_E_UNSUPPORTED, "user operators run on the TSP path and on user problems "
-                                  "(CudaProblem), not on the built-in row kernels");
+  if (p->family == 1) return set_rowops_problem_ops(p, ops, n_ops, probe_genes, probe_sizes,
+                                                    probe_seed, status_out, note);
   int layout = 0, E = 0;
   choose_layout(p, 128, 0, &layout, &E);
   // compile each operator on its own first so a broken snippet only excludes
@@ -1312,8 +1445,6 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
   e->n = p->n;
   e->W = p->n;
   if (p->family == 1) {
-    if (!p->ops.empty() && p->row_kind != go::RK_USER)
-      return fail(GO_E_UNSUPPORTED, "user operators run on the TSP path and on user problems");
     if (!choose_row(p, e->TS, c->teams_per_cta, &e->layout, &e->E, &e->smem))
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
     e->inst = p->d_img;

@@ -355,4 +355,55 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
   return GO_OK;
 }
 
+// ---- user operators on the built-in row kernels (QAP / knapsack / JSP-int /
+// partition problems): the hand-written evolve kernel of `kind` instantiated
+// with the operators as U::op slots (register_custom, operators.py:634-669)
+int jit_build_rowops(const RowOpsSrc& ro, const std::vector<UserOpSrc>& ops, JitModule* out,
+                     std::string* log) {
+  const auto t0 = std::chrono::steady_clock::now();
+  std::ostringstream src;
+  src << "// generated by go_jit.cpp — user operators on a built-in row problem\n"
+      << "#include \"go_row_entry.cuh\"\n"
+      << "namespace go { namespace user {\n";
+  for (size_t i = 0; i < ops.size(); ++i)
+    src << "// user operator " << ops[i].id << " (" << ops[i].name << ")\n"
+        << "template <class Ctx> __device__ __forceinline__ void op_slot" << i
+        << "(Ctx& ctx) {\n#line 1 \"@OPDIR@/" << ops[i].name << ".cuh\"\n" << ops[i].body
+        << "\n}\n";
+  src << "}  // namespace user\n"
+      << "struct RowUserOps : NoUser {\n"
+      << "  template <class C> __device__ __forceinline__ static void op(int slot, C& ctx, "
+         "const unsigned char*) {\n    switch (slot) {\n";
+  for (size_t i = 0; i < ops.size(); ++i)
+    src << "      case " << i << ": user::op_slot" << i << "(ctx); break;\n";
+  src << "      default: ctx.err() |= ERR_UNKNOWN_SEQ;\n    }\n  }\n};\n}  // namespace go\n"
+      << "GO_ROWOPS_KERNELS(" << ro.kind << ", " << ro.elem_type << ", " << ro.gene_type
+      << ", go::RowUserOps, " << (ro.rows_global ? "true" : "false") << ")\n";
+  std::string cubin;
+  bool hit = false;
+  int rc = jit_compile_source(src.str(), ops, &cubin, &out->key, &hit, log);
+  if (rc) return rc;
+  const Drv* d = drv();
+  if (!d) {
+    *log = "CUDA driver API unavailable";
+    return GO_E_NODEVICE;
+  }
+  CUresult cr = d->ModuleLoadData(&out->mod, cubin.data());
+  if (cr != CUDA_SUCCESS) {
+    const char* es = nullptr;
+    d->GetErrorString(cr, &es);
+    *log = std::string("cuModuleLoadData: ") + (es ? es : "?");
+    return GO_E_CUDA;
+  }
+  if (d->ModuleGetFunction(&out->evolve, out->mod, "go_evolve_rowops") != CUDA_SUCCESS ||
+      d->ModuleGetFunction(&out->probe_op, out->mod, "go_probe_rowop") != CUDA_SUCCESS) {
+    *log = "JIT module lacks go_evolve_rowops / go_probe_rowop";
+    return GO_E_COMPILE;
+  }
+  out->cache_hit = hit;
+  out->compile_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return GO_OK;
+}
+
 }  // namespace gohost

@@ -52,4 +52,13 @@ struct UserProblemSrc {
 // Builds go_evolve_user (JitModule::evolve) and go_eval_user (JitModule::probe).
 int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log);
 
+// A built-in row problem's evolve kernel with user operators compiled in:
+// kind / element / gene type names as in engine.cu's GO_ROW_KERNEL list.
+struct RowOpsSrc {
+  std::string kind, elem_type, gene_type;
+  bool rows_global = false;
+};
+int jit_build_rowops(const RowOpsSrc& ro, const std::vector<UserOpSrc>& ops, JitModule* out,
+                     std::string* log);
+
 }  // namespace gohost

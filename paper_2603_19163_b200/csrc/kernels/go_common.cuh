@@ -357,6 +357,13 @@ struct MateSel {
     }
     pos = ev - start;
   }
+  // the evolver pick() would choose, without consuming `rng` (0xFFFF: none)
+  __device__ __forceinline__ int peek(Stream rng) const {
+    if (rows == nullptr || size <= 1) return 0xFFFF;
+    int j = rng.randbelow(size - 1);
+    j += j >= pos;
+    return j + start;
+  }
   template <class R>
   __device__ __forceinline__ const short* pick(R& rng) const {
     if (rows == nullptr || size <= 1) return nullptr;

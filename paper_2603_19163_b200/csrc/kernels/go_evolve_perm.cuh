@@ -57,7 +57,8 @@ struct TeamShared {  // (row kernels: go_evolve_row.cuh)
 // partials, lane-sort counts) follow it, sized by the team's warp count.
 struct PermTeam {
   int accept;
-  int dnext;                       // next deferred request to hand out (dynamic, per warp)
+  int dnext;                       // (unused)
+  unsigned dclaim[16];             // deferred requests handed out this step (bit per request)
   int nreq;                        // pending cooperative relocations this step
   int ndreq;                       // pending deferred whole-row operators this step
   int ngr;                         // ... of which guided rebuilds (queued from the back)
@@ -93,8 +94,9 @@ struct LaneArrays {
   unsigned short* order;  // [TS] thread slot -> logical lane
   unsigned short* req;    // [TS] lanes with a pending cooperative relocation
   unsigned short* dreq;   // [TS] lanes with a pending deferred whole-row operator
+  unsigned short* mate;   // [TS] crossover mate a deferred OX lane will wait for (0xFFFF none)
   static __host__ __device__ unsigned bytes(int TS) {
-    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2 + 2));
+    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2 + 2 + 2));
   }
   __device__ __forceinline__ void bind(unsigned char* p, int TS) {
     mv = (u64*)p;
@@ -104,6 +106,7 @@ struct LaneArrays {
     order = (unsigned short*)(meta + TS);
     req = order + TS;
     dreq = req + TS;
+    mate = dreq + TS;
   }
 };
 
@@ -347,6 +350,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         ts->ngr = 0;
         ts->dnext = 0;
       }
+      if (lane < 16) ts->dclaim[lane] = 0u;
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
       if (wl < nseq) {
@@ -395,6 +399,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         bool pending = false;
         if (perm_deferred(kind)) {  // whole-row operator: resolved by a warp below
           // guided rebuilds (the longest) queue from the back and are handed out first
+          la.mate[L] = kind == SEQ_OX ? (unsigned short)ms.peek(rng) : (unsigned short)0xFFFF;
           if (kind == SEQ_GUIDED_REBUILD) la.dreq[TS - 1 - atomicAdd(&ts->ngr, 1)] = (unsigned short)L;
           else la.dreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
           pending = true;
@@ -520,11 +525,25 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       const int ngr = ts->ngr, ndreq = ts->ndreq + ngr;
       if (ndreq > 0) {
 #pragma unroll 1
-        for (;;) {  // warps take requests as they free up (longest first)
-          int r = 0;
-          if (wl == 0) r = atomicAdd(&ts->dnext, 1);
+        for (;;) {  // warps take requests as they free up: guided rebuilds first
+          // (longest), then requests whose crossover mate has already published
+          // this generation's snapshot, then the rest in order
+          int r = -1;
+          if (wl == 0) {
+            for (int pass = 0; pass < 3 && r < 0; ++pass) {
+              for (int i = pass == 0 ? 0 : ngr; i < (pass == 0 ? ngr : ndreq) && r < 0; ++i) {
+                const unsigned bit = 1u << (i & 31);
+                if (*(volatile unsigned*)&ts->dclaim[i >> 5] & bit) continue;
+                if (pass == 1) {
+                  const int mj = la.mate[la.dreq[i - ngr]];
+                  if (mj != 0xFFFF && ld_acquire(A.prog + mj) < (int)g) continue;
+                }
+                if (!(atomicOr(&ts->dclaim[i >> 5], bit) & bit)) r = i;
+              }
+            }
+          }
           r = __shfl_sync(0xffffffffu, r, 0);
-          if (r >= ndreq) break;
+          if (r < 0) break;
           const int L = r < ngr ? la.dreq[TS - 1 - r] : la.dreq[r - ngr];
           const u32 meta = la.meta[L];
           const int nm = meta_nm(meta), k = meta_k(meta);

@@ -90,30 +90,184 @@ struct UserScore {
   }
 };
 
+// Instance data a user operator on a BUILT-IN row problem may read (the
+// reference hands operators ctx.problem, whose arrays they index directly,
+// e.g. demo_ops.py:18-21): QAP flow / distance, knapsack weights / values /
+// capacity, JSP machine / duration per operation.  Out-of-range indices set
+// the sticky error bit (the registration probe then excludes the operator).
+enum { RI_NONE = 0, RI_QAP = 1, RI_KNAP = 2, RI_JSP = 3 };
+struct RowInst {
+  const unsigned char* b;  // instance image (shared or global memory)
+  unsigned off1;           // second array (QAP D, knapsack v, JSP durations)
+  int kind, elem, n;       // elem: QAP element bytes (2, 4) or 8 = float64
+  double cap;
+  int n_ops;               // JSP operations
+  __device__ __forceinline__ double mat(unsigned off, int i, int j) const {
+    const unsigned k = off + (unsigned)(i * n + j) * (unsigned)elem;
+    return elem == 2 ? (double)*(const short*)(b + k)
+                     : (elem == 4 ? (double)*(const int*)(b + k) : *(const double*)(b + k));
+  }
+};
+
 // What a user operator snippet on a row problem sees as `ctx` (the reference's
 // CustomOperator.apply(sol, rng, ctx), operators.py:79-88): the lane's candidate
 // (d1 x d2 genes, row-major, flat index i < ctx.n), the lane stream with
-// CPython's draw algorithms, and Φ of the candidate (the `ctx.phi` the reference
-// hands operators, engine.py:215-222) through the problem's own objective.
+// CPython's draw algorithms, Φ of the candidate (the `ctx.phi` the reference
+// hands operators, engine.py:215-222) through the problem's own objective, and
+// on built-in problems the instance arrays (RowInst).
 template <class G, class U>
 struct RowOpCtx {
   RowCtx<G>* c;
   UserScore us;
   int n, rows, width;  // flat genes, d1, d2
-  __device__ __forceinline__ int get(int i) const { return c->full[i]; }
-  __device__ __forceinline__ void set(int i, int v) { c->full[i] = (G)v; }
+  RowInst in;          // kind RI_NONE on user (NVRTC-objective) problems
+  __device__ __forceinline__ bool ok(int i, int lim) {
+    const bool good = (unsigned)i < (unsigned)lim;
+    c->err |= good ? 0 : ERR_OP_RANGE;
+    return good;
+  }
+  __device__ __forceinline__ int get(int i) { return ok(i, n) ? (int)c->full[i] : 0; }
+  __device__ __forceinline__ void set(int i, int v) {
+    if (ok(i, n)) c->full[i] = (G)v;
+  }
   __device__ __forceinline__ void swap(int i, int j) {
+    if (!ok(i, n) || !ok(j, n)) return;
     const G t = c->full[i];
     c->full[i] = c->full[j];
     c->full[j] = t;
   }
-  __device__ __forceinline__ int randbelow(int k) { return c->rng.randbelow(k); }
-  __device__ __forceinline__ int randrange(int a, int b) { return c->rng.randrange(a, b); }
-  __device__ __forceinline__ double random() { return c->rng.random(); }
-  __device__ __forceinline__ double phi() const {
-    const RowSol<G> s{c->full, n};
-    return us.template phi<U>(s);
+  __device__ __forceinline__ int randbelow(int k) {
+    if (k <= 0) { c->err |= ERR_OP_RANGE; return 0; }
+    return c->rng.randbelow(k);
   }
+  __device__ __forceinline__ int randrange(int a, int b) {
+    if (b <= a) { c->err |= ERR_OP_RANGE; return a; }
+    return c->rng.randrange(a, b);
+  }
+  __device__ __forceinline__ double random() { return c->rng.random(); }
+  // QAP (builtins.py:265-290): flow F[i][j] between facilities, distance D[a][b]
+  // between locations
+  __device__ __forceinline__ double flow(int i, int j) {
+    if (in.kind != RI_QAP || !ok(i, in.n) || !ok(j, in.n)) return 0.0;
+    return in.mat(0, i, j);
+  }
+  __device__ __forceinline__ double dist(int a, int b) {
+    if (in.kind != RI_QAP || !ok(a, in.n) || !ok(b, in.n)) return 0.0;
+    return in.mat(in.off1, a, b);
+  }
+  // knapsack (builtins.py:240-262)
+  __device__ __forceinline__ double weight(int i) {
+    return in.kind == RI_KNAP && ok(i, in.n) ? ((const double*)in.b)[i] : 0.0;
+  }
+  __device__ __forceinline__ double value(int i) {
+    return in.kind == RI_KNAP && ok(i, in.n) ? ((const double*)(in.b + in.off1))[i] : 0.0;
+  }
+  __device__ __forceinline__ double capacity() const { return in.cap; }
+  // JSP-int (builtins.py:408-456): operation op = job * ops_per_job + k
+  __device__ __forceinline__ int machine(int op) {
+    return in.kind == RI_JSP && ok(op, in.n_ops) ? ((const int*)in.b)[op] : 0;
+  }
+  __device__ __forceinline__ int duration(int op) {
+    return in.kind == RI_JSP && ok(op, in.n_ops) ? ((const int*)(in.b + in.off1))[op] : 0;
+  }
+  __device__ __forceinline__ double phi() {
+    if (in.kind == RI_NONE) {
+      const RowSol<G> s{c->full, n};
+      return us.template phi<U>(s);
+    }
+    if (in.kind == RI_QAP) {  // Σ F_ij · D_{π_i π_j} (exact: products of integers)
+      double t = 0.0;
+      for (int i = 0; i < in.n; ++i)
+        for (int j = 0; j < in.n; ++j)
+          t += in.mat(0, i, j) * in.mat(in.off1, c->full[i], c->full[j]);
+      return __dmul_rn(us.w, t);
+    }
+    if (in.kind == RI_KNAP) {  // Maximize value, penalty = weight over capacity
+      double v = 0.0, w = 0.0;
+      for (int i = 0; i < in.n; ++i) {
+        v += value(i) * (double)c->full[i];
+        w += weight(i) * (double)c->full[i];
+      }
+      const double over = __dsub_rn(w, in.cap);
+      return __dadd_rn(__dmul_rn(us.w, -v), __dmul_rn(us.pw, over > 0.0 ? over : 0.0));
+    }
+    c->err |= ERR_OP_RANGE;  // JSP: the schedule decode is not offered to operators
+    return 0.0;
+  }
+  __device__ __forceinline__ int& err() { return c->err; }
+};
+
+// What a user operator on a partition problem (VRPTW / CVRP, builtins.py:80-190)
+// sees as `ctx`: routes (rows) of customer ids 0..n-1, a customer's matrix index
+// is id + 1 with the depot at 0 (builtins.py:3-6, :122-123).  Moves keep the
+// solution a partition; out-of-range arguments set the sticky error bit.
+template <class U>
+struct PartOpCtx {
+  PartCtx* c;
+  PartView pv;
+  const RowArgs* X;
+  double pw;
+  int n, rows, width;  // customers, vehicles (d1), route capacity (d2)
+  __device__ __forceinline__ bool ok(int i, int lim) {
+    const bool good = (unsigned)i < (unsigned)lim;
+    c->err |= good ? 0 : ERR_OP_RANGE;
+    return good;
+  }
+  __device__ __forceinline__ int size(int r) { return ok(r, rows) ? (int)c->sz[r] : 0; }
+  __device__ __forceinline__ int get(int r, int p) {
+    if (!ok(r, rows) || !ok(p, c->sz[r])) return 0;
+    return c->cells[c->start(r) + p];
+  }
+  // remove the customer at (r0, p0) and insert it at position p1 of route r1
+  // (positions of the route after the removal, p1 <= its size)
+  __device__ __forceinline__ void move(int r0, int p0, int r1, int p1) {
+    if (!ok(r0, rows) || !ok(p0, c->sz[r0]) || !ok(r1, rows)) return;
+    const int room = c->sz[r1] - (r1 == r0 ? 1 : 0);
+    if ((unsigned)p1 > (unsigned)room || (r1 != r0 && c->sz[r1] >= width)) {
+      c->err |= ERR_OP_MOVE;
+      return;
+    }
+    const short v = c->remove(r0, p0);
+    c->insert(r1, p1, v);
+  }
+  __device__ __forceinline__ void swap(int r0, int p0, int r1, int p1) {
+    if (!ok(r0, rows) || !ok(p0, c->sz[r0]) || !ok(r1, rows) || !ok(p1, c->sz[r1])) return;
+    const int a = c->start(r0) + p0, b = c->start(r1) + p1;
+    const short t = c->cells[a];
+    c->cells[a] = c->cells[b];
+    c->cells[b] = t;
+  }
+  __device__ __forceinline__ void reverse(int r, int i, int j) {  // [i, j] of route r
+    if (!ok(r, rows) || !ok(i, c->sz[r]) || !ok(j, c->sz[r]) || i > j) return;
+    const int s = c->start(r);
+    rev_short(c->cells + s, i, j);
+  }
+  // matrix distance between customers (-1 = the depot)
+  __device__ __forceinline__ double dist(int a, int b) {
+    if (!ok(a + 1, n + 1) || !ok(b + 1, n + 1)) return 0.0;
+    return pv.dist[(a + 1) * (n + 1) + (b + 1)];
+  }
+  __device__ __forceinline__ double demand(int cst) { return ok(cst, n) ? pv.demand[cst] : 0.0; }
+  __device__ __forceinline__ double ready(int cst) {
+    return X->tw && ok(cst + 1, n + 1) ? pv.ready[cst + 1] : 0.0;
+  }
+  __device__ __forceinline__ double due(int cst) {
+    return X->tw && ok(cst + 1, n + 1) ? pv.due[cst + 1] : 0.0;
+  }
+  __device__ __forceinline__ double service(int cst) {
+    return X->tw && ok(cst + 1, n + 1) ? pv.service[cst + 1] : 0.0;
+  }
+  __device__ __forceinline__ double capacity() const { return X->capacity; }
+  __device__ __forceinline__ int randbelow(int k) {
+    if (k <= 0) { c->err |= ERR_OP_RANGE; return 0; }
+    return c->rng.randbelow(k);
+  }
+  __device__ __forceinline__ int randrange(int a, int b) {
+    if (b <= a) { c->err |= ERR_OP_RANGE; return a; }
+    return c->rng.randrange(a, b);
+  }
+  __device__ __forceinline__ double random() { return c->rng.random(); }
+  __device__ __forceinline__ double phi();  // defined after part_scal
   __device__ __forceinline__ int& err() { return c->err; }
 };
 
@@ -1072,6 +1226,15 @@ __device__ __forceinline__ double part_scal(const RowArgs& X, double dist, int v
   return X.mo.m == 2 ? __dadd_rn(s, __dmul_rn(X.w2, b)) : s;
 }
 
+// Φ of a partition candidate with the run's penalty weight (engine.py:215-222)
+template <class U>
+__device__ __forceinline__ double PartOpCtx<U>::phi() {
+  double d, p;
+  int veh;
+  part_eval(pv, c->cells, c->sz, d, p, &veh);
+  return __dadd_rn(part_scal(*X, d, veh, nullptr, nullptr), __dmul_rn(pw, p));
+}
+
 __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_cells, int d1,
                              int d2, const RowArgs& X, double pw, const GrShared& g, double* sbuf,
                              TeamShared<double>* ts, int lane, int team, int TS) {
@@ -1467,6 +1630,9 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
             la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
             pending = true;
+          } else if (kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+            PartOpCtx<U> oc{&c, pv, &X, pwt, X.n_cells, X.d1, X.d2};
+            U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
           } else {
             run_part_op(kind, c);
           }
@@ -1501,9 +1667,12 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           } else if (kind == SEQ_UNIFORM_X) {  // warp-resolved below
             la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
             pending = true;
-          } else if (KIND == RK_USER && kind >= SEQ_CUSTOM_BASE) {  // user operator
+          } else if (kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+            RowInst ri{inst, X.off1, KIND == RK_QAP ? RI_QAP : (KIND == RK_KNAP ? RI_KNAP :
+                                                                 (KIND == RK_JSP ? RI_JSP : RI_NONE)),
+                       KIND == RK_QAP ? (int)sizeof(E) : 8, n, X.capacity, n};
             RowOpCtx<G, U> oc{&c, UserScore{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m},
-                              n, c.d1, X.d2};
+                              n, c.d1, X.d2, ri};
             U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
             c.mark_all();
           } else {

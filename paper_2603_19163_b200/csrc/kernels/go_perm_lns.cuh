@@ -100,9 +100,23 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     a0 = __shfl_sync(FULL, a0, 0);
     const int c1 = __shfl_sync(FULL, a1, 0), c2 = __shfl_sync(FULL, a2, 0);
     const short* mate = ms->rows + (size_t)a0 * n;
-    unsigned* mask = (unsigned*)wrow;  // n bits (the row holds 16 n)
+    const int s0 = c2 + 1 == n ? 0 : c2 + 1;
+    // rows up to 32 * WINTS values: the slice bit set lives in wint and the mate
+    // row, rotated to start at c2+1, is staged into wrow with all its loads in
+    // flight at once (one L2 round trip instead of one per 32 values);
+    // longer rows keep the bit set in wrow and read the mate from L2
+    const bool staged = n <= 32 * 32;
+    unsigned* mask = staged ? (unsigned*)wint : (unsigned*)wrow;
     const int nwords = (n + 31) >> 5;
     for (int i = wl; i < nwords; i += 32) mask[i] = 0u;
+    if (staged) {
+#pragma unroll 8
+      for (int t = wl; t < n; t += 32) {
+        int src = s0 + t;
+        src = src >= n ? src - n : src;
+        wrow[t] = __ldcg(mate + src);
+      }
+    }
     __syncwarp();
     // kept slice child[c1..c2] = parent[c1..c2]: copied, marked, inner edges summed
     Acc len = 0;
@@ -127,7 +141,6 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     // fill: mate values from c2+1 (cyclic) not in the slice, into the free
     // positions from c2+1 (cyclic); with F the fill sequence and S the slice
     // the child read cyclically from c2+1 is F ++ S
-    const int s0 = c2 + 1 == n ? 0 : c2 + 1;
     int filled = 0, f_first = -1, f_last = -1;
     const unsigned lt = (1u << wl) - 1u;
 #pragma unroll 2
@@ -136,9 +149,13 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
       int v = 0;
       bool keep = false;
       if (t < n) {
-        int src = s0 + t;
-        src = src >= n ? src - n : src;
-        v = __ldcg(mate + src);
+        if (staged) {
+          v = wrow[t];
+        } else {
+          int src = s0 + t;
+          src = src >= n ? src - n : src;
+          v = __ldcg(mate + src);
+        }
         keep = !((mask[v >> 5] >> (v & 31)) & 1u);
       }
       const unsigned bal = __ballot_sync(FULL, keep);

@@ -149,8 +149,73 @@ __device__ __forceinline__ void user_probe_entry(const void* inst, RowArgs x, in
   RowOpCtx<short, U> oc{&c,
                         UserScore{(const unsigned char*)inst, x.obj_weight, x.penalty_weight,
                                   x.mo.maxmask, x.w2, x.mo.m},
-                        n, c.d1, x.d2};
+                        n, c.d1, x.d2, RowInst{(const unsigned char*)inst, x.off1, RI_NONE, 8, n,
+                                               x.capacity, n}};
   U::op(slot, oc, (const unsigned char*)inst);
+  *err = c.err;
+}
+
+// register_custom's probe for a user operator on a BUILT-IN row problem (QAP /
+// knapsack / JSP-int: one flat row; partition problems: cells + route sizes),
+// one application, single thread, stream key `key`.
+template <int KIND, class E, class U>
+__device__ __forceinline__ void rowops_probe_entry(const void* inst, RowArgs x, int n, int slot,
+                                                   unsigned long long key, short* genes,
+                                                   int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned char* b = (const unsigned char*)inst;
+  if (KIND == RK_PART) {
+    PartCtx c;
+    c.rng.init(key);
+    c.cells = genes;
+    c.sz = genes + x.n_cells;
+    c.n = x.n_cells;
+    c.d1 = x.d1;
+    c.d2 = x.d2;
+    c.n_cfg = x.n_cfg;
+    c.total = x.n_cells;
+    c.err = 0;
+    c.mates = nullptr;
+    PartView pv;
+    pv.dist = (const double*)b;
+    pv.demand = (const double*)(b + x.off1);
+    pv.ready = (const double*)(b + x.off2);
+    pv.due = (const double*)(b + x.off3);
+    pv.service = (const double*)(b + x.off4);
+    pv.n = x.n_cells;
+    pv.d1 = x.d1;
+    pv.d2 = x.d2;
+    pv.cap = x.capacity;
+    pv.tw = x.tw;
+    pv.variant = x.pvar;
+    pv.prio = (const double*)(b + x.off2);
+    PartOpCtx<U> oc{&c, pv, &x, x.penalty_weight, x.n_cells, x.d1, x.d2};
+    U::op(slot, oc, b);
+    *err = c.err;
+    return;
+  }
+  RowCtx<short> c;
+  c.rng.init(key);
+  c.row = genes;
+  c.full = genes;
+  c.mf = 0;
+  c.d1 = 1;
+  c.d2 = n;
+  c.n = n;
+  c.n_cfg = x.n_cfg;
+  c.lb = x.lb;
+  c.ub = x.ub;
+  short dummy[MAX_RANGES * 2];
+  c.rlo = dummy;
+  c.rhi = dummy + MAX_RANGES;
+  c.rstride = 1;
+  c.nr = 0;
+  c.err = 0;
+  c.mates = nullptr;
+  const RowInst ri{b, x.off1, KIND == RK_QAP ? RI_QAP : (KIND == RK_KNAP ? RI_KNAP : RI_JSP),
+                   KIND == RK_QAP ? (int)sizeof(E) : 8, n, x.capacity, n};
+  RowOpCtx<short, U> oc{&c, UserScore{b, x.obj_weight, x.penalty_weight, 0, 0.0, 1}, n, 1, n, ri};
+  U::op(slot, oc, b);
   *err = c.err;
 }
 
@@ -171,6 +236,18 @@ __device__ __forceinline__ void user_probe_entry(const void* inst, RowArgs x, in
   extern "C" __global__ void go_probe_user_op(const void* inst, go::RowArgs x, int n, int slot, \
                                               unsigned long long key, short* g, int* err) {   \
     go::user_probe_entry<U>(inst, x, n, slot, key, g, err);                                   \
+  }
+
+// Kernels of a built-in row problem with NVRTC-compiled user operators
+// (register_custom, operators.py:634-669): evolve + probe
+#define GO_ROWOPS_KERNELS(KIND, E, G, U, RG)                                                  \
+  extern "C" __global__ void __launch_bounds__(512, 1) go_evolve_rowops(go::EvolveArgs a,      \
+                                                                        go::RowArgs x) {      \
+    go::evolve_row<KIND, E, G, U, RG>(a, x);                                                  \
+  }                                                                                           \
+  extern "C" __global__ void go_probe_rowop(const void* inst, go::RowArgs x, int n, int slot,  \
+                                            unsigned long long key, short* g, int* err) {     \
+    go::rowops_probe_entry<KIND, E, U>(inst, x, n, slot, key, g, err);                        \
   }
 
 #define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \

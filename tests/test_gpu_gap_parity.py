@@ -89,3 +89,42 @@ def test_row_family_gap_no_worse_than_reference(name):
     if out.is_dir():
         (out / f"gap_parity_{name}.json").write_text(json.dumps(summary, indent=1))
     assert p > 0.05, summary
+
+
+GOLD_BENCH = Path(__file__).with_name("golden") / "gap_bench.json"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2", "r101"])
+def test_benchmark_shape_gap_no_worse_than_reference(name):
+    """The same bar on the benchmark shapes themselves: C2 (pcb442-shaped
+    lattice + tsp-delta, P=32, T=128, G=200 as SURVEY §8d sets) and C3 on the
+    reference's R101 fixture (VRPTW, float distances).  Reference runs frozen
+    by tests/golden/make_gap_golden_bench.py; feasibility first, then the
+    objective, as the reference's comparison orders them (core.py:315-347)."""
+    from scipy.stats import mannwhitneyu
+
+    from paper_2603_19163_b200 import instances as I
+    data = json.loads(GOLD_BENCH.read_text())
+    c = data["cases"][name]
+    kind, inst, _ = I.baseline_instances()[c["workload"]]
+    prob = G.builtin_problem(kind, inst)
+    ops = G.tsp_delta_operators() if c["workload"] == "C2" else ()
+
+    def score(obj, pen):  # infeasible runs rank behind every feasible one
+        return obj + (1e9 * (1.0 + pen) if pen > 0 else 0.0)
+    ours = []
+    for seed in data["seeds"]:
+        res = G.run(prob, G.EngineConfig(population=c["population"], team_size=c["team_size"],
+                                         max_generations=c["max_generations"], seed=seed,
+                                         custom_operators=ops))
+        assert res.generations_completed == c["max_generations"]
+        ours.append(score(float(res.objectives[0]), float(res.penalty)))
+    ref = [score(*data["runs"][name][str(s)]) for s in data["seeds"]]
+    p = mannwhitneyu(ours, ref, alternative="greater").pvalue
+    summary = {"case": name, "ours": ours, "reference": ref, "mean_ours": float(np.mean(ours)),
+               "mean_reference": float(np.mean(ref)), "p_worse": p}
+    out = Path("gpurun_out")
+    if out.is_dir():
+        (out / f"gap_parity_{name}.json").write_text(json.dumps(summary, indent=1))
+    assert p > 0.05, summary
