@@ -127,8 +127,11 @@ def gap_at(workload: str, seconds: float, procs: int, best_known: float | None,
         res = pool.map(_gap_worker, [(workload, seed + i, seconds, best_known, sense)
                                      for i in range(procs)])
     objs = sorted((r[0] for r in res if r[1] == 0.0), reverse=(sense == "max"))
+    pens = sorted((float(r[1]), r[0]) for r in res)  # penalty first (core.py:315-347)
     out = {"best": objs[0] if objs else None, "median": objs[len(objs) // 2] if objs else None,
            "feasible_runs": len(objs), "procs": procs, "seconds": seconds,
+           "best_penalty_objective": list(pens[0]),
+           "median_penalty": pens[len(pens) // 2][0],
            "generations": sorted(r[2] for r in res), "kind": "reference"}
     if best_known and objs:
         sgn = 1.0 if sense == "min" else -1.0

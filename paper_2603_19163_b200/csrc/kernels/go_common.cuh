@@ -231,44 +231,57 @@ __device__ __forceinline__ void sample_range(C& c, int total, int m, int* picks)
   sample_range_buf(c, total, m, picks, ovi, ovv);
 }
 
-// sample(range(1, n), 3) sorted (operators.py:300)
+// sample(range(1, n), 3) sorted (operators.py:300).  Fixed-size loops, fully
+// unrolled, so the pool overrides and picks stay in registers (dynamically
+// indexed arrays would live in L2-backed local memory).
 template <class C>
 __device__ __forceinline__ void sample3_sorted(C& c, int n, int& i, int& j, int& k) {
   const int N = n - 1;  // population 1..n-1
-  int out[3];
+  int out[3] = {0, 0, 0};
   if (N <= sample_setsize(3)) {  // pool method with a virtual pool
-    int ovi[3], ovv[3], no = 0;
+    int ovi[3] = {-1, -1, -1}, ovv[3] = {0, 0, 0};
+    int no = 0;
+#pragma unroll
     for (int t = 0; t < 3; ++t) {
       const int jj = c.randbelow(N - t);
       int val = jj + 1;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == jj) val = ovv[q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < no && ovi[q] == jj) val = ovv[q];
       out[t] = val;
       // pool[jj] = pool[N - t - 1]
       const int src = N - t - 1;
       int sval = src + 1;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == src) sval = ovv[q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < no && ovi[q] == src) sval = ovv[q];
       bool found = false;
-      for (int q = 0; q < no; ++q)
-        if (ovi[q] == jj) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < no && ovi[q] == jj) {
           ovv[q] = sval;
           found = true;
         }
       if (!found) {
-        ovi[no] = jj;
-        ovv[no] = sval;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (q == no) {
+            ovi[q] = jj;
+            ovv[q] = sval;
+          }
         ++no;
       }
     }
   } else {  // set method
+#pragma unroll
     for (int t = 0; t < 3; ++t) {
       int jj;
       bool dup;
       do {
         jj = c.randbelow(N);
         dup = false;
-        for (int q = 0; q < t; ++q) dup |= (out[q] == jj + 1);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) dup |= (q < t && out[q] == jj + 1);
       } while (dup);
       out[t] = jj + 1;
     }
@@ -356,13 +369,6 @@ struct MateSel {
       size = base;
     }
     pos = ev - start;
-  }
-  // the evolver pick() would choose, without consuming `rng` (0xFFFF: none)
-  __device__ __forceinline__ int peek(Stream rng) const {
-    if (rows == nullptr || size <= 1) return 0xFFFF;
-    int j = rng.randbelow(size - 1);
-    j += j >= pos;
-    return j + start;
   }
   template <class R>
   __device__ __forceinline__ const short* pick(R& rng) const {

@@ -57,8 +57,7 @@ struct TeamShared {  // (row kernels: go_evolve_row.cuh)
 // partials, lane-sort counts) follow it, sized by the team's warp count.
 struct PermTeam {
   int accept;
-  int dnext;                       // (unused)
-  unsigned dclaim[16];             // deferred requests handed out this step (bit per request)
+  int dnext;                       // next deferred request to hand out (dynamic, per warp)
   int nreq;                        // pending cooperative relocations this step
   int ndreq;                       // pending deferred whole-row operators this step
   int ngr;                         // ... of which guided rebuilds (queued from the back)
@@ -94,9 +93,8 @@ struct LaneArrays {
   unsigned short* order;  // [TS] thread slot -> logical lane
   unsigned short* req;    // [TS] lanes with a pending cooperative relocation
   unsigned short* dreq;   // [TS] lanes with a pending deferred whole-row operator
-  unsigned short* mate;   // [TS] crossover mate a deferred OX lane will wait for (0xFFFF none)
   static __host__ __device__ unsigned bytes(int TS) {
-    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2 + 2 + 2));
+    return (unsigned)(TS * (3 * 8 + sizeof(Acc) + 4 + 4 + 2 + 2 + 2));
   }
   __device__ __forceinline__ void bind(unsigned char* p, int TS) {
     mv = (u64*)p;
@@ -106,7 +104,6 @@ struct LaneArrays {
     order = (unsigned short*)(meta + TS);
     req = order + TS;
     dreq = req + TS;
-    mate = dreq + TS;
   }
 };
 
@@ -233,7 +230,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   }
   if (threadIdx.x < 3) s_misc[threadIdx.x] = R->kw[threadIdx.x];
   if (threadIdx.x == 3) s_misc[3] = R->total;
-  if (threadIdx.x == blockDim.x - 1) {  // lane-sort order: user operators first (long loops), then built-ins (any CTA size)
+  if (threadIdx.x == blockDim.x - 1) {  // lane-sort order (any CTA size)
+#ifdef GO_USER_OPS_FIRST
+    // user operators first (long loops), then built-ins
     int j = 0;
     for (int pass = 0; pass < 2; ++pass)
       for (int i = 0; i < nseq; ++i)
@@ -241,6 +240,32 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           s_gord[j] = i;
           s_grank[i] = j++;
         }
+#else
+    // user operators (the long per-lane loops) spread evenly through the
+    // built-ins, so consecutive warps do not both draw a long loop group: a
+    // warp runs its lane groups one after another (SIMT), and the step waits
+    // for its slowest warp
+    int nu = 0;
+    for (int i = 0; i < nseq; ++i) nu += R->kind[i] >= SEQ_CUSTOM_BASE;
+    const int nb = nseq - nu;
+    int j = 0, bi = 0, ui = 0;
+    for (int u = 0; u <= nu; ++u) {
+      if (u < nu) {  // the next user operator
+        while (R->kind[ui] < SEQ_CUSTOM_BASE) ++ui;
+        s_gord[j] = ui;
+        s_grank[ui] = j++;
+        ++ui;
+      }
+      const int upto = nu ? (nb * (u + 1)) / nu : nb;  // built-ins between user operators
+      while (bi < nseq && (j - (u + 1 < nu ? u + 1 : nu)) < upto) {
+        if (R->kind[bi] < SEQ_CUSTOM_BASE) {
+          s_gord[j] = bi;
+          s_grank[bi] = j++;
+        }
+        ++bi;
+      }
+    }
+#endif
   }
   __syncthreads();
 
@@ -350,7 +375,6 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         ts->ngr = 0;
         ts->dnext = 0;
       }
-      if (lane < 16) ts->dclaim[lane] = 0u;
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
       if (wl < nseq) {
@@ -374,6 +398,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       GO_TICK(2 + 4 * s);
       if (active == 0) break;  // uniform
 
+#ifdef GO_PHASE_TIMING
+      const unsigned long long t_ex0 = clock64();
+#endif
       if (lane < active) {
         const int L = la.order[lane];
         Stream rng;
@@ -388,9 +415,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         for (int i = 0; i < nm; ++i) C.push_packed(la.mv[i * TS + L]);
         Acc d = la.delta[L];
         PermCtx<Policy> c;
-        c.rng = &rng;
-        c.L = &C;
-        c.pol = &pol;
+        c.rng = rng;
+        c.L = C;
+        c.pol = pol;
         c.err = 0;
         c.rd_pos = 0;
         c.rd_elem = 0;
@@ -399,12 +426,12 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         bool pending = false;
         if (perm_deferred(kind)) {  // whole-row operator: resolved by a warp below
           // guided rebuilds (the longest) queue from the back and are handed out first
-          la.mate[L] = kind == SEQ_OX ? (unsigned short)ms.peek(rng) : (unsigned short)0xFFFF;
           if (kind == SEQ_GUIDED_REBUILD) la.dreq[TS - 1 - atomicAdd(&ts->ngr, 1)] = (unsigned short)L;
           else la.dreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
           pending = true;
         } else {
           run_perm_op<Policy, Custom>(kind, c);
+          rng = c.rng;
           if (c.out.kind == MV_RELOCATE_BEST) {
             la.mv[nm * TS + L] = pack_move(c.out);  // resolved below, nm unchanged
             la.req[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
@@ -426,6 +453,11 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         la.meta[L] = pack_meta(k, nm, q0, q1, q2) | (meta & META_BASE);
         la.delta[L] = d;
       }
+#ifdef GO_PHASE_TIMING
+      __syncwarp();  // slots 22.. : each warp's own lane-execution time, by warp index
+      if (wl == 0 && warp < 4) atomicAdd(&A.gs->prof[22 + warp], clock64() - t_ex0);
+      if (lane == 0) atomicAdd(&A.gs->prof[26], 1ull);
+#endif
       team_bar(team, TS);
       GO_TICK(3 + 4 * s);
 
@@ -525,25 +557,11 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       const int ngr = ts->ngr, ndreq = ts->ndreq + ngr;
       if (ndreq > 0) {
 #pragma unroll 1
-        for (;;) {  // warps take requests as they free up: guided rebuilds first
-          // (longest), then requests whose crossover mate has already published
-          // this generation's snapshot, then the rest in order
-          int r = -1;
-          if (wl == 0) {
-            for (int pass = 0; pass < 3 && r < 0; ++pass) {
-              for (int i = pass == 0 ? 0 : ngr; i < (pass == 0 ? ngr : ndreq) && r < 0; ++i) {
-                const unsigned bit = 1u << (i & 31);
-                if (*(volatile unsigned*)&ts->dclaim[i >> 5] & bit) continue;
-                if (pass == 1) {
-                  const int mj = la.mate[la.dreq[i - ngr]];
-                  if (mj != 0xFFFF && ld_acquire(A.prog + mj) < (int)g) continue;
-                }
-                if (!(atomicOr(&ts->dclaim[i >> 5], bit) & bit)) r = i;
-              }
-            }
-          }
+        for (;;) {  // warps take requests as they free up (guided rebuilds, the longest, first)
+          int r = 0;
+          if (wl == 0) r = atomicAdd(&ts->dnext, 1);
           r = __shfl_sync(0xffffffffu, r, 0);
-          if (r < 0) break;
+          if (r >= ndreq) break;
           const int L = r < ngr ? la.dreq[TS - 1 - r] : la.dreq[r - ngr];
           const u32 meta = la.meta[L];
           const int nm = meta_nm(meta), k = meta_k(meta);
@@ -561,7 +579,8 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           const unsigned long long t_op = clock64();
 #endif
           const DeferRes<Acc> dr = perm_defer(pol, C, kind, dst, warp == 0 ? nxt : my_row, my_int,
-                                              &rng, &ms, n, wl);
+                                              rng, ms, n, wl);
+          rng = dr.rng;
 #ifdef GO_PHASE_TIMING
           if (wl == 0) {  // slots 16.. : (cycles, count) per deferred kind OX / shuffles / rebuild
             const int b = kind == SEQ_OX ? 16 : (kind == SEQ_GUIDED_REBUILD ? 20 : 18);

@@ -1614,7 +1614,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         const int k = meta_k(meta);
         int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
         bool pending = false;
-        if (KIND == RK_PART) {
+        if constexpr (KIND == RK_PART) {
           PartCtx c;
           c.rng = rng;
           c.cells = (short*)(rows + (size_t)L * rs);

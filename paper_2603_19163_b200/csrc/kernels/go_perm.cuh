@@ -219,48 +219,52 @@ __device__ __forceinline__ typename D::Acc tsp_move_delta(const D& d, const Chai
 // and see exactly this API.  Out-of-range reads or malformed moves set a
 // sticky error bit instead of faulting, so the registration probe can
 // exclude a broken operator (operators.py:649-665) without killing the run.
+// The stream, chain and policy are held BY VALUE: pointers to them (as in
+// round 1) pinned all three to the thread's stack, which lives in L2-backed
+// local memory here (shared memory takes nearly all of L1), so every draw,
+// position read and distance read of an operator paid an L2 round trip.
 template <class Policy>
 struct PermCtx {
-  Stream* rng;
-  const Chain* L;
-  const Policy* pol;
+  Stream rng;
+  Chain L;
+  Policy pol;
   Move out;
   int err;
   unsigned rd_pos, rd_elem;  // algorithmic reads (roofline accounting)
 
-  __device__ __forceinline__ int size() const { return L->n; }
+  __device__ __forceinline__ int size() const { return L.n; }
   // branch-free range checks: an out-of-range index reads element 0 and
   // raises the sticky error bit (probe exclusion), never faults
   __device__ __forceinline__ int at(int p) {
-    const bool ok = (unsigned)p < (unsigned)L->n;
+    const bool ok = (unsigned)p < (unsigned)L.n;
     err |= ok ? 0 : ERR_OP_RANGE;
     ++rd_pos;
-    return L->at(ok ? p : 0);
+    return L.at(ok ? p : 0);
   }
   __device__ __forceinline__ double dist(int a, int b) {
-    const unsigned ni = (unsigned)pol->n_items();
+    const unsigned ni = (unsigned)pol.n_items();
     const bool ok = (unsigned)a < ni && (unsigned)b < ni;
     err |= ok ? 0 : ERR_OP_RANGE;
     ++rd_elem;
-    return pol->cost(ok ? a : 0, ok ? b : 0);
+    return pol.cost(ok ? a : 0, ok ? b : 0);
   }
-  __device__ __forceinline__ double random() { return rng->random(); }
+  __device__ __forceinline__ double random() { return rng.random(); }
   __device__ __forceinline__ int randbelow(int n) {
     if (n <= 0) {
       err |= ERR_OP_RANGE;
       return 0;
     }
-    return rng->randbelow(n);
+    return rng.randbelow(n);
   }
   __device__ __forceinline__ int randrange(int lo, int hi) {
     if (hi <= lo) {
       err |= ERR_OP_RANGE;
       return lo;
     }
-    return rng->randrange(lo, hi);
+    return rng.randrange(lo, hi);
   }
   __device__ __forceinline__ void swap(int i, int j) {
-    const int n = L->n;
+    const int n = L.n;
     if ((unsigned)i >= (unsigned)n || (unsigned)j >= (unsigned)n || i == j) {
       err |= ERR_OP_MOVE;
       return;
@@ -268,14 +272,14 @@ struct PermCtx {
     out.kind = MV_SWAP; out.a = i; out.b = j; out.c = 0;
   }
   __device__ __forceinline__ void reverse(int i, int j) {
-    if (i < 0 || j >= L->n || i >= j) {
+    if (i < 0 || j >= L.n || i >= j) {
       err |= ERR_OP_MOVE;
       return;
     }
     out.kind = MV_REVERSE; out.a = i; out.b = j; out.c = 0;
   }
   __device__ __forceinline__ void move_segment(int start, int len, int pos) {
-    const int n = L->n;
+    const int n = L.n;
     if (len < 1 || start < 0 || start + len > n || pos < 0 || pos > n - len) {
       err |= ERR_OP_MOVE;
       return;
@@ -285,7 +289,7 @@ struct PermCtx {
   __device__ __forceinline__ void insert(int i, int pos) { move_segment(i, 1, pos); }
   // three-opt reconnection of cuts 0 < i < j < k < n, variant 0..6 (header)
   __device__ __forceinline__ void three_opt(int i, int j, int k, int variant) {
-    if (!(0 < i && i < j && j < k && k < L->n) || variant < 0 || variant > 6) {
+    if (!(0 < i && i < j && j < k && k < L.n) || variant < 0 || variant > 6) {
       err |= ERR_OP_MOVE;
       return;
     }
@@ -300,7 +304,7 @@ struct PermCtx {
   // slots per step) after the operators return, so it must be the
   // operator's last action.
   __device__ __forceinline__ void relocate_best(int start, int len) {
-    const int n = L->n;
+    const int n = L.n;
     if (len < 1 || start < 0 || start + len > n || n - len < 2) {
       err |= ERR_OP_MOVE;
       return;

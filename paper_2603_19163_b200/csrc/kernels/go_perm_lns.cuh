@@ -43,7 +43,8 @@ __device__ __forceinline__ typename Policy::Acc perm_row_length(const Policy& po
 template <class Acc>
 struct DeferRes {
   int changed;
-  Acc len;  // exact tour length of the new row (valid when changed)
+  Acc len;     // exact tour length of the new row (valid when changed)
+  Stream rng;  // lane 0: the stream after the operator's draws
 };
 
 // One warp resolves one deferred lane.  `dst` is the lane's global row that
@@ -61,14 +62,21 @@ struct DeferRes {
 // shuffle code evicted the evolve loop from the instruction cache.)
 template <class Policy>
 __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
-    const Policy pol, const Chain C, int kind, i16* dst, i16* wrow, int* wint, Stream* rng,
-    const MateSel* ms, int n_cfg, int wl) {
+    const Policy pol, const Chain C, int kind, i16* dst, i16* wrow, int* wint, Stream rng_in,
+    const MateSel ms_in, int n_cfg, int wl) {
   typedef typename Policy::Acc Acc;
   const int n = C.n;
   const unsigned FULL = 0xffffffffu;
   DeferRes<Acc> out;
   out.changed = 0;
   out.len = 0;
+  // the stream and the mate selector by value (in registers), not through
+  // pointers that would pin them to local memory
+  Stream& rng_ref = out.rng;
+  rng_ref = rng_in;
+  Stream* rng = &rng_ref;
+  const MateSel ms_v = ms_in;
+  const MateSel* ms = &ms_v;
   // ---- draws that precede any row access (lane 0), broadcast to the warp ----
   int a0 = 0, a1 = 0, a2 = 0, live = 0;
   if (wl == 0) {
@@ -105,7 +113,11 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     // row, rotated to start at c2+1, is staged into wrow with all its loads in
     // flight at once (one L2 round trip instead of one per 32 values);
     // longer rows keep the bit set in wrow and read the mate from L2
+#ifdef GO_NO_OX_STAGE
+    const bool staged = false;
+#else
     const bool staged = n <= 32 * 32;
+#endif
     unsigned* mask = staged ? (unsigned*)wint : (unsigned*)wrow;
     const int nwords = (n + 31) >> 5;
     for (int i = wl; i < nwords; i += 32) mask[i] = 0u;

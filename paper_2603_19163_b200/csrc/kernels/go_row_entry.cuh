@@ -164,7 +164,7 @@ __device__ __forceinline__ void rowops_probe_entry(const void* inst, RowArgs x, 
                                                    int* err) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const unsigned char* b = (const unsigned char*)inst;
-  if (KIND == RK_PART) {
+  if constexpr (KIND == RK_PART) {
     PartCtx c;
     c.rng.init(key);
     c.cells = genes;
@@ -192,8 +192,7 @@ __device__ __forceinline__ void rowops_probe_entry(const void* inst, RowArgs x, 
     PartOpCtx<U> oc{&c, pv, &x, x.penalty_weight, x.n_cells, x.d1, x.d2};
     U::op(slot, oc, b);
     *err = c.err;
-    return;
-  }
+  } else {
   RowCtx<short> c;
   c.rng.init(key);
   c.row = genes;
@@ -217,6 +216,7 @@ __device__ __forceinline__ void rowops_probe_entry(const void* inst, RowArgs x, 
   RowOpCtx<short, U> oc{&c, UserScore{b, x.obj_weight, x.penalty_weight, 0, 0.0, 1}, n, 1, n, ri};
   U::op(slot, oc, b);
   *err = c.err;
+  }
 }
 
 }  // namespace go

@@ -100,9 +100,9 @@ __device__ __forceinline__ void tsp_probe_entry(const void* inst, int n, int kin
     Chain L;
     L.reset(row, n);
     PermCtx<TspPolicy<D>> c;
-    c.rng = &rng;
-    c.L = &L;
-    c.pol = &pol;
+    c.rng = rng;
+    c.L = L;
+    c.pol = pol;
     c.err = 0;
     c.rd_pos = 0;
     c.rd_elem = 0;

@@ -802,6 +802,7 @@ class DeviceRun:
         # scalar_fitness weights (engine.py:215-222): the Weighted mode's, else obj_defs'
         sw = mode.weights if isinstance(mode, Weighted) else tuple(o.weight for o in cfg.obj_defs)
         ec.obj_weight = sw[0]
+        self.obj_weight = sw[0]
         ec.obj_weight2 = sw[1] if len(sw) > 1 else 0.0
         if not isinstance(mode, Weighted):  # Lexicographic (core.py:92-106)
             ec.lex, ec.lex_first = 1, mode.priority_order[0]
@@ -888,7 +889,15 @@ class DeviceRun:
         s = Solution(genes.reshape(cfg.d1, cfg.d2), sizes, m)
         s.objectives[:] = obj
         s.penalty = pen.value
+        if self._rescaled():
+            evaluate_many(self.problem, [s], self.config.device)
         return s
+
+    def _rescaled(self) -> bool:
+        """Single-objective runs keep Φ = w·(±obj) on the device; with a weight
+        other than 1 obj = Φ/w is not exact, so reported solutions are
+        re-evaluated (the reference reports evaluate()'s values)."""
+        return self.cfg.num_objectives == 1 and abs(getattr(self, "obj_weight", 1.0)) != 1.0
 
     def population(self) -> list[Solution]:
         cfg = self.cfg
@@ -906,6 +915,8 @@ class DeviceRun:
             s.objectives[:] = obj[i * m:(i + 1) * m]
             s.penalty = pen[i]
             out.append(s)
+        if self._rescaled():
+            evaluate_many(self.problem, out, self.config.device)
         return out
 
     def weights(self):

@@ -35,7 +35,13 @@ def main():
         for s in range(seeds):
             r = G.run(prob, G.EngineConfig(seed=9000 + s, custom_operators=ops, device_init=True,
                                            time_limit_seconds=seconds, max_generations=10 ** 9))
-            if r.penalty != 0.0:
+            if r.penalty != 0.0:  # (C3's R101 fixture: no zero-penalty solution exists)
+                old = entry.get("best_penalized")
+                cand = [float(r.penalty), float(r.objectives[0])]
+                if old is None or cand < old:
+                    entry["best_penalized"] = cand
+                    entry["best_penalized_how"] = f"device run, {seconds:.0f} s, seed {9000 + s}"
+                print(name, s, "penalty", cand, flush=True)
                 continue
             v = float(r.objectives[0])
             old = entry.get("best_known")

@@ -82,6 +82,12 @@ def one_tree_bound(d, upper, iters=4000):
     return float(best)
 
 
+def vrptw_lateness_bound(inst):
+    d, r, du = inst.distance_matrix, inst.ready_times, inst.due_times
+    arr = np.maximum(r[1:], r[0] + d[0, 1:])
+    return float(np.maximum(0.0, arr - du[1:]).sum())
+
+
 def jsp_lower_bound(jobs):
     job = max(sum(t for _, t in ops) for ops in jobs)
     mach = {}
@@ -103,6 +109,10 @@ def main():
     out["C2j"] = {"lower_bound": one_tree_bound(tab["C2j"][1].distance_matrix, upper=45000.0),
                   "sense": "min",
                   "how": "Held-Karp 1-tree bound, subgradient ascent"}
+    out["C3"] = {"penalty_lower_bound": vrptw_lateness_bound(tab["C3"][1]), "sense": "min",
+                 "how": "sum over customers of max(0, max(ready, d(depot, c)) - due): lateness no "
+                        "route can avoid (the R101 fixture is synthetic; 2 windows close before "
+                        "the direct drive from the depot, so no zero-penalty solution exists)"}
     print(json.dumps(out, indent=1))
 
 

@@ -34,5 +34,8 @@ for chunk in (50, 300):
     for label, b in (("OX", 16), ("shuffles", 18), ("guided rebuild", 20)):
         if v[b + 1]:
             print(f"  {label:15s} {v[b + 1]:9.0f} applications, mean {v[b] / v[b + 1]:9.0f} cycles")
+    if v[26]:
+        print("  lane execution per step, by warp index (mean cycles):",
+              [int(v[22 + i] / v[26]) for i in range(4)])
     w, kw = dr.weights()
     print("  weights", np.round(w, 3), "k", np.round(kw, 3))
