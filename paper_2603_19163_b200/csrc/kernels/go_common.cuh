@@ -370,14 +370,20 @@ struct MateSel {
     }
     pos = ev - start;
   }
+  // the mate's evolver index (-1: none), after waiting for its snapshot
   template <class R>
-  __device__ __forceinline__ const short* pick(R& rng) const {
-    if (rows == nullptr || size <= 1) return nullptr;
+  __device__ __forceinline__ int pick_index(R& rng) const {
+    if (rows == nullptr || size <= 1) return -1;
     int j = rng.randbelow(size - 1);
     j += j >= pos;
     j += start;
     while (ld_acquire(prog + j) < gen) __nanosleep(256);
-    return rows + (size_t)j * n;
+    return j;
+  }
+  template <class R>
+  __device__ __forceinline__ const short* pick(R& rng) const {
+    const int j = pick_index(rng);
+    return j < 0 ? nullptr : rows + (size_t)j * n;
   }
 };
 

@@ -71,8 +71,11 @@ struct MatFull {
   int use_s;       // 1: read through ld.shared at sbase
   __device__ __forceinline__ Val operator()(int a, int b) const {
     if (GLOBAL) return (Val)__ldg(m + a * n + b);
-    if (use_s) return (Val)LdShared<E>::load(sbase + (unsigned)(a * n + b) * (unsigned)sizeof(E));
+    if (use_s) return smem(a, b);
     return (Val)m[a * n + b];
+  }
+  __device__ __forceinline__ Val smem(int a, int b) const {
+    return (Val)LdShared<E>::load(sbase + (unsigned)(a * n + b) * (unsigned)sizeof(E));
   }
   static __host__ __device__ long long bytes(int n) { return (long long)n * n * sizeof(E); }
 };
@@ -99,10 +102,28 @@ struct MatTri {
     else v = (Val)m[a == b ? 0 : idx];
     return a == b ? (Val)0 : v;
   }
+  __device__ __forceinline__ Val smem(int a, int b) const {
+    const int lo = a < b ? a : b, hi = a ^ b ^ lo;
+    const int idx = ((lo * (2 * n - lo - 1)) >> 1) + (hi - lo - 1);
+    const Val v = (Val)LdShared<E>::load(sbase + (unsigned)(a == b ? 0 : idx) * (unsigned)sizeof(E));
+    return a == b ? (Val)0 : v;
+  }
   static __host__ __device__ long long bytes(int n) {
     return (long long)n * (n - 1) / 2 * sizeof(E);
   }
 };
+
+// The evolve kernel's view of a matrix it has staged into shared memory (every
+// layout but the *_G ones): one ld.shared path per distance read instead of a
+// runtime choice between shared and global code at every call site.
+template <class D, bool S = D::kInSmem>
+struct StagedView : D {
+  __device__ __forceinline__ typename D::Val operator()(int a, int b) const {
+    return D::smem(a, b);
+  }
+};
+template <class D>
+struct StagedView<D, false> : D {};
 
 typedef MatFull<short, false> DistI16Full;
 typedef MatTri<short> DistI16Tri;

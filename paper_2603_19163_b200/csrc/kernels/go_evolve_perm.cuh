@@ -58,6 +58,7 @@ struct TeamShared {  // (row kernels: go_evolve_row.cuh)
 struct PermTeam {
   int accept;
   int dnext;                       // next deferred request to hand out (dynamic, per warp)
+  int rnext;                       // next cooperative relocation / sampled-probe request
   int nreq;                        // pending cooperative relocations this step
   int ndreq;                       // pending deferred whole-row operators this step
   int ngr;                         // ... of which guided rebuilds (queued from the back)
@@ -374,6 +375,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         ts->ndreq = 0;
         ts->ngr = 0;
         ts->dnext = 0;
+        ts->rnext = 0;
       }
       // exclusive scan of per-sequence totals in sort order (each warp redundantly)
       int tj = 0;
@@ -461,11 +463,16 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       team_bar(team, TS);
       GO_TICK(3 + 4 * s);
 
-      // ---- cooperative relocations: one warp per request, 32 slots per step
+      // ---- cooperative best-slot relocations: one warp per request (32
+      //      slots per step), handed out as warps free up
       const int nreq = ts->nreq;
       if (nreq > 0) {
 #pragma unroll 1
-        for (int r = warp; r < nreq; r += nwarps) {
+        for (;;) {
+          int r = 0;
+          if (wl == 0) r = atomicAdd(&ts->rnext, 1);
+          r = __shfl_sync(0xffffffffu, r, 0);
+          if (r >= nreq) break;
           const int L = la.req[r];
           const u32 meta = la.meta[L];
           const int nm = meta_nm(meta);
@@ -488,7 +495,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           int bp = 0x7fffffff;
           int carry = C.at(m - 1 < st ? m - 1 : m - 1 + len);  // rest[m-1] = prev of slot 0
           Scan carry_b = pol.cost_scan(l, carry);
-#pragma unroll 2
+#pragma unroll 1
           for (int p0 = 0; p0 < m; p0 += 32) {
             const int p = p0 + wl;
             const bool in = p < m;

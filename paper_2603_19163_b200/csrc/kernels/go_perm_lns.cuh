@@ -40,6 +40,14 @@ __device__ __forceinline__ typename Policy::Acc perm_row_length(const Policy& po
   return s;
 }
 
+// random.sample(range(total), m) on a lane stream, one out-of-line copy for
+// the scatter shuffle and guided rebuild (code size: both inline it otherwise)
+__device__ __noinline__ Stream sample_range_stream(Stream rng, int total, int m, int* picks,
+                                                   int* ovi, int* ovv) {
+  sample_range_buf(rng, total, m, picks, ovi, ovv);
+  return rng;
+}
+
 template <class Acc>
 struct DeferRes {
   int changed;
@@ -81,9 +89,9 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
   int a0 = 0, a1 = 0, a2 = 0, live = 0;
   if (wl == 0) {
     if (kind == SEQ_OX) {
-      const short* mate = ms->pick(*rng);
-      if (mate != nullptr && n >= 2) {
-        a0 = (int)((mate - ms->rows) / n);  // mate evolver
+      const int mj = ms->pick_index(*rng);
+      if (mj >= 0 && n >= 2) {
+        a0 = mj;  // mate evolver
         int c1 = rng->randbelow(n), c2 = rng->randbelow(n);
         if (c1 > c2) {
           const int t = c1;
@@ -122,7 +130,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     const int nwords = (n + 31) >> 5;
     for (int i = wl; i < nwords; i += 32) mask[i] = 0u;
     if (staged) {
-#pragma unroll 8
+#pragma unroll 4
       for (int t = wl; t < n; t += 32) {
         int src = s0 + t;
         src = src >= n ? src - n : src;
@@ -155,7 +163,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     // the child read cyclically from c2+1 is F ++ S
     int filled = 0, f_first = -1, f_last = -1;
     const unsigned lt = (1u << wl) - 1u;
-#pragma unroll 2
+#pragma unroll 1
     for (int b = 0; b < n; b += 32) {
       const int t = b + wl;
       int v = 0;
@@ -211,7 +219,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     // then both shuffles permute the parent in place in wrow
     const int m = ls < n ? ls : n;
     if (kind == SEQ_SCATTER_SHUFFLE && wl == 0)
-      sample_range_buf(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
+      *rng = sample_range_stream(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
     __syncwarp();
     for (int p = wl; p < n; p += 32) wrow[p] = (i16)C.at(p);
     __syncwarp();
@@ -248,7 +256,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
   // chunks in flight) plus one rotation of the span between its old and new
   // slot.  Lane t tracks the position of taken value t.
   const int m = ls < n - 1 ? ls : n - 1;
-  if (wl == 0) sample_range_buf(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
+  if (wl == 0) *rng = sample_range_stream(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
   __syncwarp();
   // sorted by (r, -p): descending positions; picks are distinct, so a pick's
   // rank is the number of larger picks

@@ -8,12 +8,12 @@ namespace go {
 
 template <class D, class Custom>
 __device__ __forceinline__ void tsp_evolve_entry(const EvolveArgs& a) {
-  TspPolicy<D> pol;
+  TspPolicy<StagedView<D>> pol;  // shared-memory layouts are always staged (evolve_perm)
   pol.d.m = (const typename D::Elem*)a.inst;
   pol.d.n = a.n;
   pol.d.sbase = 0;
   pol.d.use_s = 0;
-  evolve_perm<TspPolicy<D>, Custom>(a, pol);
+  evolve_perm<TspPolicy<StagedView<D>>, Custom>(a, pol);
 }
 
 // evaluate() for m tours (problems.py:77-94 -> builtins.py:67-71)

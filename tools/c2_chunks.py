@@ -14,8 +14,11 @@ from paper_2603_19163_b200 import instances as I  # noqa: E402
 
 def make(name):
     if name == "C2":
+        import os
         d, _ = I.tsp_lattice()
-        return G.builtin_problem("tsp", G.InstanceData(distance_matrix=d)), G.tsp_delta_operators()
+        coop = os.environ.get("GO_DEMO_LOOPS", "0") != "1"  # per-lane loop snippets when set
+        return (G.builtin_problem("tsp", G.InstanceData(distance_matrix=d)),
+                G.tsp_delta_operators(cooperative=coop))
     from tools.op_cost import problems  # noqa: E402
     return problems()[name](), ()
 
