@@ -87,9 +87,10 @@ class ClockSampler:
 
 
 def ncu_traffic():
-    """DRAM bytes per evolve launch from the committed ncu --set full capture
-    (profiles/r01_ncu_traffic.json), or None."""
-    p = ROOT / "profiles" / "r01_ncu_traffic.json"
+    """DRAM bytes per evolve launch of the current kernel from its committed ncu
+    --set full capture (profiles/r02_ncu_traffic.json, written by
+    tools/ncu_traffic.py from the .ncu-rep of the same head), or None."""
+    p = ROOT / "profiles" / "r02_ncu_traffic.json"
     try:
         return json.loads(p.read_text())["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):

@@ -307,7 +307,7 @@ int jit_build_user(const UserProblemSrc& up, JitModule* out, std::string* log) {
         << "(Ctx& ctx, const Data& data) {\n#line 1 \"@OPDIR@/" << up.ops[i].name << ".cuh\"\n"
         << up.ops[i].body << "\n}\n";
   src << "}  // namespace user\n"
-      << "struct UserProblem {\n"
+      << "struct UserProblem {\n  static constexpr bool kHasOps = true;\n"
       << "  template <class C> __device__ __forceinline__ static void op(int slot, C& ctx, "
          "const unsigned char* b) {\n"
       << "    const user::Data data = user::make_data(b);\n    (void)data;\n    switch (slot) {\n";
@@ -371,7 +371,7 @@ int jit_build_rowops(const RowOpsSrc& ro, const std::vector<UserOpSrc>& ops, Jit
         << "(Ctx& ctx) {\n#line 1 \"@OPDIR@/" << ops[i].name << ".cuh\"\n" << ops[i].body
         << "\n}\n";
   src << "}  // namespace user\n"
-      << "struct RowUserOps : NoUser {\n"
+      << "struct RowUserOps : NoUser {\n  static constexpr bool kHasOps = true;\n"
       << "  template <class C> __device__ __forceinline__ static void op(int slot, C& ctx, "
          "const unsigned char*) {\n    switch (slot) {\n";
   for (size_t i = 0; i < ops.size(); ++i)

@@ -343,7 +343,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     // ---- A: every lane draws k and its first sequence (identity mapping) ----
     if (lane < T) {
       Stream rng;
-      rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)lane, 0));
+      rng.init(mix64_5_ool(A.seed, (u64)evg, (u64)g, (u64)lane, 0));
       const int k = sample_k(kw, rng);
       const int s0 = sample_seq(s_cum, nseq, total, rng);
       la.pos[lane] = rng.tell();
@@ -406,7 +406,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       if (lane < active) {
         const int L = la.order[lane];
         Stream rng;
-        rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+        rng.init(mix64_5_ool(A.seed, (u64)evg, (u64)g, (u64)L, 0));
         rng.seek(la.pos[L]);
         const u32 meta = la.meta[L];
         const int k = meta_k(meta);
@@ -546,7 +546,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
             int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
             if (s + 1 < k) {  // continue the lane's stream after its operator's draws
               Stream rng;
-              rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+              rng.init(mix64_5_ool(A.seed, (u64)evg, (u64)g, (u64)L, 0));
               rng.seek(la.pos[L]);
               const int nq = sample_seq(s_cum, nseq, total, rng);
               if (s == 0) q1 = nq; else q2 = nq;
@@ -580,7 +580,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
           const int nsel = (meta & META_MAT) && !(meta & META_SEL) ? 1 : 0;
           i16* dst = lrow + ((size_t)L * 2 + nsel) * n;
           Stream rng;
-          rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+          rng.init(mix64_5_ool(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
 #ifdef GO_PHASE_TIMING
           const unsigned long long t_op = clock64();
@@ -645,7 +645,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       int acc = bdd < 0.0;
       if (!acc && temp > 0.0) {
         Stream ar;
-        ar.init(mix64_5(A.seed, (u64)evg, (u64)g, 0, 1));
+        ar.init(mix64_5_ool(A.seed, (u64)evg, (u64)g, 0, 1));
         acc = ar.random() < exp(-bdd / temp);
       }
       ts->accept = acc;

@@ -56,7 +56,16 @@ struct InsSol {  // v moved from slot q0 to slot pos of the row block [off, off 
   __device__ __forceinline__ int size() const { return n; }
 };
 
+// lane / accept stream keys of the row kernels: out of line for the partition
+// kernel (large, instruction-cache bound: C3 -14 % per chunk), inline for the
+// others (QAP / knapsack: +4-8 % with a call per draw site)
+template <int KIND>
+__device__ __forceinline__ u64 row_key_k(u64 a, u64 b, u64 c, u64 d, u64 e) {
+  return KIND == RK_PART ? mix64_5_ool(a, b, c, d, e) : mix64_5(a, b, c, d, e);
+}
+
 struct NoUser {  // built-in kinds: never called
+  static constexpr bool kHasOps = false;  // user operator slots compiled in
   template <class S>
   __device__ __forceinline__ static double obj(const S&, const unsigned char*) { return 0.0; }
   template <class S>
@@ -339,12 +348,18 @@ struct RowLaneState {
 
 struct RowSmem {
   static __host__ __device__ unsigned align(unsigned x, unsigned a) { return (x + a - 1) / a * a; }
-  static __host__ __device__ unsigned row_stride(int n, int gsize) { return align((unsigned)(n * gsize), 16); }
+  // lane-row stride: an ODD number of 4-byte words, so the lanes of a warp
+  // reading position j of their own rows hit 32 different banks (a 16-byte
+  // aligned stride is a multiple of 4 words: 4-way conflicts on every such read)
+  static __host__ __device__ unsigned row_stride(int n, int gsize) {
+    const unsigned w = (unsigned)(n * gsize + 3) / 4;
+    return 4u * (w | 1u);
+  }
   // rows_smem: the T lane rows live in shared memory after the current row;
   // otherwise (long rows) they live in global memory (EvolveArgs::lane_rows)
   static __host__ __device__ unsigned team_bytes(int n, int gsize, int TS, int scratch_per_lane,
                                                  bool rows_smem = true) {
-    return align(row_stride(n, gsize) * (rows_smem ? TS + 1 : 1) + RowLaneState::bytes(TS) +
+    return align(align(row_stride(n, gsize) * (rows_smem ? TS + 1 : 1), 16) + RowLaneState::bytes(TS) +
                      (unsigned)sizeof(TeamShared<double>) + (unsigned)(scratch_per_lane * TS),
                  16);
   }
@@ -1464,7 +1479,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
   // the opt-in shared memory) this team's slice of the global lane_rows buffer
   constexpr bool rows_g = RG;
   unsigned char* rows = rows_g ? (unsigned char*)A.lane_rows + (size_t)ev * TS * rs : tb + rs;
-  unsigned char* lst = tb + rs * (rows_g ? 1 : TS + 1);
+  unsigned char* lst = tb + RowSmem::align(rs * (rows_g ? 1 : TS + 1), 16);
   RowLaneState la;
   la.bind(lst, TS);
   TeamShared<double>* ts =
@@ -1548,16 +1563,16 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
 
     // ---- A: copy the current row into every lane row; draw k and sequence 0
     {
-      const int words = (int)(rs / 16);
-      const int4* src = (const int4*)cur;
+      const int words = (int)(rs / 4);
+      const int* src = (const int*)cur;
       for (int idx = lane; idx < T * words; idx += TS) {
         const int L = idx / words, w = idx - L * words;
-        ((int4*)(rows + (size_t)L * rs))[w] = src[w];
+        ((int*)(rows + (size_t)L * rs))[w] = src[w];
       }
     }
     if (lane < T) {
       Stream rng;
-      rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)lane, 0));
+      rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)lane, 0));
       const int k = sample_k(kw, rng);
       const int s0 = sample_seq(s_cum, nseq, total, rng);
       la.pos[lane] = rng.tell();
@@ -1608,7 +1623,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       if (lane < active) {
         const int L = la.order[lane];
         Stream rng;
-        rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+        rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
         rng.seek(la.pos[L]);
         const u32 meta = la.meta[L];
         const int k = meta_k(meta);
@@ -1630,9 +1645,11 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
             la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
             pending = true;
-          } else if (kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
-            PartOpCtx<U> oc{&c, pv, &X, pwt, X.n_cells, X.d1, X.d2};
-            U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
+          } else if (U::kHasOps && kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+            if constexpr (U::kHasOps) {
+              PartOpCtx<U> oc{&c, pv, &X, pwt, X.n_cells, X.d1, X.d2};
+              U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
+            }
           } else {
             run_part_op(kind, c);
           }
@@ -1667,7 +1684,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           } else if (kind == SEQ_UNIFORM_X) {  // warp-resolved below
             la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
             pending = true;
-          } else if (kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+          } else if (U::kHasOps && kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+            if constexpr (U::kHasOps) {
             RowInst ri{inst, X.off1, KIND == RK_QAP ? RI_QAP : (KIND == RK_KNAP ? RI_KNAP :
                                                                  (KIND == RK_JSP ? RI_JSP : RI_NONE)),
                        KIND == RK_QAP ? (int)sizeof(E) : 8, n, X.capacity, n};
@@ -1675,6 +1693,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
                               n, c.d1, X.d2, ri};
             U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
             c.mark_all();
+            }
           } else {
             run_row_op(kind, c);
           }
@@ -1700,7 +1719,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         for (int r = warp; r < nux; r += nwarps) {
           const int L = la.uxreq[r];
           Stream rng;
-          rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+          rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
           int lo, hi;
           const u32 pend = warp_uniform_x((G*)(rows + (size_t)L * rs), n, ms, rng, wl, lo, hi);
@@ -1739,7 +1758,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           G* lrow = (G*)(rows + (size_t)L * rs);
           if (lane == 0) {
             Stream rng;
-            rng.init(mix64_5(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+            rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
             rng.seek(la.pos[L]);
             // MULTI_FIXED permutation rows: home_row = randrange(d1) (operators.py:519-521)
             gsh.row() = (KIND == RK_USER && X.mf == 1) ? rng.randbelow(X.d1) : 0;
@@ -1876,7 +1895,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       int acc = bd < 0.0;
       if (!acc && temp > 0.0) {
         Stream ar;
-        ar.init(mix64_5(A.seed, (u64)evg, (u64)g, 0, 1));
+        ar.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, 0, 1));
         acc = ar.random() < exp(-bd / temp);
       }
       ts->accept = acc;
@@ -1895,8 +1914,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     }
     team_bar(team, TS);
     if (ts->accept) {
-      const int4* src = (const int4*)(rows + (size_t)bl * rs);
-      for (int w = lane; w < (int)(rs / 16); w += TS) ((int4*)cur)[w] = src[w];
+      const int* src = (const int*)(rows + (size_t)bl * rs);
+      for (int w = lane; w < (int)(rs / 4); w += TS) ((int*)cur)[w] = src[w];
       scal = la.nscal[bl];
       pen = la.npen[bl];
       V = la.aux0[bl];

@@ -187,10 +187,14 @@ __device__ __noinline__ DeltaOut<typename D::Acc> tsp_move_delta_ool(const D d, 
   int so[4], sn[4], no, nn;
   move_slots(mv, n, so, no, sn, nn);
   Acc delta = 0;
+  // one copy of each loop body (code size: move_src is a switch over every
+  // move kind and would be inlined once per unrolled slot)
+#pragma unroll 1
   for (int i = 0; i < no; ++i) {
     const int p = so[i], q = p + 1 == n ? 0 : p + 1;
     delta -= (Acc)d(L.at(p), L.at(q));
   }
+#pragma unroll 1
   for (int i = 0; i < nn; ++i) {
     const int p = sn[i], q = p + 1 == n ? 0 : p + 1;
     delta += (Acc)d(L.at_after(mv, p), L.at_after(mv, q));

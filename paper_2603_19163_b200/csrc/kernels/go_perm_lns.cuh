@@ -28,12 +28,13 @@ __device__ __forceinline__ bool perm_deferred(int kind) {
          kind == SEQ_GUIDED_REBUILD;
 }
 
-// exact tour length of a materialised row (whole warp)
+// exact tour length of a materialised row (whole warp; one out-of-line copy)
 template <class Policy>
-__device__ __forceinline__ typename Policy::Acc perm_row_length(const Policy& pol, const i16* row,
-                                                                int n, int wl) {
+__device__ __noinline__ typename Policy::Acc perm_row_length(const Policy pol, const i16* row,
+                                                             int n, int wl) {
   typedef typename Policy::Acc Acc;
   Acc s = 0;
+#pragma unroll 1
   for (int p = wl; p < n; p += 32) s += pol.cost_acc(row[p], row[p + 1 == n ? 0 : p + 1]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -128,6 +129,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
 #endif
     unsigned* mask = staged ? (unsigned*)wint : (unsigned*)wrow;
     const int nwords = (n + 31) >> 5;
+#pragma unroll 1
     for (int i = wl; i < nwords; i += 32) mask[i] = 0u;
     if (staged) {
 #pragma unroll 4
@@ -221,6 +223,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     if (kind == SEQ_SCATTER_SHUFFLE && wl == 0)
       *rng = sample_range_stream(*rng, n, m, wint, (int*)wrow, (int*)wrow + m);
     __syncwarp();
+#pragma unroll 1
     for (int p = wl; p < n; p += 32) wrow[p] = (i16)C.at(p);
     __syncwarp();
     if (wl == 0) {
@@ -244,6 +247,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
       }
     }
     __syncwarp();
+#pragma unroll 1
     for (int p = wl; p < n; p += 32) dst[p] = wrow[p];
     out.len = perm_row_length(pol, wrow, n, wl);
     return out;
@@ -352,6 +356,7 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     if (wl == t) mypos = bp;
     __syncwarp();
   }
+#pragma unroll 1
   for (int p = wl; p < n; p += 32) dst[p] = aux[p];
   out.len = perm_row_length(pol, aux, n, wl);
   return out;
