@@ -197,3 +197,11 @@ def device_info(device: int = 0) -> DeviceInfo:
     info = DeviceInfo()
     check(lib.go_device_query(device, C.byref(info)))
     return info
+
+
+def device_count() -> int:
+    """CUDA devices visible to the engine (raises NativeUnavailable on none)."""
+    lib = load()
+    n = C.c_int(0)
+    check(lib.go_device_count(C.byref(n)))
+    return n.value

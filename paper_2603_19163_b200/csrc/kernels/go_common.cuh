@@ -383,6 +383,7 @@ __device__ __forceinline__ void snap_publish(short* snap, int* prog, int P, int 
   }
   team_bar(team, nthreads);
   short* dst = snap + ((size_t)(gnext % SNAP_DEPTH) * P + ev) * n;
+#pragma unroll 1
   for (int p = lane; p < n; p += nthreads) dst[p] = (short)cur[p];
   team_bar(team, nthreads);
   if (lane == 0) {

@@ -247,6 +247,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     // warp runs its lane groups one after another (SIMT), and the step waits
     // for its slowest warp
     int nu = 0;
+    #pragma unroll 1
     for (int i = 0; i < nseq; ++i) nu += R->kind[i] >= SEQ_CUSTOM_BASE;
     const int nb = nseq - nu;
     int j = 0, bi = 0, ui = 0;
@@ -291,6 +292,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   LaneArrays<Acc> la;
   la.bind(tb + PermSmem::lanes_off<Acc>(n, TS), TS);
 
+  #pragma unroll 1
   for (int p = lane; p < n; p += TS) cur[p] = A.genes[(size_t)ev * n + p];
   // lane-private global rows of deferred whole-row operators (2 per lane)
   i16* const lrow = A.lane_rows ? A.lane_rows + (size_t)ev * T * 2 * n : nullptr;
@@ -381,6 +383,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       int tj = 0;
       if (wl < nseq) {
         const int q = s_gord[wl];
+        #pragma unroll 1
         for (int w = 0; w < nwarps; ++w) tj += wa.cnt[w * MAX_SEQ + q];
       }
       int incl = tj;
@@ -393,6 +396,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       const int my_pos = hold_seq != 31 ? s_grank[hold_seq] : 0;
       int base = __shfl_sync(0xffffffffu, incl - tj, my_pos);
       if (hold_seq != 31) {
+        #pragma unroll 1
         for (int w = 0; w < warp; ++w) base += wa.cnt[w * MAX_SEQ + hold_seq];
         la.order[base + rank] = (unsigned short)lane;
       }
@@ -683,6 +687,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     if (A.snap && gi + 1 < A.ngen)
       snap_publish(A.snap, A.prog, A.P, ev, n, (int)g + 1, cur, snap_min, lane, team, TS);
     if (strictly_better(0.0, phi, bpen, bscal) && !target_reached(A, bpen, bscal)) {  // team best-ever, first occurrence
+      #pragma unroll 1
       for (int p = lane; p < n; p += TS) A.best_genes[(size_t)ev * n + p] = cur[p];
       bscal = phi;
       bpen = 0.0;
@@ -697,6 +702,7 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
   if (lane == 0)
     for (int i = 0; i < 16; ++i) atomicAdd(&A.gs->prof[i], prof[i]);
 #endif
+  #pragma unroll 1
   for (int p = lane; p < n; p += TS) A.genes[(size_t)ev * n + p] = cur[p];
   for (int i = lane; i < MAX_SEQ; i += TS) {
     A.usage[ev * MAX_SEQ + i] = ts->usage[i];

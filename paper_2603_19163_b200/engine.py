@@ -684,14 +684,37 @@ def run(problem: ProblemDefinition, config: EngineConfig,
         return run_distributed(problem, config, best_known)
     if config.replicas == 1:
         return _run_single(problem, config, config.seed, best_known)
-    results = [_run_single(problem, config, config.seed + i, best_known)
-               for i in range(config.replicas)]
+    results = _run_replicas(problem, config, best_known)
     cfg = problem.config()
     best = results[0]
     for r in results[1:]:
         if compare(r.best, best.best, cfg) == A_BETTER:
             best = r
     return best
+
+
+def _run_replicas(problem, config: EngineConfig, best_known) -> list:
+    """The paper's multi-GPU mode (reference replicas,
+    engine.py:605-614): replica i runs the whole pipeline with seed + i.  With
+    several GPUs visible the replicas are spread over them (replica i on device
+    (config.device + i) mod count, each device running its replicas in order,
+    devices concurrently — the C ABI releases the GIL); results do not depend
+    on the placement."""
+    from dataclasses import replace as _replace
+    count = max(1, N.device_count())
+    ndev = min(config.replicas, count)
+    if ndev == 1:
+        return [_run_single(problem, config, config.seed + i, best_known)
+                for i in range(config.replicas)]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def on_device(d):
+        dcfg = _replace(config, device=(config.device + d) % count)
+        return [(i, _run_single(problem, dcfg, config.seed + i, best_known))
+                for i in range(d, config.replicas, ndev)]
+    with ThreadPoolExecutor(max_workers=ndev) as ex:
+        parts = list(ex.map(on_device, range(ndev)))
+    return [r for _, r in sorted((x for p in parts for x in p), key=lambda t: t[0])]
 
 
 class DeviceRun:

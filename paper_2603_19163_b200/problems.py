@@ -82,8 +82,8 @@ class ProblemDefinition:
         return sum(m.nbytes for m in self.init_matrices())
 
     # -- device plumbing -------------------------------------------------------
-    _handle = None
-    _handle_device = None
+    # one native problem handle per device (replicas may run on several GPUs)
+    _handles = None
     #: built-in sequence ids the device kernel for this problem implements
     DEVICE_SEQUENCES: tuple = ()
 
@@ -96,25 +96,34 @@ class ProblemDefinition:
             "built-in problems (and NVRTC objectives) only; Python callbacks are not a "
             "supported path")
 
+    def _cached_handle(self, device: int):
+        if self._handles is None:
+            self._handles = {}
+        return self._handles.get(device)
+
+    def _store_handle(self, device: int, h, keep):
+        self._handles[device] = h
+        self._keepalive = getattr(self, "_keepalive", {})
+        self._keepalive[device] = keep
+
     def device_handle(self, device: int = 0):
-        if self._handle is not None and self._handle_device == device:
-            return self._handle
+        h = self._cached_handle(device)
+        if h is not None:
+            return h
         lib = N.load()
         desc, keep = self._native_desc()
         h = C.c_void_p()
         N.check(lib.go_problem_create(C.byref(desc), device, C.byref(h)))
-        self._keepalive = keep
-        self._handle = h
-        self._handle_device = device
+        self._store_handle(device, h, keep)
         return h
 
     def __del__(self):
-        h = getattr(self, "_handle", None)
-        if h is not None and N._lib is not None:
-            try:
-                N._lib.go_problem_destroy(h)
-            except Exception:  # noqa: BLE001
-                pass
+        for h in (getattr(self, "_handles", None) or {}).values():
+            if N._lib is not None:
+                try:
+                    N._lib.go_problem_destroy(h)
+                except Exception:  # noqa: BLE001
+                    pass
 
 
 def check_distance_matrix(d, symmetric: bool = True) -> np.ndarray:
@@ -581,8 +590,9 @@ class CudaProblem(ProblemDefinition):
         return self._SEQS[self.encoding]
 
     def device_handle(self, device: int = 0):
-        if self._handle is not None and self._handle_device == device:
-            return self._handle
+        h = self._cached_handle(device)
+        if h is not None:
+            return h
         lib = N.load()
         names = list(self.data)
         arrays = [self.data[k] for k in names]
@@ -599,9 +609,7 @@ class CudaProblem(ProblemDefinition):
         h = C.c_void_p()
         log = C.create_string_buffer(8192)
         N.check(lib.go_problem_create_user(C.byref(desc), device, C.byref(h), log, len(log)))
-        self._keepalive = (arrays, c_names, c_ptrs, c_lens)
-        self._handle = h
-        self._handle_device = device
+        self._store_handle(device, h, (arrays, c_names, c_ptrs, c_lens))
         return h
 
 

@@ -152,3 +152,16 @@ def test_target_stop_mid_chunk_returns_genes_of_that_generation(kind):
     G.evaluate(prob, check)
     assert check.objectives[0] == r.objectives[0] and check.penalty == r.penalty
     assert r.history["best_phi"][-1] == hist[g - 1]
+
+
+@pytest.mark.gpu
+def test_replicas_spread_over_devices_match_sequential_replicas():
+    """Replicas (engine.py:605-614) are placed round-robin over the visible GPUs
+    and run concurrently; the returned comparison-best must not depend on the
+    placement: it equals the best of the single-seed runs."""
+    prob = G.builtin_problem("tsp", G.InstanceData(distance_matrix=I.tsp_random(30, 5)))
+    base = dict(population=6, team_size=32, max_generations=40, seed=17)
+    r = G.run(prob, G.EngineConfig(**base, replicas=3))
+    singles = [G.run(prob, G.EngineConfig(**{**base, "seed": 17 + i})) for i in range(3)]
+    best = min(singles, key=lambda x: (x.penalty, x.objectives[0]))
+    assert r.objectives == best.objectives and r.best.row(0).tolist() == best.best.row(0).tolist()
