@@ -292,27 +292,41 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     Acc best = 0;
     int bp = 0x7fffffff;
     int carry = last;  // element before slot 0 (cyclic)
+    // d(prev, v) of slot p is d(v, next) of slot p-1 (symmetric matrices,
+    // problems.py:97-107): two matrix reads per slot instead of three
+    Acc carry_b = pol.cost_acc(v, last);
     for (int b = 0; b < n; b += 64) {  // two chunks in flight
       const int p0 = b + wl, p1 = b + 32 + wl;
       const int e0 = p0 < sz ? rv(p0) : first;
       const int e1 = p1 < sz ? rv(p1) : first;
+      const Acc b0 = pol.cost_acc(v, e0), b1 = pol.cost_acc(v, e1);
       int pv0 = __shfl_up_sync(FULL, e0, 1);
       int pv1 = __shfl_up_sync(FULL, e1, 1);
+      Acc a0 = __shfl_up_sync(FULL, b0, 1);
+      Acc a1 = __shfl_up_sync(FULL, b1, 1);
       const int e0_31 = __shfl_sync(FULL, e0, 31);
+      const Acc b0_31 = __shfl_sync(FULL, b0, 31);
       if (wl == 0) {
         pv0 = carry;
         pv1 = e0_31;
+        a0 = carry_b;
+        a1 = b0_31;
       }
       carry = __shfl_sync(FULL, e1, 31);
-      if (p0 < n) {
-        const Acc sc = pol.insertion(pv0, v, v, e0);
+      carry_b = __shfl_sync(FULL, b1, 31);
+      if (p0 < n) {  // the reference's float64 order: (d(prev,v) + d(v,next)) - d(prev,next)
+        const Acc c0 = pol.cost_acc(pv0, e0);
+        const Acc sc = Policy::kIntegral ? a0 + b0 - c0
+                                         : (Acc)(((double)a0 + (double)b0) - (double)c0);
         if (bp == 0x7fffffff || sc < best) {
           best = sc;
           bp = p0;
         }
       }
       if (p1 < n) {
-        const Acc sc = pol.insertion(pv1, v, v, e1);
+        const Acc c1 = pol.cost_acc(pv1, e1);
+        const Acc sc = Policy::kIntegral ? a1 + b1 - c1
+                                         : (Acc)(((double)a1 + (double)b1) - (double)c1);
         if (bp == 0x7fffffff || sc < best) {
           best = sc;
           bp = p1;
