@@ -916,12 +916,18 @@ __device__ void team_gr_user_cells(G* row, int n, const GrShared& g, const UserS
 // Warp-cooperative decode state (lane j owns job j and machine j).
 struct JspWarp {
   int nx, jf, mfr, pr, pn, span, step;  // pn: priority of the op after the head
+  int mh, dh, mh2, dh2;                 // machine / duration of the head op and of the next
 };
 
 // Runs steps of the fast-path decode from `st` until every operation is
 // scheduled, or (stop_job >= 0) until job stop_job's next operation index
 // becomes stop_k (that operation is then a candidate and its priority matters).
-// Priority of operation ovp is ovv.
+// Priority of operation ovp is ovv.  Every lane computes the completion time its
+// head operation would have if chosen (its job's finish vs its machine's, read
+// from the machine's lane) while the warp reduces the keys, so a step is one
+// min-reduction and one shuffle of the winner's time instead of reduction ->
+// operation load -> two shuffles; machines and durations of each job's next
+// two operations are prefetched into registers.
 template <class G>
 __device__ __forceinline__ void jsp_warp_run(const JspView& J, const G* prio, int ovp, int ovv,
                                              int wl, JspWarp& st, int stop_job, int stop_k) {
@@ -930,23 +936,28 @@ __device__ __forceinline__ void jsp_warp_run(const JspView& J, const G* prio, in
   const int n_ops = J.n_jobs * pj;
   for (; st.step < n_ops; ++st.step) {
     if (stop_job >= 0 && __shfl_sync(0xffffffffu, st.nx, stop_job) == stop_k) return;
-    const unsigned key = mine && st.nx < pj
-                             ? ((unsigned)st.pr << 16) | ((unsigned)wl << 8) | (unsigned)st.nx
-                             : 0xFFFFFFFFu;
+    const bool live = mine && st.nx < pj;
+    const unsigned key = live ? ((unsigned)st.pr << 16) | ((unsigned)wl << 8) | (unsigned)st.nx
+                              : 0xFFFFFFFFu;
+    const int mfm = __shfl_sync(0xffffffffu, st.mfr, st.mh & 31);
+    const int cand = (st.jf > mfm ? st.jf : mfm) + st.dh;
     const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
     const int j = (int)((kmin >> 8) & 0xFFu);
-    const int op = j * pj + (int)(kmin & 0xFFu);
-    const int m = J.mach[op], du = J.dur[op];
-    const int mfm = __shfl_sync(0xffffffffu, st.mfr, m);
-    const int jfo = __shfl_sync(0xffffffffu, st.jf, j);
-    const int done = (jfo > mfm ? jfo : mfm) + du;
+    const int done = __shfl_sync(0xffffffffu, cand, j);
+    const int m = __shfl_sync(0xffffffffu, st.mh, j);
     if (wl == m) st.mfr = done;
     if (wl == j) {
       st.jf = done;
       ++st.nx;
       st.pr = st.pn;  // prefetched priority of the new head
-      const int o2 = op + 2;  // and the one after it, off the critical path
-      if (st.nx + 1 < pj) st.pn = o2 == ovp ? ovv : (int)prio[o2];
+      st.mh = st.mh2;
+      st.dh = st.dh2;
+      const int o2 = j * pj + st.nx + 1;  // and the one after it, off the critical path
+      if (st.nx + 1 < pj) {
+        st.pn = o2 == ovp ? ovv : (int)prio[o2];
+        st.mh2 = J.mach[o2];
+        st.dh2 = J.dur[o2];
+      }
     }
     st.span = done > st.span ? done : st.span;
   }
@@ -957,9 +968,18 @@ __device__ __forceinline__ JspWarp jsp_warp_start(const JspView& J, const G* pri
                                                   int ovv, int wl) {
   JspWarp st;
   st.nx = st.jf = st.mfr = st.span = st.step = 0;
+  st.mh = st.dh = st.mh2 = st.dh2 = 0;
   const int op0 = wl * J.per_job;
   st.pr = wl < J.n_jobs ? (op0 == ovp ? ovv : (int)prio[op0]) : 0;
   st.pn = wl < J.n_jobs && J.per_job > 1 ? (op0 + 1 == ovp ? ovv : (int)prio[op0 + 1]) : 0;
+  if (wl < J.n_jobs) {
+    st.mh = J.mach[op0];
+    st.dh = J.dur[op0];
+    if (J.per_job > 1) {
+      st.mh2 = J.mach[op0 + 1];
+      st.dh2 = J.dur[op0 + 1];
+    }
+  }
   return st;
 }
 
