@@ -408,7 +408,10 @@ __device__ __forceinline__ double qap_delta(const QapView<E>& q, const G* cur, c
     rd += 3u * (unsigned)(n * n);
     return (double)d;
   }
-  // pairs with i touched
+  // pairs with i touched.  The range loops stay rolled (lo / hi indexed from
+  // local memory once per range): unrolled over MAX_RANGES they multiplied the
+  // inner loops into half of the QAP kernel's instructions.
+#pragma unroll 1
   for (int r = 0; r < nm; ++r)
     for (int i = lo[r]; i < hi[r]; ++i) {
       const int pi = row[i], ci = cur[i];
@@ -417,10 +420,12 @@ __device__ __forceinline__ double qap_delta(const QapView<E>& q, const G* cur, c
     }
   // pairs with only j touched
   int gap_lo = 0;
+#pragma unroll 1
   for (int r = 0; r <= nm; ++r) {
     const int gap_hi = r < nm ? lo[r] : n;
     for (int i = gap_lo; i < gap_hi; ++i) {
       const int ci = cur[i];
+#pragma unroll 1
       for (int s = 0; s < nm; ++s)
         for (int j = lo[s]; j < hi[s]; ++j) d += q.F(i, j) * (q.D(ci, row[j]) - q.D(ci, cur[j]));
     }
@@ -445,6 +450,7 @@ __device__ __forceinline__ void knap_delta(const KnapView& k, const G* cur, cons
     }
     return;
   }
+#pragma unroll 1
   for (int r = 0; r < nm; ++r)
     for (int p = lo[r]; p < hi[r]; ++p) {
       const double x = (double)((int)row[p] - (int)cur[p]);
@@ -1322,7 +1328,12 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       double dist, pen;
       int veh;
       if (cached) part_eval_trial(pv, cells, sz, pc, r, k, v, dist, pen, veh);
-      else part_eval_ins(pv, cells, sz, r, k, v, dist, pen, veh);
+      else {
+        const PartEval e = part_eval_ins(pv, cells, sz, r, k, v);
+        dist = e.distance;
+        pen = e.penalty;
+        veh = e.veh;
+      }
       const double sc = __dadd_rn(part_scal(X, dist, veh, nullptr, nullptr), __dmul_rn(pw, pen));
       if (bi == 0x7fffffff || sc < bs) {
         bs = sc;

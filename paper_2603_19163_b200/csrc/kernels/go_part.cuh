@@ -39,10 +39,12 @@ struct PartCtx {
   __device__ __forceinline__ int randrange(int lo, int hi) { return rng.randrange(lo, hi); }
   __device__ __forceinline__ int start(int r) const {
     int s = 0;
+#pragma unroll 1
     for (int q = 0; q < r; ++q) s += sz[q];
     return s;
   }
   __device__ __forceinline__ void cell_at(int g, int& r, int& p) const {
+#pragma unroll 1
     for (int q = 0; q < d1; ++q) {
       if (g < sz[q]) {
         r = q;
@@ -72,9 +74,11 @@ struct PartCtx {
   // _pick_row: rows with size >= min_size, uniform (operators.py:140-144)
   __device__ __forceinline__ int pick_row(int min_size) {
     int cnt = 0;
+#pragma unroll 1
     for (int q = 0; q < d1; ++q) cnt += sz[q] >= min_size;
     if (cnt == 0) return -1;
     int k = randbelow(cnt);
+#pragma unroll 1
     for (int q = 0; q < d1; ++q)
       if (sz[q] >= min_size && k-- == 0) return q;
     return -1;
@@ -346,6 +350,7 @@ template <class F>
 __device__ __forceinline__ double np_pairwise_leaf(const F& f, int lo, int n) {
   if (n < 8) {
     double res = -0.0;
+#pragma unroll 1
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, f(lo + i));
     return res;
   }
@@ -353,11 +358,13 @@ __device__ __forceinline__ double np_pairwise_leaf(const F& f, int lo, int n) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
   int i = 8;
+#pragma unroll 1
   for (; i < n - (n % 8); i += 8)
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(lo + i + j));
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll 1
   for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
   return res;
 }
@@ -423,12 +430,17 @@ struct DemV {
 };
 
 // part_eval (go_part.cuh) of the row with v inserted at (ri, pi): the same
-// arithmetic in the same order, element access through RouteIns
-__device__ __forceinline__ void part_eval_ins(const PartView& v, const short* cells, const short* sz,
-                                              int ri, int pi, int val, double& distance,
-                                              double& penalty, int& veh) {
+// arithmetic in the same order, element access through RouteIns.  Out of line:
+// one copy for the lane evaluation, the guided-rebuild trials and the cache build
+// (the inlined copies were a third of the partition kernel's instructions).
+struct PartEval {
+  double distance, penalty;
+  int veh;
+};
+__device__ __noinline__ PartEval part_eval_ins(const PartView& v, const short* cells,
+                                               const short* sz, int ri, int pi, int val) {
   const int n1 = v.n + 1;
-  veh = 0;
+  int veh = 0;
   for (int r = 0; r < v.d1; ++r) veh += (sz[r] + (r == ri)) > 0;
   PySum dsum;
   dsum.init();
@@ -493,18 +505,22 @@ __device__ __forceinline__ void part_eval_ins(const PartView& v, const short* ce
     }
     at += len0;
   }
-  distance = v.variant == 2 ? nl_total : dsum.result();
-  penalty = v.tw ? __dadd_rn(cap_pen, late) : cap_pen;
-  if (v.variant == 1) penalty = __dadd_rn(penalty, (double)viol);
+  PartEval e;
+  e.distance = v.variant == 2 ? nl_total : dsum.result();
+  e.penalty = v.tw ? __dadd_rn(cap_pen, late) : cap_pen;
+  if (v.variant == 1) e.penalty = __dadd_rn(e.penalty, (double)viol);
+  e.veh = veh;
+  return e;
 }
 
 // Φ parts of a compact partition row: distance objective and penalty
 // (+ the "vehicles" objective, builtins.py:133: non-empty routes)
 __device__ __forceinline__ void part_eval(const PartView& v, const short* cells, const short* sz,
                                           double& distance, double& penalty, int* veh = nullptr) {
-  int vh;
-  part_eval_ins(v, cells, sz, -1, 0, 0, distance, penalty, vh);
-  if (veh) *veh = vh;
+  const PartEval e = part_eval_ins(v, cells, sz, -1, 0, 0);
+  distance = e.distance;
+  penalty = e.penalty;
+  if (veh) *veh = e.veh;
 }
 
 }  // namespace go
