@@ -969,6 +969,50 @@ __device__ __forceinline__ void jsp_warp_run(const JspView& J, const G* prio, in
   }
 }
 
+// K guided-rebuild trials of one warp decoded together: the trials share the
+// prefix `st[k]` starts from and differ only in the priority of an operation that
+// is already a job head, so every later prefetch reads the row itself.  The K
+// step bodies are independent dependency chains (shuffle -> min-reduce ->
+// shuffles), interleaved by the unrolled loop to hide their latency; updates are
+// selects, not branches, so the scheduler can mix them.
+template <int K, class G>
+__device__ __forceinline__ void jsp_warp_run_k(const JspView& J, const G* prio, int wl,
+                                               JspWarp (&st)[K]) {
+  const int pj = J.per_job;
+  const bool mine = wl < J.n_jobs;
+  const int n_ops = J.n_jobs * pj;
+#pragma unroll 1
+  for (int step = st[0].step; step < n_ops; ++step) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      JspWarp& w = st[k];
+      const bool live = mine && w.nx < pj;
+      const unsigned key = live ? ((unsigned)w.pr << 16) | ((unsigned)wl << 8) | (unsigned)w.nx
+                                : 0xFFFFFFFFu;
+      const int mfm = __shfl_sync(0xffffffffu, w.mfr, w.mh & 31);
+      const int cand = (w.jf > mfm ? w.jf : mfm) + w.dh;
+      const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
+      const int j = (int)((kmin >> 8) & 0xFFu);
+      const int done = __shfl_sync(0xffffffffu, cand, j);
+      const int m = __shfl_sync(0xffffffffu, w.mh, j);
+      w.mfr = wl == m ? done : w.mfr;
+      const bool me = wl == j;
+      w.jf = me ? done : w.jf;
+      w.nx += me ? 1 : 0;
+      w.pr = me ? w.pn : w.pr;
+      w.mh = me ? w.mh2 : w.mh;
+      w.dh = me ? w.dh2 : w.dh;
+      if (me && w.nx + 1 < pj) {
+        const int o2 = j * pj + w.nx + 1;
+        w.pn = (int)prio[o2];
+        w.mh2 = J.mach[o2];
+        w.dh2 = J.dur[o2];
+      }
+      w.span = done > w.span ? done : w.span;
+    }
+  }
+}
+
 template <class G>
 __device__ __forceinline__ JspWarp jsp_warp_start(const JspView& J, const G* prio, int ovp,
                                                   int ovv, int wl) {
@@ -1052,6 +1096,28 @@ __device__ __forceinline__ int jsp_decode_warp(const JspView& J, const G* prio, 
   return __reduce_max_sync(0xFFFFFFFFu, (unsigned)span);
 }
 
+template <int K, class G>
+__device__ __forceinline__ void jsp_gr_trials(const JspView& J, const G* row, const GrShared& g,
+                                              const JspWarp& base, int jp, int kp, int nd,
+                                              int warp, int nwarps, int wl) {
+#pragma unroll 1
+  for (int i0 = warp * K; i0 < nd; i0 += nwarps * K) {
+    JspWarp st[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      st[k] = base;
+      const int v = g.dom()[i0 + k < nd ? i0 + k : nd - 1];
+      if (wl == jp && st[k].nx == kp) st[k].pr = v;  // op p is job jp's head: its trial priority
+    }
+    jsp_warp_run_k<K>(J, row, wl, st);
+    if (wl == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (i0 + k < nd) g.score()[i0 + k] = st[k].span;
+    }
+  }
+}
+
 template <class G>
 __device__ void team_gr_jsp(const JspView& J, G* row, const GrShared& g, int* scratch,
                             int scratch_ints, int lane, int team, int TS) {
@@ -1068,13 +1134,9 @@ __device__ void team_gr_jsp(const JspView& J, G* row, const GrShared& g, int* sc
       const int jp = p / J.per_job, kp = p - jp * J.per_job;
       JspWarp base = jsp_warp_start(J, row, -1, 0, wl);
       jsp_warp_run(J, row, -1, 0, wl, base, jp, kp);
-      for (int i = warp; i < nd; i += nwarps) {
-        JspWarp st = base;
-        const int v = g.dom()[i];
-        if (wl == jp && st.nx == kp) st.pr = v;  // op p is job jp's head: its trial priority
-        jsp_warp_run(J, row, p, v, wl, st, -1, 0);
-        if (wl == 0) g.score()[i] = st.span;
-      }
+      // warp w takes trials [K w, K w + K) of each group of K * nwarps
+      if (nd > 2 * nwarps) jsp_gr_trials<4>(J, row, g, base, jp, kp, nd, warp, nwarps, wl);
+      else jsp_gr_trials<2>(J, row, g, base, jp, kp, nd, warp, nwarps, wl);
     } else {
       for (int i = warp; i < nd; i += nwarps) {
         const int sp = jsp_decode_warp(J, row, p, g.dom()[i], mf, wl);
