@@ -19,8 +19,8 @@ enum Layout {
   L_I16_FULL_G = 6, L_I32_FULL_G = 7, L_F64_FULL_G = 8
 };
 
-template <class E> struct AccOf { typedef i64 T; };
-template <> struct AccOf<double> { typedef double T; };
+template <class E> struct AccOf { typedef i64 T; static constexpr bool kInt = true; };
+template <> struct AccOf<double> { typedef double T; static constexpr bool kInt = false; };
 
 template <class E> struct ValOf { typedef int T; };
 template <> struct ValOf<double> { typedef double T; };

@@ -434,6 +434,92 @@ __device__ __forceinline__ double qap_delta(const QapView<E>& q, const G* cur, c
   return (double)d;
 }
 
+// Integer QAP: the lanes' deltas evaluated by the whole team.  A lane's delta is
+// a sum of one term per touched position x (qap_delta's two parts regrouped:
+// row x against every column, plus column x against every untouched row), each
+// O(n); the team flattens the (lane, x) items, splits them evenly over its
+// threads and accumulates in int64 shared-memory atomics.  Integer sums are
+// order-free, so the deltas are bit-identical to qap_delta's; per-lane
+// evaluation left 3/4 of every warp idle behind the lanes with the most touched
+// positions (whole-row lanes cost n^2, a swap 4n).  Called by every thread of
+// the team after each lane < T wrote its merged ranges (nr = 255: whole row) and
+// touched count; acc / pre alias la.delta / la.nscal.
+template <class E, class G>
+__device__ __noinline__ void team_qap_delta_int(const QapView<E>& q, const G* cur,
+                                                const unsigned char* rows, unsigned rs,
+                                                const RowLaneState& la, int* wsum, int lane,
+                                                int team, int TS) {
+  typedef typename AccOf<E>::T A;
+  const int n = q.n;
+  int* pre = (int*)la.nscal;  // [TS] inclusive prefix of the touched counts
+  unsigned long long* acc = (unsigned long long*)la.delta;
+  const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
+  int c = pre[lane];  // the lane's count, replaced by its inclusive prefix
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, c, o);
+    if (wl >= o) c += y;
+  }
+  if (wl == 31) wsum[warp] = c;
+  team_bar(team, TS);
+  for (int w = 0; w < warp; ++w) c += wsum[w];
+  int total = 0;
+  for (int w = 0; w < nwarps; ++w) total += wsum[w];
+  pre[lane] = c;
+  team_bar(team, TS);
+#pragma unroll 1
+  for (int it = lane; it < total; it += TS) {
+    int a = 0, b = TS - 1;  // first L with pre[L] > it
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (pre[m] > it) b = m;
+      else a = m + 1;
+    }
+    const int L = a;
+    int x = it - (L > 0 ? pre[L - 1] : 0);
+    const G* row = (const G*)(rows + (size_t)L * rs);
+    const int nm = la.nr[L];
+    A d = 0;
+    if (nm == 255) {  // whole row: row x of sum F(i,j) (D(row_i,row_j) - D(cur_i,cur_j))
+      const int pi = row[x], ci = cur[x];
+      const int s0 = wl % n;  // rotated start: F row reads spread over the banks
+#pragma unroll 4
+      for (int j = s0; j < n; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+#pragma unroll 4
+      for (int j = 0; j < s0; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+    } else {
+      int r = 0;
+#pragma unroll 1
+      for (; r < nm; ++r) {
+        const int len = la.rhi[r * TS + L] - la.rlo[r * TS + L];
+        if (x < len) break;
+        x -= len;
+      }
+      x += la.rlo[r * TS + L];
+      const int pi = row[x], ci = cur[x];
+      const int s0 = wl % n;
+#pragma unroll 4
+      for (int j = s0; j < n; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+#pragma unroll 4
+      for (int j = 0; j < s0; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+      // column x against the untouched rows (the gaps between the ranges)
+      const int rx = row[x], cx = cur[x];
+      int gap_lo = 0;
+#pragma unroll 1
+      for (int g = 0; g <= nm; ++g) {
+        const int gap_hi = g < nm ? la.rlo[g * TS + L] : n;
+#pragma unroll 4
+        for (int i = gap_lo; i < gap_hi; ++i) {
+          const int ci2 = cur[i];
+          d += q.F(i, x) * (q.D(ci2, rx) - q.D(ci2, cx));
+        }
+        if (g < nm) gap_lo = la.rhi[g * TS + L];
+      }
+    }
+    atomicAdd(&acc[L], (unsigned long long)(long long)d);
+  }
+}
+
 template <class G>
 __device__ __forceinline__ void knap_delta(const KnapView& k, const G* cur, const G* row, int n,
                                            int nm, const int* lo, const int* hi, double& dv,
@@ -1889,7 +1975,47 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     }
 
     // ---- C: evaluate every lane (identity mapping) --------------------------------
-    if (lane < T) {
+    constexpr bool kQapInt = KIND == RK_QAP && AccOf<E>::kInt;
+    if constexpr (kQapInt) {  // team-cooperative deltas (team_qap_delta_int)
+      int t = 0;
+      if (lane < T) {
+        const int nr = la.nr[lane];
+        int lo[MAX_RANGES], hi[MAX_RANGES];
+        short l_in[MAX_RANGES], h_in[MAX_RANGES];
+        for (int r = 0; r < nr && r < MAX_RANGES; ++r) {
+          l_in[r] = la.rlo[r * TS + lane];
+          h_in[r] = la.rhi[r * TS + lane];
+        }
+        const int nm = merge_ranges(nr, l_in, h_in, n, lo, hi);
+        if (nm < 0) {
+          t = n;
+          la.nr[lane] = 255;
+        } else {
+          la.nr[lane] = (unsigned char)nm;
+#pragma unroll 1
+          for (int r = 0; r < nm; ++r) {
+            la.rlo[r * TS + lane] = (short)lo[r];
+            la.rhi[r * TS + lane] = (short)hi[r];
+            t += hi[r] - lo[r];
+          }
+        }
+        rd_elem += nm < 0 ? 3u * (unsigned)(n * n) : 3u * (unsigned)(n * t);
+        rd_pos += 2u * (unsigned)n;
+      }
+      ((unsigned long long*)la.delta)[lane] = 0ull;
+      ((int*)la.nscal)[lane] = t;
+      team_qap_delta_int(qv, cur, rows, rs, la, ts->wl, lane, team, TS);
+      team_bar(team, TS);
+      if (lane < T) {
+        const double dq = (double)(long long)((unsigned long long*)la.delta)[lane];
+        la.delta[lane] = dq;
+        la.nscal[lane] = scal + dq;
+        la.npen[lane] = pen;
+        la.aux0[lane] = 0.0;
+        la.aux1[lane] = 0.0;
+      }
+    }
+    if (!kQapInt && lane < T) {
       const G* row = (const G*)(rows + (size_t)lane * rs);
       int lo[MAX_RANGES], hi[MAX_RANGES];
       short l_in[MAX_RANGES], h_in[MAX_RANGES];
