@@ -211,6 +211,24 @@ __device__ __forceinline__ void rop_seg_reset(RowCtx<G>& c) {
 // refilled in cyclic order from c2+1 with the mate's values (rotated to start
 // after c2) that are not in the slice.  Mate rows are read from the snapshot
 // with ld.global.cg (written by other SMs during this launch).
+// Membership of values < 128 in four registers (selects, no local memory).
+struct Bits128 {
+  u32 b0, b1, b2, b3;
+  __device__ __forceinline__ void clear() { b0 = b1 = b2 = b3 = 0u; }
+  __device__ __forceinline__ void set(int v) {
+    const u32 w = (u32)v >> 5, m = 1u << (v & 31);
+    b0 |= w == 0 ? m : 0u;
+    b1 |= w == 1 ? m : 0u;
+    b2 |= w == 2 ? m : 0u;
+    b3 |= w == 3 ? m : 0u;
+  }
+  __device__ __forceinline__ bool test(int v) const {
+    const u32 w = (u32)v >> 5;
+    const u32 x = w == 0 ? b0 : (w == 1 ? b1 : (w == 2 ? b2 : (w == 3 ? b3 : 0u)));
+    return (x >> (v & 31)) & 1u;
+  }
+};
+
 template <class G, class R>
 __device__ __forceinline__ void ox_in_place(G* row, const short* mate, int n, R& rng) {
   int c1 = rng.randbelow(n), c2 = rng.randbelow(n);
@@ -221,6 +239,17 @@ __device__ __forceinline__ void ox_in_place(G* row, const short* mate, int n, R&
   }
   int w = c2 + 1 == n ? 0 : c2 + 1;  // next free position
   int src = w;
+  Bits128 kept;
+  kept.clear();
+  bool small = n <= 128;  // slice membership as a bit set: O(n) instead of O(n * slice)
+  if (small) {
+#pragma unroll 1
+    for (int q = c1; q <= c2; ++q) {
+      const int v = (int)row[q];
+      small &= (unsigned)v < 128u;
+      kept.set(v);
+    }
+  }
   for (int t0 = 0; t0 < n; t0 += 8) {  // 8 mate loads in flight per batch
     G mv[8];
 #pragma unroll
@@ -232,9 +261,14 @@ __device__ __forceinline__ void ox_in_place(G* row, const short* mate, int n, R&
     for (int i = 0; i < 8; ++i) {
       if (t0 + i >= n) break;
       const G v = mv[i];
-      bool kept = false;
-      for (int q = c1; q <= c2; ++q) kept |= row[q] == v;
-      if (kept) continue;
+      bool in_slice = false;
+      if (small) {
+        in_slice = kept.test((int)v);
+      } else {
+#pragma unroll 1
+        for (int q = c1; q <= c2; ++q) in_slice |= row[q] == v;
+      }
+      if (in_slice) continue;
       row[w] = v;
       w = w + 1 == n ? 0 : w + 1;
       if (w == c1) w = c2 + 1 == n ? 0 : c2 + 1;  // never lands inside the slice
