@@ -42,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = LIB.parent / (src.stem + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
                "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include"), "-I", str(CSRC),
+               *os.environ.get("GO_NVCC_DEFINES", "").split(),  # diagnostic builds only
                "-c", str(src), "-o", str(obj)]
         if src.suffix == ".cu":
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []

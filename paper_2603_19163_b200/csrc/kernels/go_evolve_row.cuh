@@ -1569,6 +1569,18 @@ __device__ __forceinline__ u32 warp_uniform_x(G* row, int n, const MateSel& ms, 
 // RG: lane rows in global memory (long rows); a template constant so the
 // shared-memory variant keeps ld.shared / st.shared on its lane rows
 template <int KIND, class E, class G, class U = NoUser, bool RG = false>
+// GO_ROW_TIMING (diagnostic build, tools/row_phase.py): team lane 0 charges
+// clock64 intervals to prof[0..6] (copy, regroup, lane execution incl. the
+// barrier wait, deferred uniform crossover, deferred guided rebuild, evaluation,
+// acceptance), warp leaders their execution time to prof[8..11], and every lane
+// the cycles of each operator kind to prof[12 + kind] (+ 2^40 per application).
+#ifdef GO_ROW_TIMING
+#define GO_RT_DECL unsigned long long rt_[8] = {0}, rt_last_ = clock64()
+#define GO_RT(slot) do { const unsigned long long t_ = clock64(); rt_[(slot)] += t_ - rt_last_; rt_last_ = t_; } while (0)
+#else
+#define GO_RT_DECL do {} while (0)
+#define GO_RT(slot) do {} while (0)
+#endif
 __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X) {
   extern __shared__ __align__(128) unsigned char sm[];
   if (A.gs->stop) return;
@@ -1731,9 +1743,11 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
 
   MateSel ms;
   int snap_min = (int)A.gen0;  // every team has published gen0 (host)
+  GO_RT_DECL;
   for (int gi = 0; gi < A.ngen; ++gi) {
     const long long g = A.gen0 + gi;
     const double temp = A.temps[gi];
+    GO_RT(6);
     // crossover snapshot of this generation (see EvolveArgs::snap)
     ms.init(A.snap, A.prog, (int)g, ev, A.P, A.islands, n);
 
@@ -1757,6 +1771,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     }
     team_bar(team, TS);
 
+    GO_RT(0);
     // ---- B: chain steps, lanes regrouped by sequence ------------------------------
 #pragma unroll 1
     for (int s = 0; s < MAX_CHAIN; ++s) {
@@ -1794,6 +1809,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         la.order[base + rank] = (unsigned short)lane;
       }
       team_bar(team, TS);
+      GO_RT(1);
+#ifdef GO_ROW_TIMING
+      const unsigned long long t_ex0 = clock64();
+#endif
       if (active == 0) break;
 
       if (lane < active) {
@@ -1827,7 +1846,15 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
               U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
             }
           } else {
-            run_part_op(kind, c);
+            {
+#ifdef GO_ROW_TIMING
+              const unsigned long long t_op = clock64();
+#endif
+              run_part_op(kind, c);
+#ifdef GO_ROW_TIMING
+              if (kind < 16) atomicAdd(&A.gs->prof[12 + kind], (clock64() - t_op) + (1ull << 40));
+#endif
+            }
           }
           rng = c.rng;
           err |= c.err;
@@ -1871,7 +1898,15 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
             c.mark_all();
             }
           } else {
-            run_row_op(kind, c);
+            {
+#ifdef GO_ROW_TIMING
+              const unsigned long long t_op = clock64();
+#endif
+              run_row_op(kind, c);
+#ifdef GO_ROW_TIMING
+              if (kind < 16) atomicAdd(&A.gs->prof[12 + kind], (clock64() - t_op) + (1ull << 40));
+#endif
+            }
           }
           rng = c.rng;
           err |= c.err;
@@ -1886,7 +1921,11 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           la.meta[L] = pack_meta(k, 0, q0, q1, q2);
         }
       }
+#ifdef GO_ROW_TIMING
+      if (wl == 0 && warp < 4) atomicAdd(&A.gs->prof[8 + warp], clock64() - t_ex0);
+#endif
       team_bar(team, TS);
+      GO_RT(2);
 
       // ---- deferred uniform crossovers: one warp per lane -------------------------
       const int nux = ts->ndreq;
@@ -1924,6 +1963,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
         team_bar(team, TS);
       }
 
+      GO_RT(3);
       // ---- deferred guided rebuilds: the whole team, one lane at a time ------------
       const int ngr = ts->nreq;
       if (ngr > 0) {
@@ -1972,8 +2012,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
           team_bar(team, TS);
         }
       }
+      GO_RT(4);
     }
 
+    GO_RT(4);
     // ---- C: evaluate every lane (identity mapping) --------------------------------
     constexpr bool kQapInt = KIND == RK_QAP && AccOf<E>::kInt;
     if constexpr (kQapInt) {  // team-cooperative deltas (team_qap_delta_int)
@@ -2089,6 +2131,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       rd_pos += 2u * (unsigned)n;
     }
 
+    GO_RT(5);
     // ---- argmin over (delta, lane), acceptance, credit ----------------------------
     double bd = lane < T ? la.delta[lane] : 1.7976931348623157e308;
     int bl = lane < T ? lane : 0x7fffffff;
@@ -2182,6 +2225,10 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       A.best_obj2[2 * ev + 1] = bo1;
     }
   }
+#ifdef GO_ROW_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 7; ++i) atomicAdd(&A.gs->prof[i], rt_[i]);
+#endif
   if (err) atomicOr(&A.gs->err, err);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {

@@ -10,7 +10,7 @@ shift
 shapes=${*:-C2 C3 C4 C5a C5b}
 mkdir -p gpurun_out/profiles
 for s in $shapes; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:go_evolve \
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:go_evolve \
       -s 5 -c 1 -o gpurun_out/${tag}_${s} python tools/c2_chunks.py $s 7 > gpurun_out/ncu_${tag}_${s}.log 2>&1
   extra=""; [ "$s" = "C2" ] && extra="--traffic"
   python tools/ncu_traffic.py gpurun_out/${tag}_${s}.ncu-rep ${tag}_${s} $extra > /dev/null 2>&1
