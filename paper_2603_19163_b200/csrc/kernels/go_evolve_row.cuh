@@ -1398,8 +1398,6 @@ __device__ __forceinline__ void part_eval_trial(const PartView& v, const short* 
   penalty = v.tw ? __dadd_rn(cap, late) : cap;
 }
 
-// partitions (operators.py:520-546): thread 0 pops / parks / re-inserts, the
-// team scores every trial slot of every open row in parallel (full evaluation)
 // scalar_fitness (engine.py:215-222) of a routing solution from its distance,
 // penalty and vehicle count, objectives in the problem's order
 __device__ __forceinline__ double part_scal(const RowArgs& X, double dist, int veh, double* o0,
@@ -1421,40 +1419,113 @@ __device__ __forceinline__ double PartOpCtx<U>::phi() {
   return __dadd_rn(part_scal(*X, d, veh, nullptr, nullptr), __dmul_rn(pw, p));
 }
 
+// Warp-cooperative edits of a compact partition row (cells, then the row sizes):
+// the same removals / insertions as PartCtx::remove / insert, in the same order,
+// with the O(n) shifts and the O(rows) scans spread over the 32 lanes.  Every
+// lane returns the same value; the row is consistent after each call.
+__device__ __forceinline__ int warp_row_start(const short* sz, int r, int wl) {
+  int s = 0;
+#pragma unroll 1
+  for (int q = wl; q < r; q += 32) s += sz[q];
+  return __reduce_add_sync(0xffffffffu, s);
+}
+__device__ __noinline__ short warp_cells_remove(short* cells, short* sz, int total, int r, int p,
+                                                int wl) {
+  const int gi = warp_row_start(sz, r, wl) + p;
+  const short v = cells[gi];
+#pragma unroll 1
+  for (int base = gi; base < total - 1; base += 32) {  // ascending: a[q] = a[q + 1]
+    const int q = base + wl;
+    const short x = q < total - 1 ? cells[q + 1] : (short)0;
+    __syncwarp();
+    if (q < total - 1) cells[q] = x;
+    __syncwarp();
+  }
+  if (wl == 0) sz[r] -= 1;
+  __syncwarp();
+  return v;
+}
+__device__ __noinline__ void warp_cells_insert(short* cells, short* sz, int total, int r, int p,
+                                               short v, int wl) {
+  const int gi = warp_row_start(sz, r, wl) + p;
+#pragma unroll 1
+  for (int top = total; top > gi; top -= 32) {  // descending: a[q] = a[q - 1]
+    const int q = top - wl;
+    const short x = q > gi ? cells[q - 1] : (short)0;
+    __syncwarp();
+    if (q > gi) cells[q] = x;
+    __syncwarp();
+  }
+  if (wl == 0) {
+    cells[gi] = v;
+    sz[r] += 1;
+  }
+  __syncwarp();
+}
+// (row, position) of the cell holding value v
+__device__ __noinline__ int2 warp_cells_find(const short* cells, const short* sz, int total, int d1,
+                                             short v, int wl) {
+  int gi = 0;
+#pragma unroll 1
+  for (int base = 0; base < total; base += 32) {
+    const int q = base + wl;
+    const unsigned hit = __ballot_sync(0xffffffffu, q < total && cells[q] == v);
+    if (hit) {
+      gi = base + __ffs(hit) - 1;
+      break;
+    }
+  }
+  // PartCtx::cell_at: first row whose running size exceeds gi
+  int carry = 0;
+#pragma unroll 1
+  for (int base = 0; base < d1; base += 32) {
+    const int q = base + wl;
+    int incl = q < d1 ? sz[q] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (wl >= o) incl += y;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, q < d1 && gi < carry + incl);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      const int before = carry + __shfl_sync(0xffffffffu, incl, l) - sz[base + l];
+      return make_int2(base + l, gi - before);
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return make_int2(d1 - 1, 0);
+}
+
+// partitions (operators.py:520-546): warp 0 pops / parks / re-inserts, the
+// team scores every trial slot of every open row in parallel
 __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_cells, int d1,
                              int d2, const RowArgs& X, double pw, const GrShared& g, double* sbuf,
                              TeamShared<double>* ts, int lane, int team, int TS) {
   const int m = g.m();
   if (m == 0) return;
   const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
-  PartCtx c;
-  c.cells = cells;
-  c.sz = sz;
-  c.n = n_cells;
-  c.d1 = d1;
-  c.d2 = d2;
-  c.total = n_cells;
-  if (lane == 0) {
+  if (warp == 0) {
+    int total = n_cells;
     for (int t = 0; t < m; ++t) {
       const int rp = g.picks()[t];
-      g.taken()[t] = c.remove(rp >> 16, rp & 0xFFFF);
+      const short v = warp_cells_remove(cells, sz, total, rp >> 16, rp & 0xFFFF, wl);
+      --total;
+      if (wl == 0) g.taken()[t] = v;
     }
     for (int t = 0; t < m; ++t) {  // park at the end of the first open row
       int r = 0;
       while (r < d1 - 1 && sz[r] >= d2) ++r;
-      c.insert(r, sz[r], (short)g.taken()[t]);
+      warp_cells_insert(cells, sz, total, r, sz[r], (short)g.taken()[t], wl);
+      ++total;
     }
   }
   team_bar(team, TS);
   for (int t = 0; t < m; ++t) {
     const short v = (short)g.taken()[t];
-    if (lane == 0) {
-      c.total = n_cells;
-      int gi = 0;
-      while (cells[gi] != v) ++gi;
-      int r0, p0;
-      c.cell_at(gi, r0, p0);
-      c.remove(r0, p0);
+    if (warp == 0) {
+      const int2 rp = warp_cells_find(cells, sz, n_cells, d1, v, wl);
+      warp_cells_remove(cells, sz, n_cells, rp.x, rp.y, wl);
     }
     team_bar(team, TS);  // the trials below read the row without v
     PartCache pc;
@@ -1502,7 +1573,7 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       ts->wl[warp] = bi;
     }
     team_bar(team, TS);
-    if (lane == 0) {
+    if (warp == 0) {
       double b = 0.0;
       int ib = 0x7fffffff;
       for (int w = 0; w < nwarps; ++w) {
@@ -1518,8 +1589,7 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
         if (k <= sz[r]) break;
         k -= sz[r] + 1;
       }
-      c.total = n_cells - 1;
-      c.insert(r, k, v);
+      warp_cells_insert(cells, sz, n_cells - 1, r, k, v, wl);
     }
     team_bar(team, TS);
   }
