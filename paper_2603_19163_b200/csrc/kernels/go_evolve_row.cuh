@@ -298,6 +298,20 @@ struct QapView {  // F then D, n x n each
     return use_s ? (A)LdShared<E>::load(ds + (unsigned)(a * n + b) * (unsigned)sizeof(E))
                  : (A)d[a * n + b];
   }
+  // the same with the instance's location fixed at compile time (hot loops are
+  // instantiated for both, dispatched once on use_s)
+  template <bool S>
+  __device__ __forceinline__ typename AccOf<E>::T Fx(int i, int j) const {
+    typedef typename AccOf<E>::T A;
+    if constexpr (S) return (A)LdShared<E>::load(fs + (unsigned)(i * n + j) * (unsigned)sizeof(E));
+    else return (A)f[i * n + j];
+  }
+  template <bool S>
+  __device__ __forceinline__ typename AccOf<E>::T Dx(int a, int b) const {
+    typedef typename AccOf<E>::T A;
+    if constexpr (S) return (A)LdShared<E>::load(ds + (unsigned)(a * n + b) * (unsigned)sizeof(E));
+    else return (A)d[a * n + b];
+  }
 };
 
 struct KnapView {  // w[n], v[n] float64
@@ -444,13 +458,15 @@ __device__ __forceinline__ double qap_delta(const QapView<E>& q, const G* cur, c
 // positions (whole-row lanes cost n^2, a swap 4n).  Called by every thread of
 // the team after each lane < T wrote its merged ranges (nr = 255: whole row) and
 // touched count; acc / pre alias la.delta / la.nscal.
-template <class E, class G>
+template <bool S, class E, class G>
 __device__ __noinline__ void team_qap_delta_int(const QapView<E>& q, const G* cur,
                                                 const unsigned char* rows, unsigned rs,
                                                 const RowLaneState& la, int* wsum, int lane,
                                                 int team, int TS) {
   typedef typename AccOf<E>::T A;
   const int n = q.n;
+  auto F = [&](int x, int y) { return q.template Fx<S>(x, y); };
+  auto D = [&](int x, int y) { return q.template Dx<S>(x, y); };
   int* pre = (int*)la.nscal;  // [TS] inclusive prefix of the touched counts
   unsigned long long* acc = (unsigned long long*)la.delta;
   const int warp = lane >> 5, wl = lane & 31, nwarps = TS >> 5;
@@ -484,9 +500,9 @@ __device__ __noinline__ void team_qap_delta_int(const QapView<E>& q, const G* cu
       const int pi = row[x], ci = cur[x];
       const int s0 = wl % n;  // rotated start: F row reads spread over the banks
 #pragma unroll 4
-      for (int j = s0; j < n; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+      for (int j = s0; j < n; ++j) d += F(x, j) * (D(pi, row[j]) - D(ci, cur[j]));
 #pragma unroll 4
-      for (int j = 0; j < s0; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+      for (int j = 0; j < s0; ++j) d += F(x, j) * (D(pi, row[j]) - D(ci, cur[j]));
     } else {
       int r = 0;
 #pragma unroll 1
@@ -499,9 +515,9 @@ __device__ __noinline__ void team_qap_delta_int(const QapView<E>& q, const G* cu
       const int pi = row[x], ci = cur[x];
       const int s0 = wl % n;
 #pragma unroll 4
-      for (int j = s0; j < n; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+      for (int j = s0; j < n; ++j) d += F(x, j) * (D(pi, row[j]) - D(ci, cur[j]));
 #pragma unroll 4
-      for (int j = 0; j < s0; ++j) d += q.F(x, j) * (q.D(pi, row[j]) - q.D(ci, cur[j]));
+      for (int j = 0; j < s0; ++j) d += F(x, j) * (D(pi, row[j]) - D(ci, cur[j]));
       // column x against the untouched rows (the gaps between the ranges)
       const int rx = row[x], cx = cur[x];
       int gap_lo = 0;
@@ -511,7 +527,7 @@ __device__ __noinline__ void team_qap_delta_int(const QapView<E>& q, const G* cu
 #pragma unroll 4
         for (int i = gap_lo; i < gap_hi; ++i) {
           const int ci2 = cur[i];
-          d += q.F(i, x) * (q.D(ci2, rx) - q.D(ci2, cx));
+          d += F(i, x) * (D(ci2, rx) - D(ci2, cx));
         }
         if (g < nm) gap_lo = la.rhi[g * TS + L];
       }
@@ -796,20 +812,22 @@ __device__ __forceinline__ void gr_draw(Stream& rng, const GrShared& g, int n, i
 // QAP swap delta of positions (a, a+1) in the row r (size n-1, without v) with v
 // inserted at a+1 (= the walk step moving v from a+1 to a).  r(k) is virtual:
 // r[k] = row[k < q0 ? k : k + 1] (row still holds v at q0).
-template <class E, class G>
+template <bool S, class E, class G>
 __device__ __forceinline__ typename AccOf<E>::T qap_walk_delta(const QapView<E>& q, const G* row,
                                                                int n, int q0, int v, int a) {
   typedef typename AccOf<E>::T A;
+  auto F = [&](int x, int y) { return q.template Fx<S>(x, y); };
+  auto D = [&](int x, int y) { return q.template Dx<S>(x, y); };
   const int b = a + 1;
   auto rr = [&](int k) -> int { return row[k < q0 ? k : k + 1]; };
   const int pa = rr(a), pb = v;  // before the swap: r[a] at a, v at b
-  A d = (q.F(a, a) - q.F(b, b)) * (q.D(pb, pb) - q.D(pa, pa)) +
-        (q.F(a, b) - q.F(b, a)) * (q.D(pb, pa) - q.D(pa, pb));
+  A d = (F(a, a) - F(b, b)) * (D(pb, pb) - D(pa, pa)) +
+        (F(a, b) - F(b, a)) * (D(pb, pa) - D(pa, pb));
   for (int k = 0; k < n; ++k) {
     if (k == a || k == b) continue;
     const int pk = rr(k < a ? k : k - 1);
-    d += (q.F(a, k) - q.F(b, k)) * (q.D(pb, pk) - q.D(pa, pk)) +
-         (q.F(k, a) - q.F(k, b)) * (q.D(pk, pb) - q.D(pk, pa));
+    d += (F(a, k) - F(b, k)) * (D(pb, pk) - D(pa, pk)) +
+         (F(k, a) - F(k, b)) * (D(pk, pb) - D(pk, pa));
   }
   return d;
 }
@@ -902,7 +920,9 @@ __device__ void team_gr_qap(const QapView<E>& q, G* row, int n, const GrShared& 
     int bp = n - 1;
     for (int hi = n - 1; hi > 0; hi -= cap) {
       const int lo = hi - cap > 0 ? hi - cap : 0;
-      for (int a = lo + lane; a < hi; a += TS) sd[a - lo] = qap_walk_delta(q, row, n, q0, v, a);
+      for (int a = lo + lane; a < hi; a += TS)
+        sd[a - lo] = q.use_s ? qap_walk_delta<true>(q, row, n, q0, v, a)
+                             : qap_walk_delta<false>(q, row, n, q0, v, a);
       team_bar(team, TS);
       if (lane == 0)
         for (int a = hi - 1; a >= lo; --a) {
@@ -2116,7 +2136,8 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       }
       ((unsigned long long*)la.delta)[lane] = 0ull;
       ((int*)la.nscal)[lane] = t;
-      team_qap_delta_int(qv, cur, rows, rs, la, ts->wl, lane, team, TS);
+      if (qv.use_s) team_qap_delta_int<true>(qv, cur, rows, rs, la, ts->wl, lane, team, TS);
+      else team_qap_delta_int<false>(qv, cur, rows, rs, la, ts->wl, lane, team, TS);
       team_bar(team, TS);
       if (lane < T) {
         const double dq = (double)(long long)((unsigned long long*)la.delta)[lane];
