@@ -62,6 +62,9 @@ GO_ROW_KERNEL(go_evolve_qap_f64, go::RK_QAP, double, short)
 GO_ROW_KERNEL(go_evolve_knap, go::RK_KNAP, double, unsigned char)
 GO_ROW_KERNEL(go_evolve_jsp, go::RK_JSP, int, short)
 GO_ROW_KERNEL(go_evolve_part, go::RK_PART, double, short)
+GO_ROW_KERNEL_WIDE(go_evolve_knap, go::RK_KNAP, double, unsigned char)
+GO_ROW_KERNEL_WIDE(go_evolve_jsp, go::RK_JSP, int, short)
+GO_ROW_KERNEL_WIDE(go_evolve_part, go::RK_PART, double, short)
 extern "C" __global__ void go_eval_part(const void* inst, go::RowArgs x, const short* g, double* obj,
                                         double* pen) {
   go::part_eval_entry(inst, x, g, obj, pen);
@@ -728,9 +731,14 @@ int eval_device_rows(go_problem* p, const short* d_g, int m, double* d_o, double
 bool row_rows_smem(int layout) { return layout == 10 || layout == 11; }
 bool row_inst_smem(int layout) { return layout == 10 || layout == 12; }
 
-void* row_kernel(const go_problem* p, int layout) {
+void* row_kernel(const go_problem* p, int layout, int TS) {
   if (p->row_kind == go::RK_USER) return nullptr;  // JIT (row_kernel_jit)
   const bool s = row_rows_smem(layout);
+  if (TS > go::row_max_threads(p->row_kind)) {  // one team wider than the default bound
+    if (p->row_kind == go::RK_KNAP) return s ? (void*)go_evolve_knap_w : (void*)go_evolve_knap_gw;
+    if (p->row_kind == go::RK_PART) return s ? (void*)go_evolve_part_w : (void*)go_evolve_part_gw;
+    return s ? (void*)go_evolve_jsp_w : (void*)go_evolve_jsp_gw;
+  }
   if (p->row_kind == go::RK_QAP) {
     if (p->elem == E_I16) return s ? (void*)go_evolve_qap_i16 : (void*)go_evolve_qap_i16_g;
     if (p->elem == E_I32) return s ? (void*)go_evolve_qap_i32 : (void*)go_evolve_qap_i32_g;
@@ -794,7 +802,7 @@ unsigned row_team_bytes(const go_problem* p, int TS, int layout = 10) {
 
 bool choose_row(const go_problem* p, int TS, int E_req, int* layout, int* E_out, size_t* smem) {
   const size_t optin = (size_t)p->dev.smem_optin;
-  const int Emax = std::max(1, std::min(8, 512 / TS));
+  const int Emax = std::max(1, std::min(8, go::row_max_threads(p->row_kind) / TS));
   const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
   for (int L = 10; L <= 13; ++L) {
     const unsigned inst = row_inst_smem(L) ? pad16(p->img_bytes) : 0u;
@@ -918,7 +926,7 @@ int go_problem_occupancy(go_problem* p, int team_size, int teams_per_cta, int32_
     size_t smem = 0;
     if (!choose_row(p, TS, teams_per_cta, &L, &E, &smem))
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
-    void* fn = row_kernel(p, L);
+    void* fn = row_kernel(p, L, TS);
     CUfunction jf = nullptr;
     int jrc = row_kernel_jit(p, L, &jf);
     if (jrc) return jrc;
@@ -1449,7 +1457,7 @@ int go_engine_create(go_problem* p, const go_engine_config* c, go_engine** out) 
       return fail(GO_E_UNSUPPORTED, "row problem does not fit one team in shared memory");
     e->inst = p->d_img;
     e->inst_bytes = row_inst_smem(e->layout) ? pad16(p->img_bytes) : 0u;
-    e->k_evolve = row_kernel(p, e->layout);
+    e->k_evolve = row_kernel(p, e->layout, e->TS);
     if (int jrc = row_kernel_jit(p, e->layout, &e->k_evolve_jit)) return jrc;
   } else {
   choose_layout(p, e->TS, c->teams_per_cta, &e->layout, &e->E);

@@ -22,6 +22,16 @@
 namespace go {
 
 enum RowKind { RK_QAP = 0, RK_KNAP = 1, RK_JSP = 2, RK_PART = 3, RK_USER = 4 };
+
+// Threads per CTA the statically built evolve kernel of a row kind is compiled
+// for (__launch_bounds__(., 1)): 384 leaves 168 registers per thread (fewer
+// spills into L2-backed local memory) and covers three teams of 128, the most
+// the partition / JSP / knapsack BASELINE instances fit in shared memory; QAP
+// (four teams of 128 fit) and the NVRTC user kernels keep 512.  choose_row()
+// caps teams per CTA accordingly.
+__host__ __device__ constexpr int row_max_threads(int kind) {
+  return kind == RK_QAP || kind == RK_USER ? 512 : 384;
+}
 enum UserEnc { ENC_PERM = 0, ENC_BINARY = 1, ENC_INTEGER = 2 };
 
 // ---- solution views handed to NVRTC-compiled user objectives ----------------------

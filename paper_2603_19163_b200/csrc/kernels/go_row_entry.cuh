@@ -251,10 +251,23 @@ __device__ __forceinline__ void rowops_probe_entry(const void* inst, RowArgs x, 
   }
 
 #define GO_ROW_KERNEL(NAME, KIND, E, G)                                                       \
-  extern "C" __global__ void __launch_bounds__(512, 1) NAME(go::EvolveArgs a, go::RowArgs x) { \
+  extern "C" __global__ void __launch_bounds__(go::row_max_threads(KIND), 1)                   \
+      NAME(go::EvolveArgs a, go::RowArgs x) {                                                  \
     go::evolve_row<KIND, E, G>(a, x);                                                         \
   }                                                                                           \
-  extern "C" __global__ void __launch_bounds__(512, 1) NAME##_g(go::EvolveArgs a,              \
+  extern "C" __global__ void __launch_bounds__(go::row_max_threads(KIND), 1)                   \
+      NAME##_g(go::EvolveArgs a, go::RowArgs x) {                                              \
+    go::evolve_row<KIND, E, G, go::NoUser, true>(a, x);                                       \
+  }
+
+// Teams wider than row_max_threads(KIND) (team_size up to 512): the same kernels
+// compiled for 512 threads
+#define GO_ROW_KERNEL_WIDE(NAME, KIND, E, G)                                                  \
+  extern "C" __global__ void __launch_bounds__(512, 1) NAME##_w(go::EvolveArgs a,              \
                                                               go::RowArgs x) {                \
+    go::evolve_row<KIND, E, G>(a, x);                                                         \
+  }                                                                                           \
+  extern "C" __global__ void __launch_bounds__(512, 1) NAME##_gw(go::EvolveArgs a,             \
+                                                               go::RowArgs x) {               \
     go::evolve_row<KIND, E, G, go::NoUser, true>(a, x);                                       \
   }

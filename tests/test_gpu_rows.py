@@ -52,7 +52,9 @@ def test_eval_matches_oracle_and_reference_golden(golden, name, key):
 @pytest.mark.parametrize("name,small,P,T,Gn,seed", [
     ("qap", True, 4, 32, 25, 11), ("qap", False, 2, 32, 6, 456),
     ("knap", True, 4, 32, 25, 12), ("knap", False, 2, 32, 8, 2024),
-    ("jsp", True, 4, 16, 12, 13), ("jsp", False, 2, 16, 3, 789)])
+    ("jsp", True, 4, 16, 12, 13), ("jsp", False, 2, 16, 3, 789),
+    # teams wider than the 384-thread row kernels: the 512-thread variants
+    ("knap", True, 2, 448, 4, 31), ("jsp", True, 2, 448, 3, 32)])
 def test_evolve_bit_identical_to_oracle(name, small, P, T, Gn, seed):
     prob, ref = _pair(name, small)
     res = G.run(prob, G.EngineConfig(population=P, team_size=T, max_generations=Gn, seed=seed,
@@ -114,7 +116,8 @@ def test_vrptw_eval_bit_exact_against_reference_golden(golden):
 
 @pytest.mark.parametrize("tw,n,veh,P,T,Gn,seed", [(True, 30, 6, 4, 32, 20, 21),
                                                   (False, 30, 6, 4, 32, 20, 22),
-                                                  (True, None, None, 2, 16, 4, 42)])
+                                                  (True, None, None, 2, 16, 4, 42),
+                                                  (True, 30, 6, 2, 448, 3, 23)])
 def test_routing_evolve_bit_identical_to_oracle(tw, n, veh, P, T, Gn, seed):
     prob, ref = _vrptw_pair(n, veh, tw)
     res = G.run(prob, G.EngineConfig(population=P, team_size=T, max_generations=Gn, seed=seed,
