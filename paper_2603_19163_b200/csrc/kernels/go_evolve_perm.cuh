@@ -407,8 +407,14 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
 #ifdef GO_PHASE_TIMING
       const unsigned long long t_ex0 = clock64();
 #endif
-      if (lane < active) {
-        const int L = la.order[lane];
+      // the active lanes (sorted by sequence) in nwarps contiguous chunks, one per
+      // warp: when fewer than TS lanes are active (later chain steps) every warp
+      // gets a share instead of the first warps all of them (the step waits for
+      // its slowest warp; a warp runs its sequence groups one after another)
+      const int chunk = min(32, (active + nwarps - 1) / nwarps);
+      const int pos = wl < chunk ? warp * chunk + wl : active;
+      if (pos < active) {
+        const int L = la.order[pos];
         Stream rng;
         rng.init(mix64_5_ool(A.seed, (u64)evg, (u64)g, (u64)L, 0));
         rng.seek(la.pos[L]);
