@@ -1647,28 +1647,40 @@ __device__ __forceinline__ u32 warp_uniform_x(G* row, int n, const MateSel& ms, 
   if (mate < 0) return pos0;
   const short* mrow = ms.rows + (size_t)mate * n;
   // lane wl draws a contiguous run of cells, so consecutive random() calls
-  // share Philox blocks (one block per two draws instead of one per draw)
+  // share Philox blocks (one block per two draws instead of one per draw); the
+  // draws of a round of 32 cells become a bit mask, then the warp copies the
+  // taken mate cells owner by owner with coalesced, independent loads (the
+  // per-lane copy waited one L2 round trip per taken cell)
   const int c = (n + 31) >> 5, p0 = wl * c, p1 = p0 + c < n ? p0 + c : n;
-  if (p0 < p1) {
-    Stream r;
-    r.k0 = rng.k0;
-    r.k1 = rng.k1;
-    r.seek(pos0 + 2u * (u32)p0);
-    for (int p = p0; p < p1; ++p)
-      if (r.random() < 0.5) {
-        row[p] = (G)__ldcg(mrow + p);
-        lo = p < lo ? p : lo;
-        hi = p + 1;
-      }
+  Stream r;
+  r.k0 = rng.k0;
+  r.k1 = rng.k1;
+  if (p0 < p1) r.seek(pos0 + 2u * (u32)p0);
+#pragma unroll 1
+  for (int base = 0; base < c; base += 32) {
+    unsigned mask = 0u;
+#pragma unroll 1
+    for (int i = 0; i < 32; ++i) {
+      const int p = p0 + base + i;
+      if (base + i >= c || p >= p1) break;
+      if (r.random() < 0.5) mask |= 1u << i;
+    }
+    if (mask) {
+      lo = min(lo, p0 + base + __ffs(mask) - 1);
+      hi = p0 + base + 32 - __clz(mask);
+    }
+#pragma unroll 4
+    for (int o = 0; o < 32; ++o) {  // owner lane o's cells p0(o) + base + wl
+      const unsigned mo = __shfl_sync(0xffffffffu, mask, o);
+      const int p = o * c + base + wl;
+      if ((mo >> wl) & 1u) row[p] = (G)__ldcg(mrow + p);
+    }
   }
   lo = (int)__reduce_min_sync(0xffffffffu, (unsigned)lo);
   hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)hi);
   return pos0 + 2u * (u32)n;
 }
 
-// RG: lane rows in global memory (long rows); a template constant so the
-// shared-memory variant keeps ld.shared / st.shared on its lane rows
-template <int KIND, class E, class G, class U = NoUser, bool RG = false>
 // GO_ROW_TIMING (diagnostic build, tools/row_phase.py): team lane 0 charges
 // clock64 intervals to prof[0..6] (copy, regroup, lane execution incl. the
 // barrier wait, deferred uniform crossover, deferred guided rebuild, evaluation,
@@ -1681,6 +1693,10 @@ template <int KIND, class E, class G, class U = NoUser, bool RG = false>
 #define GO_RT_DECL do {} while (0)
 #define GO_RT(slot) do {} while (0)
 #endif
+
+// RG: lane rows in global memory (long rows); a template constant so the
+// shared-memory variant keeps ld.shared / st.shared on its lane rows
+template <int KIND, class E, class G, class U = NoUser, bool RG = false>
 __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X) {
   extern __shared__ __align__(128) unsigned char sm[];
   if (A.gs->stop) return;
