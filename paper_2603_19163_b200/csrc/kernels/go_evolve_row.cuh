@@ -1905,6 +1905,7 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       if (lane == 0) {  // after the barrier: every thread has read the previous step's counts
         ts->nreq = 0;
         ts->ndreq = 0;
+        ts->ngr = 0;
       }
       int tj = 0;
       if (wl < nseq) {
@@ -1931,204 +1932,223 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
 #endif
       if (active == 0) break;
 
-      if (lane < active) {
-        const int L = la.order[lane];
-        Stream rng;
-        rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
-        rng.seek(la.pos[L]);
-        const u32 meta = la.meta[L];
-        const int k = meta_k(meta);
-        int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
-        bool pending = false;
-        if constexpr (KIND == RK_PART) {
-          PartCtx c;
-          c.rng = rng;
-          c.cells = (short*)(rows + (size_t)L * rs);
-          c.sz = c.cells + X.n_cells;
-          c.n = X.n_cells;
-          c.d1 = X.d1;
-          c.d2 = X.d2;
-          c.n_cfg = X.n_cfg;
-          c.total = X.n_cells;
-          c.err = 0;
-          c.mates = &ms;
-          const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
-          if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
-            la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
-            pending = true;
-          } else if (U::kHasOps && kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
-            if constexpr (U::kHasOps) {
-              PartOpCtx<U> oc{&c, pv, &X, pwt, X.n_cells, X.d1, X.d2};
-              U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
-            }
-          } else {
-            {
-#ifdef GO_ROW_TIMING
-              const unsigned long long t_op = clock64();
-#endif
-              run_part_op(kind, c);
-#ifdef GO_ROW_TIMING
-              if (kind < 16) atomicAdd(&A.gs->prof[12 + kind], (clock64() - t_op) + (1ull << 40));
-#endif
-            }
-          }
-          rng = c.rng;
-          err |= c.err;
-        } else {
-          RowCtx<G> c;
-          c.rng = rng;
-          c.row = (G*)(rows + (size_t)L * rs);
-          c.full = c.row;
-          c.mf = X.mf;
-          c.d1 = X.mf ? X.d1 : 1;
-          c.d2 = X.d2;
-          c.n = X.mf == 1 ? X.d2 : n;  // permutation rows: ops see one row
-          c.n_cfg = X.n_cfg;
-          c.lb = X.lb;
-          c.ub = X.ub;
-          c.err = 0;
-          c.nr = la.nr[L];
-          c.rlo = la.rlo + L;
-          c.rhi = la.rhi + L;
-          c.rstride = TS;
-          c.mates = &ms;
-          const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
-          if (kind == SEQ_GUIDED_REBUILD && KIND == RK_KNAP) {  // O(1) trials: inline
-            gr_cells<KIND>(kv, jv, c.row, n, X.n_cfg, X.lb, X.ub, X.obj_weight, pwt,
-                           scratch + L * X.scratch_ints, c);
-            c.mark_all();
-          } else if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
-            la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
-            pending = true;
-          } else if (kind == SEQ_UNIFORM_X) {  // warp-resolved below
-            la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
-            pending = true;
-          } else if (U::kHasOps && kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
-            if constexpr (U::kHasOps) {
-            RowInst ri{inst, X.off1, KIND == RK_QAP ? RI_QAP : (KIND == RK_KNAP ? RI_KNAP :
-                                                                 (KIND == RK_JSP ? RI_JSP : RI_NONE)),
-                       KIND == RK_QAP ? (int)sizeof(E) : 8, n, X.capacity, n};
-            RowOpCtx<G, U> oc{&c, UserScore{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m},
-                              n, c.d1, X.d2, ri};
-            U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
-            c.mark_all();
-            }
-          } else {
-            {
-#ifdef GO_ROW_TIMING
-              const unsigned long long t_op = clock64();
-#endif
-              run_row_op(kind, c);
-#ifdef GO_ROW_TIMING
-              if (kind < 16) atomicAdd(&A.gs->prof[12 + kind], (clock64() - t_op) + (1ull << 40));
-#endif
-            }
-          }
-          rng = c.rng;
-          err |= c.err;
-          la.nr[L] = (unsigned char)(c.nr > MAX_RANGES ? MAX_RANGES + 1 : c.nr);
-        }
-        if (!pending) {
-          if (s + 1 < k) {
-            const int nq = sample_seq(s_cum, nseq, total, rng);
-            if (s == 0) q1 = nq; else q2 = nq;
-          }
-          la.pos[L] = rng.tell();
-          la.meta[L] = pack_meta(k, 0, q0, q1, q2);
-        }
-      }
-#ifdef GO_ROW_TIMING
-      if (wl == 0 && warp < 4) atomicAdd(&A.gs->prof[8 + warp], clock64() - t_ex0);
-#endif
-      team_bar(team, TS);
-      GO_RT(2);
-
-      // ---- deferred uniform crossovers: one warp per lane -------------------------
-      const int nux = ts->ndreq;
-      if (nux > 0) {
+      // Two passes over the lanes' operators.  Pass 0 runs this step's lanes but
+      // defers OX crossovers, which may wait for a mate team's snapshot of this
+      // generation; pass 1 runs them after the team's guided rebuilds and the
+      // uniform crossovers (warp-resolved, also mate-bound), so the wait
+      // overlaps work that needs no mate.  Lanes are independent and each keeps
+      // its own stream position, so the order between lanes changes no result.
+      // (ts->ngr counts the deferred OX lanes, queued from the back of uxreq.)
 #pragma unroll 1
-        for (int r = warp; r < nux; r += nwarps) {
-          const int L = la.uxreq[r];
+      for (int pass = 0; pass < 2; ++pass) {
+        const int nitems = pass == 0 ? active : ts->ngr;
+        if (pass == 1 && nitems == 0) break;
+        if (lane < nitems) {
+          const int L = pass == 0 ? la.order[lane] : la.uxreq[TS - 1 - lane];
           Stream rng;
           rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
-          int lo, hi;
-          const u32 pend = warp_uniform_x((G*)(rows + (size_t)L * rs), n, ms, rng, wl, lo, hi);
-          __syncwarp();  // every lane has read la.pos before lane 0 updates it
-          if (wl == 0) {
-            rng.seek(pend);
-            const u32 meta = la.meta[L];
-            const int k = meta_k(meta);
-            int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+          const u32 meta = la.meta[L];
+          const int k = meta_k(meta);
+          int q0 = meta_sq(meta, 0), q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+          bool pending = false;
+          if constexpr (KIND == RK_PART) {
+            PartCtx c;
+            c.rng = rng;
+            c.cells = (short*)(rows + (size_t)L * rs);
+            c.sz = c.cells + X.n_cells;
+            c.n = X.n_cells;
+            c.d1 = X.d1;
+            c.d2 = X.d2;
+            c.n_cfg = X.n_cfg;
+            c.total = X.n_cells;
+            c.err = 0;
+            c.mates = &ms;
+            const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
+            if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
+              la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+              pending = true;
+            } else if (pass == 0 && kind == SEQ_OX) {  // after the rebuilds (pass 1)
+              la.uxreq[TS - 1 - atomicAdd(&ts->ngr, 1)] = (unsigned short)L;
+              pending = true;
+            } else if (U::kHasOps && kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+              if constexpr (U::kHasOps) {
+                PartOpCtx<U> oc{&c, pv, &X, pwt, X.n_cells, X.d1, X.d2};
+                U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
+              }
+            } else {
+              {
+  #ifdef GO_ROW_TIMING
+                const unsigned long long t_op = clock64();
+  #endif
+                run_part_op(kind, c);
+  #ifdef GO_ROW_TIMING
+                if (kind < 16) atomicAdd(&A.gs->prof[12 + kind], (clock64() - t_op) + (1ull << 40));
+  #endif
+              }
+            }
+            rng = c.rng;
+            err |= c.err;
+          } else {
+            RowCtx<G> c;
+            c.rng = rng;
+            c.row = (G*)(rows + (size_t)L * rs);
+            c.full = c.row;
+            c.mf = X.mf;
+            c.d1 = X.mf ? X.d1 : 1;
+            c.d2 = X.d2;
+            c.n = X.mf == 1 ? X.d2 : n;  // permutation rows: ops see one row
+            c.n_cfg = X.n_cfg;
+            c.lb = X.lb;
+            c.ub = X.ub;
+            c.err = 0;
+            c.nr = la.nr[L];
+            c.rlo = la.rlo + L;
+            c.rhi = la.rhi + L;
+            c.rstride = TS;
+            c.mates = &ms;
+            const int kind = s_kind[s == 0 ? q0 : (s == 1 ? q1 : q2)];
+            if (kind == SEQ_GUIDED_REBUILD && KIND == RK_KNAP) {  // O(1) trials: inline
+              gr_cells<KIND>(kv, jv, c.row, n, X.n_cfg, X.lb, X.ub, X.obj_weight, pwt,
+                             scratch + L * X.scratch_ints, c);
+              c.mark_all();
+            } else if (kind == SEQ_GUIDED_REBUILD) {  // team-resolved below
+              la.greq[atomicAdd(&ts->nreq, 1)] = (unsigned short)L;
+              pending = true;
+            } else if (kind == SEQ_UNIFORM_X) {  // warp-resolved below
+              la.uxreq[atomicAdd(&ts->ndreq, 1)] = (unsigned short)L;
+              pending = true;
+            } else if (pass == 0 && kind == SEQ_OX) {  // after the rebuilds (pass 1)
+              la.uxreq[TS - 1 - atomicAdd(&ts->ngr, 1)] = (unsigned short)L;
+              pending = true;
+            } else if (U::kHasOps && kind >= SEQ_CUSTOM_BASE) {  // user operator (register_custom)
+              if constexpr (U::kHasOps) {
+              RowInst ri{inst, X.off1, KIND == RK_QAP ? RI_QAP : (KIND == RK_KNAP ? RI_KNAP :
+                                                                   (KIND == RK_JSP ? RI_JSP : RI_NONE)),
+                         KIND == RK_QAP ? (int)sizeof(E) : 8, n, X.capacity, n};
+              RowOpCtx<G, U> oc{&c, UserScore{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m},
+                                n, c.d1, X.d2, ri};
+              U::op(kind - SEQ_CUSTOM_BASE, oc, inst);
+              c.mark_all();
+              }
+            } else {
+              {
+  #ifdef GO_ROW_TIMING
+                const unsigned long long t_op = clock64();
+  #endif
+                run_row_op(kind, c);
+  #ifdef GO_ROW_TIMING
+                if (kind < 16) atomicAdd(&A.gs->prof[12 + kind], (clock64() - t_op) + (1ull << 40));
+  #endif
+              }
+            }
+            rng = c.rng;
+            err |= c.err;
+            la.nr[L] = (unsigned char)(c.nr > MAX_RANGES ? MAX_RANGES + 1 : c.nr);
+          }
+          if (!pending) {
             if (s + 1 < k) {
               const int nq = sample_seq(s_cum, nseq, total, rng);
               if (s == 0) q1 = nq; else q2 = nq;
             }
             la.pos[L] = rng.tell();
-            la.meta[L] = pack_meta(k, 0, meta_sq(meta, 0), q1, q2);
-            if (hi > lo) {  // RowCtx::mark
-              const int nr = la.nr[L];
-              if (nr < MAX_RANGES) {
-                la.rlo[nr * TS + L] = (short)lo;
-                la.rhi[nr * TS + L] = (short)hi;
-              }
-              la.nr[L] = (unsigned char)(nr + 1 > MAX_RANGES ? MAX_RANGES + 1 : nr + 1);
-            }
+            la.meta[L] = pack_meta(k, 0, q0, q1, q2);
           }
         }
+#ifdef GO_ROW_TIMING
+        if (pass == 0 && wl == 0 && warp < 4) atomicAdd(&A.gs->prof[8 + warp], clock64() - t_ex0);
+#endif
         team_bar(team, TS);
-      }
+        GO_RT(2);
+        if (pass == 1) break;
 
-      GO_RT(3);
-      // ---- deferred guided rebuilds: the whole team, one lane at a time ------------
-      const int ngr = ts->nreq;
-      if (ngr > 0) {
-        const GrShared gsh{(int*)&ts->cnt[0][0]};
-#pragma unroll 1
-        for (int r = 0; r < ngr; ++r) {
-          const int L = la.greq[r];
-          G* lrow = (G*)(rows + (size_t)L * rs);
-          if (lane == 0) {
+        // ---- deferred guided rebuilds: the whole team, one lane at a time ------------
+        const int ngr = ts->nreq;
+        if (ngr > 0) {
+          const GrShared gsh{(int*)&ts->cnt[0][0]};
+  #pragma unroll 1
+          for (int r = 0; r < ngr; ++r) {
+            const int L = la.greq[r];
+            G* lrow = (G*)(rows + (size_t)L * rs);
+            if (lane == 0) {
+              Stream rng;
+              rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
+              rng.seek(la.pos[L]);
+              // MULTI_FIXED permutation rows: home_row = randrange(d1) (operators.py:519-521)
+              gsh.row() = (KIND == RK_USER && X.mf == 1) ? rng.randbelow(X.d1) : 0;
+              gr_draw<KIND>(rng, gsh, KIND == RK_PART ? X.n_cells : (X.mf == 1 ? X.d2 : n), X.n_cfg,
+                            X.lb, X.ub,
+                            (const short*)lrow + X.n_cells, X.d1,
+                            KIND == RK_JSP || (KIND == RK_USER && X.enc != ENC_PERM));
+              const u32 meta = la.meta[L];
+              const int k = meta_k(meta);
+              int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+              if (s + 1 < k) {
+                const int nq = sample_seq(s_cum, nseq, total, rng);
+                if (s == 0) q1 = nq; else q2 = nq;
+              }
+              la.pos[L] = rng.tell();
+              la.meta[L] = pack_meta(k, 0, meta_sq(meta, 0), q1, q2);
+              la.nr[L] = (unsigned char)(MAX_RANGES + 1);  // whole row re-evaluated
+            }
+            team_bar(team, TS);
+            if (KIND == RK_QAP) {
+              team_gr_qap(qv, lrow, n, gsh, la.delta, lane, team, TS);
+            } else if (KIND == RK_JSP) {
+              team_gr_jsp(jv, lrow, gsh, scratch, X.scratch_ints, lane, team, TS);
+            } else if (KIND == RK_PART) {
+              team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2, X,
+                           pwt, gsh, la.delta, ts, lane, team, TS);
+            } else if (KIND == RK_USER) {
+              const UserScore us{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m};
+              if (X.enc == ENC_PERM)
+                team_gr_user_perm<U>(lrow, n, gsh.row() * X.d2, X.mf == 1 ? X.d2 : n, gsh, us,
+                                     la.delta, ts, lane, team, TS);
+              else
+                team_gr_user_cells<U>(lrow, n, gsh, us, la.delta, lane, team, TS);
+            }
+            team_bar(team, TS);
+          }
+        }
+        GO_RT(4);
+        // ---- deferred uniform crossovers: one warp per lane -------------------------
+        const int nux = ts->ndreq;
+        if (nux > 0) {
+  #pragma unroll 1
+          for (int r = warp; r < nux; r += nwarps) {
+            const int L = la.uxreq[r];
             Stream rng;
             rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
             rng.seek(la.pos[L]);
-            // MULTI_FIXED permutation rows: home_row = randrange(d1) (operators.py:519-521)
-            gsh.row() = (KIND == RK_USER && X.mf == 1) ? rng.randbelow(X.d1) : 0;
-            gr_draw<KIND>(rng, gsh, KIND == RK_PART ? X.n_cells : (X.mf == 1 ? X.d2 : n), X.n_cfg,
-                          X.lb, X.ub,
-                          (const short*)lrow + X.n_cells, X.d1,
-                          KIND == RK_JSP || (KIND == RK_USER && X.enc != ENC_PERM));
-            const u32 meta = la.meta[L];
-            const int k = meta_k(meta);
-            int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
-            if (s + 1 < k) {
-              const int nq = sample_seq(s_cum, nseq, total, rng);
-              if (s == 0) q1 = nq; else q2 = nq;
+            int lo, hi;
+            const u32 pend = warp_uniform_x((G*)(rows + (size_t)L * rs), n, ms, rng, wl, lo, hi);
+            __syncwarp();  // every lane has read la.pos before lane 0 updates it
+            if (wl == 0) {
+              rng.seek(pend);
+              const u32 meta = la.meta[L];
+              const int k = meta_k(meta);
+              int q1 = meta_sq(meta, 1), q2 = meta_sq(meta, 2);
+              if (s + 1 < k) {
+                const int nq = sample_seq(s_cum, nseq, total, rng);
+                if (s == 0) q1 = nq; else q2 = nq;
+              }
+              la.pos[L] = rng.tell();
+              la.meta[L] = pack_meta(k, 0, meta_sq(meta, 0), q1, q2);
+              if (hi > lo) {  // RowCtx::mark
+                const int nr = la.nr[L];
+                if (nr < MAX_RANGES) {
+                  la.rlo[nr * TS + L] = (short)lo;
+                  la.rhi[nr * TS + L] = (short)hi;
+                }
+                la.nr[L] = (unsigned char)(nr + 1 > MAX_RANGES ? MAX_RANGES + 1 : nr + 1);
+              }
             }
-            la.pos[L] = rng.tell();
-            la.meta[L] = pack_meta(k, 0, meta_sq(meta, 0), q1, q2);
-            la.nr[L] = (unsigned char)(MAX_RANGES + 1);  // whole row re-evaluated
-          }
-          team_bar(team, TS);
-          if (KIND == RK_QAP) {
-            team_gr_qap(qv, lrow, n, gsh, la.delta, lane, team, TS);
-          } else if (KIND == RK_JSP) {
-            team_gr_jsp(jv, lrow, gsh, scratch, X.scratch_ints, lane, team, TS);
-          } else if (KIND == RK_PART) {
-            team_gr_part(pv, (short*)lrow, (short*)lrow + X.n_cells, X.n_cells, X.d1, X.d2, X,
-                         pwt, gsh, la.delta, ts, lane, team, TS);
-          } else if (KIND == RK_USER) {
-            const UserScore us{inst, X.obj_weight, pwt, X.mo.maxmask, X.w2, X.mo.m};
-            if (X.enc == ENC_PERM)
-              team_gr_user_perm<U>(lrow, n, gsh.row() * X.d2, X.mf == 1 ? X.d2 : n, gsh, us,
-                                   la.delta, ts, lane, team, TS);
-            else
-              team_gr_user_cells<U>(lrow, n, gsh, us, la.delta, lane, team, TS);
           }
           team_bar(team, TS);
         }
+
+        GO_RT(3);
       }
-      GO_RT(4);
     }
 
     GO_RT(4);
