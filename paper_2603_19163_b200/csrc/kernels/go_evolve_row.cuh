@@ -1365,8 +1365,8 @@ struct PlainRoute {
 // routes in parallel (thread r: distance, capacity term, positive lateness
 // terms), then thread 0 runs the prefix sums in part_eval's order
 __device__ void part_cache_build(const PartView& v, const short* cells, const short* sz,
-                                 PartCache& pc, int lane, int team, int TS) {
-  for (int r = lane; r < v.d1; r += TS) {
+                                 PartCache& pc, int wl) {  // one warp
+  for (int r = wl; r < v.d1; r += 32) {
     int at = 0;
     for (int q = 0; q < r; ++q) at += sz[q];
     const int base = at + r;
@@ -1378,8 +1378,8 @@ __device__ void part_cache_build(const PartView& v, const short* cells, const sh
     pc.loff[r] = base;
     pc.lcnt[r] = cnt;
   }
-  team_bar(team, TS);
-  if (lane == 0) {
+  __syncwarp();
+  if (wl == 0) {
     PySum ds;
     ds.init();
     double cap = 0.0, late = 0.0;
@@ -1395,6 +1395,7 @@ __device__ void part_cache_build(const PartView& v, const short* cells, const sh
       for (int k = b; k < e; ++k) late = __dadd_rn(late, pc.lt[k]);
     }
   }
+  __syncwarp();
 }
 
 // part_eval of the row with v inserted at (ri, pi), from the cache
@@ -1550,19 +1551,19 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       ++total;
     }
   }
-  team_bar(team, TS);
+  // per pick: warp 0 alone re-inserts the previous value, pops this one and
+  // builds the route cache; one team barrier, the trials, a second barrier
+  PartCache pc;
+  const bool cached = pv.variant == 0 && 32 + PartCache::doubles(d1, n_cells) <= 5 * TS;
+  pc.bind(sbuf + 32, d1);
   for (int t = 0; t < m; ++t) {
-    const short v = (short)g.taken()[t];
     if (warp == 0) {
-      const int2 rp = warp_cells_find(cells, sz, n_cells, d1, v, wl);
+      const int2 rp = warp_cells_find(cells, sz, n_cells, d1, (short)g.taken()[t], wl);
       warp_cells_remove(cells, sz, n_cells, rp.x, rp.y, wl);
+      if (cached) part_cache_build(pv, cells, sz, pc, wl);
     }
-    team_bar(team, TS);  // the trials below read the row without v
-    PartCache pc;
-    const bool cached = pv.variant == 0 && 32 + PartCache::doubles(d1, n_cells) <= 5 * TS;
-    pc.bind(sbuf + 32, d1);
-    if (cached) part_cache_build(pv, cells, sz, pc, lane, team, TS);
-    team_bar(team, TS);
+    team_bar(team, TS);  // the trials below read the row without v (and taken[], parked by warp 0)
+    const short v = (short)g.taken()[t];
     int ntr = 0;  // trial slots: open rows in order, positions 0..sz[r]
     for (int r = 0; r < d1; ++r) ntr += sz[r] < d2 ? sz[r] + 1 : 0;
     double bs = 0.0;
@@ -1621,8 +1622,8 @@ __device__ void team_gr_part(const PartView& pv, short* cells, short* sz, int n_
       }
       warp_cells_insert(cells, sz, n_cells - 1, r, k, v, wl);
     }
-    team_bar(team, TS);
   }
+  team_bar(team, TS);
 }
 
 // op_uniform_crossover (operators.py:451-462) resolved by one warp: lane 0 draws
