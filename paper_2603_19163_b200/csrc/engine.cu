@@ -253,6 +253,11 @@ struct go_engine {
   bool k_pending[kDepth] = {};
   cudaEvent_t t_start = nullptr, t_stop = nullptr;
   long long launches = 0;
+  // pinned host staging of go_engine_set/get_population (grown on demand);
+  // pin_ev marks the last copy out of it on `stream`
+  unsigned char* h_pin = nullptr;
+  size_t h_pin_bytes = 0;
+  cudaEvent_t pin_ev = nullptr;
 };
 
 extern "C" {
@@ -598,12 +603,12 @@ void choose_layout(const go_problem* p, int TS, int E_req, int* layout, int* E_o
 }
 
 // ---- solution layout at the ABI (genes[m][d1*d2] + sizes[m][d1]) <-> device rows --
-void to_device_rows(const go_problem* p, const int32_t* genes, const int32_t* sizes, int m,
-                    std::vector<short>& out) {
-  out.assign((size_t)m * p->n, 0);
+static void to_device_rows(const go_problem* p, const int32_t* genes, const int32_t* sizes,
+                           int m, short* out) {
   if (p->family == 1 && p->row_kind == go::RK_PART) {
+    std::fill(out, out + (size_t)m * p->n, (short)0);
     for (int s = 0; s < m; ++s) {
-      short* o = out.data() + (size_t)s * p->n;
+      short* o = out + (size_t)s * p->n;
       int at = 0;
       for (int r = 0; r < p->d1; ++r) {
         const int len = sizes ? sizes[(size_t)s * p->d1 + r] : 0;
@@ -614,7 +619,13 @@ void to_device_rows(const go_problem* p, const int32_t* genes, const int32_t* si
     }
     return;
   }
-  for (size_t i = 0; i < out.size(); ++i) out[i] = (short)genes[i];
+  for (size_t i = 0; i < (size_t)m * p->n; ++i) out[i] = (short)genes[i];
+}
+
+void to_device_rows(const go_problem* p, const int32_t* genes, const int32_t* sizes, int m,
+                    std::vector<short>& out) {
+  out.assign((size_t)m * p->n, 0);
+  to_device_rows(p, genes, sizes, m, out.data());
 }
 
 void from_device_rows(const go_problem* p, const short* rows, int m, int32_t* genes,
@@ -1560,6 +1571,8 @@ int go_engine_destroy(go_engine* e) {
     if (b) cudaFree(b);
   if (e->h_temps) cudaFreeHost(e->h_temps);
   if (e->h_stop) cudaFreeHost(e->h_stop);
+  if (e->h_pin) cudaFreeHost(e->h_pin);
+  if (e->pin_ev) cudaEventDestroy(e->pin_ev);
   for (auto& ev : e->ring_ev)
     if (ev) cudaEventDestroy(ev);
   for (int i = 0; i < go_engine::kDepth; ++i) {
@@ -1627,14 +1640,42 @@ int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const dou
   return GO_OK;
 }
 
+// Pinned staging area of at least `bytes`, free to write (the previous copy
+// out of it has completed).
+static unsigned char* engine_pinned(go_engine* e, size_t bytes) {
+  if (e->pin_ev) {
+    if (cudaEventSynchronize(e->pin_ev) != cudaSuccess) return nullptr;
+  } else if (cudaEventCreateWithFlags(&e->pin_ev, cudaEventDisableTiming) != cudaSuccess) {
+    return nullptr;
+  }
+  if (bytes > e->h_pin_bytes) {
+    if (e->h_pin) cudaFreeHost(e->h_pin);
+    e->h_pin = nullptr;
+    e->h_pin_bytes = 0;
+    if (cudaHostAlloc((void**)&e->h_pin, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    e->h_pin_bytes = bytes;
+  }
+  return e->h_pin;
+}
+
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Replaces the population (engine.py:538-560 semantics: best-evers reset to the
+// new rows, the global best re-selected).  The rows and per-evolver values are
+// staged once into pinned memory and copied asynchronously on the engine
+// stream (duplicates device-to-device); go_engine_run orders after them.
 int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* sizes,
                              const double* obj, const double* pen) {
   if (!e || !genes || !obj) return fail(GO_E_INVALID, "bad arguments");
   CK(cudaSetDevice(e->prob->device));
   const size_t P = e->P, W = e->W;
-  std::vector<short> g;
+  const size_t o_g = 0, o_sc = align16(P * W * 2), o_pe = o_sc + P * 8, o_o2 = o_pe + P * 8,
+               o_gs = align16(o_o2 + P * 16), total = o_gs + sizeof(go::GlobalState);
+  unsigned char* h = engine_pinned(e, total);
+  if (!h) return fail(GO_E_CUDA, "pinned staging allocation failed");
+  short* g = (short*)(h + o_g);
+  double *sc = (double*)(h + o_sc), *pe = (double*)(h + o_pe), *o2 = (double*)(h + o_o2);
   to_device_rows(e->prob, genes, sizes, (int)P, g);
-  std::vector<double> sc(P), pe(P), o2(P * 2, 0.0);
   const double w = e->cfg.obj_weight > 0 ? e->cfg.obj_weight : 1.0;
   const int m = e->mo.m;
   int best = 0;
@@ -1661,28 +1702,31 @@ int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* 
   };
   for (size_t i = 1; i < P; ++i)  // _best_index (engine.py:467-472)
     if (cmp(i, (size_t)best) < 0) best = (int)i;
+  go::GlobalState* gs = (go::GlobalState*)(h + o_gs);
+  *gs = go::GlobalState{};
+  gs->gscal = sc[best];
+  gs->gpen = pe[best];
+  gs->gobj[0] = o2[2 * best];
+  gs->gobj[1] = o2[2 * best + 1];
+  gs->gev = -1;
+  gs->ggen = 0;
+  const cudaStream_t s = e->stream;
+  const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2D = cudaMemcpyDeviceToDevice;
   if (e->obj2) {
-    CK(cudaMemcpy(e->obj2, o2.data(), P * 2 * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(e->best_obj2, o2.data(), P * 2 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(e->obj2, o2, P * 16, H2D, s));
+    CK(cudaMemcpyAsync(e->best_obj2, e->obj2, P * 16, D2D, s));
   }
-  std::vector<long long> zeros(P, 0);
-  CK(cudaMemcpy(e->genes, g.data(), P * W * 2, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->best_genes, g.data(), P * W * 2, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->gbest_genes, g.data() + (size_t)best * W, W * 2, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->scal, sc.data(), P * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->best_scal, sc.data(), P * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->pen, pe.data(), P * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->best_pen, pe.data(), P * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(e->best_gen, zeros.data(), P * 8, cudaMemcpyHostToDevice));
-  go::GlobalState gs{};
-  gs.gscal = sc[best];
-  gs.gpen = pe[best];
-  gs.gobj[0] = o2[2 * best];
-  gs.gobj[1] = o2[2 * best + 1];
-  gs.gev = -1;
-  gs.ggen = 0;
-  CK(cudaMemcpy(e->gs, &gs, sizeof(gs), cudaMemcpyHostToDevice));
-  CK(cudaMemset(e->agg, 0, 70 * 8));
+  CK(cudaMemcpyAsync(e->genes, g, P * W * 2, H2D, s));
+  CK(cudaMemcpyAsync(e->best_genes, e->genes, P * W * 2, D2D, s));
+  CK(cudaMemcpyAsync(e->gbest_genes, e->genes + (size_t)best * W, W * 2, D2D, s));
+  CK(cudaMemcpyAsync(e->scal, sc, P * 8, H2D, s));
+  CK(cudaMemcpyAsync(e->best_scal, e->scal, P * 8, D2D, s));
+  CK(cudaMemcpyAsync(e->pen, pe, P * 8, H2D, s));
+  CK(cudaMemcpyAsync(e->best_pen, e->pen, P * 8, D2D, s));
+  CK(cudaMemsetAsync(e->best_gen, 0, P * 8, s));
+  CK(cudaMemcpyAsync(e->gs, gs, sizeof(*gs), H2D, s));
+  CK(cudaMemsetAsync(e->agg, 0, 70 * 8, s));
+  CK(cudaEventRecord(e->pin_ev, s));
   *e->h_stop = 0;
   e->gen_enqueued = 0;
   return GO_OK;
@@ -1757,6 +1801,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
   CK(cudaSetDevice(e->prob->device));
   const go_engine_config& c = e->cfg;
   go::GlobalState gs{};
+  CK(cudaStreamSynchronize(e->stream));  // set_population's copies are asynchronous
   CK(cudaMemcpy(&gs, e->gs, sizeof(gs), cudaMemcpyDeviceToHost));
   long long done = gs.gens_done;
   const unsigned long long rp0 = gs.rd_pos, re0 = gs.rd_elem;
@@ -1972,24 +2017,30 @@ int go_engine_get_population(go_engine* e, int32_t* genes, int32_t* sizes, doubl
                              double* pen) {
   if (!e) return fail(GO_E_INVALID, "null engine");
   CK(cudaSetDevice(e->prob->device));
-  CK(cudaStreamSynchronize(e->stream));
   const size_t P = e->P, W = e->W;
-  if (genes || sizes) {
-    std::vector<short> g(P * W);
-    CK(cudaMemcpy(g.data(), e->genes, P * W * 2, cudaMemcpyDeviceToHost));
-    from_device_rows(e->prob, g.data(), (int)P, genes, sizes);
-  }
-  std::vector<double> sc(P);
-  CK(cudaMemcpy(sc.data(), e->scal, P * 8, cudaMemcpyDeviceToHost));
-  if (obj && e->obj2) {
-    std::vector<double> o2(P * 2);
-    CK(cudaMemcpy(o2.data(), e->obj2, P * 2 * 8, cudaMemcpyDeviceToHost));
+  const size_t o_g = 0, o_sc = align16(P * W * 2), o_pe = o_sc + P * 8, o_o2 = o_pe + P * 8,
+               total = o_o2 + P * 16;
+  unsigned char* h = engine_pinned(e, total);
+  if (!h) return fail(GO_E_CUDA, "pinned staging allocation failed");
+  short* g = (short*)(h + o_g);
+  double *sc = (double*)(h + o_sc), *pe = (double*)(h + o_pe), *o2 = (double*)(h + o_o2);
+  const cudaStream_t s = e->stream;
+  const cudaMemcpyKind D2H = cudaMemcpyDeviceToHost;
+  const bool rows = genes || sizes, want_o2 = obj && e->obj2;
+  if (rows) CK(cudaMemcpyAsync(g, e->genes, P * W * 2, D2H, s));
+  if (obj && !want_o2) CK(cudaMemcpyAsync(sc, e->scal, P * 8, D2H, s));
+  if (want_o2) CK(cudaMemcpyAsync(o2, e->obj2, P * 16, D2H, s));
+  if (pen) CK(cudaMemcpyAsync(pe, e->pen, P * 8, D2H, s));
+  CK(cudaEventRecord(e->pin_ev, s));
+  CK(cudaEventSynchronize(e->pin_ev));
+  if (rows) from_device_rows(e->prob, g, (int)P, genes, sizes);
+  if (want_o2) {
     for (size_t i = 0; i < P; ++i)
       for (int k = 0; k < e->mo.m; ++k) obj[i * e->mo.m + k] = o2[2 * i + k];
   } else if (obj) {
     for (size_t i = 0; i < P; ++i) obj[i] = sc[i] * e->obj_sign_over_w;
   }
-  if (pen) CK(cudaMemcpy(pen, e->pen, P * 8, cudaMemcpyDeviceToHost));
+  if (pen) std::memcpy(pen, pe, P * 8);
   return GO_OK;
 }
 

@@ -284,58 +284,47 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
   i16* aux = wrow;
   int mypos = keep + wl;  // current slot of taken value wl
   const int sz = n - 1;  // trials pos = 0 .. n-1 of the (n-1)-row without v (cyclic tour)
+  const int seg = (n + 31) >> 5;  // trial slots per lane
   for (int t = 0; t < m; ++t) {
     const int v = __shfl_sync(FULL, mytaken, t);
     const int q0 = __shfl_sync(FULL, mypos, t);
     auto rv = [&](int i) -> int { return aux[i < q0 ? i : i + 1]; };  // row without v
-    const int first = rv(0), last = rv(sz - 1);
-    Acc best = 0;
+    // Each lane scans a contiguous run of `seg` slots: the element before a
+    // slot is the previous slot's element, already in registers, so the only
+    // dependency between slots is the running first-minimum and the loads of
+    // a run are all independent (no shuffles in the scan).  Runs are in slot
+    // order across lanes, so the (score, slot) reduction below keeps the
+    // reference's first minimum.
+    typedef typename Policy::Scan Scan;
+    Scan best = 0;
     int bp = 0x7fffffff;
-    int carry = last;  // element before slot 0 (cyclic)
-    // d(prev, v) of slot p is d(v, next) of slot p-1 (symmetric matrices,
-    // problems.py:97-107): two matrix reads per slot instead of three
-    Acc carry_b = pol.cost_acc(v, last);
-    for (int b = 0; b < n; b += 64) {  // two chunks in flight
-      const int p0 = b + wl, p1 = b + 32 + wl;
-      const int e0 = p0 < sz ? rv(p0) : first;
-      const int e1 = p1 < sz ? rv(p1) : first;
-      const Acc b0 = pol.cost_acc(v, e0), b1 = pol.cost_acc(v, e1);
-      int pv0 = __shfl_up_sync(FULL, e0, 1);
-      int pv1 = __shfl_up_sync(FULL, e1, 1);
-      Acc a0 = __shfl_up_sync(FULL, b0, 1);
-      Acc a1 = __shfl_up_sync(FULL, b1, 1);
-      const int e0_31 = __shfl_sync(FULL, e0, 31);
-      const Acc b0_31 = __shfl_sync(FULL, b0, 31);
-      if (wl == 0) {
-        pv0 = carry;
-        pv1 = e0_31;
-        a0 = carry_b;
-        a1 = b0_31;
-      }
-      carry = __shfl_sync(FULL, e1, 31);
-      carry_b = __shfl_sync(FULL, b1, 31);
-      if (p0 < n) {  // the reference's float64 order: (d(prev,v) + d(v,next)) - d(prev,next)
-        const Acc c0 = pol.cost_acc(pv0, e0);
-        const Acc sc = Policy::kIntegral ? a0 + b0 - c0
-                                         : (Acc)(((double)a0 + (double)b0) - (double)c0);
+    const int s_lo = wl * seg;
+    const int s_hi = s_lo + seg < n ? s_lo + seg : n;
+    if (s_lo < n) {
+      const int first = rv(0);
+      // d(prev, v) of slot p is d(v, next) of slot p-1 (symmetric matrices,
+      // problems.py:97-107): two matrix reads per slot instead of three
+      int pe = rv(s_lo == 0 ? sz - 1 : s_lo - 1);  // element before slot s_lo (cyclic)
+      Scan pb = pol.cost_scan(v, pe);
+#pragma unroll 2
+      for (int p = s_lo; p < s_hi; ++p) {
+        const int e = p < sz ? rv(p) : first;
+        const Scan b = pol.cost_scan(v, e);
+        const Scan c = pol.cost_scan(pe, e);
+        // the reference's float64 order: (d(prev,v) + d(v,next)) - d(prev,next)
+        const Scan sc = Policy::kIntegral ? pb + b - c
+                                          : (Scan)(((double)pb + (double)b) - (double)c);
         if (bp == 0x7fffffff || sc < best) {
           best = sc;
-          bp = p0;
+          bp = p;
         }
-      }
-      if (p1 < n) {
-        const Acc c1 = pol.cost_acc(pv1, e1);
-        const Acc sc = Policy::kIntegral ? a1 + b1 - c1
-                                         : (Acc)(((double)a1 + (double)b1) - (double)c1);
-        if (bp == 0x7fffffff || sc < best) {
-          best = sc;
-          bp = p1;
-        }
+        pe = e;
+        pb = b;
       }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      const Acc ob = __shfl_xor_sync(FULL, best, off);
+      const Scan ob = __shfl_xor_sync(FULL, best, off);
       const int op = __shfl_xor_sync(FULL, bp, off);
       if (op != 0x7fffffff && (bp == 0x7fffffff || ob < best || (ob == best && op < bp))) {
         best = ob;
