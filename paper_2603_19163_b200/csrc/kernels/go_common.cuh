@@ -400,6 +400,9 @@ struct MateSel {
   const short* rows;  // snapshot of this generation, [P][n]
   const int* prog;
   int start, size, pos, n, gen;
+#ifdef GO_PHASE_TIMING
+  unsigned long long* prof;  // GlobalState::prof (set by the kernel)
+#endif
   __device__ __forceinline__ void init(const short* snap, const int* prog_, int g, int ev, int P,
                                        int islands, int n_) {
     rows = snap ? snap + (size_t)(g % SNAP_DEPTH) * P * n_ : nullptr;
@@ -426,7 +429,18 @@ struct MateSel {
     int j = rng.randbelow(size - 1);
     j += j >= pos;
     j += start;
+#ifdef GO_PHASE_TIMING
+    // prof[27] cycles spent waiting, prof[28] waits, prof[29] picks
+    if (ld_acquire(prog + j) < gen) {
+      const unsigned long long t0 = clock64();
+      while (ld_acquire(prog + j) < gen) __nanosleep(256);
+      atomicAdd(prof + 27, clock64() - t0);
+      atomicAdd(prof + 28, 1ull);
+    }
+    atomicAdd(prof + 29, 1ull);
+#else
     while (ld_acquire(prog + j) < gen) __nanosleep(256);
+#endif
     return j;
   }
   template <class R>

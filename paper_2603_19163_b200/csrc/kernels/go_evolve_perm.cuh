@@ -341,6 +341,9 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
     const double temp = A.temps[gi];
     // crossover snapshot of this generation (see EvolveArgs::snap)
     ms.init(A.snap, A.prog, (int)g, ev, A.P, A.islands, n);
+#ifdef GO_PHASE_TIMING
+    ms.prof = A.gs->prof;
+#endif
 
     // ---- A: every lane draws k and its first sequence (identity mapping) ----
     if (lane < T) {

@@ -1867,6 +1867,9 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
     GO_RT(6);
     // crossover snapshot of this generation (see EvolveArgs::snap)
     ms.init(A.snap, A.prog, (int)g, ev, A.P, A.islands, n);
+#ifdef GO_PHASE_TIMING
+    ms.prof = A.gs->prof;
+#endif
 
     // ---- A: copy the current row into every lane row; draw k and sequence 0
     {

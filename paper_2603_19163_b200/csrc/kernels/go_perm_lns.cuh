@@ -114,6 +114,9 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
   out.changed = 1;
 
   if (kind == SEQ_OX) {  // _ox_sequence (operators.py:412-425)
+#ifdef GO_PHASE_TIMING
+    const unsigned long long t_ox0 = clock64();
+#endif
     a0 = __shfl_sync(FULL, a0, 0);
     const int c1 = __shfl_sync(FULL, a1, 0), c2 = __shfl_sync(FULL, a2, 0);
     const short* mate = ms->rows + (size_t)a0 * n;
@@ -160,6 +163,10 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
     }
     const int s_last = carry;
     __syncwarp();
+#ifdef GO_PHASE_TIMING
+    const unsigned long long t_ox1 = clock64();
+    if (wl == 0) atomicAdd(ms->prof + 30, t_ox1 - t_ox0);  // staging + kept slice
+#endif
     // fill: mate values from c2+1 (cyclic) not in the slice, into the free
     // positions from c2+1 (cyclic); with F the fill sequence and S the slice
     // the child read cyclically from c2+1 is F ++ S
@@ -212,6 +219,9 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
       __threadfence_block();
       out.len = perm_row_length(pol, dst, n, wl);
     }
+#ifdef GO_PHASE_TIMING
+    if (wl == 0) atomicAdd(ms->prof + 31, clock64() - t_ox1);  // fill + length
+#endif
     return out;
   }
 

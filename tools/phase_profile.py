@@ -34,6 +34,13 @@ for chunk in (50, 300):
     for label, b in (("OX", 16), ("shuffles", 18), ("guided rebuild", 20)):
         if v[b + 1]:
             print(f"  {label:15s} {v[b + 1]:9.0f} applications, mean {v[b] / v[b + 1]:9.0f} cycles")
+    if v[29]:
+        print(f"  crossover mates: {v[29]:.0f} picks, {v[28]:.0f} waited "
+              f"({v[28] / v[29] * 100:.1f} %), mean wait {v[27] / max(v[28], 1):.0f} cycles, "
+              f"{v[27] / v[29]:.0f} cycles per pick")
+    if v[17]:
+        print(f"  OX parts (mean cycles): staging + kept slice {v[30] / v[17]:.0f}, "
+              f"fill + length {v[31] / v[17]:.0f}")
     if v[26]:
         print("  lane execution per step, by warp index (mean cycles):",
               [int(v[22 + i] / v[26]) for i in range(4)])
