@@ -190,53 +190,96 @@ __global__ void __launch_bounds__(EPI_THREADS, 1) go_epilogue_kernel(EpilogueArg
   const SolKeys pop{A.pen, A.scal, A.obj2};
 
   // ---- 1. per-generation global best / stagnation / target -----------------
-  if (threadIdx.x == 0) s_stop = 0;
+  // engine.py:703-708: each evolver in order against the running global best
+  // (a population argmin is the same thing unless the comparison is the
+  // non-transitive Lexicographic one).  The chunk's per-generation argmins are
+  // independent: one warp each, all in flight at once; thread 0 then walks the
+  // generations with the global state in registers and writes it back once.
+  __shared__ Cand s_gb[MAX_CHUNK];
+  __shared__ long long s_last;
+  const int ngen = A.ngen < MAX_CHUNK ? A.ngen : MAX_CHUNK;
+  if (!mo.lex) {
+    const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int gi = warp; gi < ngen; gi += nw) {
+      const SolKeys rec{A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
+                        A.rec_obj2 ? A.rec_obj2 + (size_t)gi * P * 2 : nullptr};
+      Cand c;
+      c.idx = 0x7fffffff;
+      c.pen = c.scal = c.o0 = c.o1 = 0;
+      for (int i = ln; i < P; i += 32) {
+        const Cand x = rec.at(i);
+        if (c.idx == 0x7fffffff || best_first(x, c, mo)) c = x;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        Cand o;
+        o.pen = __shfl_xor_sync(0xffffffffu, c.pen, off);
+        o.scal = __shfl_xor_sync(0xffffffffu, c.scal, off);
+        o.o0 = __shfl_xor_sync(0xffffffffu, c.o0, off);
+        o.o1 = __shfl_xor_sync(0xffffffffu, c.o1, off);
+        o.idx = __shfl_xor_sync(0xffffffffu, c.idx, off);
+        if (o.idx != 0x7fffffff && (c.idx == 0x7fffffff || best_first(o, c, mo))) c = o;
+      }
+      if (ln == 0) s_gb[gi] = c;
+    }
+  }
   __syncthreads();
-  long long last = A.gen0 - 1;
-  for (int gi = 0; gi < A.ngen; ++gi) {
-    const long long g = A.gen0 + gi;
-    const SolKeys rec{A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
-                      A.rec_obj2 ? A.rec_obj2 + (size_t)gi * P * 2 : nullptr};
-    // engine.py:703-708: each evolver in order against the running global best
-    // (a population argmin is the same thing unless the comparison is the
-    // non-transitive Lexicographic one)
-    const Cand b = mo.lex ? Cand{} : block_select<false>(rec, 0, P, nullptr, 0, red, mo);
-    if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
+    Cand gb = gbest_cand(gs);
+    int gev = gs->gev, stop = 0;
+    long long ggen = gs->ggen, stall = gs->stall, gens_done = gs->gens_done;
+    long long hist_count = gs->hist_count;
+    long long last = A.gen0 - 1;
+    for (int gi = 0; gi < ngen; ++gi) {
+      const long long g = A.gen0 + gi;
       bool improved = false;
       auto take = [&](const Cand& x) {
-        gs->gpen = x.pen;
-        gs->gscal = x.scal;
-        gs->gobj[0] = x.o0;
-        gs->gobj[1] = x.o1;
-        gs->gev = x.idx;
-        gs->ggen = g;
+        gb = x;
+        gev = x.idx;
+        ggen = g;
         improved = true;
       };
       if (mo.lex) {
+        const SolKeys rec{A.rec_pen + (size_t)gi * P, A.rec_scal + (size_t)gi * P,
+                          A.rec_obj2 ? A.rec_obj2 + (size_t)gi * P * 2 : nullptr};
         for (int ev = 0; ev < P; ++ev) {
           const Cand x = rec.at(ev);
-          if (cand_cmp(x, gbest_cand(gs), mo) < 0) take(x);
+          if (cand_cmp(x, gb, mo) < 0) take(x);
         }
-      } else if (cand_cmp(b, gbest_cand(gs), mo) < 0) {
-        take(b);
+      } else if (cand_cmp(s_gb[gi], gb, mo) < 0) {
+        take(s_gb[gi]);
       }
-      if (improved) gs->stall = 0;
-      else gs->stall += 1;
-      gs->gens_done = g;
+      if (improved) stall = 0;
+      else stall += 1;
+      gens_done = g;
       if (A.history && g - 1 < A.hist_cap) {
-        A.history[g - 1] = __dadd_rn(gs->gscal, __dmul_rn(A.pw, gs->gpen));
-        gs->hist_count = g;
+        A.history[g - 1] = __dadd_rn(gb.scal, __dmul_rn(A.pw, gb.pen));
+        hist_count = g;
       }
-      if (A.has_target && !(gs->gpen > 0.0)) {
-        const double v = gs->gscal * A.obj_sign_over_w;
+      last = g;
+      if (A.has_target && !(gb.pen > 0.0)) {
+        const double v = gb.scal * A.obj_sign_over_w;
         const bool hit = A.obj_sign_over_w > 0 ? v <= A.target + 1e-9 : v >= A.target - 1e-9;
-        if (hit) s_stop = 2;
+        if (hit) {
+          stop = 2;
+          break;
+        }
       }
     }
-    __syncthreads();
-    last = g;
-    if (s_stop) break;
+    gs->gpen = gb.pen;
+    gs->gscal = gb.scal;
+    gs->gobj[0] = gb.o0;
+    gs->gobj[1] = gb.o1;
+    gs->gev = gev;
+    gs->ggen = ggen;
+    gs->stall = stall;
+    gs->gens_done = gens_done;
+    gs->hist_count = hist_count;
+    s_stop = stop;
+    s_last = last;
   }
+  __syncthreads();
+  const long long last = s_last;
   // the global best's genes: the team best-ever of its evolver.
   // Under the non-transitive Lexicographic comparison a new global best need
   // not be its team's best-ever; those runs use one-generation chunks and take

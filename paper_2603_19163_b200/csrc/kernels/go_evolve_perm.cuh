@@ -267,6 +267,18 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
         ++bi;
       }
     }
+    // the deferred whole-row sequences (no lane-execution work) right after the
+    // first user operator: the warp holding that operator's long per-lane
+    // loops gets as few other sequence groups as possible
+    if (nu > 0) {
+      int j2 = 0;
+      s_grank[j2++] = s_gord[0];
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 1; i < nseq; ++i)
+          if (perm_deferred(R->kind[s_gord[i]]) == (pass == 0)) s_grank[j2++] = s_gord[i];
+      for (int i = 0; i < nseq; ++i) s_gord[i] = s_grank[i];
+      for (int i = 0; i < nseq; ++i) s_grank[s_gord[i]] = i;
+    }
 #endif
   }
   __syncthreads();
