@@ -357,6 +357,17 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Polling loads: ld.acquire compiles to a strong load plus an L1 invalidation
+// (CCTL.IVALL) of the whole SM, so spin loops poll with relaxed loads and
+// acquire once, after the wait is over.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -372,7 +383,7 @@ __device__ __forceinline__ void snap_publish(short* snap, int* prog, int P, int 
     for (;;) {
       int mn = 0x7fffffff;
       for (int t = lane; t < P; t += 32) {
-        const int v = ld_acquire(prog + t);
+        const int v = ld_relaxed(prog + t);
         mn = v < mn ? v : mn;
       }
       mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
@@ -380,6 +391,7 @@ __device__ __forceinline__ void snap_publish(short* snap, int* prog, int P, int 
       if (mn >= target) break;
       __nanosleep(256);
     }
+    fence_acq_rel_gpu();  // pairs with the readers' st.release of their progress
   }
   team_bar(team, nthreads);
   short* dst = snap + ((size_t)(gnext % SNAP_DEPTH) * P + ev) * n;
@@ -429,17 +441,27 @@ struct MateSel {
     int j = rng.randbelow(size - 1);
     j += j >= pos;
     j += start;
-#ifdef GO_PHASE_TIMING
-    // prof[27] cycles spent waiting, prof[28] waits, prof[29] picks
+    // one acquire load (pairs with the mate's st.release); if the mate is not
+    // there yet, poll relaxed and acquire again once it is
     if (ld_acquire(prog + j) < gen) {
+#ifdef GO_PHASE_TIMING
       const unsigned long long t0 = clock64();
-      while (ld_acquire(prog + j) < gen) __nanosleep(256);
-      atomicAdd(prof + 27, clock64() - t0);
+#endif
+      // exponential back-off: a waiting mate is typically tens of microseconds
+      // behind, and every poll costs issue slots the SM's other warps could use
+      unsigned ns = 128;
+      while (ld_relaxed(prog + j) < gen) {
+        __nanosleep(ns);
+        ns = ns < 4096 ? ns * 2 : ns;
+      }
+      (void)ld_acquire(prog + j);
+#ifdef GO_PHASE_TIMING
+      atomicAdd(prof + 27, clock64() - t0);  // prof[27] cycles spent waiting, [28] waits
       atomicAdd(prof + 28, 1ull);
+#endif
     }
-    atomicAdd(prof + 29, 1ull);
-#else
-    while (ld_acquire(prog + j) < gen) __nanosleep(256);
+#ifdef GO_PHASE_TIMING
+    atomicAdd(prof + 29, 1ull);  // picks
 #endif
     return j;
   }
