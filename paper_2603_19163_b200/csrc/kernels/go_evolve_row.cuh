@@ -575,8 +575,11 @@ __device__ __forceinline__ void knap_delta(const KnapView& k, const G* cur, cons
 
 // serial schedule generator (builtins.py:429-453); scratch: job_free[n_jobs],
 // mach_free[n_mach] (ints) then next[n_jobs] (bytes): jsp_scratch_ints() ints
+// An odd count: the evaluation decodes one row per lane with every lane at the
+// same offset of its own scratch at once, so an even stride (40 words for
+// 20 x 15) put 8 lanes on each bank; an odd one gives 32 different banks.
 __host__ __device__ __forceinline__ int jsp_scratch_ints(int n_jobs, int n_mach) {
-  return n_jobs + n_mach + (n_jobs + 3) / 4;
+  return (n_jobs + n_mach + (n_jobs + 3) / 4) | 1;
 }
 template <class G>
 __device__ __forceinline__ int jsp_decode(const JspView& J, const G* prio, int* scratch) {
