@@ -811,22 +811,56 @@ unsigned row_team_bytes(const go_problem* p, int TS, int layout = 10) {
   return go::RowSmem::team_bytes(p->n, p->gsize, TS, p->scratch_ints * 4, row_rows_smem(layout));
 }
 
+// Layouts 10..13: lane rows / instance in shared memory (10), rows only (11),
+// instance only (12), neither (13); the first that fits one team is the
+// default.  Lane rows move to global memory (L2-resident, layout 12/13) when
+// shared memory would hold fewer than half the teams per SM the thread bound
+// allows: C5b's 1000-gene rows take 128 KB per team in shared memory (one
+// team per SM, P = 148) against three teams per SM with global rows (P = 444,
+// 1.75x the move evaluations per second, tools/row_layout_probe.py).
 bool choose_row(const go_problem* p, int TS, int E_req, int* layout, int* E_out, size_t* smem) {
   const size_t optin = (size_t)p->dev.smem_optin;
   const int Emax = std::max(1, std::min(8, go::row_max_threads(p->row_kind) / TS));
   const int E0 = E_req > 0 ? std::min(E_req, Emax) : std::min(4, Emax);
-  for (int L = 10; L <= 13; ++L) {
+  auto fit = [&](int L, int& E, size_t& need) -> bool {
     const unsigned inst = row_inst_smem(L) ? pad16(p->img_bytes) : 0u;
     const unsigned tb = row_team_bytes(p, TS, L);
-    for (int E = E0; E >= 1; --E) {
-      const size_t need = go::PermSmem::team_off(inst) + (size_t)E * tb;
-      if (need <= optin) {
-        *layout = L;
-        *E_out = E;
-        *smem = need;
-        return true;
+    for (E = E0; E >= 1; --E) {
+      need = go::PermSmem::team_off(inst) + (size_t)E * tb;
+      if (need <= optin) return true;
+    }
+    return false;
+  };
+  // teams per SM: E per CTA x CTAs that fit the SM's shared memory (the
+  // opt-in limit + the 1 KB per-CTA reserve), at most the thread bound
+  auto teams = [&](int E, size_t need) -> int {
+    const size_t per_sm = optin + 1024;
+    return std::min(E0, E * (int)(per_sm / (need + 1024)));
+  };
+  int L0 = 10;
+  const char* f = getenv("GO_ROW_LAYOUT");  // diagnostic: first layout to try
+  if (f) L0 = std::max(10, std::min(13, atoi(f)));
+  for (int L = L0; L <= 13; ++L) {
+    int E = 0;
+    size_t need = 0;
+    if (!fit(L, E, need)) continue;
+    if (!f && row_rows_smem(L)) {
+      for (int Lg = 12; Lg <= 13; ++Lg) {
+        int Eg = 0;
+        size_t ng = 0;
+        if (!fit(Lg, Eg, ng)) continue;
+        if (teams(Eg, ng) >= 2 * teams(E, need)) {
+          L = Lg;
+          E = Eg;
+          need = ng;
+        }
+        break;
       }
     }
+    *layout = L;
+    *E_out = E;
+    *smem = need;
+    return true;
   }
   return false;
 }
