@@ -246,6 +246,10 @@ int go_engine_destroy(go_engine* e);
 int go_engine_set_registry(go_engine* e, int nseq, const int32_t* ids, const double* weights,
                            const double* floors, const double* caps, double total,
                            const double* k_weights);
+/* replace the population (engine.py:538-560).  The caller's buffers are
+ * copied into the engine's pinned staging area before the call returns and
+ * may be reused at once; the device copies run asynchronously on the engine
+ * stream, ordered before the next run / step / get call. */
 int go_engine_set_population(go_engine* e, const int32_t* genes, const int32_t* sizes,
                              const double* obj, const double* pen);
 /* run until `max_generations` total generations or the wall-clock deadline
