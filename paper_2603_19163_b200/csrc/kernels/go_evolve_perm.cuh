@@ -426,8 +426,12 @@ __device__ __forceinline__ void evolve_perm(const EvolveArgs& A, Policy pol) {
       // warp: when fewer than TS lanes are active (later chain steps) every warp
       // gets a share instead of the first warps all of them (the step waits for
       // its slowest warp; a warp runs its sequence groups one after another)
+      // Chunk c goes to warp (c + team) mod nwarps: a CTA's warp w runs on
+      // scheduler w mod 4, so without the rotation every team's first chunk
+      // (the long user-operator loops, sorted first) would share one scheduler
       const int chunk = min(32, (active + nwarps - 1) / nwarps);
-      const int pos = wl < chunk ? warp * chunk + wl : active;
+      const int vwarp = (warp + nwarps - team % nwarps) % nwarps;
+      const int pos = wl < chunk ? vwarp * chunk + wl : active;
       if (pos < active) {
         const int L = la.order[pos];
         Stream rng;
