@@ -1950,8 +1950,12 @@ __device__ __forceinline__ void evolve_row(const EvolveArgs& A, const RowArgs& X
       for (int pass = 0; pass < 2; ++pass) {
         const int nitems = pass == 0 ? active : ts->ngr;
         if (pass == 1 && nitems == 0) break;
-        if (lane < nitems) {
-          const int L = pass == 0 ? la.order[lane] : la.uxreq[TS - 1 - lane];
+        // item i runs on warp (i / 32 + team) mod nwarps: a CTA's warp w runs
+        // on scheduler w mod 4, so the teams' equal sort orders would otherwise
+        // put every team's most expensive sequence groups on one scheduler
+        const int item = ((warp + nwarps - team % nwarps) % nwarps) * 32 + wl;
+        if (item < nitems) {
+          const int L = pass == 0 ? la.order[item] : la.uxreq[TS - 1 - item];
           Stream rng;
           rng.init(row_key_k<KIND>(A.seed, (u64)evg, (u64)g, (u64)L, 0));
           rng.seek(la.pos[L]);
