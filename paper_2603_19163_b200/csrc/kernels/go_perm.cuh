@@ -37,7 +37,7 @@ enum MoveKind {
 __device__ __forceinline__ bool is_3opt(int kind) { return kind >= MV_3OPT && kind < MV_3OPT + 7; }
 
 // source position inside [i, k) of three-opt variant v (see header)
-__device__ __forceinline__ int three_opt_src(int v, int i, int j, int k, int p) {
+__device__ __noinline__ int three_opt_src(int v, int i, int j, int k, int p) {
   const int lc = k - j, q = p - i;
   switch (v) {
     case 0: return p < j ? i + j - 1 - p : p;
