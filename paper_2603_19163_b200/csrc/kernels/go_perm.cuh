@@ -401,6 +401,8 @@ template <class D>
 struct TspPolicy {
   typedef typename D::Acc Acc;
   static constexpr bool kIntegral = D::kIntegral;
+  // instance staged in shared memory: rows are then at most ~480 long
+  static constexpr bool kInSmem = D::kInSmem;
   D d;
   __device__ __forceinline__ int n_items() const { return d.n; }
   __device__ __forceinline__ double cost(int a, int b) const { return (double)d(a, b); }

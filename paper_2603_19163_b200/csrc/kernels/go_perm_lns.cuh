@@ -128,7 +128,9 @@ __device__ __noinline__ DeferRes<typename Policy::Acc> perm_defer(
 #ifdef GO_NO_OX_STAGE
     const bool staged = false;
 #else
-    const bool staged = n <= 32 * 32;
+    // a shared-memory instance bounds n far below 32 * 32: the staged path is
+    // then a compile-time choice and the L2 fallback is not compiled in
+    const bool staged = Policy::kInSmem || n <= 32 * 32;
 #endif
     unsigned* mask = staged ? (unsigned*)wint : (unsigned*)wrow;
     const int nwords = (n + 31) >> 5;
