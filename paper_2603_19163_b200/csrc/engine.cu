@@ -1857,7 +1857,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(e->t_start, e->stream));
-  long long launches = 0;
+  long long launches = time_limit_s > 0 ? 1 : 0;  // the deadline kernel
   long long chunk = 0;
   const int I = c.aos_interval, EI = c.elite_interval, MI = c.migration_interval;
   auto next_mult = [](long long g, long long m) { return (g / m + 1) * m; };
@@ -1962,7 +1962,7 @@ int go_engine_run(go_engine* e, int64_t max_generations, double time_limit_s,
     go::go_epilogue_kernel<<<1, go::EPI_THREADS, 0, e->stream>>>(q);
     CK(cudaGetLastError());
     CK(cudaEventRecord(e->ring_ev[slot], e->stream));
-    launches += 2;
+    launches += e->xover ? 3 : 2;  // (+ the snapshot progress fill) evolve, epilogue
     done = end;
     ++chunk;
   }
